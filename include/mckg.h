@@ -1,0 +1,217 @@
+/*
+ * mckg.h -- C ABI of the B200-native checker core (paper_1211_6193_b200).
+ *
+ * This is the drop-in boundary between host C++ (the mck:: API that mirrors
+ * /root/reference/proj/include/minicudak/ headers) and the hand-written sm_100a
+ * kernels in paper_1211_6193_b200/csrc/.  Plain pointers and sizes only; every
+ * entry point returns an int status (0 = MCKG_OK) and never throws.
+ *
+ * Reference interfaces each entry point replaces (file:line in
+ * /root/reference/proj):
+ *
+ *   mckg_detect_shared      Machine::recordAccess + Machine::clearEpoch
+ *                           (src/racecheck.cpp:9-73, include/minicudak/machine.hpp:407-409),
+ *                           batched over a per-block access trace; the
+ *                           RaceState::reported set (machine.hpp:86-94) and the
+ *                           first-detection order of the Race diagnostics
+ *                           (addDiagnostic, src/machine.cpp:41-46).
+ *   mckg_detect_shared_host the same, from HOST buffers (copies pipelined with
+ *                           detection); the call a CPU-side user makes.
+ *   mckg_sort_triples       iteration order of std::set<tuple<ObjectId,int64_t,int>>
+ *                           RaceState::reported (machine.hpp:91).
+ *   mckg_scan_stuck         the BarrierDeadlock part of Machine::scanStuck
+ *                           (src/deadlock.cpp:12-34): per-block waiting /
+ *                           finished-or-absent thread sets at quiescence.
+ *   mckg_gen_c3             synthetic workload generator (BASELINE config 3);
+ *                           not a reference interface.
+ *
+ * Device pointers are CUDA device pointers on the current device; `stream` is
+ * a cudaStream_t (NULL = legacy default stream).  All launches are
+ * asynchronous on `stream` unless stated otherwise.
+ */
+#ifndef MCKG_H
+#define MCKG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCKG_ABI_VERSION 1
+
+/* ---- status codes ---- */
+#define MCKG_OK 0
+#define MCKG_E_ARG 1       /* invalid argument (null pointer, bad size)            */
+#define MCKG_E_RANGE 2     /* a field exceeds the packed-record limits below       */
+#define MCKG_E_CUDA 3      /* a CUDA runtime call failed (see mckg_last_error)     */
+#define MCKG_E_OVERFLOW 4  /* output capacity exceeded; counts are still complete  */
+#define MCKG_E_ORDER 5     /* trace not in per-block timestamp order (epoch went back) */
+
+/* ---- limits of the packed 16-byte access record ---- */
+#define MCKG_MAX_OFF (1u << 20)   /* byte offset inside a block's shared object  */
+#define MCKG_MAX_LEN 8u           /* scalar access length (char/int/long/ptr)     */
+#define MCKG_MAX_TID (1u << 11)   /* blockDim <= 2048 (reference default 1024)    */
+#define MCKG_MAX_EPOCH (1u << 21) /* barrier episodes per thread                  */
+#define MCKG_MAX_LINES 65536u     /* source lines 0..65535 (line-first table)     */
+#define MCKG_MAX_BID (1u << 22)   /* global block index inside a timestamp key    */
+
+/*
+ * One shared-memory access event, exactly what Machine::recordAccess receives
+ * (racecheck.cpp:9: object, offset, len, ThreadKey, AccessKind, SourceLoc),
+ * with the object and block implied by the trace segment it sits in.
+ *
+ *   w0  bits  0..19  byte offset inside the block's shared object
+ *       bits 20..23  length in bytes (1..8)
+ *       bit  24      1 = write, 0 = read
+ *   w1  bits  0..10  tid (threadIdx.x)
+ *       bits 11..31  epoch = barrier episodes the accessing thread has passed
+ *   line            SourceLoc::line of the access (the reported line)
+ *   sweep           round-robin sweep of the access; the global timestamp of
+ *                   an access is (sweep, gid, bid, tid)
+ *
+ * Within one block segment records are in timestamp order, so epochs are
+ * non-decreasing (every epoch-e access precedes the Turnaround that clears
+ * epoch e, device.cpp:168-178).
+ */
+typedef struct mckg_access {
+  uint32_t w0;
+  uint32_t w1;
+  int32_t line;
+  uint32_t sweep;
+} mckg_access;
+
+#define MCKG_ACC_OFF(a) ((a).w0 & 0xFFFFFu)
+#define MCKG_ACC_LEN(a) (((a).w0 >> 20) & 0xFu)
+#define MCKG_ACC_WRITE(a) (((a).w0 >> 24) & 1u)
+#define MCKG_ACC_TID(a) ((a).w1 & 0x7FFu)
+#define MCKG_ACC_EPOCH(a) ((a).w1 >> 11)
+
+static inline mckg_access mckg_make_access(uint32_t off, uint32_t len, int write, uint32_t tid,
+                                           uint32_t epoch, int32_t line, uint32_t sweep) {
+  mckg_access a;
+  a.w0 = (off & 0xFFFFFu) | ((len & 0xFu) << 20) | ((uint32_t)(write ? 1 : 0) << 24);
+  a.w1 = (tid & 0x7FFu) | (epoch << 11);
+  a.line = line;
+  a.sweep = sweep;
+  return a;
+}
+
+/* Timestamp key of an access: (sweep, bid, tid) packed so that unsigned
+ * comparison is the reference's first-detection order within one grid. */
+static inline uint64_t mckg_ts_key(uint32_t sweep, uint32_t bid, uint32_t tid) {
+  return ((uint64_t)sweep << 32) | ((uint64_t)(bid & (MCKG_MAX_BID - 1)) << 10) | (tid & 0x3FFu);
+}
+#define MCKG_TS_NONE UINT64_MAX
+
+/*
+ * A block-segmented access trace: the events of simulated block b are
+ * events[block_start[b] .. block_start[b+1]).  Block b owns the shared object
+ * obj_base + b (spawnGrid allocates one DeviceShared object per block in bid
+ * order, device.cpp:33-38) of shmem_bytes bytes.
+ */
+typedef struct mckg_trace {
+  const mckg_access* events;
+  const uint64_t* block_start; /* n_blocks + 1 entries, block_start[0] == 0 */
+  uint64_t n_events;
+  uint32_t n_blocks;
+  uint32_t max_block_events;   /* upper bound on any block's event count (staging size) */
+  uint32_t obj_base;
+  uint32_t bid_base;           /* global bid of block 0 (shards of a grid) */
+  uint32_t shmem_bytes;
+  uint32_t gid;
+} mckg_trace;
+
+/* One element of RaceState::reported (machine.hpp:91). */
+typedef struct mckg_race_triple {
+  uint32_t obj;
+  uint32_t byte;
+  int32_t line;
+} mckg_race_triple;
+
+/*
+ * Detector outputs (device memory, caller-owned).  `triples` receives each
+ * reported (obj, byte, line) exactly once, grouped by block in no particular
+ * block order (mckg_sort_triples orders them).  `line_first[l]` receives the
+ * minimum timestamp key at which line l raced (MCKG_TS_NONE if never): the
+ * Race diagnostics are the lines with a key, in increasing key order.
+ * mckg_race_out_reset() initialises counters and the line table.
+ */
+typedef struct mckg_race_out {
+  mckg_race_triple* triples;
+  uint64_t capacity;
+  unsigned long long* n_triples; /* device counter: total reported triples   */
+  unsigned long long* line_first;/* device, MCKG_MAX_LINES entries            */
+  uint32_t* status;              /* device: bit0 overflow, bit1 range, bit2 order */
+} mckg_race_out;
+
+/* Stats of the last launch made through this library on the calling thread. */
+typedef struct mckg_launch_stats {
+  uint32_t kernels;      /* kernels launched by the last entry point call */
+  uint32_t grid;         /* CTAs of the main detector kernel              */
+  uint32_t block;        /* threads per CTA                               */
+  uint32_t smem_bytes;   /* dynamic shared memory per CTA                 */
+} mckg_launch_stats;
+
+int mckg_abi_version(void);
+const char* mckg_last_error(void);
+int mckg_device_count(int* n);
+int mckg_get_launch_stats(mckg_launch_stats* out);
+
+int mckg_race_out_reset(const mckg_race_out* out, void* stream);
+int mckg_detect_shared(const mckg_trace* trace, const mckg_race_out* out, void* stream);
+
+/* Host-buffer entry point: trace->events and trace->block_start are HOST
+ * pointers (pinned or pageable); the events are streamed to the device in
+ * chunks overlapped with detection.  Results are copied back to host:
+ * triples_host (capacity entries; may be NULL when capacity == 0),
+ * *n_triples_host, line_first_host (MCKG_MAX_LINES entries), *status_host.
+ * Synchronous. */
+int mckg_detect_shared_host(const mckg_trace* trace, mckg_race_triple* triples_host,
+                            uint64_t capacity, uint64_t* n_triples_host,
+                            uint64_t* line_first_host, uint32_t* status_host);
+
+/* Sort n device triples into std::set order (obj, byte, line); in place.
+ * obj must lie in [obj_base, obj_base + 2^22). */
+int mckg_sort_triples(mckg_race_triple* triples, uint64_t n, uint32_t obj_base, void* stream);
+
+/*
+ * Deadlock classification at quiescence (deadlock.cpp:12-34).  arrivals[b *
+ * block_dim + t] = number of __syncthreads*() arrivals of thread t of block b
+ * when nothing can move (finished / halted threads keep their final count, a
+ * thread blocked at a barrier counts the barrier it waits at).  A block is
+ * deadlocked iff its counts differ; its waiting threads are those above the
+ * block minimum (the token protocol of device.cpp:111-200 can
+ * never pass a finished thread).  Outputs (device):
+ *   waiting_mask  n_blocks * ceil(block_dim/32) words, bit t = thread t waits
+ *   dl_bids       ascending bids (bid_base + b) of deadlocked blocks
+ *   n_dl          device counter of deadlocked blocks
+ */
+int mckg_scan_stuck(const uint32_t* arrivals, uint32_t n_blocks, uint32_t block_dim,
+                    uint32_t bid_base, uint32_t* waiting_mask, uint32_t* dl_bids,
+                    uint32_t* n_dl, void* stream);
+
+/*
+ * Synthetic BASELINE config-3 trace, generated on the device: blocks
+ * [blk0, blk0 + n_blocks) of the 2^20-block, 1024-event-per-block layout
+ * (256 threads x 2 epochs x 2 accesses of 4 bytes at slot tid*4+k; 1% of the
+ * accesses redirected to thread (tid+1)%256's slot; write with p = 1/2;
+ * line 100+k; sweep = global event index).  Identical, record for record, to
+ * oracle/tracegen.c (the CPU copy used by the tests).  events must hold
+ * n_blocks*1024 records; block_start n_blocks+1 entries (relative to events).
+ */
+int mckg_gen_c3(mckg_access* events, uint64_t* block_start, uint32_t blk0, uint32_t n_blocks,
+                uint64_t seed, void* stream);
+
+#define MCKG_C3_THREADS 256u
+#define MCKG_C3_EPOCHS 2u
+#define MCKG_C3_K 2u
+#define MCKG_C3_EVENTS_PER_BLOCK (MCKG_C3_THREADS * MCKG_C3_EPOCHS * MCKG_C3_K)
+#define MCKG_C3_SHMEM 4096u
+#define MCKG_C3_SEED 0x12116193ull
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCKG_H */

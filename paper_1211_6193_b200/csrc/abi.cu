@@ -1,0 +1,207 @@
+// abi.cu -- C-ABI plumbing (errors, stats, device info) and the host-buffer
+// entry point mckg_detect_shared_host, which streams a host-resident trace to
+// the device in chunks on two CUDA streams so that the PCIe copies of chunk
+// c+1 overlap the detection of chunk c.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mckg {
+
+namespace {
+thread_local std::string g_err;
+thread_local mckg_launch_stats g_stats{};
+}  // namespace
+
+void set_error(const char* what, cudaError_t e) {
+  g_err = what;
+  if (e != cudaSuccess) {
+    g_err += ": ";
+    g_err += cudaGetErrorString(e);
+  }
+}
+
+void note_launch(uint32_t kernels, uint32_t grid, uint32_t block, uint32_t smem) {
+  g_stats.kernels = kernels;
+  g_stats.grid = grid;
+  g_stats.block = block;
+  g_stats.smem_bytes = smem;
+}
+
+void add_launches(uint32_t kernels) { g_stats.kernels = kernels; }
+
+int sm_count() {
+  static thread_local int dev = -1, sms = 0;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d != dev) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+    if (sms <= 0) sms = 148;
+    dev = d;
+  }
+  return sms;
+}
+
+}  // namespace mckg
+
+using namespace mckg;
+
+extern "C" int mckg_abi_version(void) { return MCKG_ABI_VERSION; }
+
+extern "C" const char* mckg_last_error(void) { return g_err.c_str(); }
+
+extern "C" int mckg_device_count(int* n) {
+  if (!n) return MCKG_E_ARG;
+  MCKG_CUDA_TRY(cudaGetDeviceCount(n));
+  return MCKG_OK;
+}
+
+extern "C" int mckg_get_launch_stats(mckg_launch_stats* out) {
+  if (!out) return MCKG_E_ARG;
+  *out = g_stats;
+  return MCKG_OK;
+}
+
+extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* triples_host,
+                                       uint64_t capacity, uint64_t* n_triples_host,
+                                       uint64_t* line_first_host, uint32_t* status_host) {
+  if (!tr || !n_triples_host || !line_first_host || !status_host ||
+      (!triples_host && capacity)) {
+    set_error("mckg_detect_shared_host: null argument");
+    return MCKG_E_ARG;
+  }
+  if (tr->n_blocks && (!tr->events || !tr->block_start)) {
+    set_error("mckg_detect_shared_host: null trace");
+    return MCKG_E_ARG;
+  }
+  const uint64_t* hbs = tr->block_start;
+  // chunk the blocks so each chunk holds <= kChunkEvents records (>= 1 block)
+  const uint64_t kChunkEvents = 1ull << 25;  // 512 MiB of records per chunk
+  std::vector<uint32_t> cuts{0};
+  for (uint32_t b = 0; b < tr->n_blocks;) {
+    uint32_t e = b + 1;
+    while (e < tr->n_blocks && hbs[e + 1] - hbs[b] <= kChunkEvents) ++e;
+    cuts.push_back(e);
+    b = e;
+  }
+  const size_t n_chunks = cuts.size() - 1;
+  uint64_t max_ev = 0;
+  uint32_t max_nb = 0;
+  for (size_t c = 0; c < n_chunks; ++c) {
+    max_ev = std::max<uint64_t>(max_ev, hbs[cuts[c + 1]] - hbs[cuts[c]]);
+    max_nb = std::max<uint32_t>(max_nb, cuts[c + 1] - cuts[c]);
+  }
+  cudaStream_t st[2];
+  MCKG_CUDA_TRY(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
+  MCKG_CUDA_TRY(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+  mckg_access* dev_ev[2] = {nullptr, nullptr};
+  uint64_t* dev_bs[2] = {nullptr, nullptr};
+  uint64_t* pin_bs = nullptr;
+  mckg_race_out out{};
+  int rc = MCKG_OK;
+  uint32_t launches = 0;
+  auto fail = [&](const char* what, cudaError_t e) {
+    set_error(what, e);
+    rc = MCKG_E_CUDA;
+  };
+  do {
+    cudaError_t e;
+    for (int k = 0; k < 2 && n_chunks; ++k) {
+      if ((e = cudaMalloc(&dev_ev[k], std::max<uint64_t>(1, max_ev) * sizeof(mckg_access)))) {
+        fail("cudaMalloc(events)", e);
+        break;
+      }
+      if ((e = cudaMalloc(&dev_bs[k], (max_nb + 1ull) * sizeof(uint64_t)))) {
+        fail("cudaMalloc(block_start)", e);
+        break;
+      }
+    }
+    if (rc) break;
+    if ((e = cudaMallocHost(&pin_bs, (tr->n_blocks + n_chunks + 1ull) * sizeof(uint64_t)))) {
+      fail("cudaMallocHost", e);
+      break;
+    }
+    if ((e = cudaMalloc(&out.triples, std::max<uint64_t>(1, capacity) * sizeof(mckg_race_triple)))) {
+      fail("cudaMalloc(triples)", e);
+      break;
+    }
+    out.capacity = capacity;
+    if ((e = cudaMalloc(&out.n_triples, sizeof(unsigned long long))) ||
+        (e = cudaMalloc(&out.line_first, MCKG_MAX_LINES * sizeof(unsigned long long))) ||
+        (e = cudaMalloc(&out.status, sizeof(uint32_t)))) {
+      fail("cudaMalloc(outputs)", e);
+      break;
+    }
+    if ((rc = mckg_race_out_reset(&out, st[0]))) break;
+    ++launches;
+    if ((e = cudaStreamSynchronize(st[0]))) {
+      fail("reset", e);
+      break;
+    }
+    size_t pos = 0;
+    for (size_t c = 0; c < n_chunks && !rc; ++c) {
+      const int k = (int)(c & 1);
+      const uint32_t b0 = cuts[c], b1 = cuts[c + 1];
+      uint64_t* rb = pin_bs + pos;
+      for (uint32_t b = b0; b <= b1; ++b) rb[b - b0] = hbs[b] - hbs[b0];
+      pos += (b1 - b0) + 1;
+      const uint64_t nev = hbs[b1] - hbs[b0];
+      if ((e = cudaMemcpyAsync(dev_ev[k], tr->events + hbs[b0], nev * sizeof(mckg_access),
+                               cudaMemcpyHostToDevice, st[k]))) {
+        fail("cudaMemcpyAsync(events)", e);
+        break;
+      }
+      if ((e = cudaMemcpyAsync(dev_bs[k], rb, (b1 - b0 + 1ull) * sizeof(uint64_t),
+                               cudaMemcpyHostToDevice, st[k]))) {
+        fail("cudaMemcpyAsync(block_start)", e);
+        break;
+      }
+      mckg_trace sub = *tr;
+      sub.events = dev_ev[k];
+      sub.block_start = dev_bs[k];
+      sub.n_events = nev;
+      sub.n_blocks = b1 - b0;
+      sub.obj_base = tr->obj_base + b0;
+      sub.bid_base = tr->bid_base + b0;
+      rc = mckg_detect_shared(&sub, &out, st[k]);
+      ++launches;
+    }
+    if (rc) break;
+    if ((e = cudaStreamSynchronize(st[0])) || (e = cudaStreamSynchronize(st[1]))) {
+      fail("detect", e);
+      break;
+    }
+    unsigned long long n = 0;
+    if ((e = cudaMemcpy(&n, out.n_triples, sizeof n, cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(line_first_host, out.line_first, MCKG_MAX_LINES * sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost)) ||
+        (e = cudaMemcpy(status_host, out.status, sizeof(uint32_t), cudaMemcpyDeviceToHost))) {
+      fail("cudaMemcpy(results)", e);
+      break;
+    }
+    *n_triples_host = n;
+    uint64_t nc = std::min<uint64_t>(n, capacity);
+    if (nc && (e = cudaMemcpy(triples_host, out.triples, nc * sizeof(mckg_race_triple),
+                              cudaMemcpyDeviceToHost))) {
+      fail("cudaMemcpy(triples)", e);
+      break;
+    }
+    if (n > capacity) rc = MCKG_E_OVERFLOW;
+  } while (0);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(dev_ev[k]);
+    cudaFree(dev_bs[k]);
+  }
+  cudaFreeHost(pin_bs);
+  cudaFree(out.triples);
+  cudaFree(out.n_triples);
+  cudaFree(out.line_first);
+  cudaFree(out.status);
+  cudaStreamDestroy(st[0]);
+  cudaStreamDestroy(st[1]);
+  add_launches(launches);
+  return rc;
+}
