@@ -143,8 +143,15 @@ typedef struct mckg_race_out {
   uint64_t capacity;
   unsigned long long* n_triples; /* device counter: total reported triples   */
   unsigned long long* line_first;/* device, MCKG_MAX_LINES entries            */
-  uint32_t* status;              /* device: bit0 overflow, bit1 range, bit2 order */
+  uint32_t* status;              /* device: MCKG_ST_* bits                     */
 } mckg_race_out;
+
+/* status bits written by the detector */
+#define MCKG_ST_OVERFLOW 1u  /* triples exceeded `capacity` (n_triples is still the full count) */
+#define MCKG_ST_RANGE 2u     /* an event or block exceeded the record / staging limits; skipped */
+#define MCKG_ST_ORDER 4u     /* a block's epochs decreased (trace not in timestamp order)       */
+#define MCKG_ST_DUP 8u       /* the per-block dedup set overflowed: triples may repeat, run
+                                mckg_sort_triples with n_unique to restore the exact set     */
 
 /* Stats of the last launch made through this library on the calling thread. */
 typedef struct mckg_launch_stats {
@@ -173,8 +180,11 @@ int mckg_detect_shared_host(const mckg_trace* trace, mckg_race_triple* triples_h
                             uint64_t* line_first_host, uint32_t* status_host);
 
 /* Sort n device triples into std::set order (obj, byte, line); in place.
- * obj must lie in [obj_base, obj_base + 2^22). */
-int mckg_sort_triples(mckg_race_triple* triples, uint64_t n, uint32_t obj_base, void* stream);
+ * obj must lie in [obj_base, obj_base + 2^22).  When n_unique (a device
+ * counter) is non-NULL, duplicates are removed and the unique count written
+ * there (needed only after MCKG_ST_DUP). */
+int mckg_sort_triples(mckg_race_triple* triples, uint64_t n, uint32_t obj_base,
+                      unsigned long long* n_unique, void* stream);
 
 /*
  * Deadlock classification at quiescence (deadlock.cpp:12-34).  arrivals[b *

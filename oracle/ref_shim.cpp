@@ -245,7 +245,32 @@ int mckref_run(const char* src, const char* filename, int policy, uint64_t seed,
         o << (first ? "" : ",") << "[" << obj << "," << byte << "," << line << "]";
         first = false;
     }
-    o << "],\"events\":[";
+    o << "],\"arrivals\":{";
+    // per grid, per block: __syncthreads arrivals of every thread at the end
+    // of the run (releases + 1 if still waiting), the input of the K4 check
+    {
+        bool firstG = true;
+        for (const auto& [gid, g] : m.config().grids) {
+            if (g.gridDim * g.blockDim > (1 << 16)) continue;
+            o << (firstG ? "" : ",") << "\"" << gid << "\":[";
+            firstG = false;
+            for (int64_t b = 0; b < g.gridDim; ++b) {
+                o << (b ? "," : "") << "[";
+                for (int64_t t = 0; t < g.blockDim; ++t) {
+                    ThreadKey k{gid, static_cast<int>(b), static_cast<int>(t)};
+                    uint32_t c = 0;
+                    auto e = epochOf.find(k);
+                    if (e != epochOf.end()) c = e->second;
+                    auto d = m.config().device.find(k);
+                    if (d != m.config().device.end() && d->second.barrier.waiting) ++c;
+                    o << (t ? "," : "") << c;
+                }
+                o << "]";
+            }
+            o << "]";
+        }
+    }
+    o << "},\"events\":[";
     for (size_t i = 0; i < ev.size(); ++i) {
         const CapEvent& e = ev[i];
         o << (i ? "," : "") << "[" << e.gid << "," << e.bid << "," << e.tid << "," << e.obj << ","

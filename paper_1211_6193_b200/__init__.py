@@ -6,6 +6,8 @@ classification (K4) and report ordering (K5) as hand-written sm_100a kernels in
 ``csrc/``, behind the C ABI ``include/mckg.h`` (``libmckg.so``).  torch is used
 for device memory and streams only.  There is no CPU fallback.
 """
+import importlib
+
 from . import _abi  # noqa: F401
 
 __all__ = ["_abi", "race"]
@@ -13,6 +15,5 @@ __all__ = ["_abi", "race"]
 
 def __getattr__(name):
     if name == "race":
-        from . import race as _race
-        return _race
+        return importlib.import_module(".race", __name__)
     raise AttributeError(name)

@@ -25,6 +25,7 @@ C3_SEED = 0x12116193
 STATUS_OVERFLOW = 1
 STATUS_RANGE = 2
 STATUS_ORDER = 4
+STATUS_DUP = 8
 
 EXPORTS = [
     "mckg_abi_version",
@@ -97,7 +98,7 @@ def load():
     lib.mckg_detect_shared.argtypes = [ctypes.POINTER(Trace), ctypes.POINTER(RaceOut), vp]
     lib.mckg_detect_shared_host.argtypes = [ctypes.POINTER(Trace), vp, u64, ctypes.POINTER(u64),
                                             vp, ctypes.POINTER(u32)]
-    lib.mckg_sort_triples.argtypes = [vp, u64, u32, vp]
+    lib.mckg_sort_triples.argtypes = [vp, u64, u32, vp, vp]
     lib.mckg_scan_stuck.argtypes = [vp, u32, u32, u32, vp, vp, vp, vp]
     lib.mckg_gen_c3.argtypes = [vp, vp, u32, u32, u64, vp]
     _lib = lib

@@ -182,6 +182,19 @@ extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* t
       fail("cudaMemcpy(results)", e);
       break;
     }
+    if ((*status_host & MCKG_ST_DUP) && n > 0) {
+      // the per-block dedup set overflowed: restore the exact set on device
+      if ((rc = mckg_sort_triples(out.triples, std::min<uint64_t>(n, capacity), tr->obj_base,
+                                  out.n_triples, st[0])))
+        break;
+      launches += 4;
+      if ((e = cudaMemcpyAsync(&n, out.n_triples, sizeof n, cudaMemcpyDeviceToHost, st[0])) ||
+          (e = cudaStreamSynchronize(st[0]))) {
+        fail("dedup", e);
+        break;
+      }
+      *status_host &= ~MCKG_ST_DUP;
+    }
     *n_triples_host = n;
     uint64_t nc = std::min<uint64_t>(n, capacity);
     if (nc && (e = cudaMemcpy(triples_host, out.triples, nc * sizeof(mckg_race_triple),

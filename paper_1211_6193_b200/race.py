@@ -100,9 +100,13 @@ def fetch(out, obj_base=1, sort=True, stream=None):
     n = int(out.n_triples.item())
     status = int(out.status.item())
     nc = min(n, out.capacity)
-    if sort and nc > 0:
-        _abi.check(_abi.load().mckg_sort_triples(_ptr(out.triples), nc, obj_base,
+    if (sort or status & _abi.STATUS_DUP) and nc > 0:
+        uniq = out.n_triples if status & _abi.STATUS_DUP else None
+        _abi.check(_abi.load().mckg_sort_triples(_ptr(out.triples), nc, obj_base, _ptr(uniq),
                                                  _stream_handle(stream)), "mckg_sort_triples")
+        if uniq is not None:
+            n = nc = int(out.n_triples.item())
+            status &= ~_abi.STATUS_DUP
     tri = out.triples[:nc].cpu().numpy().view(TRIPLE_DTYPE).reshape(-1)
     lf = out.line_first.cpu().numpy().view(np.uint64)
     return RaceResult(tri.copy(), n, lf.copy(), status)

@@ -1,0 +1,202 @@
+"""CUDA-C programs for parity fixtures (test infrastructure).
+
+* Fig. 1 (the reference corpus sum.cu, tests/golden/sum.cu) and its two
+  mutants that keep line numbers;
+* the scaled Fig. 1 reduction (SURVEY Appendix D gen.sh: one launch, host sum)
+  and its racy variant without the second barrier (C2 shape);
+* the barrier-divergence kernel of C4 (`if (v % 2) __syncthreads();`);
+* random racy kernels (SURVEY Appendix D gen_rand.py shape): 3-11 statements
+  over int / char / misaligned shared accesses, +=, tid-dependent loops,
+  divergent stores and barriers; launched <<<{1,2,3}, {1,2,3,5,8,13,32,33}, 4*{4,8,16,64}>>>.
+"""
+import os
+import random
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def fig1():
+    with open(os.path.join(HERE, "golden", "sum.cu")) as f:
+        return f.read()
+
+
+def fig1_race():
+    lines = fig1().split("\n")
+    lines[13] = ""  # line 14: the second __syncthreads()
+    return "\n".join(lines)
+
+
+def fig1_deadlock():
+    lines = fig1().split("\n")
+    lines[11] = lines[11] + " __syncthreads();"  # inside `if (tid < bdim/2)`
+    return "\n".join(lines)
+
+
+def scaled(n, nthreads, racy=False):
+    """Fig. 1 kernel verbatim (second barrier dropped when racy), host sum."""
+    nb = n // nthreads
+    sync2 = "" if racy else "  __syncthreads();"
+    return f"""#include <stdio.h>
+#include <cuda.h>
+#define N {n}
+#define NBLOCKS {nb}
+#define NTHREADS (N/NBLOCKS)
+__global__ void sum(int* in, int* out) {{
+  extern __shared__ int shared[];
+  int i, tid = threadIdx.x, bid = blockIdx.x, bdim = blockDim.x;
+  shared[tid] = in[bid * bdim + tid];
+  __syncthreads();
+  if (tid < bdim/2) {{
+    shared[tid] += shared[bdim/2 + tid];
+  }}
+{sync2}
+  if (tid == 0) {{
+    for (i=1; i != (bdim/2)+(bdim%2); ++i) {{
+      shared[0] += shared[i];
+    }}
+    out[bid] = shared[0];
+  }}
+}}
+int main(void) {{
+  int i, s, *dev_in, *dev_out, host[N], part[NBLOCKS];
+  for(i = 0; i != N; ++i) {{
+    host[i] = (21*i + 29) % 100;
+  }}
+  cudaMalloc(&dev_in, N * sizeof(int));
+  cudaMalloc(&dev_out, NBLOCKS * sizeof(int));
+  cudaMemcpy(dev_in, host, N * sizeof(int), cudaMemcpyHostToDevice);
+  sum<<<NBLOCKS, NTHREADS, NTHREADS * sizeof(int)>>>(dev_in, dev_out);
+  cudaMemcpy(part, dev_out, NBLOCKS * sizeof(int), cudaMemcpyDeviceToHost);
+  s = 0;
+  for(i = 0; i != NBLOCKS; ++i) {{
+    s += part[i];
+  }}
+  printf("OUTPUT: %d\\n", s);
+  cudaFree(dev_in);
+  cudaFree(dev_out);
+  return 0;
+}}
+"""
+
+
+def divergent_barrier(nblocks, nthreads, seed=0):
+    """C4 miniature: per block all-even / all-odd / mixed values."""
+    rng = random.Random(seed)
+    vals = []
+    for b in range(nblocks):
+        pat = rng.randrange(3)
+        for t in range(nthreads):
+            v = rng.randrange(1 << 20)
+            if pat == 0:
+                v &= ~1
+            elif pat == 1:
+                v |= 1
+            vals.append(v)
+    n = nblocks * nthreads
+    init = ", ".join(str(v) for v in vals)
+    return f"""__global__ void k(int* in, int* out) {{
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  int v = in[g];
+  if (v % 2) {{
+    __syncthreads();
+  }}
+  out[g] = v;
+}}
+int main(void) {{
+  int host[{n}] ;
+  int i, *din, *dout;
+  int vals[{n}] = {{{init}}};
+  for (i = 0; i != {n}; ++i) host[i] = vals[i];
+  cudaMalloc(&din, {n} * sizeof(int));
+  cudaMalloc(&dout, {n} * sizeof(int));
+  cudaMemcpy(din, host, {n} * sizeof(int), cudaMemcpyHostToDevice);
+  k<<<{nblocks}, {nthreads}>>>(din, dout);
+  cudaDeviceSynchronize();
+  return 0;
+}}
+""", vals
+
+
+def divergent_barrier_gen(nblocks, nthreads, seed=0):
+    """Same kernel, inputs computed on the host by a formula (no initializer list)."""
+    a = 2 * seed + 3
+    return f"""__global__ void k(int* in, int* out) {{
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  int v = in[g];
+  if (v % 2) {{
+    __syncthreads();
+  }}
+  out[g] = v;
+}}
+int main(void) {{
+  int host[{nblocks * nthreads}];
+  int i, b, *din, *dout;
+  for (i = 0; i != {nblocks * nthreads}; ++i) {{
+    b = i / {nthreads};
+    if (b % 3 == 0) host[i] = 2 * i;
+    else if (b % 3 == 1) host[i] = 2 * i + 1;
+    else host[i] = (i * {a} + b) % 7;
+  }}
+  cudaMalloc(&din, {nblocks * nthreads} * sizeof(int));
+  cudaMalloc(&dout, {nblocks * nthreads} * sizeof(int));
+  cudaMemcpy(din, host, {nblocks * nthreads} * sizeof(int), cudaMemcpyHostToDevice);
+  k<<<{nblocks}, {nthreads}>>>(din, dout);
+  cudaDeviceSynchronize();
+  return 0;
+}}
+"""
+
+
+def random_kernel(seed):
+    rng = random.Random(seed)
+    nb = rng.choice([1, 2, 3])
+    nt = rng.choice([1, 2, 3, 5, 8, 13, 32, 33])
+    sh = 4 * rng.choice([4, 8, 16, 64])
+    m = sh // 4
+    stmts = []
+    for _ in range(rng.randint(3, 11)):
+        k = rng.randrange(0, 7)
+        c = rng.randrange(0, 5)
+        r = rng.randrange(10)
+        if r == 0:
+            stmts.append(f"s[(t + {k}) % {m}] = t + {c};")
+        elif r == 1:
+            stmts.append(f"x += s[(t * {k + 1} + {c}) % {m}];")
+        elif r == 2:
+            stmts.append(f"c[(t + {k}) % {sh}] = t;")
+        elif r == 3:
+            stmts.append(f"x += c[(t * {k + 1} + {c}) % {sh}];")
+        elif r == 4:
+            stmts.append(f"*(int*)(c + ((t + {k}) % {sh - 4})) = x;")
+        elif r == 5:
+            stmts.append(f"x += *(int*)(c + ((t * {k + 1}) % {sh - 4}));")
+        elif r == 6:
+            stmts.append(f"s[(t + {k}) % {m}] += {c};")
+        elif r == 7:
+            stmts.append(f"for (j = 0; j < t % 3; ++j) {{ s[(t + j + {k}) % {m}] += j; }}")
+        elif r == 8:
+            stmts.append(f"if (t % 2 == 0) {{ s[(t + {k}) % {m}] = x; }}")
+        else:
+            stmts.append("__syncthreads();")
+    body = "\n  ".join(stmts)
+    src = f"""__global__ void k(int* g) {{
+  extern __shared__ int s[];
+  char* c;
+  int t, j, x;
+  c = (char*)s;
+  t = threadIdx.x;
+  x = 0;
+  j = 0;
+  {body}
+  g[blockIdx.x * blockDim.x + t] = x + j;
+}}
+int main(void) {{
+  int* g;
+  cudaMalloc(&g, 4096);
+  cudaMemset(g, 0, 4096);
+  k<<<{nb}, {nt}, {sh}>>>(g);
+  cudaDeviceSynchronize();
+  return 0;
+}}
+"""
+    return src
