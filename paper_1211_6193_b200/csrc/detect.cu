@@ -40,17 +40,17 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
-constexpr int NSTAGE = 2;
+constexpr int NSTAGE = 3;
 constexpr int EPT_MAX = 16;     // records per thread kept in registers (cap <= 4096)
-constexpr uint32_t HS = 1024;   // (byte, line) dedup set entries
-constexpr uint32_t TBN = 512;   // staged triples before a global flush
+constexpr uint32_t HS = 512;    // (byte, line) dedup set entries
+constexpr uint32_t TBN = 256;   // staged triples before a global flush
 constexpr uint32_t LTN = 32;    // line-first local table entries
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t INV = 0xFFFFFFFFu;
 constexpr uint32_t ST_OVERFLOW = MCKG_ST_OVERFLOW, ST_RANGE = MCKG_ST_RANGE,
                    ST_ORDER = MCKG_ST_ORDER, ST_DUP = MCKG_ST_DUP;
 // misc[] slots
-constexpr int M_TBN = 0, M_CLN = 1, M_BASE_LO = 3, M_BASE_HI = 4, M_FLAGS = 5;
+constexpr int M_TBN = 0, M_CLN = 1, M_NSEG = 2, M_BASE_LO = 3, M_BASE_HI = 4, M_FLAGS = 5;
 
 struct Params {
   const mckg_access* ev;
@@ -61,33 +61,37 @@ struct Params {
   unsigned long long* n_tri;
   unsigned long long* line_first;
   uint32_t* status;
+  uint32_t debug;  // experiments only: bit0 skip exact pass, bit1 skip filter
 };
 
 extern __shared__ __align__(128) uint8_t smem_raw[];
+// fixed-size per-CTA state (static shared memory: compile-time addresses)
+__shared__ unsigned long long s_hset[HS];
+__shared__ unsigned long long s_lt_ts[LTN];
+__shared__ mckg_race_triple s_tbuf[TBN];
+__shared__ uint32_t s_lt_line[LTN];
+__shared__ uint32_t s_misc[16];
+__shared__ uint32_t s_info[2][4];  // per cl buffer: n, b, m
+__shared__ uint64_t s_full_cl[2], s_free_cl[2];
+__shared__ uint64_t s_mbar[NSTAGE];
 
-// Byte offsets into the dynamic shared memory (32-bit, so every access is a
-// plain LDS/STS with a register offset).
+// Byte offsets of the size-dependent state in the dynamic shared memory.
 struct Lay {
-  uint32_t stage, tag, multi, anyw, hset, lt_ts, tbuf, lt_line, bitmap, cl, mbar, misc, end;
+  uint32_t tag, multi, anyw, bitmap, cl, seg, stage, end;
 };
 
 __host__ __device__ inline Lay layout(uint32_t cap, uint32_t wpad) {
   Lay L;
   uint32_t p = 0;
-  L.stage = p;   p += NSTAGE * cap * 16;
   L.tag = p;     p += wpad * 4;
   L.multi = p;   p += wpad * 4;
   L.anyw = p;    p += wpad * 4;
-  L.hset = p;    p += HS * 8;
-  L.lt_ts = p;   p += LTN * 8;
-  L.tbuf = p;    p += TBN * 12;
-  L.lt_line = p; p += LTN * 4;
   L.bitmap = p;  p += (cap / 32 + 1) * 4;
-  L.cl = p;      p += cap * 2;
-  p = (p + 7u) & ~7u;
-  L.mbar = p;    p += NSTAGE * 8;
-  L.misc = p;    p += 8 * 4;
-  L.end = (p + 127u) & ~127u;
+  L.cl = p;      p += 2 * cap * 2;
+  L.seg = p;     p += (cap + 2) * 2;
+  p = (p + 127u) & ~127u;
+  L.stage = p;   p += NSTAGE * cap * 16;
+  L.end = p;
   return L;
 }
 
@@ -105,7 +109,7 @@ __device__ __forceinline__ bool valid_ev(uint32_t w0, int32_t line, uint32_t shm
 
 // 1 = inserted, 0 = already present, 2 = probe limit (caller flags ST_DUP)
 __device__ int hset_insert(const Lay& L, unsigned long long key, unsigned long long bstamp) {
-  unsigned long long* hs = sp<unsigned long long>(L.hset);
+  unsigned long long* hs = s_hset;
   uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) & (HS - 1);
   for (uint32_t probe = 0; probe < 64; ++probe) {
     unsigned long long cur = hs[h];
@@ -121,8 +125,8 @@ __device__ int hset_insert(const Lay& L, unsigned long long key, unsigned long l
 }
 
 __device__ void line_note(const Lay& L, const Params& P, int32_t line, unsigned long long ts) {
-  uint32_t* lt_line = sp<uint32_t>(L.lt_line);
-  unsigned long long* lt_ts = sp<unsigned long long>(L.lt_ts);
+  uint32_t* lt_line = s_lt_line;
+  unsigned long long* lt_ts = s_lt_ts;
   uint32_t l = (uint32_t)line;
   uint32_t h = l & (LTN - 1);
   for (uint32_t probe = 0; probe < LTN; ++probe) {
@@ -140,318 +144,443 @@ __device__ void line_note(const Lay& L, const Params& P, int32_t line, unsigned 
   atomicMin(P.line_first + l, ts);
 }
 
-// Flushes the staged triples (uniform call, all threads).
-__device__ void flush_tbuf(const Lay& L, const Params& P) {
-  uint32_t* misc = sp<uint32_t>(L.misc);
-  mckg_race_triple* tbuf = sp<mckg_race_triple>(L.tbuf);
-  __syncthreads();
-  uint32_t n = misc[M_TBN] < TBN ? misc[M_TBN] : TBN;
-  if (n == 0) return;
-  if (threadIdx.x == 0) {
-    unsigned long long base = atomicAdd(P.n_tri, (unsigned long long)n);
-    misc[M_BASE_LO] = (uint32_t)base;
-    misc[M_BASE_HI] = (uint32_t)(base >> 32);
-  }
-  __syncthreads();
-  unsigned long long base = ((unsigned long long)misc[M_BASE_HI] << 32) | misc[M_BASE_LO];
-  for (uint32_t i = threadIdx.x; i < n; i += NT) {
-    if (base + i < P.capacity)
-      P.tri[base + i] = tbuf[i];
-    else
-      atomicOr(misc + M_FLAGS, ST_OVERFLOW);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) misc[M_TBN] = 0;
+
+
+// ---- 32-bit shared-window accessors (plain LDS/STS, predicated stores) ----
+__device__ __forceinline__ uint32_t lds(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n}" ::"r"(a),
+      "r"(v), "r"((uint32_t)p)
+      : "memory");
 }
 
-// Next epoch start at index >= p (bit set in the bitmap), or n.  Uniform.
-__device__ uint32_t next_start(const uint32_t* bitmap, uint32_t p, uint32_t n) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t nwords = (n + 31u) / 32u;
-  for (uint32_t base = p >> 5; base < nwords; base += 32) {
-    uint32_t wi = base + lane;
-    uint32_t word = wi < nwords ? bitmap[wi] : 0u;
-    if (wi == (p >> 5)) word &= ~0u << (p & 31u);
-    uint32_t m = __ballot_sync(0xFFFFFFFFu, word != 0);
-    if (m) {
-      uint32_t f = __ffs(m) - 1u;
-      uint32_t wf = __shfl_sync(0xFFFFFFFFu, word, f);
-      uint32_t idx = (base + f) * 32u + (__ffs(wf) - 1u);
-      return idx < n ? idx : n;
-    }
-  }
-  return n;
-}
+// Barrier among the NT filter threads only (the exact warp runs decoupled).
+__device__ __forceinline__ void fsync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 
 // Rare path: the 2nd/3rd word of an access spanning several 4-byte words.
-__device__ __noinline__ bool extra_words(const Lay L, uint32_t w0, uint32_t tid, int phase,
-                                         uint32_t st16) {
-  uint32_t* tag = sp<uint32_t>(L.tag);
-  uint32_t* multi = sp<uint32_t>(L.multi);
-  uint32_t* anyw = sp<uint32_t>(L.anyw);
+__device__ __noinline__ bool extra_words(uint32_t tag_base, uint32_t d1, uint32_t d2, uint32_t w0,
+                                         uint32_t tid, int phase, uint32_t st) {
   const uint32_t off = acc_off(w0), len = acc_len(w0);
   const bool wr = acc_write(w0);
   bool cand = false;
   for (uint32_t w = (off >> 2) + 1; w <= (off + len - 1u) >> 2; ++w) {
-    const uint32_t x = sw(w);
+    const uint32_t a = tag_base + sw(w) * 4u;
     if (phase == 1) {
-      tag[x] = tid;
+      sts_if(true, a, tid);
     } else if (phase == 2) {
-      if (tag[x] != tid) multi[x] = st16;
-      if (wr) anyw[x] = st16;
+      sts_if(lds(a) != tid, a + d1, st);
+      sts_if(wr, a + d2, st);
     } else {
-      cand |= multi[x] == st16 && anyw[x] == st16;
+      cand |= lds(a + d1) == st && lds(a + d2) == st;
     }
   }
   return cand;
 }
 
-// Exact pass over the block's candidate list (all warps; see header).
-__device__ void exact_block(const Lay& L, const Params& P, const uint4* src, uint32_t m,
-                            uint32_t obj, uint32_t bid, unsigned long long bstamp) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint16_t* cl = sp<uint16_t>(L.cl);
-  uint32_t* misc = sp<uint32_t>(L.misc);
-  mckg_race_triple* tbuf = sp<mckg_race_triple>(L.tbuf);
-  // lanes hold the first 32 candidates (later ones are re-read per X)
-  uint32_t yi0 = INV, yx0 = 0, yy0 = 0;
-  if (lane < m) {
-    yi0 = cl[lane];
-    const uint4 Y = src[yi0];
-    yx0 = Y.x;
-    yy0 = Y.y;
+// Epoch segment starts from the start bitmap, in order (warp 0 only).
+__device__ void build_segments(const Lay& L, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t* bitmap = sp<uint32_t>(L.bitmap);
+  uint16_t* seg = sp<uint16_t>(L.seg);
+  const uint32_t nwords = (n + 31u) / 32u;
+  uint32_t total = 0;
+  for (uint32_t base = 0; base < nwords; base += 32) {
+    uint32_t word = base + lane < nwords ? bitmap[base + lane] : 0u;
+    const uint32_t c = __popc(word);
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= (uint32_t)d) incl += v;
+    }
+    uint32_t pos = total + incl - c;
+    while (word) {
+      const uint32_t b = __ffs(word) - 1u;
+      seg[pos++] = (uint16_t)((base + lane) * 32u + b);
+      word &= word - 1u;
+    }
+    total += __shfl_sync(0xFFFFFFFFu, incl, 31);
   }
-  for (uint32_t xp = warp; xp < m; xp += NWARP) {
-    const uint32_t xi = cl[xp];
+  if (lane == 0) {
+    seg[total] = (uint16_t)n;
+    s_misc[M_NSEG] = total;
+  }
+}
+
+// Per-lane cache of first racing timestamps by line (exact warp only; lane l
+// owns one entry), flushed to the global line table on eviction / at exit.
+struct ExactState {
+  uint32_t lc_line;
+  unsigned long long lc_ts;
+  uint32_t lc_next;  // uniform: next slot to allocate
+  uint32_t tbn;      // uniform: staged triples in s_tbuf
+};
+
+__device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
+  return ((unsigned long long)__shfl_sync(0xFFFFFFFFu, (uint32_t)(v >> 32), src) << 32) |
+         __shfl_sync(0xFFFFFFFFu, (uint32_t)v, src);
+}
+
+__device__ void line_cache_put(ExactState& E, const Params& P, bool leader, uint32_t line,
+                               unsigned long long ts) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t lm = __ballot_sync(0xFFFFFFFFu, leader); lm; lm &= lm - 1u) {
+    const int src = __ffs(lm) - 1;
+    const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, src);
+    const unsigned long long T = shfl64(ts, src);
+    const uint32_t own = __ballot_sync(0xFFFFFFFFu, E.lc_line == L);
+    if (own) {
+      if (lane == (uint32_t)(__ffs(own) - 1) && T < E.lc_ts) E.lc_ts = T;
+    } else {
+      if (lane == E.lc_next) {
+        if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
+        E.lc_line = L;
+        E.lc_ts = T;
+      }
+      E.lc_next = (E.lc_next + 1u) & 31u;
+    }
+  }
+}
+
+// Flushes the staged triples (exact warp only).
+__device__ void flush_tbuf(ExactState& E, const Params& P) {
+  const uint32_t lane = threadIdx.x & 31u;
+  __syncwarp();
+  const uint32_t n = E.tbn;
+  if (n == 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(P.n_tri, (unsigned long long)n);
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  for (uint32_t i = lane; i < n; i += 32) {
+    if (base + i < P.capacity)
+      P.tri[base + i] = s_tbuf[i];
+    else
+      atomicOr(s_misc + M_FLAGS, ST_OVERFLOW);
+  }
+  __syncwarp();
+  E.tbn = 0;
+}
+
+// Appends k (warp-uniform) triples per `emit` lane: bytes b0..b0+k-1.
+__device__ void append_triples(ExactState& E, const Params& P, bool emit, uint32_t obj,
+                               uint32_t b0, uint32_t k, int32_t line) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t em = __ballot_sync(0xFFFFFFFFu, emit);
+  if (!em) return;
+  const uint32_t need = k * __popc(em);
+  if (E.tbn + need > TBN) flush_tbuf(E, P);
+  const uint32_t pre = k * __popc(em & ((1u << lane) - 1u));
+  if (emit)
+    for (uint32_t q = 0; q < k; ++q) s_tbuf[E.tbn + pre + q] = mckg_race_triple{obj, b0 + q, line};
+  __syncwarp();
+  E.tbn += need;
+}
+
+// Exact pass over a block's candidate list, run by the dedicated exact warp:
+// lane-per-X, each lane scans every candidate Y (broadcast loads).
+__device__ void exact_block(ExactState& E, const Lay& L, const Params& P, const uint4* src,
+                            const uint16_t* cl, uint32_t m, uint32_t obj, uint32_t bid,
+                            unsigned long long bstamp) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t* misc = s_misc;
+  for (uint32_t xb = 0; xb < m; xb += 32u) {
+    const uint32_t xp = xb + lane;
+    const bool act = xp < m;
+    const uint32_t xi = act ? cl[xp] : 0u;
     const uint4 X = src[xi];
-    const uint32_t xoff = acc_off(X.x), xend = xoff + acc_len(X.x);
+    const uint32_t xlen = acc_len(X.x);
+    const uint32_t xoff = acc_off(X.x), xend = xoff + xlen;
     const uint32_t xtid = acc_tid(X.y), xep = acc_epoch(X.y);
     const bool xw = acc_write(X.x);
     uint32_t bits = 0;
-    for (uint32_t base = 0; base < m; base += 32) {
-      uint32_t yi, yx, yy;
-      if (base == 0) {
-        yi = yi0; yx = yx0; yy = yy0;
-      } else {
-        yi = INV; yx = 0; yy = 0;
-        if (base + lane < m) {
-          yi = cl[base + lane];
-          const uint4 Y = src[yi];
-          yx = Y.x;
-          yy = Y.y;
-        }
-      }
-      if (yi < xi && acc_epoch(yy) == xep && acc_tid(yy) != xtid && (xw || acc_write(yx))) {
-        const uint32_t yoff = acc_off(yx), yend = yoff + acc_len(yx);
-        const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
-        if (lo < hi) bits |= ((1u << (hi - lo)) - 1u) << (lo - xoff);
-      }
+#pragma unroll 4
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t yi = cl[j];
+      const uint2 Y = *reinterpret_cast<const uint2*>(src + yi);
+      const uint32_t yoff = acc_off(Y.x), yend = yoff + acc_len(Y.x);
+      const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
+      const bool hit = yi < xi && acc_epoch(Y.y) == xep && acc_tid(Y.y) != xtid &&
+                       (xw || acc_write(Y.x)) && lo < hi;
+      if (hit) bits |= ((1u << (hi - lo)) - 1u) << (lo - xoff);
     }
-    bits = __reduce_or_sync(0xFFFFFFFFu, bits);
-    if (!bits) continue;
+    if (!act) bits = 0;
+    const bool racing = bits != 0;
+    if (!__any_sync(0xFFFFFFFFu, racing)) continue;
     const int32_t line = (int32_t)X.z;
-    // lanes q < 8 report byte xoff + q
-    bool fresh = false;
-    if (lane < 8 && ((bits >> lane) & 1u)) {
-      const uint32_t byte = xoff + lane;
-      const unsigned long long key = (bstamp << 40) |
-                                     ((unsigned long long)(byte & 0xFFFFFu) << 16) |
-                                     ((uint32_t)line & 0xFFFFu);
-      const int r = hset_insert(L, key, bstamp);
-      if (r == 2) atomicOr(misc + M_FLAGS, ST_DUP);
-      fresh = r != 0;
+    const unsigned long long ts = ts_key(X.w, bid, xtid);
+    // first racing timestamp per line: min within the warp, then the cache
+    const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
+    const uint32_t gm = __match_any_sync(0xFFFFFFFFu, racing ? (uint32_t)line : (0x80000000u | lane));
+    unsigned long long mn = ts;
+    for (uint32_t tmp = rm; tmp; tmp &= tmp - 1u) {
+      const int s = __ffs(tmp) - 1;
+      const unsigned long long v = shfl64(ts, s);
+      if ((gm >> s) & 1u) mn = v < mn ? v : mn;
     }
-    const uint32_t fm = __ballot_sync(0xFFFFFFFFu, fresh);
-    if (fm) {
-      uint32_t pos = 0;
-      if (lane == 0) pos = atomicAdd(misc + M_TBN, (uint32_t)__popc(fm));
-      pos = __shfl_sync(0xFFFFFFFFu, pos, 0) + __popc(fm & ((1u << lane) - 1u));
-      if (fresh) {
-        const mckg_race_triple tr{obj, xoff + lane, line};
-        if (pos < TBN) {
-          tbuf[pos] = tr;
-        } else {
-          unsigned long long gp = atomicAdd(P.n_tri, 1ull);
-          if (gp < P.capacity)
-            P.tri[gp] = tr;
-          else
-            atomicOr(misc + M_FLAGS, ST_OVERFLOW);
+    line_cache_put(E, P, racing && lane == (uint32_t)(__ffs(gm) - 1), (uint32_t)line, mn);
+    // reported triples, deduplicated per block
+    const bool simple = m <= 32u &&
+        __all_sync(0xFFFFFFFFu, !racing || (xlen == 4u && (xoff & 3u) == 0u && bits == 0xFu));
+    if (simple) {
+      // whole aligned words: (word, line) identifies the 4 bytes exactly
+      const uint32_t km = __match_any_sync(0xFFFFFFFFu, racing ? ((xoff >> 2) | ((uint32_t)line << 18))
+                                                                : (0xFFFFFFFFu - lane));
+      const bool lead = racing && lane == (uint32_t)(__ffs(km) - 1);
+      append_triples(E, P, lead, obj, xoff, 4u, line);
+    } else {
+      for (uint32_t q = 0; q < MCKG_MAX_LEN; ++q) {
+        bool fresh = false;
+        if ((bits >> q) & 1u) {
+          const uint32_t byte = xoff + q;
+          const unsigned long long key = (bstamp << 40) |
+                                         ((unsigned long long)(byte & 0xFFFFFu) << 16) |
+                                         ((uint32_t)line & 0xFFFFu);
+          const int r = hset_insert(L, key, bstamp);
+          if (r == 2) atomicOr(misc + M_FLAGS, ST_DUP);
+          fresh = r != 0;
         }
+        append_triples(E, P, fresh, obj, xoff + q, 1u, line);
       }
     }
-    if (lane == 0) line_note(L, P, line, ts_key(X.w, bid, xtid));
   }
 }
 
 template <int EPT>
 __device__ void process_block(const Lay& L, const Params& P, const uint4* src, uint32_t n,
-                              uint32_t obj, uint32_t bid, uint32_t& stamp,
-                              unsigned long long bstamp) {
+                              uint16_t* cl, uint32_t* clcount, uint32_t& stamp) {
   const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
   const uint32_t shm = P.shmem_bytes;
-  uint32_t* tag = sp<uint32_t>(L.tag);
-  uint32_t* multi = sp<uint32_t>(L.multi);
-  uint32_t* anyw = sp<uint32_t>(L.anyw);
+  const uint32_t tag_base = smem_u32(smem_raw) + L.tag;
+  const uint32_t d1 = L.multi - L.tag, d2 = L.anyw - L.tag;
   uint32_t* bitmap = sp<uint32_t>(L.bitmap);
-  uint16_t* cl = sp<uint16_t>(L.cl);
-  uint32_t* misc = sp<uint32_t>(L.misc);
-  // Per owned record i = k*NT + t: epoch, first word (swizzled; INV = skip),
-  // and meta = tid | write << 11 | spans-several-words << 12.
-  uint32_t ep[EPT], x0[EPT], meta[EPT];
-  uint32_t flags = 0;
+  const uint16_t* seg = sp<uint16_t>(L.seg);
+  uint32_t* misc = s_misc;
+  // Per owned record i = k*NT + t: epoch (INV = absent or invalid), shared
+  // address of its first word's tag, meta = tid | write << 11 | spans << 12.
+  uint32_t ep[EPT], xa[EPT], meta[EPT];
+  uint32_t flags = 0, mw = 0;
+  const uint32_t cur0 = acc_epoch(src[0].y);
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const uint32_t i = (uint32_t)k * NT + t;
     const bool in = i < n;
     const uint4 r = in ? src[i] : make_uint4(0, 0, 0, 0);
-    ep[k] = acc_epoch(r.y);
-    uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, ep[k], 1);
+    const uint32_t e = acc_epoch(r.y);
+    uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, e, 1);
     if (lane == 0 && in && i > 0) prev = acc_epoch(src[i - 1].y);
-    const bool start = in && (i == 0 || ep[k] != prev);
-    if (in && i > 0 && ep[k] < prev) flags |= ST_ORDER;
-    const bool ok = in && valid_ev(r.x, (int32_t)r.z, shm);
-    if (in && !ok) flags |= ST_RANGE;
+    const bool start = in && (i == 0 || e != prev);
+    if (in && i > 0 && e < prev) flags |= ST_ORDER;
     const uint32_t off = acc_off(r.x), len = acc_len(r.x);
-    x0[k] = ok ? sw(off >> 2) : INV;
-    meta[k] = acc_tid(r.y) | (acc_write(r.x) << 11) |
-              ((uint32_t)(((off & 3u) + len) > 4u) << 12);
+    const bool ok = in && (len - 1u) < MCKG_MAX_LEN && off + len <= shm &&
+                    ((uint32_t)r.z >> 16) == 0u;
+    if (in && !ok) flags |= ST_RANGE;
+    ep[k] = ok ? e : INV;
+    xa[k] = tag_base + (ok ? sw(off >> 2) * 4u : 0u);
+    const uint32_t spans = ok && ((off & 3u) + len) > 4u;
+    meta[k] = acc_tid(r.y) | (acc_write(r.x) << 11) | (spans << 12);
+    mw |= spans;
     const uint32_t bm = __ballot_sync(0xFFFFFFFFu, start);
     if (lane == 0 && (uint32_t)k * NT < n) bitmap[(uint32_t)k * NWARP + warp] = bm;
+    // P1 of the first epoch, fused with the load
+    sts_if(ep[k] == cur0, xa[k], meta[k] & 0x7FFu);
   }
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if (lane == 0 && flags) atomicOr(misc + M_FLAGS, flags);
-
-  auto p1 = [&](uint32_t cur, uint32_t st) {
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      if (ep[k] == cur && x0[k] != INV) {
-        const uint32_t tid = meta[k] & 0x7FFu;
-        tag[x0[k]] = tid;
-        if (meta[k] & 0x1000u) extra_words(L, src[k * NT + t].x, tid, 1, st);
-      }
-    }
-  };
-  uint32_t s = 0;
-  uint32_t cur = acc_epoch(src[0].y);
+  const bool wmw = __any_sync(0xFFFFFFFFu, mw);  // warp has multi-word accesses
   uint32_t st = ++stamp;
-  p1(cur, st);
-  if (t == 0) misc[M_CLN] = 0;
-  __syncthreads();
+  if (wmw) {
+    for (int k = 0; k < EPT; ++k)
+      if (ep[k] == cur0 && (meta[k] & 0x1000u))
+        extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 1, st);
+  }
+  if (t == 0) *clcount = 0;
+  fsync();
+  if (warp == 0) build_segments(L, n);
+  uint32_t cur = cur0;
+  uint32_t sidx = 0;
   while (true) {
     // P2: words seen by a second thread; written words
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
-      if (ep[k] == cur && x0[k] != INV) {
-        const uint32_t tid = meta[k] & 0x7FFu;
-        if (tag[x0[k]] != tid) multi[x0[k]] = st;
-        if (meta[k] & 0x800u) anyw[x0[k]] = st;
-        if (meta[k] & 0x1000u) extra_words(L, src[k * NT + t].x, tid, 2, st);
-      }
+      const bool a = ep[k] == cur;
+      const uint32_t tg = lds(xa[k]);
+      sts_if(a && tg != (meta[k] & 0x7FFu), xa[k] + d1, st);
+      sts_if(a && (meta[k] & 0x800u), xa[k] + d2, st);
     }
-    __syncthreads();
-    const uint32_t e = next_start(bitmap, s + 1, n);
+    if (wmw) {
+      for (int k = 0; k < EPT; ++k)
+        if (ep[k] == cur && (meta[k] & 0x1000u))
+          extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 2, st);
+    }
+    fsync();
+    const uint32_t e = seg[sidx + 1];
     // P3: candidates -> block list cl (warp-aggregated compaction)
+    uint32_t cmask = 0;  // bit k: record k is a candidate
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
-      bool cand = false;
-      if (ep[k] == cur && x0[k] != INV) {
-        cand = multi[x0[k]] == st && anyw[x0[k]] == st;
-        if (meta[k] & 0x1000u) cand |= extra_words(L, src[k * NT + t].x, meta[k] & 0x7FFu, 3, st);
-      }
-      const uint32_t bm = __ballot_sync(0xFFFFFFFFu, cand);
-      if (bm) {
-        const uint32_t leader = __ffs(bm) - 1u;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(misc + M_CLN, (uint32_t)__popc(bm));
-        base = __shfl_sync(0xFFFFFFFFu, base, leader);
-        if (cand) cl[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)((uint32_t)k * NT + t);
+      const uint32_t mv = lds(xa[k] + d1), av = lds(xa[k] + d2);
+      if (ep[k] == cur && mv == st && av == st) cmask |= 1u << k;
+    }
+    if (wmw) {
+      for (int k = 0; k < EPT; ++k)
+        if (ep[k] == cur && (meta[k] & 0x1000u) &&
+            extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 3, st))
+          cmask |= 1u << k;
+    }
+    if (__any_sync(0xFFFFFFFFu, cmask)) {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const bool cand = (cmask >> k) & 1u;
+        const uint32_t bm = __ballot_sync(0xFFFFFFFFu, cand);
+        if (bm) {
+          const uint32_t leader = __ffs(bm) - 1u;
+          uint32_t base = 0;
+          if (lane == leader) base = atomicAdd(clcount, (uint32_t)__popc(bm));
+          base = __shfl_sync(0xFFFFFFFFu, base, leader);
+          if (cand) cl[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)((uint32_t)k * NT + t);
+        }
       }
     }
     const bool more = e < n;
     if (more) {  // P1 of the next epoch shares this barrier interval
-      s = e;
-      cur = acc_epoch(src[s].y);
+      cur = acc_epoch(src[e].y);
       st = ++stamp;
-      p1(cur, st);
+      ++sidx;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) sts_if(ep[k] == cur, xa[k], meta[k] & 0x7FFu);
+      if (wmw) {
+        for (int k = 0; k < EPT; ++k)
+          if (ep[k] == cur && (meta[k] & 0x1000u))
+            extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 1, st);
+      }
     }
-    __syncthreads();
+    fsync();
     if (!more) break;
   }
-  const uint32_t m = misc[M_CLN];
-  if (m) exact_block(L, P, src, m, obj, bid, bstamp);
 }
 
+// One CTA = 8 filter warps + 1 exact warp (warp specialised).  Filter warps
+// run the epoch filter of block b+1 while the exact warp finishes block b;
+// they hand candidate lists over through two mbarrier-guarded buffers.  The
+// exact warp also owns the report state and re-issues the TMA load into the
+// stage it has just released.
+constexpr int NTHREADS = NT + 32;
+
 template <int EPT>
-__global__ void __launch_bounds__(NT, EPT <= 4 ? 3 : (EPT <= 8 ? 2 : 1))
+__global__ void __launch_bounds__(NTHREADS, EPT <= 4 ? 3 : (EPT <= 8 ? 2 : 1))
     race_detect_kernel(Params P) {
   const Lay L = layout(P.cap, P.wpad);
-  const uint32_t t = threadIdx.x;
-  unsigned long long* hset = sp<unsigned long long>(L.hset);
-  uint32_t* lt_line = sp<uint32_t>(L.lt_line);
-  unsigned long long* lt_ts = sp<unsigned long long>(L.lt_ts);
-  uint32_t* misc = sp<uint32_t>(L.misc);
-  uint64_t* mbar = sp<uint64_t>(L.mbar);
+  const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31u;
+  uint32_t* misc = s_misc;
+  uint64_t* mbar = s_mbar;
   uint4* stage = sp<uint4>(L.stage);
-  for (uint32_t i = t; i < HS; i += NT) hset[i] = 0ull;
-  for (uint32_t i = t; i < LTN; i += NT) {
-    lt_line[i] = INF;
-    lt_ts[i] = ~0ull;
+  uint16_t* clbuf = sp<uint16_t>(L.cl);  // 2 x cap
+  for (uint32_t i = t; i < HS; i += NTHREADS) s_hset[i] = 0ull;
+  for (uint32_t i = t; i < LTN; i += NTHREADS) {
+    s_lt_line[i] = INF;
+    s_lt_ts[i] = ~0ull;
   }
-  for (uint32_t i = t; i < 3 * P.wpad; i += NT) sp<uint32_t>(L.tag)[i] = 0u;
-  if (t < 8) misc[t] = 0u;
+  for (uint32_t i = t; i < 3 * P.wpad; i += NTHREADS) sp<uint32_t>(L.tag)[i] = 0u;
+  if (t < 16) misc[t] = 0u;
   if (t == 0) {
     for (int k = 0; k < NSTAGE; ++k) mbar_init(mbar + k, 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(s_full_cl + k, 1);
+      mbar_init(s_free_cl + k, 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
   const uint32_t G = gridDim.x;
-  auto fits = [&](uint32_t b) {
-    uint64_t n = P.bstart[b + 1] - P.bstart[b];
-    return n > 0 && n <= P.cap;
-  };
-  auto issue = [&](uint32_t b, int st) {
-    uint64_t s0 = P.bstart[b];
-    uint32_t bytes = (uint32_t)((P.bstart[b + 1] - s0) * 16);
+  auto nev = [&](uint32_t b) { return P.bstart[b + 1] - P.bstart[b]; };
+  auto issue = [&](uint32_t b, int st) {  // one thread
+    const uint64_t n = nev(b);
+    if (n == 0 || n > P.cap) return;
+    const uint64_t s0 = P.bstart[b];
+    const uint32_t bytes = (uint32_t)(n * 16);
     mbar_expect_tx(mbar + st, bytes);
     bulk_g2s(stage + (size_t)st * P.cap, P.ev + s0, bytes, mbar + st);
   };
-  if (t == 0) {
-    for (int k = 0; k < NSTAGE; ++k) {
-      uint32_t b = blockIdx.x + (uint32_t)k * G;
-      if (b < P.n_blocks && fits(b)) issue(b, k);
+
+  if (warp < NT / 32) {
+    // ---------------- filter warps ----------------
+    uint32_t sphase = 0, stamp = 0;
+    int it = 0;
+    for (uint32_t b = blockIdx.x; b < P.n_blocks; b += G, ++it) {
+      const int st = it % NSTAGE;
+      const int p = it & 1;
+      const uint32_t u = (uint32_t)(it >> 1);
+      mbar_wait(s_free_cl + p, (u & 1u) ^ 1u);  // exact warp done with this buffer
+      const uint64_t n_all = nev(b);
+      const uint32_t n = n_all <= P.cap ? (uint32_t)n_all : 0u;
+      uint32_t* clcount = misc + 8 + p;
+      if (n > 0 && (P.debug & 2u)) {
+        mbar_wait(mbar + st, (sphase >> st) & 1u);
+        sphase ^= 1u << st;
+        if (t == 0) *clcount = 0;
+        fsync();
+      } else if (n > 0) {
+        mbar_wait(mbar + st, (sphase >> st) & 1u);
+        sphase ^= 1u << st;
+        process_block<EPT>(L, P, stage + (size_t)st * P.cap, n, clbuf + (size_t)p * P.cap,
+                           clcount, stamp);
+      } else {
+        if (t == 0) {
+          *clcount = 0;
+          if (n_all > 0) atomicOr(misc + M_FLAGS, ST_RANGE);  // exceeds the staging capacity
+        }
+        fsync();
+      }
+      if (t == 0) {
+        s_info[p][0] = n;
+        s_info[p][1] = b;
+        s_info[p][2] = *clcount;
+        mbar_arrive(s_full_cl + p);
+      }
     }
+  } else {
+    // ---------------- exact / report warp ----------------
+    if (lane == 0)
+      for (int k = 0; k < NSTAGE; ++k) {
+        const uint32_t b = blockIdx.x + (uint32_t)k * G;
+        if (b < P.n_blocks) issue(b, k);
+      }
+    unsigned long long bstamp = 0;
+    ExactState E{INF, ~0ull, 0u, 0u};
+    int it = 0;
+    for (uint32_t b = blockIdx.x; b < P.n_blocks; b += G, ++it) {
+      const int st = it % NSTAGE;
+      const int p = it & 1;
+      const uint32_t u = (uint32_t)(it >> 1);
+      mbar_wait(s_full_cl + p, u & 1u);
+      const uint32_t n = s_info[p][0], m = s_info[p][2];
+      ++bstamp;
+      if (n > 0 && m > 0 && !(P.debug & 1u))
+        exact_block(E, L, P, stage + (size_t)st * P.cap, clbuf + (size_t)p * P.cap, m,
+                    P.obj_base + b, P.bid_base + b, bstamp);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(s_free_cl + p);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t nb = b + (uint32_t)NSTAGE * G;
+        if (nb < P.n_blocks) issue(nb, st);
+      }
+    }
+    flush_tbuf(E, P);
+    if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
   }
-  uint32_t phase = 0;
-  uint32_t stamp = 0;
-  unsigned long long bstamp = 0;
-  int it = 0;
-  for (uint32_t b = blockIdx.x; b < P.n_blocks; b += G, ++it) {
-    const int st = it % NSTAGE;
-    const uint64_t n_all = P.bstart[b + 1] - P.bstart[b];
-    const uint32_t n = n_all <= P.cap ? (uint32_t)n_all : 0u;
-    ++bstamp;
-    if (n > 0) {
-      mbar_wait(mbar + st, (phase >> st) & 1u);
-      phase ^= 1u << st;
-      process_block<EPT>(L, P, stage + (size_t)st * P.cap, n, P.obj_base + b, P.bid_base + b,
-                         stamp, bstamp);
-    } else if (n_all > 0 && t == 0) {
-      atomicOr(misc + M_FLAGS, ST_RANGE);  // block larger than the staging capacity
-    }
-    __syncthreads();  // stage `st` fully consumed (including the exact pass)
-    if (t == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const uint32_t nb = b + (uint32_t)NSTAGE * G;
-      if (nb < P.n_blocks && fits(nb)) issue(nb, st);
-    }
-    if (misc[M_TBN] >= TBN / 2) flush_tbuf(L, P);
-  }
-  flush_tbuf(L, P);
   __syncthreads();
-  for (uint32_t i = t; i < LTN; i += NT)
-    if (lt_line[i] != INF) atomicMin(P.line_first + lt_line[i], lt_ts[i]);
   if (t == 0 && misc[M_FLAGS]) atomicOr(P.status, misc[M_FLAGS]);
+  if (t == 0 && (P.debug & 12u)) {
+    atomicAdd(P.status + 1, misc[12]);
+    atomicAdd(P.status + 2, misc[13]);
+  }
 }
 
 __global__ void reset_kernel(unsigned long long* n_tri, unsigned long long* line_first,
@@ -546,7 +675,7 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     configured[ki] = smem;
   }
   int per_sm = 0;
-  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
+  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, smem));
   if (per_sm < 1) per_sm = 1;
   uint32_t grid = (uint32_t)sm_count() * (uint32_t)per_sm;
   if (grid > tr->n_blocks) grid = tr->n_blocks;
@@ -564,9 +693,13 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.n_tri = out->n_triples;
   P.line_first = out->line_first;
   P.status = out->status;
-  kern<<<grid, NT, smem, (cudaStream_t)stream>>>(P);
+  {
+    const char* dbg = getenv("MCKG_DEBUG");
+    P.debug = dbg ? (uint32_t)atoi(dbg) : 0u;
+  }
+  kern<<<grid, NTHREADS, smem, (cudaStream_t)stream>>>(P);
   MCKG_CUDA_TRY(cudaGetLastError());
-  note_launch(1, grid, NT, (uint32_t)smem);
+  note_launch(1, grid, NTHREADS, (uint32_t)smem);
   return MCKG_OK;
 }
 
