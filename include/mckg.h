@@ -24,6 +24,13 @@
  *                           finished-or-absent thread sets at quiescence.
  *   mckg_gen_c3             synthetic workload generator (BASELINE config 3);
  *                           not a reference interface.
+ *   mck_run_source          mck::runFile / Machine::run end to end
+ *                           (include/minicudak/driver.hpp:25-36,
+ *                           machine.hpp:359-375): compile a CUDA-C program,
+ *                           interpret the host thread, run every grid on the
+ *                           B200 (K1 + fused race detector + K4), return the
+ *                           RunResult as JSON.
+ *   mck_disassemble         the step-exact IR of a program (debugging aid).
  *
  * Device pointers are CUDA device pointers on the current device; `stream` is
  * a cudaStream_t (NULL = legacy default stream).  All launches are
@@ -213,6 +220,24 @@ int mckg_scan_stuck(const uint32_t* arrivals, uint32_t n_blocks, uint32_t block_
  */
 int mckg_gen_c3(mckg_access* events, uint64_t* block_start, uint32_t blk0, uint32_t n_blocks,
                 uint64_t seed, void* stream);
+
+/* ---- whole-program checking (host + B200 grid engine) ---- */
+typedef struct mck_run_opts {
+  uint64_t step_limit;        /* 0 = reference default 50,000,000 (machine.hpp:313) */
+  uint64_t seed;              /* RunOptions::seed                                     */
+  int32_t race_check;         /* RunOptions::raceCheck                                 */
+  int32_t round_robin;        /* 1 = SchedulePolicy::RoundRobin (the engine's schedule) */
+  int32_t device;             /* CUDA device ordinal                                    */
+  int32_t max_threads_per_block; /* ArchParams::maxThreadsPerBlock, 0 = 1024           */
+} mck_run_opts;
+
+/* JSON keys: exit, output, steps, stuck, main_return, diags[{cat,sev,msg,line}],
+ * stuck_reports[{kind,gid,bid,waiting,missing,reason}], report_text,
+ * reported[[obj,byte,line]], stats{...}, engine_error; or frontend_error.
+ * *json is malloc'ed: release with mck_free. */
+int mck_run_source(const char* src, const char* filename, const mck_run_opts* opts, char** json);
+int mck_disassemble(const char* src, const char* filename, char** text);
+void mck_free(char* p);
 
 #define MCKG_C3_THREADS 256u
 #define MCKG_C3_EPOCHS 2u

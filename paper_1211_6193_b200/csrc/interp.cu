@@ -1,0 +1,1638 @@
+// interp.cu -- K1: the sm_100a thread-stepping interpreter of a simulated
+// CUDA grid, with the shared-memory race detector (K2 contract) and the
+// barrier-deadlock classification (K4) fused in.
+//
+// Mapping: one CTA = one simulated block, one GPU thread = one simulated
+// thread (threadIdx.x == tid).  The CTA runs the block in lockstep SWEEPS:
+// in sweep s every runnable thread executes exactly one IR instruction (one
+// small step of Machine::execThreadStep, /root/reference/proj/src/machine.cpp:
+// 493-1178), in the round-robin order of the reference (tid order inside a
+// sweep, machine.cpp:411-429).  Barrier rules are not simulated one by one:
+// SURVEY Appendix A gives their round-robin timing in closed form -- the
+// episode completes in the sweep T of the last arrival (up-sweep chain +
+// Turnaround, which clears the epoch, device.cpp:143-200), thread t >= 1 is
+// released in sweep T + (L - t) and thread 0 in T + L (L = blockDim - 1), so
+// thread t steps again from sweep T + L - t + 1 (t >= 1) / T + L + 1 (t = 0).
+//
+// Memory order inside a sweep.  Each step performs at most one memory access.
+// Accesses to private objects (a thread's locals/params, virtual ids) never
+// interact.  Shared/global accesses of one sweep are checked for word-level
+// overlap with a write (a CTA-wide hash); without overlap they run in
+// parallel, otherwise the memory phase is replayed in tid order (a warp at a
+// time, lane by lane), which is exactly the reference's sequential order.
+// Cross-block ordering of global accesses inside one sweep is NOT reproduced
+// (blocks run independently); it only matters for programs with cross-block
+// global races, the extension of SURVEY Appendix E.
+//
+// Race detection (racecheck.cpp:9-73) is online: a 32-bit shadow word per
+// shared byte holds {one accessor tid, multi flag, one writer tid, multi
+// flag, epoch stamp}; X races iff (X writes and some OTHER thread accessed
+// the byte in this epoch) or (X reads and some other thread wrote it).
+// Triples (obj, byte, line) are deduplicated per block and appended; the
+// first racing timestamp per line is atomicMin'ed into a line table.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "../host/engine.hpp"
+#include "core.cuh"
+
+namespace mckb {
+namespace k1 {
+
+using namespace mck_core;
+
+// ---- per-thread capacity (local memory) ----
+constexpr int VS = 48;       // value stack entries
+constexpr int SCOPES = 32;
+constexpr int OWNED = 48;
+constexpr int FRAMES = 16;
+constexpr int BINDS = 96;
+constexpr int POBJ = 48;
+constexpr int PB = 768;      // private bytes (locals and params of all frames)
+
+constexpr uint32_t PRIV = 0x80000000u;
+constexpr uint32_t NONE_TID = 0x7FFu;
+constexpr int LINES = 65536;
+constexpr int RACE_SET = 1024;  // per-block (byte, line) dedup entries
+
+enum : int { ERR_NONE = 0, ERR_STACK, ERR_PRIV, ERR_SHARED_PTR_ESCAPE, ERR_DIAG_FULL, ERR_TRIPLES_FULL,
+             ERR_LINE, ERR_SWEEPS, ERR_OPCODE };
+
+struct PObj {
+  uint16_t off, size, gen;
+  uint8_t live, pad;
+  int32_t name;
+};
+
+struct Frame {
+  int32_t retPc, bindBase, fn;
+  uint8_t scopeDepth, valueDepth, pad0, pad1;
+};
+
+struct TS {
+  int pc;
+  int nv, nscope, nowned, nframe, npobj, ptop;
+  uint32_t steps, allocs;
+  Val vals[VS];
+  uint8_t scopeMark[SCOPES];
+  uint8_t owned[OWNED];
+  Frame frames[FRAMES];
+  uint32_t binds[BINDS];
+  PObj pobj[POBJ];
+  uint8_t pbytes[PB];
+  uint8_t pmeta[PB];
+};
+
+struct DevDiagRec {
+  unsigned long long hkey;  // tuple hash (0 = empty)
+  unsigned long long ts;    // min timestamp key
+  int32_t code, line, name, pad;
+  long long p[4];
+};
+
+struct BlockOut {
+  unsigned long long steps;
+  unsigned long long rules;
+  unsigned long long allocs;
+  unsigned long long sharedEvents;
+  uint32_t lastSweep;
+  uint32_t deadlocked;
+};
+
+struct KP {
+  const mck_ins* code;
+  const mck_fn* fns;
+  const mck_local* locals;
+  int kernel;
+  int nargs;
+  const Val* args;
+  uint32_t gid, sharedBase, nextId;
+  int64_t gridDim, blockDim, shmem;
+  int sharedName;
+  int64_t warpSize;
+  const uint32_t* objIds;     // sorted
+  const DevObjInfo* objs;
+  int nobjs;
+  const uint32_t* globalIds;
+  const uint32_t* shRanges;   // (first, count, gid) triples
+  int nranges;
+  uint8_t* gbytes;
+  uint8_t* gmeta;
+  int raceCheck;
+  int htBits;                 // conflict hash size = 1 << htBits
+  uint32_t maxSweeps;         // < 2^26; each sweep takes >= 1 step (step limit)
+  // outputs
+  unsigned long long* lineFirst;
+  long long* triples;         // (obj, byte, line)
+  unsigned long long tripleCap;
+  unsigned long long* nTriples;
+  DevDiagRec* diags;
+  uint32_t diagMask;          // table size - 1
+  BlockOut* blocks;
+  uint32_t* waitMask;         // gridDim x words
+  int* error;
+  int* errorInfo;
+};
+
+// ---------------- shared-memory layout ----------------
+struct SmemLay {
+  uint32_t bytes, meta, shadow, htKey, htVal, raceSet, end;
+};
+__host__ __device__ inline SmemLay smemLayout(int64_t shmem, int raceCheck, int htBits) {
+  SmemLay L;
+  uint32_t S = (uint32_t)((shmem + 15) & ~15ll);
+  uint32_t p = 0;
+  L.bytes = p; p += S;
+  L.meta = p; p += S;
+  L.shadow = p; p += raceCheck ? 4 * S : 0;
+  p = (p + 15) & ~15u;
+  L.htKey = p; p += 8u << htBits;
+  L.htVal = p; p += 4u << htBits;
+  L.raceSet = p; p += raceCheck ? 8 * RACE_SET : 0;
+  L.end = p;
+  return L;
+}
+
+extern __shared__ __align__(16) uint8_t smem[];
+
+struct BlockShared {
+  int wait[2];      // threads waiting in the open episode (by parity)
+  int nz[2];        // nonzero __syncthreads_* operands (by parity)
+  int allc[2];      // (operand != 0 || plain) (by parity)
+  int fin;          // finished threads
+  int conflict;
+  unsigned long long steps;
+  unsigned long long allocs;
+  unsigned long long sharedEvents;
+  uint32_t lastSweep;
+};
+
+__device__ __forceinline__ void set_error(const KP& P, int code, int info) {
+  if (atomicCAS(P.error, 0, code) == 0) *P.errorInfo = info;
+}
+
+// ---------------- diagnostics ----------------
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return x;
+}
+
+__device__ __forceinline__ unsigned long long tskey(uint32_t sweep, uint32_t bid, uint32_t tid, uint32_t sub) {
+  return ((unsigned long long)sweep << 38) | ((unsigned long long)(bid & 0x3FFFFFFu) << 12) |
+         ((unsigned long long)(tid & 1023u) << 2) | (sub & 3u);
+}
+
+struct Ctx {  // per-thread context of the current step
+  uint32_t sweep, bid, tid, sub;
+};
+
+__device__ void emit_diag(const KP& P, Ctx& c, int code, int line, long long p0 = 0, long long p1 = 0,
+                          long long p2 = 0, long long p3 = 0, int name = -1) {
+  unsigned long long ts = tskey(c.sweep, c.bid, c.tid, c.sub);
+  c.sub = c.sub < 3 ? c.sub + 1 : 3;
+  unsigned long long h = mix64((unsigned long long)code * 0x9E3779B97F4A7C15ull ^ (unsigned long long)line);
+  h = mix64(h ^ (unsigned long long)p0);
+  h = mix64(h ^ (unsigned long long)p1);
+  h = mix64(h ^ (unsigned long long)p2);
+  h = mix64(h ^ (unsigned long long)p3);
+  h = mix64(h ^ (unsigned long long)(unsigned)name);
+  if (code == MCK_D_MEMBOUNDARY) h = mix64(h ^ (((unsigned long long)c.bid << 16) | c.tid));
+  if (h == 0) h = 1;
+  uint32_t slot = (uint32_t)h & P.diagMask;
+  for (uint32_t probe = 0; probe <= P.diagMask; ++probe) {
+    DevDiagRec* r = P.diags + slot;
+    unsigned long long old = atomicCAS(&r->hkey, 0ull, h);
+    if (old == 0ull) {
+      r->code = code;
+      r->line = line;
+      r->name = name;
+      r->p[0] = p0;
+      r->p[1] = p1;
+      r->p[2] = p2;
+      r->p[3] = p3;
+      atomicMin(&r->ts, ts);
+      return;
+    }
+    if (old == h) {
+      atomicMin(&r->ts, ts);
+      return;
+    }
+    slot = (slot + 1) & P.diagMask;
+  }
+  set_error(P, ERR_DIAG_FULL, 0);
+}
+
+__device__ __forceinline__ void emit_ops(const KP& P, Ctx& c, const Diags& d, int line) {
+  for (int i = 0; i < d.n; ++i) emit_diag(P, c, d.code[i], line);
+}
+
+// ---------------- private objects ----------------
+__device__ __forceinline__ uint32_t priv_id(int idx, uint16_t gen) {
+  return PRIV | ((uint32_t)(gen & 0x7FF) << 20) | (uint32_t)idx;
+}
+
+__device__ bool priv_alloc(TS& t, const KP& P, int size, int name, uint32_t& id) {
+  if (t.npobj >= POBJ || t.ptop + size > PB || size < 0 || t.nowned >= OWNED) {
+    set_error(P, ERR_PRIV, size);
+    return false;
+  }
+  int idx = t.npobj++;
+  PObj& o = t.pobj[idx];
+  o.gen = (uint16_t)(o.gen + 1);
+  o.off = (uint16_t)t.ptop;
+  o.size = (uint16_t)size;
+  o.live = 1;
+  o.name = name;
+  for (int i = 0; i < size; ++i) t.pmeta[t.ptop + i] = 0;
+  t.ptop += size;
+  t.owned[t.nowned++] = (uint8_t)idx;
+  ++t.allocs;
+  id = priv_id(idx, o.gen);
+  return true;
+}
+
+// scopes die LIFO: release private storage back to the first owned object
+__device__ void pop_scopes(TS& t, int depth) {
+  while (t.nscope > depth) {
+    int m = t.scopeMark[--t.nscope];
+    for (int i = m; i < t.nowned; ++i) t.pobj[t.owned[i]].live = 0;
+    if (m < t.nowned) {
+      int first = t.owned[m];
+      t.ptop = t.pobj[first].off;
+      t.npobj = first;
+    }
+    t.nowned = m;
+  }
+}
+
+// private scalar poke (memory.cpp:184-206)
+__device__ void priv_poke(TS& t, const PObj& o, int64_t off, uint8_t ty, const Val& v) {
+  int len = (int)t_scalar(ty);
+  int base = o.off;
+  for (int64_t s = off - 7 < 0 ? 0 : off - 7; s < off + len && s < o.size; ++s)
+    if (s + 8 > off) t.pmeta[base + s] &= (uint8_t)~META_PTR;
+  uint64_t raw = encode_scalar(v, ty);
+  for (int i = 0; i < len; ++i) {
+    t.pbytes[base + off + i] = (uint8_t)(raw >> (8 * i));
+    t.pmeta[base + off + i] |= META_DEF;
+  }
+  if (v.kind == MCK_K_PTR && v.obj != 0) t.pmeta[base + off] |= META_PTR;
+}
+
+// ---------------- object resolution ----------------
+enum : int { R_OK_PRIV, R_OK_SHARED, R_OK_GLOBAL, R_NULL, R_BOUNDARY, R_DEAD, R_OOB };
+
+struct Res {
+  int kind;
+  int space;       // for R_BOUNDARY: 0 host, 2 shared
+  long long target;
+  int name;
+  int64_t size;
+  uint64_t base;   // byte offset (shared: in smem block; global: in arena; private: pbytes)
+};
+
+__device__ Res resolve(TS& t, const KP& P, uint32_t bid, uint32_t obj, int64_t off, int len) {
+  Res r;
+  r.name = -1;
+  r.size = 0;
+  r.base = 0;
+  r.space = 0;
+  r.target = 0;
+  if (obj == 0) {
+    r.kind = R_NULL;
+    return r;
+  }
+  if (obj & PRIV) {
+    int idx = (int)(obj & 0xFFFFF);
+    uint16_t gen = (uint16_t)((obj >> 20) & 0x7FF);
+    if (idx >= POBJ) {
+      r.kind = R_NULL;
+      return r;
+    }
+    const PObj& o = t.pobj[idx];
+    r.name = o.name;
+    r.size = o.size;
+    r.base = o.off;
+    if (idx >= t.npobj || !o.live || (o.gen & 0x7FF) != gen) {
+      r.kind = R_DEAD;
+      return r;
+    }
+    r.kind = (off < 0 || off + len > o.size) ? R_OOB : R_OK_PRIV;
+    return r;
+  }
+  if (obj >= P.sharedBase && (int64_t)(obj - P.sharedBase) < P.gridDim) {
+    uint32_t b = obj - P.sharedBase;
+    if (b != bid) {
+      r.kind = R_BOUNDARY;
+      r.space = 2;
+      r.target = ((long long)P.gid << 32) | b;
+      return r;
+    }
+    r.name = P.sharedName;
+    r.size = P.shmem;
+    r.kind = (off < 0 || off + len > P.shmem) ? R_OOB : R_OK_SHARED;
+    return r;
+  }
+  // device-global table (ascending ids)
+  int lo = 0, hi = P.nobjs;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (P.objIds[mid] < obj) lo = mid + 1; else hi = mid;
+  }
+  if (lo < P.nobjs && P.objIds[lo] == obj) {
+    const DevObjInfo& o = P.objs[lo];
+    r.name = o.name;
+    r.size = o.size;
+    r.base = o.base;
+    if (!o.live) {
+      r.kind = R_DEAD;
+      return r;
+    }
+    r.kind = (off < 0 || off + len > o.size) ? R_OOB : R_OK_GLOBAL;
+    return r;
+  }
+  for (int i = 0; i < P.nranges; ++i) {
+    uint32_t f = P.shRanges[3 * i], n = P.shRanges[3 * i + 1];
+    if (obj >= f && obj - f < n) {
+      r.kind = R_BOUNDARY;
+      r.space = 2;
+      r.target = ((long long)P.shRanges[3 * i + 2] << 32) | (obj - f);
+      return r;
+    }
+  }
+  if (obj < P.sharedBase) {  // a host object
+    r.kind = R_BOUNDARY;
+    r.space = 0;
+    return r;
+  }
+  r.kind = R_NULL;
+  return r;
+}
+
+// ---------------- raw memory (shared / global) ----------------
+__device__ __forceinline__ uint64_t load_raw(const uint8_t* b, int len, bool& undef, const uint8_t* m,
+                                             bool& ptrStart) {
+  uint64_t raw = 0;
+  undef = false;
+  for (int i = 0; i < len; ++i) {
+    raw |= (uint64_t)b[i] << (8 * i);
+    if (!(m[i] & META_DEF)) undef = true;
+  }
+  ptrStart = (m[0] & META_PTR) != 0;
+  return raw;
+}
+
+// meta update with word atomics (neighbouring bytes may be written by other
+// threads in the same sweep)
+__device__ __forceinline__ void meta_and(uint8_t* m, int64_t i, uint8_t mask) {
+  uintptr_t a = (uintptr_t)(m + i);
+  uint32_t* w = (uint32_t*)(a & ~(uintptr_t)3);
+  uint32_t sh = (uint32_t)(a & 3) * 8;
+  atomicAnd(w, ~((uint32_t)(uint8_t)~mask << sh));
+}
+__device__ __forceinline__ void meta_or(uint8_t* m, int64_t i, uint8_t bits) {
+  uintptr_t a = (uintptr_t)(m + i);
+  uint32_t* w = (uint32_t*)(a & ~(uintptr_t)3);
+  uint32_t sh = (uint32_t)(a & 3) * 8;
+  atomicOr(w, (uint32_t)bits << sh);
+}
+
+__device__ void store_raw(uint8_t* b, uint8_t* m, int64_t objSize, int64_t off, int len, uint64_t raw,
+                          bool ptr) {
+  // erase pointer slots overlapping [off, off + len) (memory.cpp:89-97)
+  for (int64_t s = off - 7 < 0 ? 0 : off - 7; s < off + len && s < objSize; ++s)
+    if (s + 8 > off && (m[s] & META_PTR)) meta_and(m, s, (uint8_t)~META_PTR);
+  for (int i = 0; i < len; ++i) b[off + i] = (uint8_t)(raw >> (8 * i));
+  for (int i = 0; i < len; ++i)
+    if ((m[off + i] & META_DEF) == 0) meta_or(m, off + i, META_DEF);
+  if (ptr) meta_or(m, off, META_PTR);
+}
+
+// ---------------- race shadow (shared memory) ----------------
+__device__ __forceinline__ uint32_t shadow_empty(uint32_t stamp) {
+  return NONE_TID | (NONE_TID << 12) | (stamp << 24);
+}
+__device__ __forceinline__ bool other_than(uint32_t tidf, uint32_t multi, uint32_t x) {
+  return (tidf != NONE_TID && tidf != x) || multi;
+}
+
+struct RaceOut {
+  uint32_t bytes;  // bit q: byte off+q raced
+};
+
+// Records one access in the shadow; returns the raced byte mask.
+__device__ uint32_t shadow_access(uint32_t* sh, int64_t off, int len, uint32_t x, bool w, uint32_t stamp) {
+  uint32_t raced = 0;
+  for (int q = 0; q < len; ++q) {
+    uint32_t* p = sh + off + q;
+    uint32_t cur = *p;
+    while (true) {
+      uint32_t s = (cur >> 24) == stamp ? cur : shadow_empty(stamp);
+      uint32_t at = s & 0x7FF, am = (s >> 11) & 1, wt = (s >> 12) & 0x7FF, wm = (s >> 23) & 1;
+      bool r = w ? other_than(at, am, x) : other_than(wt, wm, x);
+      uint32_t nat = at, nam = am, nwt = wt, nwm = wm;
+      if (nat == NONE_TID) nat = x; else if (nat != x) nam = 1;
+      if (w) {
+        if (nwt == NONE_TID) nwt = x; else if (nwt != x) nwm = 1;
+      }
+      uint32_t ns = nat | (nam << 11) | (nwt << 12) | (nwm << 23) | (stamp << 24);
+      if (ns == cur) {
+        if (r) raced |= 1u << q;
+        break;
+      }
+      uint32_t old = atomicCAS(p, cur, ns);
+      if (old == cur) {
+        if (r) raced |= 1u << q;
+        break;
+      }
+      cur = old;
+    }
+  }
+  return raced;
+}
+
+__device__ void report_race(const KP& P, Ctx& c, unsigned long long* set, uint32_t obj, int64_t off,
+                            uint32_t raced, int line, uint32_t bstamp) {
+  if (!raced) return;
+  if (line < 0 || line >= LINES) {
+    set_error(P, ERR_LINE, line);
+    return;
+  }
+  unsigned long long ts = tskey(c.sweep, c.bid, c.tid, c.sub);
+  atomicMin(P.lineFirst + line, ts);
+  for (int q = 0; q < 8; ++q) {
+    if (!((raced >> q) & 1u)) continue;
+    unsigned long long key = ((unsigned long long)(bstamp & 0xFFFF) << 48) |
+                             ((unsigned long long)((off + q) & 0xFFFFFFFF) << 16) | (uint32_t)line;
+    key |= 1ull << 63;
+    uint32_t h = (uint32_t)(mix64(key) & (RACE_SET - 1));
+    bool fresh = true;
+    for (int probe = 0; probe < RACE_SET; ++probe) {
+      unsigned long long curk = set[h];
+      if (curk == key) {
+        fresh = false;
+        break;
+      }
+      if (curk == 0) {
+        unsigned long long old = atomicCAS(set + h, 0ull, key);
+        if (old == 0ull) break;
+        if (old == key) {
+          fresh = false;
+          break;
+        }
+      }
+      h = (h + 1) & (RACE_SET - 1);
+    }
+    // (a full set appends duplicates; the host dedups the triples)
+    if (fresh) {
+      unsigned long long i = atomicAdd(P.nTriples, 1ull);
+      if (i < P.tripleCap) {
+        P.triples[3 * i] = obj;
+        P.triples[3 * i + 1] = off + q;
+        P.triples[3 * i + 2] = line;
+      } else {
+        set_error(P, ERR_TRIPLES_FULL, 0);
+      }
+    }
+  }
+  c.sub = c.sub < 3 ? c.sub + 1 : 3;
+}
+
+// ---------------- the memory request of one step ----------------
+struct Req {
+  int kind;     // 0 none, 1 read, 2 write
+  int space;    // R_OK_SHARED / R_OK_GLOBAL
+  uint8_t ty;
+  uint32_t obj;
+  int64_t off;
+  uint64_t base;
+  int64_t size;
+  int name;
+  uint64_t raw;
+  bool ptr;
+  int line;
+  // results
+  bool ok;
+  Val val;
+};
+
+__device__ __forceinline__ int push(TS& t, const KP& P, const Val& v) {
+  if (t.nv >= VS) {
+    set_error(P, ERR_STACK, 0);
+    return 0;
+  }
+  t.vals[t.nv++] = v;
+  return 1;
+}
+__device__ __forceinline__ Val pop(TS& t) { return t.vals[--t.nv]; }
+
+// thread states
+enum : int { S_READY = 0, S_WAIT = 1, S_FIN = 2 };
+
+struct Thread {
+  int state;
+  uint32_t readyAt;
+  int syncKind;
+  long long operand;
+  uint32_t E;  // completed episodes (the race epoch)
+};
+
+__device__ __forceinline__ const mck_local& local_of(const KP& P, int fn, int slot) {
+  return P.locals[P.fns[fn].local_base + slot];
+}
+
+__device__ bool enter_fn(TS& t, const KP& P, int fn, int retPc) {
+  if (t.nframe >= FRAMES || t.nscope >= SCOPES) {
+    set_error(P, ERR_STACK, 1);
+    return false;
+  }
+  Frame f;
+  f.retPc = retPc;
+  f.bindBase = t.nframe == 0 ? 0 : t.frames[t.nframe - 1].bindBase + P.fns[t.frames[t.nframe - 1].fn].n_slots;
+  f.fn = fn;
+  f.scopeDepth = (uint8_t)t.nscope;
+  f.valueDepth = (uint8_t)t.nv;
+  if (f.bindBase + P.fns[fn].n_slots > BINDS) {
+    set_error(P, ERR_STACK, 2);
+    return false;
+  }
+  t.frames[t.nframe++] = f;
+  t.scopeMark[t.nscope++] = (uint8_t)t.nowned;
+  return true;
+}
+
+// Leaves the current function; returns false when the thread is finished.
+__device__ bool leave_fn(TS& t, const KP& P, Ctx& c, const Val* v, int line, bool conv, Thread& th) {
+  Frame f = t.frames[t.nframe - 1];
+  pop_scopes(t, f.scopeDepth);
+  t.nv = f.valueDepth;
+  --t.nframe;
+  uint8_t ret = P.fns[f.fn].ret;
+  Val out;
+  if (conv) {
+    Diags d{};
+    bool ok = convert(*v, ret, out, d);
+    emit_ops(P, c, d, line);
+    if (!ok) {
+      th.state = S_FIN;
+      return false;
+    }
+  } else {
+    out = t_is_void(ret) ? v_void() : v_int(0, ret);
+  }
+  if (t.nframe == 0) {
+    th.state = S_FIN;
+    return false;
+  }
+  push(t, P, out);
+  t.pc = f.retPc;
+  return true;
+}
+
+// Read / write through a resolved object for NON-private targets: fills the
+// request, the memory phase performs it.  For private targets performs it now.
+// Returns: 0 = done (value pushed / halted), 1 = request pending.
+__device__ int mem_read(TS& t, const KP& P, Ctx& c, Thread& th, uint32_t obj, int64_t off, uint8_t ty, int line,
+                        Req& rq) {
+  int len = (int)t_scalar(ty);
+  Res r = resolve(t, P, c.bid, obj, off, len);
+  switch (r.kind) {
+    case R_NULL: emit_diag(P, c, MCK_D_NULL_RW, line, 0); th.state = S_FIN; return 0;
+    case R_BOUNDARY: emit_diag(P, c, MCK_D_MEMBOUNDARY, line, 0, r.space, r.target); th.state = S_FIN; return 0;
+    case R_DEAD: emit_diag(P, c, MCK_D_DEAD, line, 0, 0, 0, 0, r.name); th.state = S_FIN; return 0;
+    case R_OOB: emit_diag(P, c, MCK_D_OOB, line, 0, len, off, r.size, r.name); th.state = S_FIN; return 0;
+    default: break;
+  }
+  if (r.kind == R_OK_PRIV) {
+    bool undef, ps;
+    uint64_t raw = load_raw(t.pbytes + r.base + off, len, undef, t.pmeta + r.base + off, ps);
+    rq.kind = 0;
+    rq.ok = true;
+    if (MCK_T_PTR(ty) > 0) {
+      if (ps) { rq.val = v_ptr((uint32_t)(raw >> 32), (int32_t)(raw & 0xffffffffu), ty); return 0; }
+      if (undef) { emit_diag(P, c, MCK_D_UNINIT_PTR, line, 0, 0, 0, 0, r.name); th.state = S_FIN; rq.ok = false; return 0; }
+      if (raw == 0) { rq.val = v_ptr(0, 0, ty); return 0; }
+      emit_diag(P, c, MCK_D_NONPTR_AS_PTR, line);
+      th.state = S_FIN;
+      rq.ok = false;
+      return 0;
+    }
+    if (undef) emit_diag(P, c, MCK_D_UNINIT, line, 0, 0, 0, 0, r.name);
+    rq.val = decode_scalar(raw, ty);
+    return 0;
+  }
+  rq.kind = 1;
+  rq.space = r.kind;
+  rq.ty = ty;
+  rq.obj = obj;
+  rq.off = off;
+  rq.base = r.base;
+  rq.size = r.size;
+  rq.name = r.name;
+  rq.line = line;
+  return 1;
+}
+
+__device__ int mem_write(TS& t, const KP& P, Ctx& c, Thread& th, uint32_t obj, int64_t off, uint8_t ty,
+                         const Val& v, int line, Req& rq) {
+  int len = (int)t_scalar(ty);
+  Res r = resolve(t, P, c.bid, obj, off, len);
+  switch (r.kind) {
+    case R_NULL: emit_diag(P, c, MCK_D_NULL_RW, line, 1); th.state = S_FIN; return 0;
+    case R_BOUNDARY: emit_diag(P, c, MCK_D_MEMBOUNDARY, line, 1, r.space, r.target); th.state = S_FIN; return 0;
+    case R_DEAD: emit_diag(P, c, MCK_D_DEAD, line, 1, 0, 0, 0, r.name); th.state = S_FIN; return 0;
+    case R_OOB: emit_diag(P, c, MCK_D_OOB, line, 1, len, off, r.size, r.name); th.state = S_FIN; return 0;
+    default: break;
+  }
+  if (r.kind == R_OK_PRIV) {
+    priv_poke(t, t.pobj[obj & 0xFFFFF], off, ty, v);
+    rq.kind = 0;
+    rq.ok = true;
+    return 0;
+  }
+  if (v.kind == MCK_K_PTR && (v.obj & PRIV)) {
+    // a private pointer escaping to memory other threads can read: the
+    // engine's virtual ids are thread-relative (documented limitation)
+    set_error(P, ERR_SHARED_PTR_ESCAPE, line);
+    th.state = S_FIN;
+    return 0;
+  }
+  rq.kind = 2;
+  rq.space = r.kind;
+  rq.ty = ty;
+  rq.obj = obj;
+  rq.off = off;
+  rq.base = r.base;
+  rq.size = r.size;
+  rq.name = r.name;
+  rq.line = line;
+  rq.raw = encode_scalar(v, ty);
+  rq.ptr = v.kind == MCK_K_PTR && v.obj != 0;
+  rq.val = v;
+  return 1;
+}
+
+// Performs a pending shared/global request (memory phase).
+__device__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq, const SmemLay& L, uint32_t stamp,
+                           uint32_t bstamp, unsigned long long& sharedEvents) {
+  int len = (int)t_scalar(rq.ty);
+  uint8_t *b, *m;
+  if (rq.space == R_OK_SHARED) {
+    b = smem + L.bytes + rq.off;
+    m = smem + L.meta + rq.off;
+    if (P.raceCheck) {
+      ++sharedEvents;
+      uint32_t raced = shadow_access((uint32_t*)(smem + L.shadow), rq.off, len, c.tid, rq.kind == 2, stamp);
+      report_race(P, c, (unsigned long long*)(smem + L.raceSet), rq.obj, rq.off, raced, rq.line, bstamp);
+    }
+  } else {
+    b = P.gbytes + rq.base + rq.off;
+    m = P.gmeta + rq.base + rq.off;
+  }
+  if (rq.kind == 2) {
+    if (rq.space == R_OK_SHARED)
+      store_raw(smem + L.bytes, smem + L.meta, rq.size, rq.off, len, rq.raw, rq.ptr);
+    else
+      store_raw(P.gbytes + rq.base, P.gmeta + rq.base, rq.size, rq.off, len, rq.raw, rq.ptr);
+    rq.ok = true;
+    return;
+  }
+  bool undef, ps;
+  uint64_t raw = load_raw(b, len, undef, m, ps);
+  rq.ok = true;
+  if (MCK_T_PTR(rq.ty) > 0) {
+    if (ps) { rq.val = v_ptr((uint32_t)(raw >> 32), (int32_t)(raw & 0xffffffffu), rq.ty); return; }
+    if (undef) { emit_diag(P, c, MCK_D_UNINIT_PTR, rq.line, 0, 0, 0, 0, rq.name); th.state = S_FIN; rq.ok = false; return; }
+    if (raw == 0) { rq.val = v_ptr(0, 0, rq.ty); return; }
+    emit_diag(P, c, MCK_D_NONPTR_AS_PTR, rq.line);
+    th.state = S_FIN;
+    rq.ok = false;
+    return;
+  }
+  if (undef) emit_diag(P, c, MCK_D_UNINIT, rq.line, 0, 0, 0, 0, rq.name);
+  rq.val = decode_scalar(raw, rq.ty);
+}
+
+// After-memory continuation of the instruction that issued a request.
+// pendOp: the opcode; for LOADKEEP the LValue is kept in `lv`.
+struct Pend {
+  int op;
+  Val lv;
+  Val keep;  // STORE_INC postfix: the old value
+  bool postfix;
+};
+
+__device__ void finish_request(TS& t, const KP& P, Thread& th, const Req& rq, const Pend& pd) {
+  if (th.state == S_FIN || !rq.ok) return;
+  switch (pd.op) {
+    case OP_LOADRV: push(t, P, rq.val); break;
+    case OP_LOADKEEP:
+      push(t, P, pd.lv);
+      push(t, P, rq.val);
+      break;
+    default:  // stores push the stored (or old) value
+      push(t, P, pd.postfix ? pd.keep : rq.val);
+      break;
+  }
+}
+
+// One small step of thread `t`.  Returns 1 when a shared/global request is
+// pending (rq/pd filled), else 0.
+__device__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req& rq, Pend& pd, BlockShared& bs, uint32_t nthreads) {
+  const mck_ins* code = P.code;
+  mck_ins in = code[t.pc];
+  while (in.op == OP_JMP) {
+    t.pc = in.a;
+    in = code[t.pc];
+  }
+  ++t.pc;
+  ++t.steps;
+  const int L = in.line;
+  Diags d{};
+  rq.kind = 0;
+  switch (in.op) {
+    case OP_NOP: break;
+    case OP_SCOPE_PUSH:
+      if (t.nscope >= SCOPES) { set_error(P, ERR_STACK, 3); th.state = S_FIN; break; }
+      t.scopeMark[t.nscope++] = (uint8_t)t.nowned;
+      break;
+    case OP_SCOPE_POP: pop_scopes(t, t.nscope - 1); break;
+    case OP_PUSH_INT:
+      push(t, P, v_int((int64_t)(((uint64_t)(uint32_t)in.b << 32) | (uint32_t)in.a), in.t));
+      break;
+    case OP_PUSH_FLT:
+      push(t, P, mk(MCK_K_FLOAT, in.t, 0, (int64_t)(((uint64_t)(uint32_t)in.b << 32) | (uint32_t)in.a)));
+      break;
+    case OP_PUSH_LOCAL: {
+      uint32_t o = t.binds[t.frames[t.nframe - 1].bindBase + in.a];
+      if (!o) {
+        emit_diag(P, c, MCK_D_FIXED_UB, L, MCK_UB_UNBOUND, 0, 0, 0, in.b);
+        th.state = S_FIN;
+        break;
+      }
+      push(t, P, v_lv(o, 0, in.t));
+      break;
+    }
+    case OP_PUSH_GLOBAL: push(t, P, v_lv(P.globalIds[in.a], 0, in.t)); break;
+    case OP_PUSH_BUILTIN: {
+      int64_t v = 0;
+      switch (in.f) {
+        case MCK_B_TID: v = in.a == 0 ? c.tid : 0; break;
+        case MCK_B_BID: v = in.a == 0 ? c.bid : 0; break;
+        case MCK_B_BDIM: v = in.a == 0 ? P.blockDim : 1; break;
+        case MCK_B_GDIM: v = in.a == 0 ? P.gridDim : 1; break;
+        default: v = P.warpSize; break;
+      }
+      push(t, P, v_int(v));
+      break;
+    }
+    case OP_UB:
+      emit_diag(P, c, MCK_D_FIXED_UB, L, in.a, 0, 0, 0, in.b);
+      th.state = S_FIN;
+      break;
+    case OP_LOADRV: {
+      Val lv = pop(t);
+      if (MCK_T_ARR(lv.type)) {
+        push(t, P, v_ptr(lv.obj, lv.i, t_decay(lv.type)));
+        break;
+      }
+      pd.op = OP_LOADRV;
+      pd.postfix = false;
+      if (mem_read(t, P, c, th, lv.obj, lv.i, lv.type, L, rq)) return 1;
+      if (th.state != S_FIN) push(t, P, rq.val);
+      break;
+    }
+    case OP_LOADKEEP: {
+      Val lv = pop(t);
+      if (MCK_T_ARR(lv.type)) {
+        emit_diag(P, c, MCK_D_MODIFY_ARRAY, L);
+        th.state = S_FIN;
+        break;
+      }
+      pd.op = OP_LOADKEEP;
+      pd.lv = lv;
+      pd.postfix = false;
+      if (mem_read(t, P, c, th, lv.obj, lv.i, lv.type, L, rq)) return 1;
+      if (th.state != S_FIN) {
+        push(t, P, lv);
+        push(t, P, rq.val);
+      }
+      break;
+    }
+    case OP_STORE:
+    case OP_STORE_OP:
+    case OP_STORE_INC: {
+      Val lv, r, old{};
+      bool ok;
+      if (in.op == OP_STORE) {
+        Val rhs = pop(t);
+        lv = pop(t);
+        ok = convert(rhs, lv.type, r, d);
+      } else if (in.op == OP_STORE_OP) {
+        Val rhs = pop(t);
+        old = pop(t);
+        lv = pop(t);
+        Val x;
+        ok = binop(in.f, old, rhs, x, d) && convert(x, lv.type, r, d);
+      } else {
+        old = pop(t);
+        lv = pop(t);
+        Val x;
+        ok = binop(MCK_ADD, old, v_int(in.a), x, d) && convert(x, lv.type, r, d);
+      }
+      emit_ops(P, c, d, L);
+      if (!ok) {
+        th.state = S_FIN;
+        break;
+      }
+      pd.op = in.op;
+      pd.postfix = in.op == OP_STORE_INC && !in.f;
+      pd.keep = old;
+      if (mem_write(t, P, c, th, lv.obj, lv.i, lv.type, r, L, rq)) return 1;
+      if (th.state != S_FIN) push(t, P, pd.postfix ? old : r);
+      break;
+    }
+    case OP_ADDROF: {
+      Val lv = pop(t);
+      push(t, P, v_ptr(lv.obj, lv.i, t_addr(lv.type)));
+      break;
+    }
+    case OP_DEREF: {
+      Val v = pop(t);
+      if (v.kind == MCK_K_INT && v.i == 0) v = v_ptr(0, 0, MCK_T_VOIDP);
+      if (v.kind != MCK_K_PTR || MCK_T_PTR(v.type) == 0) {
+        emit_diag(P, c, MCK_D_DEREF_NONPTR, L);
+        th.state = S_FIN;
+        break;
+      }
+      push(t, P, v_lv(v.obj, v.i, t_elem(v.type)));
+      break;
+    }
+    case OP_INDEX: {
+      Val idx = pop(t), base = pop(t);
+      if (base.kind != MCK_K_PTR || idx.kind != MCK_K_INT) {
+        emit_diag(P, c, MCK_D_SUBSCRIPT, L);
+        th.state = S_FIN;
+        break;
+      }
+      uint8_t e = t_elem(base.type);
+      push(t, P, v_lv(base.obj, base.i + idx.i * t_scalar(e), e));
+      break;
+    }
+    case OP_UNARY: {
+      Val v = pop(t), r;
+      bool ok = unop(in.f, v, r, d);
+      emit_ops(P, c, d, L);
+      if (!ok) { th.state = S_FIN; break; }
+      push(t, P, r);
+      break;
+    }
+    case OP_BINARY: {
+      Val rr = pop(t), l = pop(t), r;
+      bool ok = binop(in.f, l, rr, r, d);
+      emit_ops(P, c, d, L);
+      if (!ok) { th.state = S_FIN; break; }
+      push(t, P, r);
+      break;
+    }
+    case OP_LOGRHS: {
+      Val l = pop(t);
+      bool isAnd = in.f == 1;
+      if (isAnd && !truthy(l)) {
+        push(t, P, v_int(0));
+        t.pc = in.a;
+      } else if (!isAnd && truthy(l)) {
+        push(t, P, v_int(1));
+        t.pc = in.a;
+      }
+      break;
+    }
+    case OP_BOOLIFY: {
+      Val v = pop(t);
+      push(t, P, v_int(truthy(v) ? 1 : 0));
+      break;
+    }
+    case OP_TERNSEL:
+    case OP_IFJUDGE:
+    case OP_WHILEJUDGE: {
+      Val cv = pop(t);
+      if (!truthy(cv)) t.pc = in.a;
+      break;
+    }
+    case OP_CAST: {
+      Val v = pop(t), r;
+      if (MCK_T_PTR(in.t) > 0 && v.kind == MCK_K_PTR) {
+        push(t, P, v_ptr(v.obj, v.i, in.t));
+        break;
+      }
+      bool ok = convert(v, in.t, r, d);
+      emit_ops(P, c, d, L);
+      if (!ok) { th.state = S_FIN; break; }
+      push(t, P, r);
+      break;
+    }
+    case OP_FORJUDGE: {
+      bool go = true;
+      if (in.f) go = truthy(pop(t));
+      if (!go) t.pc = in.a;
+      break;
+    }
+    case OP_POPVALUE: --t.nv; break;
+    case OP_RETURN: {
+      Val v = in.f ? pop(t) : v_void();
+      leave_fn(t, P, c, &v, L, true, th);
+      break;
+    }
+    case OP_FALLOFF: leave_fn(t, P, c, nullptr, L, false, th); break;
+    case OP_BREAK:
+    case OP_CONTINUE:
+      pop_scopes(t, t.nscope - in.b);
+      t.pc = in.a;
+      break;
+    case OP_CALL: {
+      const int n = in.b;
+      if (t.nv < n) { set_error(P, ERR_STACK, 4); th.state = S_FIN; break; }
+      t.nv -= n;
+      const int argBase = t.nv;
+      // args stay in vals[argBase .. argBase+n) until bound (the frame records nv)
+      if (!enter_fn(t, P, in.a, t.pc)) { th.state = S_FIN; break; }
+      const int bb = t.frames[t.nframe - 1].bindBase;
+      for (int i = 0; i < n; ++i) {
+        const mck_local& pl = local_of(P, in.a, i);
+        Val cv;
+        Diags dd{};
+        bool ok = convert(t.vals[argBase + i], pl.type, cv, dd);
+        emit_ops(P, c, dd, L);
+        if (!ok) { th.state = S_FIN; break; }
+        uint32_t id;
+        if (!priv_alloc(t, P, pl.size, pl.name, id)) { th.state = S_FIN; break; }
+        priv_poke(t, t.pobj[id & 0xFFFFF], 0, pl.type, cv);
+        t.binds[bb + i] = id;
+      }
+      if (th.state != S_FIN) t.pc = P.fns[in.a].entry;
+      break;
+    }
+    case OP_SYNC: {
+      long long operand = 0;
+      if (in.f != MCK_SYNC_PLAIN) {
+        Val v = pop(t);
+        operand = v.i;
+      }
+      th.state = S_WAIT;
+      th.syncKind = in.f;
+      th.operand = operand;
+      const int p = (th.E + 1) & 1;
+      const bool nz = operand != 0;
+      atomicAdd(&bs.wait[p], 1);
+      if (nz) atomicAdd(&bs.nz[p], 1);
+      if (nz || in.f == MCK_SYNC_PLAIN) atomicAdd(&bs.allc[p], 1);
+      break;
+    }
+    case OP_DECL: {
+      const int fn = t.frames[t.nframe - 1].fn;
+      const int bb = t.frames[t.nframe - 1].bindBase;
+      if (in.f) {  // extern __shared__: bind the block's array
+        t.binds[bb + in.a] = P.sharedBase + c.bid;
+        break;
+      }
+      const mck_local& l = local_of(P, fn, in.a);
+      uint32_t id;
+      if (!priv_alloc(t, P, l.size, l.name, id)) { th.state = S_FIN; break; }
+      t.binds[bb + in.a] = id;
+      break;
+    }
+    case OP_INITSTORE: {
+      Val v = pop(t), r;
+      bool ok = convert(v, in.t, r, d);
+      emit_ops(P, c, d, L);
+      if (!ok) { th.state = S_FIN; break; }
+      const uint32_t o = t.binds[t.frames[t.nframe - 1].bindBase + in.a];
+      pd.op = OP_INITSTORE;
+      pd.postfix = false;
+      if (mem_write(t, P, c, th, o, 0, in.t, r, L, rq)) {
+        rq.kind = 0;  // declared objects are private: never pending
+      }
+      break;
+    }
+    default:
+      set_error(P, ERR_OPCODE, in.op);
+      th.state = S_FIN;
+      break;
+  }
+  return 0;
+}
+
+// ---------------- conflict hash ----------------
+// Open addressing over (word + 1) keys; every inserter clears its own slots
+// after the check, so the table is empty again at the next sweep.
+__device__ __forceinline__ int ht_insert(unsigned long long* keys, uint32_t* vals, int bits,
+                                         unsigned long long key, uint32_t add) {
+  uint32_t mask = (1u << bits) - 1;
+  uint32_t h = (uint32_t)mix64(key) & mask;
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    unsigned long long old = atomicCAS(keys + h, 0ull, key);
+    if (old == 0ull || old == key) {
+      atomicAdd(vals + h, add);
+      return (int)h;
+    }
+    h = (h + 1) & mask;
+  }
+  return -1;
+}
+
+// ================= the kernel =================
+__global__ void __launch_bounds__(1024) grid_kernel(KP P) {
+  const uint32_t bid = blockIdx.x;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t n = (uint32_t)P.blockDim;
+  const bool active = tid < n;
+  const SmemLay L = smemLayout(P.shmem, P.raceCheck, P.htBits);
+  __shared__ BlockShared bs;
+
+  // ---- block init ----
+  for (uint32_t i = tid; i < (uint32_t)P.shmem; i += blockDim.x) {
+    smem[L.bytes + i] = 0;
+    smem[L.meta + i] = 0;
+  }
+  if (P.raceCheck) {
+    uint32_t* sh = (uint32_t*)(smem + L.shadow);
+    for (uint32_t i = tid; i < (uint32_t)P.shmem; i += blockDim.x) sh[i] = shadow_empty(0);
+    unsigned long long* rs = (unsigned long long*)(smem + L.raceSet);
+    for (uint32_t i = tid; i < RACE_SET; i += blockDim.x) rs[i] = 0;
+  }
+  {
+    unsigned long long* hk = (unsigned long long*)(smem + L.htKey);
+    uint32_t* hv = (uint32_t*)(smem + L.htVal);
+    for (uint32_t i = tid; i < (1u << P.htBits); i += blockDim.x) {
+      hk[i] = 0;
+      hv[i] = 0;
+    }
+  }
+  if (tid == 0) {
+    bs.wait[0] = bs.wait[1] = 0;
+    bs.nz[0] = bs.nz[1] = 0;
+    bs.allc[0] = bs.allc[1] = 0;
+    bs.fin = (int)(blockDim.x - n);  // padding lanes count as finished
+    bs.conflict = 0;
+    bs.steps = 0;
+    bs.allocs = 0;
+    bs.sharedEvents = 0;
+    bs.lastSweep = 0;
+  }
+
+  TS t;
+  Thread th;
+  th.state = active ? S_READY : S_FIN;
+  th.readyAt = 1;
+  th.E = 0;
+  th.syncKind = 0;
+  th.operand = 0;
+  t.pc = 0;
+  t.nv = t.nscope = t.nowned = t.nframe = t.npobj = t.ptop = 0;
+  t.steps = t.allocs = 0;
+  for (int i = 0; i < POBJ; ++i) t.pobj[i].gen = 0;
+  for (int i = 0; i < BINDS; ++i) t.binds[i] = 0;
+  Ctx c;
+  c.bid = bid;
+  c.tid = tid;
+  c.sub = 0;
+  c.sweep = 0;
+  if (active) {
+    // spawnGrid (device.cpp:40-57): params are objects owned by the spawn
+    // scope, the dynamic shared array is bound, k = [CallFrame, body]
+    const mck_fn& kf = P.fns[P.kernel];
+    t.frames[0].retPc = -1;
+    t.frames[0].bindBase = 0;
+    t.frames[0].fn = P.kernel;
+    t.frames[0].scopeDepth = 0;
+    t.frames[0].valueDepth = 0;
+    t.nframe = 1;
+    t.scopeMark[0] = 0;
+    t.nscope = 1;
+    for (int i = 0; i < P.nargs; ++i) {
+      const mck_local& pl = P.locals[kf.local_base + i];
+      uint32_t id;
+      if (!priv_alloc(t, P, pl.size, pl.name, id)) {
+        th.state = S_FIN;
+        break;
+      }
+      priv_poke(t, t.pobj[id & 0xFFFFF], 0, pl.type, P.args[i]);
+      t.binds[i] = id;
+    }
+    t.allocs = 0;  // spawn-time params are accounted for by the host
+    if (kf.dyn_shared_slot >= 0) t.binds[kf.dyn_shared_slot] = P.sharedBase + bid;
+    t.pc = kf.entry;
+    if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+  }
+  __syncthreads();
+
+  uint32_t E = 0;           // completed episodes (uniform)
+  unsigned long long rules = 0;
+  uint32_t sweep = 0;
+  bool deadlocked = false;
+  unsigned long long sharedEvents = 0;
+  uint32_t lastStep = 0;
+  const uint32_t Lt = n - 1;
+
+  while (true) {
+    // ---- barrier protocol in closed form (Appendix A) ----
+    const int p = (E + 1) & 1;
+    const int nwait = bs.wait[p];
+    const int nfin = bs.fin;
+    if (nwait == (int)n) {
+      // episode E+1 completed in sweep `sweep` (the last arrival's sweep):
+      // up-sweep + Turnaround (epoch clear) + Down(L) now, one Down per sweep
+      const uint32_t T = sweep;
+      const int nz = bs.nz[p], allc = bs.allc[p];
+      if (active) {
+        th.state = S_READY;
+        th.readyAt = tid == 0 ? T + Lt + 1 : T + (Lt - tid) + 1;
+        th.E = E + 1;
+        Val res;
+        switch (th.syncKind) {
+          case MCK_SYNC_AND: res = v_int(allc == (int)n ? 1 : 0); break;
+          case MCK_SYNC_OR: res = v_int(nz > 0 ? 1 : 0); break;
+          case MCK_SYNC_COUNT: res = v_int(nz); break;
+          default: res = v_void(); break;
+        }
+        push(t, P, res);
+      }
+      rules += 2ull * n;
+      ++E;
+      if (P.raceCheck && (E & 0xFF) == 0) {  // stamp wrap: clear the shadow
+        uint32_t* sh = (uint32_t*)(smem + L.shadow);
+        for (uint32_t i = tid; i < (uint32_t)P.shmem; i += blockDim.x) sh[i] = shadow_empty(0);
+      }
+    } else if (nfin == (int)blockDim.x) {
+      break;  // every thread finished
+    } else if (nwait + nfin == (int)blockDim.x) {
+      // quiescent with waiters: barrier deadlock (deadlock.cpp:15-34).  The
+      // up-sweep advanced from tid 0 through the waiting prefix.
+      deadlocked = true;
+      break;
+    }
+    __syncthreads();  // everyone has read the counters
+    if (tid == 0 && nwait == (int)n) {
+      bs.wait[p] = 0;
+      bs.nz[p] = 0;
+      bs.allc[p] = 0;
+    }
+    ++sweep;
+    if (sweep >= P.maxSweeps) {
+      set_error(P, ERR_SWEEPS, 0);
+      break;
+    }
+    c.sweep = sweep;
+    c.sub = 0;
+    // ---- phase 1: one step per runnable thread ----
+    Req rq;
+    Pend pd;
+    rq.kind = 0;
+    int pending = 0;
+    const bool run = active && th.state == S_READY && sweep >= th.readyAt;
+    if (run) {
+      pending = step(t, P, c, th, rq, pd, bs, n);
+      if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+    }
+    const int nreq = __syncthreads_count(pending);
+    if (run && sweep > lastStep) lastStep = sweep;
+    if (nreq > 0) {
+      bool conflict = false;
+      if (nreq > 1) {
+        // word-level overlap with a write among this sweep's requests
+        unsigned long long* hk = (unsigned long long*)(smem + L.htKey);
+        uint32_t* hv = (uint32_t*)(smem + L.htVal);
+        int slots[3] = {-1, -1, -1};
+        int ns = 0;
+        if (pending) {
+          const int len = (int)t_scalar(rq.ty);
+          const unsigned long long addr = rq.space == R_OK_SHARED
+                                              ? (unsigned long long)rq.off
+                                              : (1ull << 40) | (rq.base + (unsigned long long)rq.off);
+          const uint32_t add = rq.kind == 2 ? 0x10001u : 1u;
+          for (unsigned long long w = addr >> 2; w <= (addr + len - 1) >> 2 && ns < 3; ++w) {
+            int h = ht_insert(hk, hv, P.htBits, w + 1, add);
+            if (h < 0) conflict = true;
+            slots[ns++] = h;
+          }
+        }
+        __syncthreads();
+        for (int i = 0; i < ns; ++i)
+          if (slots[i] >= 0) {
+            uint32_t v = hv[slots[i]];
+            if ((v >> 16) >= 1 && (v & 0xFFFF) >= 2) conflict = true;
+          }
+        conflict = __syncthreads_or(conflict);
+        for (int i = 0; i < ns; ++i)
+          if (slots[i] >= 0) {
+            hk[slots[i]] = 0ull;
+            hv[slots[i]] = 0u;
+          }
+      }
+      const uint32_t stamp = E & 0xFF;
+      if (!conflict) {
+        if (pending) {
+          do_request(P, c, th, rq, L, stamp, bid, sharedEvents);
+          finish_request(t, P, th, rq, pd);
+          if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+        }
+      } else {
+        // replay the memory phase in tid order (round-robin order)
+        const uint32_t warp = tid >> 5, lane = tid & 31;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+          if (warp == w) {
+            for (uint32_t l = 0; l < 32; ++l) {
+              if (lane == l && pending) {
+                do_request(P, c, th, rq, L, stamp, bid, sharedEvents);
+                finish_request(t, P, th, rq, pd);
+                if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+              }
+              __syncwarp();
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- block outputs ----
+  const uint32_t warp = tid >> 5, lane = tid & 31;
+  const uint32_t words = (n + 31) / 32;
+  if (deadlocked) {
+    bool waiting = active && th.state == S_WAIT;
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, waiting);
+    if (lane == 0 && warp < words) P.waitMask[(size_t)bid * words + warp] = m;
+    // up-sweep rules of the stuck episode: from tid 0 along the waiting prefix
+    // (device.cpp:111-141): p - 1 rules where p = first non-waiting tid
+  }
+  atomicAdd(&bs.steps, (unsigned long long)t.steps);
+  atomicAdd(&bs.allocs, (unsigned long long)t.allocs);
+  atomicAdd(&bs.sharedEvents, sharedEvents);
+  atomicMax(&bs.lastSweep, lastStep);
+  __syncthreads();
+  if (deadlocked) {
+    // first non-waiting tid
+    __shared__ uint32_t firstNot;
+    if (tid == 0) firstNot = n;
+    __syncthreads();
+    if (active && th.state != S_WAIT) atomicMin(&firstNot, tid);
+    __syncthreads();
+    if (tid == 0 && firstNot >= 1) rules += firstNot - 1;
+  }
+  if (tid == 0) {
+    BlockOut& o = P.blocks[bid];
+    o.steps = bs.steps;
+    o.rules = rules;
+    o.allocs = bs.allocs;
+    o.sharedEvents = bs.sharedEvents;
+    o.lastSweep = bs.lastSweep;
+    o.deadlocked = deadlocked ? 1 : 0;
+  }
+}
+
+}  // namespace k1
+
+// ======================= host side of the engine =======================
+namespace {
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t e_ = (x);                                                      \
+    if (e_ != cudaSuccess) {                                                   \
+      err = std::string(#x) + ": " + cudaGetErrorString(e_);                   \
+      return false;                                                            \
+    }                                                                          \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  bool ensure(size_t count, std::string& err) {
+    if (count <= n && p) return true;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t want = count ? count : 1;
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e != cudaSuccess) {
+      err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+      p = nullptr;
+      return false;
+    }
+    n = want;
+    return true;
+  }
+};
+
+class CudaEngine final : public DeviceEngine {
+ public:
+  explicit CudaEngine(int dev) : dev_(dev) {}
+  ~CudaEngine() override {
+    if (bytes_) cudaFree(bytes_);
+    if (meta_) cudaFree(meta_);
+    if (stream_) cudaStreamDestroy(stream_);
+  }
+  bool init(std::string& err) {
+    CK(cudaSetDevice(dev_));
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    return true;
+  }
+  bool hasDevice() const override { return true; }
+
+  uint64_t alloc(int64_t size) override {
+    uint64_t b = (top_ + 15) & ~15ull;
+    uint64_t need = b + (uint64_t)size;
+    if (need > cap_) grow(need);
+    top_ = need;
+    return b;
+  }
+  void write(uint64_t base, const uint8_t* b, const uint8_t* m, int64_t n) override {
+    cudaMemcpy(bytes_ + base, b, (size_t)n, cudaMemcpyHostToDevice);
+    cudaMemcpy(meta_ + base, m, (size_t)n, cudaMemcpyHostToDevice);
+  }
+  void read(uint64_t base, uint8_t* b, uint8_t* m, int64_t n) override {
+    cudaMemcpy(b, bytes_ + base, (size_t)n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(m, meta_ + base, (size_t)n, cudaMemcpyDeviceToHost);
+  }
+  void copy(uint64_t dst, uint64_t src, int64_t n) override {
+    cudaMemcpy(bytes_ + dst, bytes_ + src, (size_t)n, cudaMemcpyDeviceToDevice);
+    cudaMemcpy(meta_ + dst, meta_ + src, (size_t)n, cudaMemcpyDeviceToDevice);
+  }
+  void fill(uint64_t base, uint8_t v, uint8_t m, int64_t n) override {
+    cudaMemset(bytes_ + base, v, (size_t)n);
+    cudaMemset(meta_ + base, m, (size_t)n);
+  }
+  bool runGrid(const GridSpec& g, GridResult& out) override {
+    std::string err;
+    bool ok = run(g, out, err);
+    if (!ok && out.error.empty()) out.error = err;
+    return ok;
+  }
+
+ private:
+  int dev_;
+  cudaStream_t stream_ = nullptr;
+  uint8_t* bytes_ = nullptr;
+  uint8_t* meta_ = nullptr;
+  uint64_t cap_ = 0, top_ = 0;
+  const Program* progCached_ = nullptr;
+  DBuf<mck_ins> code_;
+  DBuf<mck_fn> fns_;
+  DBuf<mck_local> locals_;
+
+  void grow(uint64_t need) {
+    uint64_t nc = std::max<uint64_t>(need, std::max<uint64_t>(cap_ * 2, 1ull << 20));
+    uint8_t *nb = nullptr, *nm = nullptr;
+    cudaMalloc(&nb, nc);
+    cudaMalloc(&nm, nc);
+    cudaMemset(nb, 0, nc);
+    cudaMemset(nm, 0, nc);
+    if (bytes_) {
+      cudaMemcpy(nb, bytes_, top_, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(nm, meta_, top_, cudaMemcpyDeviceToDevice);
+      cudaFree(bytes_);
+      cudaFree(meta_);
+    }
+    bytes_ = nb;
+    meta_ = nm;
+    cap_ = nc;
+  }
+
+  template <typename T>
+  bool upload(DBuf<T>& d, const std::vector<T>& v, std::string& err) {
+    if (!d.ensure(v.size(), err)) return false;
+    if (!v.empty()) CK(cudaMemcpy(d.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return true;
+  }
+
+  bool run(const GridSpec& g, GridResult& out, std::string& err) {
+    using namespace k1;
+    const Program& P = *g.prog;
+    if (g.blockDim > 1024) {
+      out.error = "blockDim > 1024 is not supported by the B200 engine";
+      return false;
+    }
+    if (g.gridDim > (1ll << 26)) {
+      out.error = "gridDim > 2^26 is not supported by the B200 engine";
+      return false;
+    }
+    CK(cudaSetDevice(dev_));
+    if (progCached_ != &P) {
+      if (!upload(code_, P.code, err) || !upload(fns_, P.fns, err) || !upload(locals_, P.locals, err)) return false;
+      progCached_ = &P;
+    }
+    const int threads = (int)((g.blockDim + 31) / 32 * 32);
+    int htBits = 1;
+    while ((1 << htBits) < 4 * threads) ++htBits;
+    const SmemLay L = smemLayout(g.shmemBytes, g.raceCheck ? 1 : 0, htBits);
+    if (L.end > 200 * 1024) {
+      out.error = "the block's shared array (" + std::to_string(g.shmemBytes) +
+                  " bytes) exceeds the engine's on-chip shadow capacity";
+      return false;
+    }
+    // tables
+    std::vector<uint32_t> ids;
+    for (const auto& o : g.objects) ids.push_back(o.id);
+    DBuf<uint32_t> dIds, dGlob, dRanges;
+    DBuf<DevObjInfo> dObjs;
+    DBuf<Val> dArgs;
+    if (!upload(dIds, ids, err) || !upload(dObjs, g.objects, err) || !upload(dGlob, g.globalIds, err) ||
+        !upload(dArgs, g.args, err))
+      return false;
+    std::vector<uint32_t> rng;
+    for (const auto& r : g.sharedRanges) rng.insert(rng.end(), r.begin(), r.end());
+    if (!upload(dRanges, rng, err)) return false;
+    // outputs
+    const size_t nb = (size_t)g.gridDim;
+    const uint32_t words = (uint32_t)((g.blockDim + 31) / 32);
+    DBuf<unsigned long long> dLine, dNTri;
+    DBuf<long long> dTri;
+    DBuf<DevDiagRec> dDiag;
+    DBuf<BlockOut> dBlocks;
+    DBuf<uint32_t> dWait;
+    DBuf<int> dErr;
+    const unsigned long long triCap = 1ull << 22;
+    const uint32_t diagN = 1u << 18;
+    if (!dLine.ensure(LINES, err) || !dNTri.ensure(1, err) || !dTri.ensure(3 * triCap, err) ||
+        !dDiag.ensure(diagN, err) || !dBlocks.ensure(nb, err) || !dWait.ensure(nb * words, err) ||
+        !dErr.ensure(2, err))
+      return false;
+    CK(cudaMemsetAsync(dLine.p, 0xFF, LINES * sizeof(unsigned long long), stream_));
+    CK(cudaMemsetAsync(dNTri.p, 0, sizeof(unsigned long long), stream_));
+    CK(cudaMemsetAsync(dDiag.p, 0, diagN * sizeof(DevDiagRec), stream_));
+    CK(cudaMemsetAsync(dWait.p, 0, nb * words * sizeof(uint32_t), stream_));
+    CK(cudaMemsetAsync(dErr.p, 0, 2 * sizeof(int), stream_));
+    KP kp;
+    kp.code = code_.p;
+    kp.fns = fns_.p;
+    kp.locals = locals_.p;
+    kp.kernel = g.kernel;
+    kp.nargs = (int)g.args.size();
+    kp.args = dArgs.p;
+    kp.gid = g.gid;
+    kp.sharedBase = g.sharedBase;
+    kp.nextId = g.nextId;
+    kp.gridDim = g.gridDim;
+    kp.blockDim = g.blockDim;
+    kp.shmem = g.shmemBytes;
+    const mck_fn& kf = P.fns[(size_t)g.kernel];
+    kp.sharedName = kf.dyn_shared_slot >= 0 ? P.locals[(size_t)(kf.local_base + kf.dyn_shared_slot)].name
+                                            : P.sharedDefaultName;
+    kp.warpSize = g.warpSize;
+    kp.objIds = dIds.p;
+    kp.objs = dObjs.p;
+    kp.nobjs = (int)g.objects.size();
+    kp.globalIds = dGlob.p;
+    kp.shRanges = dRanges.p;
+    kp.nranges = (int)g.sharedRanges.size();
+    kp.gbytes = bytes_;
+    kp.gmeta = meta_;
+    kp.raceCheck = g.raceCheck ? 1 : 0;
+    kp.htBits = htBits;
+    kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
+    kp.lineFirst = dLine.p;
+    kp.triples = dTri.p;
+    kp.tripleCap = triCap;
+    kp.nTriples = dNTri.p;
+    kp.diags = dDiag.p;
+    kp.diagMask = diagN - 1;
+    kp.blocks = dBlocks.p;
+    kp.waitMask = dWait.p;
+    kp.error = dErr.p;
+    kp.errorInfo = dErr.p + 1;
+    CK(cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.end));
+    init_diag_ts(dDiag.p, diagN, stream_);  // ts := +inf
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, stream_);
+    grid_kernel<<<(unsigned)nb, threads, L.end, stream_>>>(kp);
+    cudaEventRecord(e1, stream_);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(stream_));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    out.ms = ms;
+    out.launches = 2;
+    int herr[2];
+    CK(cudaMemcpy(herr, dErr.p, sizeof herr, cudaMemcpyDeviceToHost));
+    if (herr[0]) {
+      static const char* why[] = {"", "thread value/scope/frame stack overflow", "private memory of a thread exceeds the engine limit",
+                                  "a pointer to a thread-private object was stored to shared or global memory",
+                                  "too many distinct diagnostics", "too many reported race triples",
+                                  "source line outside 0..65535", "sweep budget exhausted (step limit or 2^26 sweeps)", "bad opcode"};
+      out.error = std::string("B200 engine limitation: ") + why[herr[0] < 9 ? herr[0] : 0] + " (info " +
+                  std::to_string(herr[1]) + ")";
+      return false;
+    }
+    // block outcomes
+    std::vector<BlockOut> bo(nb);
+    CK(cudaMemcpy(bo.data(), dBlocks.p, nb * sizeof(BlockOut), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> wm;
+    bool anyDl = false;
+    for (const auto& b : bo) {
+      out.deviceSteps += b.steps;
+      out.barrierRules += b.rules;
+      out.allocs += b.allocs;
+      out.sharedEvents += b.sharedEvents;
+      out.duration = std::max(out.duration, b.lastSweep);
+      if (b.deadlocked) anyDl = true;
+    }
+    out.deadlocked = anyDl;
+    if (anyDl) {
+      wm.resize(nb * words);
+      CK(cudaMemcpy(wm.data(), dWait.p, wm.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      for (size_t b = 0; b < nb; ++b) {
+        if (!bo[b].deadlocked) continue;
+        GridResult::Stuck s;
+        s.bid = (uint32_t)b;
+        for (uint32_t t = 0; t < (uint32_t)g.blockDim; ++t)
+          if ((wm[b * words + t / 32] >> (t % 32)) & 1u) s.waiting.push_back((int)t);
+        out.stuck.push_back(std::move(s));
+      }
+    }
+    // diagnostics
+    std::vector<DevDiagRec> dr(diagN);
+    CK(cudaMemcpy(dr.data(), dDiag.p, diagN * sizeof(DevDiagRec), cudaMemcpyDeviceToHost));
+    for (const auto& r : dr)
+      if (r.hkey) {
+        DevDiag d;
+        d.key = r.ts;
+        d.code = r.code;
+        d.line = r.line;
+        for (int i = 0; i < 4; ++i) d.p[i] = r.p[i];
+        d.name = r.name;
+        out.diags.push_back(d);
+      }
+    std::vector<unsigned long long> lf(LINES);
+    CK(cudaMemcpy(lf.data(), dLine.p, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (int l = 0; l < LINES; ++l)
+      if (lf[(size_t)l] != ~0ull) {
+        DevDiag d;
+        d.key = lf[(size_t)l];
+        d.code = MCK_D_RACE;
+        d.line = l;
+        d.p[0] = d.p[1] = d.p[2] = d.p[3] = 0;
+        d.name = -1;
+        out.diags.push_back(d);
+      }
+    unsigned long long ntri = 0;
+    CK(cudaMemcpy(&ntri, dNTri.p, sizeof ntri, cudaMemcpyDeviceToHost));
+    if (ntri) {
+      std::vector<long long> tri(3 * std::min<unsigned long long>(ntri, triCap));
+      CK(cudaMemcpy(tri.data(), dTri.p, tri.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      std::vector<std::array<int64_t, 3>> v;
+      for (size_t i = 0; i < tri.size(); i += 3) v.push_back({tri[i], tri[i + 1], tri[i + 2]});
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      out.reported = std::move(v);
+    }
+    return true;
+  }
+
+  static void init_diag_ts(k1::DevDiagRec* p, uint32_t n, cudaStream_t s);
+};
+
+__global__ void init_ts_kernel(k1::DevDiagRec* p, uint32_t n) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i].ts = ~0ull;
+}
+
+void CudaEngine::init_diag_ts(k1::DevDiagRec* p, uint32_t n, cudaStream_t s) {
+  init_ts_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, n);
+}
+
+}  // namespace
+
+std::unique_ptr<DeviceEngine> makeCudaEngine(int device, std::string& why) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n <= device) {
+    why = e != cudaSuccess ? cudaGetErrorString(e) : "no such device";
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::unique_ptr<CudaEngine> eng(new CudaEngine(device));
+  if (!eng->init(why)) return nullptr;
+  return std::unique_ptr<DeviceEngine>(eng.release());
+}
+
+}  // namespace mckb

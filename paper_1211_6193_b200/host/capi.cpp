@@ -1,0 +1,105 @@
+// capi.cpp -- C ABI over the mck:: C++ API (declared in include/mckg.h):
+// run a CUDA-C program end to end and return the RunResult as JSON, the
+// boundary the Python tests and bench.py call through ctypes.
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "mck/checker.hpp"
+#include "mckg.h"
+#include "program.hpp"
+
+namespace {
+
+std::string js(const std::string& s) {
+  std::string o = "\"";
+  for (unsigned char c : s) {
+    if (c == '"' || c == '\\') {
+      o += '\\';
+      o += static_cast<char>(c);
+    } else if (c < 0x20) {
+      char b[8];
+      std::snprintf(b, sizeof b, "\\u%04x", c);
+      o += b;
+    } else {
+      o += static_cast<char>(c);
+    }
+  }
+  return o + "\"";
+}
+
+}  // namespace
+
+extern "C" int mck_run_source(const char* src, const char* filename, const mck_run_opts* opts, char** json) {
+  if (!src || !filename || !json) return MCKG_E_ARG;
+  mck::RunOptions ro;
+  if (opts) {
+    ro.stepLimit = opts->step_limit ? opts->step_limit : ro.stepLimit;
+    ro.raceCheck = opts->race_check != 0;
+    ro.device = opts->device;
+    ro.policy = opts->round_robin ? mck::SchedulePolicy::RoundRobin : mck::SchedulePolicy::SeededRandom;
+    ro.seed = opts->seed;
+    if (opts->max_threads_per_block > 0) ro.arch.maxThreadsPerBlock = opts->max_threads_per_block;
+  }
+  std::string o;
+  try {
+    auto prog = mck::compileSource(src, filename);
+    mck::Machine m(prog, ro);
+    mck::RunResult r = m.run();
+    o = "{\"exit\":" + std::to_string(r.exitCode) + ",\"output\":" + js(r.output) +
+        ",\"steps\":" + std::to_string(r.steps) + ",\"stuck\":" + (r.stuck ? "true" : "false") +
+        ",\"main_return\":" + (r.mainReturn ? std::to_string(*r.mainReturn) : std::string("null")) +
+        ",\"engine_error\":" + js(r.engineError) + ",\"diags\":[";
+    for (size_t i = 0; i < r.diagnostics.size(); ++i) {
+      const auto& d = r.diagnostics[i];
+      o += std::string(i ? "," : "") + "{\"cat\":" + js(mck::categoryName(d.category)) + ",\"sev\":" +
+           (d.severity == mck::Severity::Error ? "\"error\"" : "\"warning\"") + ",\"msg\":" + js(d.message) +
+           ",\"line\":" + std::to_string(d.loc.line) + "}";
+    }
+    o += "],\"stuck_reports\":[";
+    for (size_t i = 0; i < r.stuckReports.size(); ++i) {
+      const auto& s = r.stuckReports[i];
+      const char* kind = s.kind == mck::StuckReport::Kind::BarrierDeadlock ? "barrier"
+                         : s.kind == mck::StuckReport::Kind::HostHang      ? "host"
+                                                                          : "stream";
+      o += std::string(i ? "," : "") + "{\"kind\":\"" + kind + "\",\"gid\":" + std::to_string(s.gid) +
+           ",\"bid\":" + std::to_string(s.bid) + ",\"waiting\":[";
+      for (size_t k = 0; k < s.waitingTids.size(); ++k) o += (k ? "," : "") + std::to_string(s.waitingTids[k]);
+      o += "],\"missing\":[";
+      for (size_t k = 0; k < s.missingTids.size(); ++k) o += (k ? "," : "") + std::to_string(s.missingTids[k]);
+      o += "],\"reason\":" + js(s.reason) + "}";
+    }
+    o += "],\"report_text\":" + js(mck::formatStuckReports(r.stuckReports)) + ",\"reported\":[";
+    for (size_t i = 0; i < r.reported.size(); ++i)
+      o += std::string(i ? "," : "") + "[" + std::to_string(r.reported[i].object) + "," +
+           std::to_string(r.reported[i].byte) + "," + std::to_string(r.reported[i].line) + "]";
+    const auto& st = r.stats;
+    o += "],\"stats\":{\"host_steps\":" + std::to_string(st.hostSteps) + ",\"device_steps\":" +
+         std::to_string(st.deviceSteps) + ",\"barrier_rules\":" + std::to_string(st.barrierRules) +
+         ",\"dispatches\":" + std::to_string(st.dispatches) + ",\"shared_events\":" +
+         std::to_string(st.sharedEvents) + ",\"grids\":" + std::to_string(st.grids) + ",\"sweeps\":" +
+         std::to_string(st.sweeps) + ",\"grid_ms\":" + std::to_string(st.gridMs) + ",\"kernel_launches\":" +
+         std::to_string(st.kernelLaunches) + "}}";
+  } catch (const mck::FrontendError& e) {
+    o = "{\"frontend_error\":" + js(e.stage + ": " + e.message) + ",\"line\":" + std::to_string(e.loc.line) +
+        ",\"exit\":2}";
+  } catch (const std::exception& e) {
+    o = "{\"internal_error\":" + js(e.what()) + ",\"exit\":5}";
+  }
+  *json = strdup(o.c_str());
+  return MCKG_OK;
+}
+
+extern "C" int mck_disassemble(const char* src, const char* filename, char** text) {
+  if (!src || !filename || !text) return MCKG_E_ARG;
+  try {
+    auto p = mckb::compileProgram(src, filename);
+    *text = strdup(p->disassemble().c_str());
+  } catch (const mckb::FrontendFailure& f) {
+    *text = strdup((f.stage + ": " + f.message).c_str());
+    return MCKG_E_ARG;
+  }
+  return MCKG_OK;
+}
+
+extern "C" void mck_free(char* p) { std::free(p); }

@@ -1,0 +1,98 @@
+// engine.hpp -- interface between the host machine (host/machine.cpp) and the
+// device grid engine (csrc/interp.cu, the K1 thread-stepping interpreter with
+// the fused shared-memory race detector and the K4 barrier-deadlock scan).
+//
+// The host dispatches a whole grid at the reference's StreamDispatch point
+// (streams.cpp:42-45 -> spawnGrid, device.cpp:19-66); the engine runs every
+// simulated block to completion or deadlock under the round-robin schedule
+// and returns step counts, the block outcomes, timestamped diagnostics and
+// the reported race triples.
+#pragma once
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../csrc/core.cuh"
+#include "program.hpp"
+
+namespace mckb {
+
+// Per-byte metadata of every memory object (host and device):
+constexpr uint8_t META_DEF = 1;  // byte defined (MemByte::defined, machine.hpp:33-37)
+constexpr uint8_t META_PTR = 2;  // a pointer slot starts here (MemObject::ptrs, machine.hpp:45)
+
+// A device-global object as the engine sees it.
+struct DevObjInfo {
+  uint32_t id;
+  int64_t size;
+  uint64_t base;  // byte offset in the device arena
+  bool live;
+  int name;       // diagnostic name handle echoed back in DevDiag::name
+};
+
+struct GridSpec {
+  const Program* prog = nullptr;
+  int kernel = -1;
+  int64_t gridDim = 1, blockDim = 1, shmemBytes = 0;
+  uint32_t gid = 0;
+  std::vector<mck_core::Val> args;  // converted to the parameter types
+  uint64_t spawnSweep = 0;          // sweep of the dispatch; first steps at +1
+  uint32_t sharedBase = 0;          // object id of block 0's shared array
+  uint32_t nextId = 0;              // ids >= nextId (and not private) are invalid
+  bool raceCheck = true;
+  int64_t warpSize = 32;
+  uint64_t stepBudget = ~0ull;      // steps left before the run's step limit
+  std::vector<DevObjInfo> objects;  // every device-global object, ascending id
+  std::vector<uint32_t> globalIds;  // object id of every TU global (host or device)
+  // shared arrays of earlier grids (for memBoundary messages): (first id, count, gid)
+  std::vector<std::array<uint32_t, 3>> sharedRanges;
+};
+
+struct DevDiag {
+  uint64_t key;      // (local sweep:26 | bid:26 | tid:10 | sub:2)
+  int code;          // MCK_D_*
+  int line;
+  int64_t p[4];
+  int name;          // string id or -1
+};
+
+struct GridResult {
+  uint64_t deviceSteps = 0;
+  uint64_t barrierRules = 0;
+  uint64_t allocs = 0;          // device-side object allocations (locals + call params)
+  uint64_t sharedEvents = 0;
+  uint32_t duration = 0;        // local sweep of the last device step (complete grids)
+  bool deadlocked = false;
+  struct Stuck {
+    uint32_t bid;
+    std::vector<int> waiting;
+  };
+  std::vector<Stuck> stuck;     // ascending bid
+  std::vector<DevDiag> diags;
+  std::vector<std::array<int64_t, 3>> reported;  // (obj, byte, line)
+  double ms = 0;
+  uint32_t launches = 0;
+  std::string error;            // engine limitation hit: run abandoned
+};
+
+class DeviceEngine {
+ public:
+  virtual ~DeviceEngine() = default;
+  virtual bool hasDevice() const = 0;
+  virtual uint64_t alloc(int64_t size) = 0;
+  virtual void write(uint64_t base, const uint8_t* bytes, const uint8_t* meta, int64_t n) = 0;
+  virtual void read(uint64_t base, uint8_t* bytes, uint8_t* meta, int64_t n) = 0;
+  virtual void copy(uint64_t dst, uint64_t src, int64_t n) = 0;
+  virtual void fill(uint64_t base, uint8_t v, uint8_t meta, int64_t n) = 0;
+  virtual bool runGrid(const GridSpec& spec, GridResult& out) = 0;
+};
+
+// The B200 engine; returns nullptr (with `why`) when no CUDA device is usable.
+std::unique_ptr<DeviceEngine> makeCudaEngine(int device, std::string& why);
+// Storage-only stand-in used when no GPU is present: device allocations and
+// copies work, launching a grid fails loudly (there is no CPU execution path).
+std::unique_ptr<DeviceEngine> makeStorageOnlyEngine(const std::string& why);
+
+}  // namespace mckb

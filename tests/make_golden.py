@@ -1,0 +1,28 @@
+"""Generates tests/golden/programs.json by running every corpus program through
+the reference checker itself (oracle/_ref/libmckref.so: /root/reference/proj
+built by oracle/Makefile) under the round-robin schedule.  Run here, where
+/root/reference exists:  python tests/make_golden.py"""
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+import oracle_bind as ob  # noqa: E402
+from program_corpus import corpus, project  # noqa: E402
+
+
+def main():
+    assert ob.ref() is not None, "oracle/_ref/libmckref.so missing: build the oracle first"
+    gold = {}
+    for name, fname, src in corpus():
+        r = ob.ref_run(src, filename=fname, policy="rr", capture=False)
+        gold[name] = project(r)
+    path = os.path.join(HERE, "golden", "programs.json")
+    with open(path, "w") as f:
+        json.dump(gold, f, separators=(",", ":"), sort_keys=True)
+    print(f"wrote {len(gold)} golden runs to {path}")
+
+
+if __name__ == "__main__":
+    main()
