@@ -38,6 +38,9 @@ EXPORTS = [
     "mckg_sort_triples",
     "mckg_scan_stuck",
     "mckg_gen_c3",
+    "mck_run_source",
+    "mck_disassemble",
+    "mck_free",
 ]
 
 

@@ -129,7 +129,7 @@ struct KP {
   uint32_t maxSweeps;         // < 2^26; each sweep takes >= 1 step (step limit)
   // outputs
   unsigned long long* lineFirst;
-  long long* triples;         // (obj, byte, line)
+  int32_t* triples;           // (obj, byte, line) records of 3 x int32
   unsigned long long tripleCap;
   unsigned long long* nTriples;
   DevDiagRec* diags;
@@ -497,8 +497,8 @@ __device__ void report_race(const KP& P, Ctx& c, unsigned long long* set, uint32
     if (fresh) {
       unsigned long long i = atomicAdd(P.nTriples, 1ull);
       if (i < P.tripleCap) {
-        P.triples[3 * i] = obj;
-        P.triples[3 * i + 1] = off + q;
+        P.triples[3 * i] = (int32_t)obj;
+        P.triples[3 * i + 1] = (int32_t)(off + q);
         P.triples[3 * i + 2] = line;
       } else {
         set_error(P, ERR_TRIPLES_FULL, 0);
@@ -1462,12 +1462,15 @@ class CudaEngine final : public DeviceEngine {
     const size_t nb = (size_t)g.gridDim;
     const uint32_t words = (uint32_t)((g.blockDim + 31) / 32);
     DBuf<unsigned long long> dLine, dNTri;
-    DBuf<long long> dTri;
+    DBuf<int32_t> dTri;
     DBuf<DevDiagRec> dDiag;
     DBuf<BlockOut> dBlocks;
     DBuf<uint32_t> dWait;
     DBuf<int> dErr;
-    const unsigned long long triCap = 1ull << 22;
+    // racy grids report up to ~shmem bytes x lines per block (C2 racy: 508/block)
+    const unsigned long long triCap =
+        g.raceCheck ? std::min<unsigned long long>(1ull << 28, std::max<unsigned long long>(1ull << 22, nb * 1024ull))
+                    : 1;
     const uint32_t diagN = 1u << 18;
     if (!dLine.ensure(LINES, err) || !dNTri.ensure(1, err) || !dTri.ensure(3 * triCap, err) ||
         !dDiag.ensure(diagN, err) || !dBlocks.ensure(nb, err) || !dWait.ensure(nb * words, err) ||
@@ -1597,10 +1600,12 @@ class CudaEngine final : public DeviceEngine {
     unsigned long long ntri = 0;
     CK(cudaMemcpy(&ntri, dNTri.p, sizeof ntri, cudaMemcpyDeviceToHost));
     if (ntri) {
-      std::vector<long long> tri(3 * std::min<unsigned long long>(ntri, triCap));
-      CK(cudaMemcpy(tri.data(), dTri.p, tri.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      std::vector<int32_t> tri(3 * std::min<unsigned long long>(ntri, triCap));
+      CK(cudaMemcpy(tri.data(), dTri.p, tri.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
       std::vector<std::array<int64_t, 3>> v;
-      for (size_t i = 0; i < tri.size(); i += 3) v.push_back({tri[i], tri[i + 1], tri[i + 2]});
+      v.reserve(tri.size() / 3);
+      for (size_t i = 0; i < tri.size(); i += 3)
+        v.push_back({(int64_t)(uint32_t)tri[i], (int64_t)(uint32_t)tri[i + 1], (int64_t)tri[i + 2]});
       std::sort(v.begin(), v.end());
       v.erase(std::unique(v.begin(), v.end()), v.end());
       out.reported = std::move(v);

@@ -52,6 +52,7 @@ struct HObj {
   std::string name;
   std::vector<uint8_t> bytes, meta;  // host objects
   uint64_t devBase = 0;              // device-global objects
+  bool hasPtr = false;               // some pointer slot was ever stored here
 };
 
 struct Frame {
@@ -161,6 +162,7 @@ class HostMachine {
   uint32_t nextEid_ = 1;
   std::map<uint32_t, GridRec> grids_;
   uint32_t nextGid_ = 1;
+  uint64_t runningGrids_ = 0;  // dispatched, not completed, will complete
   int lastApiError_ = 0;
   std::string output_;
   std::vector<DiagEv> diags_;
@@ -194,11 +196,18 @@ class HostMachine {
 
   HObj* find(uint32_t id) {
     if (id == 0) return nullptr;
+    if (cacheId_ == id && cacheVec_ == objs_.data()) return cacheObj_;
     auto it = std::lower_bound(objs_.begin(), objs_.end(), id,
                                [](const HObj& o, uint32_t x) { return o.id < x; });
     if (it == objs_.end() || it->id != id) return nullptr;
-    return &*it;
+    cacheId_ = id;
+    cacheVec_ = objs_.data();
+    cacheObj_ = &*it;
+    return cacheObj_;
   }
+  uint32_t cacheId_ = 0;
+  const HObj* cacheVec_ = nullptr;
+  HObj* cacheObj_ = nullptr;
 
   uint32_t alloc(uint8_t space, int64_t size, const std::string& name) {
     HObj o;
@@ -219,14 +228,20 @@ class HostMachine {
   // pokeValue on a host object (memory.cpp:184-206)
   static void poke(HObj& o, int64_t off, uint8_t t, const Val& v) {
     int64_t len = t_scalar(t);
-    for (int64_t s = std::max<int64_t>(0, off - 7); s < off + len && s < o.size; ++s)
-      if (s + 8 > off) o.meta[static_cast<size_t>(s)] &= static_cast<uint8_t>(~META_PTR);
+    if (o.hasPtr)
+      for (int64_t s = std::max<int64_t>(0, off - 7); s < off + len && s < o.size; ++s)
+        o.meta[static_cast<size_t>(s)] &= static_cast<uint8_t>(~META_PTR);
     uint64_t raw = encode_scalar(v, t);
+    uint8_t* b = o.bytes.data() + off;
+    uint8_t* m = o.meta.data() + off;
     for (int64_t i = 0; i < len; ++i) {
-      o.bytes[static_cast<size_t>(off + i)] = static_cast<uint8_t>(raw >> (8 * i));
-      o.meta[static_cast<size_t>(off + i)] |= META_DEF;
+      b[i] = static_cast<uint8_t>(raw >> (8 * i));
+      m[i] |= META_DEF;
     }
-    if (v.kind == MCK_K_PTR && v.obj != 0) o.meta[static_cast<size_t>(off)] |= META_PTR;
+    if (v.kind == MCK_K_PTR && v.obj != 0) {
+      m[0] |= META_PTR;
+      o.hasPtr = true;
+    }
   }
 
   std::string spaceStr(uint8_t space) const { return space == SP_HOST ? "host" : "device-global"; }
@@ -475,8 +490,11 @@ class HostMachine {
       return false;
     }
     it->second.q.push_back(std::move(item));
+    ++queued_;
     return true;
   }
+  uint64_t queued_ = 0;
+  std::vector<uint32_t> sids_;
   bool dispatchable(const StreamRec& s) const {
     if (s.running || s.q.empty()) return false;
     const StreamItem& h = s.q.front();
@@ -1329,6 +1347,7 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   nextId_ += static_cast<uint32_t>(reserve + rec.res.allocs);
   sharedRanges_.push_back({g.sharedBase, static_cast<uint32_t>(l.grid), g.gid});
   rec.endSweep = rec.res.deadlocked ? NEVER : sweep_ + rec.res.duration;
+  if (rec.endSweep != NEVER) ++runningGrids_;
   ++stats_.grids;
   stats_.gridMs += rec.res.ms;
   stats_.kernelLaunches += rec.res.launches;
@@ -1359,6 +1378,7 @@ void HostMachine::dispatch(uint32_t sid) {
   StreamRec& s = streams_.at(sid);
   StreamItem item = s.q.front();
   s.q.pop_front();
+  --queued_;
   switch (item.kind) {
     case ItemKind::Launch: spawnGrid(sid, item.launch); break;
     case ItemKind::Copy: performCopy(item.copy, sid); break;
@@ -1377,6 +1397,7 @@ void HostMachine::completeGrids(uint64_t sweep) {
   for (auto& [gid, g] : grids_) {
     if (g.completed || g.endSweep != sweep) continue;
     g.completed = true;
+    --runningGrids_;
     auto s = streams_.find(g.stream);
     if (s != streams_.end() && s->second.running && s->second.runningGid == gid) s->second.running = false;
   }
@@ -1467,11 +1488,25 @@ mck::RunResult HostMachine::run() {
   while (engineError_.empty()) {
     bool hostRun = hostRunnable();
     bool anyDispatch = false;
-    for (const auto& s : streams_)
-      if (dispatchable(s.second)) anyDispatch = true;
+    if (queued_)
+      for (const auto& s : streams_)
+        if (dispatchable(s.second)) anyDispatch = true;
     uint64_t nextEnd = NEVER;
-    for (const auto& g : grids_)
-      if (!g.second.completed && g.second.endSweep != NEVER) nextEnd = std::min(nextEnd, g.second.endSweep);
+    if (runningGrids_)
+      for (const auto& g : grids_)
+        if (!g.second.completed && g.second.endSweep != NEVER) nextEnd = std::min(nextEnd, g.second.endSweep);
+    if (hostRun && !anyDispatch && nextEnd == NEVER && !awaiting_) {
+      // fast path: only the host thread can move (one step per sweep)
+      if (steps_ >= o_.stepLimit) {
+        hitLimit = true;
+        break;
+      }
+      hostStep();
+      ++steps_;
+      ++stats_.hostSteps;
+      ++sweep_;
+      continue;
+    }
     if (!hostRun && !anyDispatch) {
       if (nextEnd == NEVER) break;  // quiescent
       sweep_ = std::max(sweep_, nextEnd);
@@ -1487,10 +1522,11 @@ mck::RunResult HostMachine::run() {
       ++steps_;
       ++stats_.hostSteps;
     }
-    completeGrids(sweep_);
-    std::vector<uint32_t> sids;
-    for (const auto& s : streams_) sids.push_back(s.first);
-    for (uint32_t sid : sids) {
+    if (runningGrids_) completeGrids(sweep_);
+    sids_.clear();
+    if (queued_)
+      for (const auto& s : streams_) sids_.push_back(s.first);
+    for (uint32_t sid : sids_) {
       auto it = streams_.find(sid);
       if (it == streams_.end() || !dispatchable(it->second)) continue;
       if (steps_ >= o_.stepLimit) {

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 import oracle_bind as ob  # noqa: E402
-from program_corpus import corpus, project  # noqa: E402
+from program_corpus import corpus, host_corpus, project, HOST_STEP_LIMIT, FRONTEND_CASES  # noqa: E402
 
 
 def main():
@@ -22,6 +22,18 @@ def main():
     with open(path, "w") as f:
         json.dump(gold, f, separators=(",", ":"), sort_keys=True)
     print(f"wrote {len(gold)} golden runs to {path}")
+    host = {}
+    for name, fname, src in host_corpus():
+        r = ob.ref_run(src, filename=fname, policy="rr", capture=False, step_limit=HOST_STEP_LIMIT)
+        host[name] = project(r)
+    for name, src in FRONTEND_CASES.items():
+        r = ob.ref_run(src, filename=name + ".cu", policy="rr", capture=False)
+        host["fe_" + name] = {"frontend_error": r.get("frontend_error"), "line": r.get("line"),
+                              "exit": r.get("exit")}
+    path = os.path.join(HERE, "golden", "host_programs.json")
+    with open(path, "w") as f:
+        json.dump(host, f, separators=(",", ":"), sort_keys=True)
+    print(f"wrote {len(host)} golden host runs to {path}")
 
 
 if __name__ == "__main__":

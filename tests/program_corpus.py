@@ -31,3 +31,34 @@ KEYS = ("exit", "output", "steps", "diags", "stuck_reports", "report_text", "rep
 def project(run):
     """The fields compared for parity (RunResult + RaceState::reported)."""
     return {k: run.get(k) for k in KEYS}
+
+
+HOST_STEP_LIMIT = 200_000
+
+
+def host_corpus():
+    """Host-only programs: the IR and value semantics without a GPU."""
+    import gen_host_programs as gh
+    out = [(f"host{i}", f"h{i}.cu", gh.host_program(i)) for i in range(400)]
+    out += [(name, name + ".cu", src) for name, src in sorted(gh.HANDWRITTEN.items())]
+    return out
+
+
+FRONTEND_CASES = {
+    "no_main": "int f(void) { return 0; }\n",
+    "bad_token": "int main(void) { int x = 3 @ 4; return 0; }\n",
+    "undeclared": "int main(void) { return y; }\n",
+    "static_shared": "__global__ void k(void) { __shared__ int s[4]; }\nint main(void) { return 0; }\n",
+    "printf_device": "__global__ void k(void) { printf(\"x\"); }\nint main(void) { return 0; }\n",
+    "kernel_call": "__global__ void k(void) { }\nint main(void) { k(); return 0; }\n",
+    "sync_host": "int main(void) { __syncthreads(); return 0; }\n",
+    "break_outside": "int main(void) { break; return 0; }\n",
+    "macro_fn": "#define F(x) x\nint main(void) { return 0; }\n",
+    "array_init": "int main(void) { int a[3] = 1; return 0; }\n",
+    "multi_dim": "int main(void) { int a[3][3]; return 0; }\n",
+    "void_var": "int main(void) { void x; return 0; }\n",
+    "kernel_ret": "__global__ int k(void) { return 1; }\nint main(void) { return 0; }\n",
+    "redecl": "int main(void) { int x; int x; return 0; }\n",
+    "unknown_api": "int main(void) { cudaFooBar(); return 0; }\n",
+    "threadidx_host": "int main(void) { return threadIdx.x; }\n",
+}

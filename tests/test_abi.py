@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "mckg.h")).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(mckg_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|const char\*)\s+(mckg?_\w+)\(", src, re.M)))
 
 
 def test_header_declares_the_exports():
