@@ -100,6 +100,9 @@ struct EngineStats {
   uint64_t sweeps = 0;           // global round-robin sweeps
   double gridMs = 0;             // device time of the grid kernels (CUDA events)
   uint32_t kernelLaunches = 0;   // sm_100a kernels launched
+  uint64_t blockSweeps = 0;      // K1: sweeps executed, summed over blocks
+  uint64_t soloSweeps = 0;       // K1: of which in single-warp mode
+  uint64_t blockCycles = 0, soloCycles = 0;  // K1: SM cycles per block, summed
 };
 
 struct RaceTriple {

@@ -97,6 +97,7 @@ struct DevDiagRec {
 };
 
 struct BlockOut {
+  unsigned long long sweeps, soloSweeps, cycles, soloCycles;
   unsigned long long steps;
   unsigned long long rules;
   unsigned long long allocs;
@@ -171,6 +172,8 @@ struct BlockShared {
   unsigned long long allocs;
   unsigned long long sharedEvents;
   uint32_t lastSweep;
+  uint32_t busy[2];    // warps holding READY threads, by sweep parity
+  uint32_t soloSweep;  // sweep reached by a solo warp
 };
 
 __device__ __forceinline__ void set_error(const KP& P, int code, int info) {
@@ -683,7 +686,7 @@ __device__ int mem_write(TS& t, const KP& P, Ctx& c, Thread& th, uint32_t obj, i
 }
 
 // Performs a pending shared/global request (memory phase).
-__device__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq, const SmemLay& L, uint32_t stamp,
+__device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq, const SmemLay& L, uint32_t stamp,
                            uint32_t bstamp, unsigned long long& sharedEvents) {
   int len = (int)t_scalar(rq.ty);
   uint8_t *b, *m;
@@ -748,7 +751,7 @@ __device__ void finish_request(TS& t, const KP& P, Thread& th, const Req& rq, co
 
 // One small step of thread `t`.  Returns 1 when a shared/global request is
 // pending (rq/pd filled), else 0.
-__device__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req& rq, Pend& pd, BlockShared& bs, uint32_t nthreads) {
+__device__ __noinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req& rq, Pend& pd, BlockShared& bs, uint32_t nthreads) {
   const mck_ins* code = P.code;
   mck_ins in = code[t.pc];
   while (in.op == OP_JMP) {
@@ -1050,6 +1053,59 @@ __device__ __forceinline__ int ht_insert(unsigned long long* keys, uint32_t* val
   return -1;
 }
 
+
+// Runs sweeps for one warp while every other thread of the block is waiting
+// at a barrier or finished (the caller checked it).  Returns after the sweep
+// in which a lane arrives at a barrier, or when no lane is READY any more.
+__device__ void solo_sweeps(TS& t, const KP& P, Ctx& c, Thread& th, BlockShared& bs, const SmemLay& L,
+                            uint32_t E, uint32_t& sweep, uint32_t& lastStep,
+                            unsigned long long& sharedEvents, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  const bool active = threadIdx.x < n;
+  while (true) {
+    if (!__any_sync(0xFFFFFFFFu, active && th.state == S_READY)) return;
+    ++sweep;
+    if (sweep >= P.maxSweeps) {
+      set_error(P, ERR_SWEEPS, 0);
+      return;
+    }
+    c.sweep = sweep;
+    c.sub = 0;
+    Req rq;
+    Pend pd;
+    rq.kind = 0;
+    int pending = 0;
+    const bool run = active && th.state == S_READY && sweep >= th.readyAt;
+    if (run) {
+      lastStep = sweep;
+      pending = step(t, P, c, th, rq, pd, bs, n);
+      if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+    }
+    const uint32_t req = __ballot_sync(0xFFFFFFFFu, pending);
+    const uint32_t wreq = __ballot_sync(0xFFFFFFFFu, pending && rq.kind == 2);
+    if (req) {
+      if ((req & (req - 1)) == 0 || wreq == 0) {
+        // one request, or reads only: no order dependence
+        if (pending) {
+          do_request(P, c, th, rq, L, E & 0xFF, c.bid, sharedEvents);
+          finish_request(t, P, th, rq, pd);
+          if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+        }
+      } else {
+        for (uint32_t l = 0; l < 32; ++l) {
+          if (lane == l && pending) {
+            do_request(P, c, th, rq, L, E & 0xFF, c.bid, sharedEvents);
+            finish_request(t, P, th, rq, pd);
+            if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+          }
+          __syncwarp();
+        }
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, active && th.state == S_WAIT && run)) return;
+  }
+}
+
 // ================= the kernel =================
 __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
   const uint32_t bid = blockIdx.x;
@@ -1088,6 +1144,8 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
     bs.allocs = 0;
     bs.sharedEvents = 0;
     bs.lastSweep = 0;
+    bs.busy[0] = bs.busy[1] = 0xFFFFFFFFu;
+    bs.soloSweep = 0;
   }
 
   TS t;
@@ -1137,23 +1195,39 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
   __syncthreads();
 
   uint32_t E = 0;           // completed episodes (uniform)
+  // barrier counters are cumulative per episode parity: episode j (parity
+  // j & 1) completes when wait[j & 1] reaches need[j & 1]
+  int need[2] = {(int)n, (int)n};
+  int nzPrev[2] = {0, 0}, allcPrev[2] = {0, 0};
   unsigned long long rules = 0;
   uint32_t sweep = 0;
   bool deadlocked = false;
   unsigned long long sharedEvents = 0;
   uint32_t lastStep = 0;
   const uint32_t Lt = n - 1;
+  unsigned long long* hk = (unsigned long long*)(smem + L.htKey);
+  uint32_t* hv = (uint32_t*)(smem + L.htVal);
+  const uint32_t hmask = (1u << P.htBits) - 1;
+  bool justSolo = true;  // the busy mask is valid only after a full sweep
+  unsigned long long soloSweeps = 0;
+  long long soloCycles = 0;
+  const long long kStart = clock64();
 
   while (true) {
-    // ---- barrier protocol in closed form (Appendix A) ----
+    // ---- barrier protocol in closed form (Appendix A); counters cover
+    // every step up to and including `sweep` ----
     const int p = (E + 1) & 1;
-    const int nwait = bs.wait[p];
+    const int arrived = bs.wait[p] - (need[p] - (int)n);
     const int nfin = bs.fin;
-    if (nwait == (int)n) {
-      // episode E+1 completed in sweep `sweep` (the last arrival's sweep):
-      // up-sweep + Turnaround (epoch clear) + Down(L) now, one Down per sweep
+    if (arrived == (int)n) {
+      // episode E+1 completed in sweep T = `sweep` (the last arrival): the
+      // up-sweep chain, Turnaround (epoch clear) and Down(L) fire in T, one
+      // Down per sweep after that, FinalRelease(0) in T + L
       const uint32_t T = sweep;
-      const int nz = bs.nz[p], allc = bs.allc[p];
+      const int nz = bs.nz[p] - nzPrev[p], allc = bs.allc[p] - allcPrev[p];
+      nzPrev[p] += nz;
+      allcPrev[p] += allc;
+      need[p] += (int)n;  // the next episode of this parity is E + 3
       if (active) {
         th.state = S_READY;
         th.readyAt = tid == 0 ? T + Lt + 1 : T + (Lt - tid) + 1;
@@ -1172,20 +1246,37 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
       if (P.raceCheck && (E & 0xFF) == 0) {  // stamp wrap: clear the shadow
         uint32_t* sh = (uint32_t*)(smem + L.shadow);
         for (uint32_t i = tid; i < (uint32_t)P.shmem; i += blockDim.x) sh[i] = shadow_empty(0);
+        __syncthreads();
       }
     } else if (nfin == (int)blockDim.x) {
       break;  // every thread finished
-    } else if (nwait + nfin == (int)blockDim.x) {
-      // quiescent with waiters: barrier deadlock (deadlock.cpp:15-34).  The
-      // up-sweep advanced from tid 0 through the waiting prefix.
+    } else if (arrived + nfin == (int)blockDim.x) {
+      // quiescent with waiters: barrier deadlock (deadlock.cpp:15-34)
       deadlocked = true;
       break;
     }
-    __syncthreads();  // everyone has read the counters
-    if (tid == 0 && nwait == (int)n) {
-      bs.wait[p] = 0;
-      bs.nz[p] = 0;
-      bs.allc[p] = 0;
+    // ---- solo mode: when a single warp holds every READY thread, no other
+    // thread can move until that warp arrives at a barrier or finishes, so it
+    // runs sweeps alone with warp-level synchronisation ----
+    {
+      const uint32_t busy = justSolo ? 0xFFFFFFFFu : bs.busy[sweep & 1];
+      justSolo = false;
+      if (busy && (busy & (busy - 1)) == 0) {
+        const uint32_t sw = (uint32_t)__ffs(busy) - 1;
+        const uint32_t s0 = sweep;
+        const long long c0 = clock64();
+        if ((tid >> 5) == sw) {
+          solo_sweeps(t, P, c, th, bs, L, E, sweep, lastStep, sharedEvents, n);
+          if ((tid & 31) == 0) bs.soloSweep = sweep;
+        }
+        __syncthreads();
+        soloCycles += clock64() - c0;
+        soloSweeps += bs.soloSweep - s0;
+        sweep = bs.soloSweep;
+        justSolo = true;
+        if (sweep >= P.maxSweeps) break;
+        continue;
+      }
     }
     ++sweep;
     if (sweep >= P.maxSweeps) {
@@ -1194,75 +1285,79 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
     }
     c.sweep = sweep;
     c.sub = 0;
-    // ---- phase 1: one step per runnable thread ----
+    // ---- phase 1: one step per runnable thread; shared/global requests
+    // are registered in the conflict hash (word granularity) ----
     Req rq;
     Pend pd;
     rq.kind = 0;
     int pending = 0;
+    bool conflict = false;
+    int slots[3] = {-1, -1, -1};
+    int ns = 0;
     const bool run = active && th.state == S_READY && sweep >= th.readyAt;
     if (run) {
+      lastStep = sweep;
       pending = step(t, P, c, th, rq, pd, bs, n);
       if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+      if (pending) {
+        const int len = (int)t_scalar(rq.ty);
+        const unsigned long long addr = rq.space == R_OK_SHARED
+                                            ? (unsigned long long)rq.off
+                                            : (1ull << 40) | (rq.base + (unsigned long long)rq.off);
+        const bool wr = rq.kind == 2;
+        for (unsigned long long w = addr >> 2; w <= (addr + len - 1) >> 2 && ns < 3; ++w) {
+          const unsigned long long key = w + 1;
+          uint32_t h = (uint32_t)mix64(key) & hmask;
+          int slot = -1;
+          for (uint32_t probe = 0; probe <= hmask; ++probe) {
+            unsigned long long old = atomicCAS(hk + h, 0ull, key);
+            if (old == 0ull || old == key) {
+              slot = (int)h;
+              break;
+            }
+            h = (h + 1) & hmask;
+          }
+          if (slot < 0) {
+            conflict = true;  // table full: replay in order (always correct)
+            continue;
+          }
+          const uint32_t old = atomicAdd(hv + slot, wr ? 0x10001u : 1u);
+          // overlap with a write: some earlier inserter, and one side writes
+          if ((old & 0xFFFF) != 0 && (wr || (old >> 16) != 0)) conflict = true;
+          slots[ns++] = slot;
+        }
+      }
     }
-    const int nreq = __syncthreads_count(pending);
-    if (run && sweep > lastStep) lastStep = sweep;
-    if (nreq > 0) {
-      bool conflict = false;
-      if (nreq > 1) {
-        // word-level overlap with a write among this sweep's requests
-        unsigned long long* hk = (unsigned long long*)(smem + L.htKey);
-        uint32_t* hv = (uint32_t*)(smem + L.htVal);
-        int slots[3] = {-1, -1, -1};
-        int ns = 0;
-        if (pending) {
-          const int len = (int)t_scalar(rq.ty);
-          const unsigned long long addr = rq.space == R_OK_SHARED
-                                              ? (unsigned long long)rq.off
-                                              : (1ull << 40) | (rq.base + (unsigned long long)rq.off);
-          const uint32_t add = rq.kind == 2 ? 0x10001u : 1u;
-          for (unsigned long long w = addr >> 2; w <= (addr + len - 1) >> 2 && ns < 3; ++w) {
-            int h = ht_insert(hk, hv, P.htBits, w + 1, add);
-            if (h < 0) conflict = true;
-            slots[ns++] = h;
+    if (__any_sync(0xFFFFFFFFu, active && th.state == S_READY) && (tid & 31) == 0)
+      atomicOr(&bs.busy[sweep & 1], 1u << (tid >> 5));
+    conflict = __syncthreads_or(conflict);
+    if (tid == 0) bs.busy[(sweep + 1) & 1] = 0;
+    if (!conflict) {
+      if (pending) {
+        do_request(P, c, th, rq, L, E & 0xFF, bid, sharedEvents);
+        finish_request(t, P, th, rq, pd);
+        if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+      }
+    } else {
+      // replay the memory phase in tid order (round-robin order)
+      const uint32_t warp = tid >> 5, lane = tid & 31;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+        if (warp == w) {
+          for (uint32_t l = 0; l < 32; ++l) {
+            if (lane == l && pending) {
+              do_request(P, c, th, rq, L, E & 0xFF, bid, sharedEvents);
+              finish_request(t, P, th, rq, pd);
+              if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+            }
+            __syncwarp();
           }
         }
         __syncthreads();
-        for (int i = 0; i < ns; ++i)
-          if (slots[i] >= 0) {
-            uint32_t v = hv[slots[i]];
-            if ((v >> 16) >= 1 && (v & 0xFFFF) >= 2) conflict = true;
-          }
-        conflict = __syncthreads_or(conflict);
-        for (int i = 0; i < ns; ++i)
-          if (slots[i] >= 0) {
-            hk[slots[i]] = 0ull;
-            hv[slots[i]] = 0u;
-          }
       }
-      const uint32_t stamp = E & 0xFF;
-      if (!conflict) {
-        if (pending) {
-          do_request(P, c, th, rq, L, stamp, bid, sharedEvents);
-          finish_request(t, P, th, rq, pd);
-          if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
-        }
-      } else {
-        // replay the memory phase in tid order (round-robin order)
-        const uint32_t warp = tid >> 5, lane = tid & 31;
-        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
-          if (warp == w) {
-            for (uint32_t l = 0; l < 32; ++l) {
-              if (lane == l && pending) {
-                do_request(P, c, th, rq, L, stamp, bid, sharedEvents);
-                finish_request(t, P, th, rq, pd);
-                if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
-              }
-              __syncwarp();
-            }
-          }
-          __syncthreads();
-        }
-      }
+    }
+    for (int i = 0; i < ns; ++i) {
+      hk[slots[i]] = 0ull;
+      hv[slots[i]] = 0u;
     }
     __syncthreads();
   }
@@ -1293,6 +1388,10 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
   }
   if (tid == 0) {
     BlockOut& o = P.blocks[bid];
+    o.sweeps = sweep;
+    o.soloSweeps = soloSweeps;
+    o.cycles = (unsigned long long)(clock64() - kStart);
+    o.soloCycles = (unsigned long long)soloCycles;
     o.steps = bs.steps;
     o.rules = rules;
     o.allocs = bs.allocs;
@@ -1552,6 +1651,10 @@ class CudaEngine final : public DeviceEngine {
     std::vector<uint32_t> wm;
     bool anyDl = false;
     for (const auto& b : bo) {
+      out.sweeps += b.sweeps;
+      out.soloSweeps += b.soloSweeps;
+      out.blockCycles += b.cycles;
+      out.soloCycles += b.soloCycles;
       out.deviceSteps += b.steps;
       out.barrierRules += b.rules;
       out.allocs += b.allocs;

@@ -79,7 +79,9 @@ extern "C" int mck_run_source(const char* src, const char* filename, const mck_r
          ",\"dispatches\":" + std::to_string(st.dispatches) + ",\"shared_events\":" +
          std::to_string(st.sharedEvents) + ",\"grids\":" + std::to_string(st.grids) + ",\"sweeps\":" +
          std::to_string(st.sweeps) + ",\"grid_ms\":" + std::to_string(st.gridMs) + ",\"kernel_launches\":" +
-         std::to_string(st.kernelLaunches) + "}}";
+         std::to_string(st.kernelLaunches) + ",\"block_sweeps\":" + std::to_string(st.blockSweeps) +
+         ",\"solo_sweeps\":" + std::to_string(st.soloSweeps) + ",\"block_cycles\":" +
+         std::to_string(st.blockCycles) + ",\"solo_cycles\":" + std::to_string(st.soloCycles) + "}}";
   } catch (const mck::FrontendError& e) {
     o = "{\"frontend_error\":" + js(e.stage + ": " + e.message) + ",\"line\":" + std::to_string(e.loc.line) +
         ",\"exit\":2}";

@@ -63,6 +63,8 @@ struct GridResult {
   uint64_t barrierRules = 0;
   uint64_t allocs = 0;          // device-side object allocations (locals + call params)
   uint64_t sharedEvents = 0;
+  uint64_t sweeps = 0, soloSweeps = 0;  // block-sweeps executed (diagnostics)
+  uint64_t blockCycles = 0, soloCycles = 0;
   uint32_t duration = 0;        // local sweep of the last device step (complete grids)
   bool deadlocked = false;
   struct Stuck {

@@ -1352,6 +1352,10 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   stats_.gridMs += rec.res.ms;
   stats_.kernelLaunches += rec.res.launches;
   stats_.sharedEvents += rec.res.sharedEvents;
+  stats_.blockSweeps += rec.res.sweeps;
+  stats_.soloSweeps += rec.res.soloSweeps;
+  stats_.blockCycles += rec.res.blockCycles;
+  stats_.soloCycles += rec.res.soloCycles;
   // device diagnostics, timestamped by (global sweep, gid, bid, tid, sub)
   for (const DevDiag& r : rec.res.diags) {
     uint64_t lsweep = r.key >> 38;
