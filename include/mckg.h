@@ -221,6 +221,82 @@ int mckg_scan_stuck(const uint32_t* arrivals, uint32_t n_blocks, uint32_t block_
 int mckg_gen_c3(mckg_access* events, uint64_t* block_start, uint32_t blk0, uint32_t n_blocks,
                 uint64_t seed, void* stream);
 
+/* ---- cross-block global-memory races (BASELINE config 5) ----
+ *
+ * NOT a reference interface: the reference checks DeviceShared objects only
+ * (memory.cpp:142-143, 240-241).  The extension applies the racecheck.cpp:24-32
+ * rule to global memory with "thread" replaced by "block": within one grid
+ * (the kernel-end barrier separates grids) an access X to byte b races iff an
+ * EARLIER access to b, in (sweep, bid, tid) order, came from another BLOCK and
+ * X or it writes.  Reported once per (byte, line); the "Possible race on
+ * global device memory detected at <file>:<line>." diagnostic of a line sits
+ * at its first racing access.  Parity is unpinned (no reference semantics);
+ * the checker is oracle/global_detector.c.
+ *
+ *   a     = addr:40 | len:4 | write:1 | tid:11 | line & 0xFF
+ *   sweep = round-robin sweep of the access
+ *   b     = bid:24 | line >> 8
+ */
+typedef struct mckg_gaccess {
+  uint64_t a;
+  uint32_t sweep;
+  uint32_t b;
+} mckg_gaccess;
+
+#define MCKG_GA_ADDR(r) ((r).a & 0xFFFFFFFFFFull)
+#define MCKG_GA_LEN(r) ((uint32_t)(((r).a >> 40) & 0xFu))
+#define MCKG_GA_WRITE(r) ((uint32_t)(((r).a >> 44) & 1u))
+#define MCKG_GA_TID(r) ((uint32_t)(((r).a >> 45) & 0x7FFu))
+#define MCKG_GA_LINE(r) ((int32_t)((((r).b >> 24) << 8) | (uint32_t)(((r).a >> 56) & 0xFFu)))
+#define MCKG_GA_BID(r) ((r).b & 0xFFFFFFu)
+
+static inline mckg_gaccess mckg_make_gaccess(uint64_t addr, uint32_t len, int write, uint32_t tid,
+                                             uint32_t bid, int32_t line, uint32_t sweep) {
+  mckg_gaccess g;
+  g.a = (addr & 0xFFFFFFFFFFull) | ((uint64_t)(len & 0xFu) << 40) | ((uint64_t)(write ? 1 : 0) << 44) |
+        ((uint64_t)(tid & 0x7FFu) << 45) | ((uint64_t)((uint32_t)line & 0xFFu) << 56);
+  g.sweep = sweep;
+  g.b = (bid & 0xFFFFFFu) | ((((uint32_t)line >> 8) & 0xFFu) << 24);
+  return g;
+}
+
+/* Timestamp key of a global access: sweep:32 | bid:22 | tid:10 (as mckg_ts_key). */
+
+/* One reported (byte address, line) pair. */
+typedef struct mckg_grace {
+  uint64_t addr;
+  int32_t line;
+  int32_t pad;
+} mckg_grace;
+
+/* Synthetic BASELINE config-5 records of blocks [blk0, blk0 + n_blocks) of an
+ * n_total-block grid: MCKG_C5_EVENTS_PER_BLOCK 4-byte accesses per block at
+ * 8-byte-aligned addresses of the block's own 64 KiB range (slot tid*16 + k);
+ * 1% go to the same slot of block (b + 1) % n_total; write with p = 1/2; line
+ * 200 + k % 4; sweep = k.  Identical to oracle_gen_c5. */
+int mckg_gen_c5(mckg_gaccess* events, uint32_t blk0, uint32_t n_blocks, uint32_t n_total, uint64_t seed,
+                void* stream);
+
+/* Stable partition of n records by owner rank (owner = addr * n_ranks / addr_space,
+ * address-range partition): out[] holds the records grouped by rank, counts[r]
+ * (device, n_ranks entries) the group sizes. */
+int mckg_partition_global(const mckg_gaccess* events, uint64_t n, uint32_t n_ranks, uint64_t addr_space,
+                          mckg_gaccess* out, uint64_t* counts, void* stream);
+
+/* Detects cross-block races among n records whose addresses lie in
+ * [addr_lo, addr_lo + 2^35).  Outputs (device, caller-owned): races[capacity]
+ * (unordered, unique per (byte, line)), *n_races (device counter; reset by the
+ * call), line_first[MCKG_MAX_LINES] (min timestamp key per line; reset by the
+ * caller with mckg_race_out_reset semantics), *status.  Scratch is allocated
+ * on `stream`. */
+int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64_t addr_lo, mckg_grace* races,
+                       uint64_t capacity, unsigned long long* n_races, unsigned long long* line_first,
+                       uint32_t* status, void* stream);
+
+#define MCKG_C5_EVENTS_PER_BLOCK 4096u
+#define MCKG_C5_RANGE 65536u
+#define MCKG_C5_SEED 0x12116193ull
+
 /* ---- whole-program checking (host + B200 grid engine) ---- */
 typedef struct mck_run_opts {
   uint64_t step_limit;        /* 0 = reference default 50,000,000 (machine.hpp:313) */

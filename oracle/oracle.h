@@ -35,6 +35,12 @@ int oracle_scan_stuck(const uint32_t* arrivals, uint32_t n_blocks, uint32_t bloc
 void oracle_gen_c3(mckg_access* events, uint64_t* block_start, uint32_t blk0, uint32_t n_blocks,
                    uint64_t seed);
 
+/* Cross-block global races (parity unpinned): see
+ * oracle/global_detector.c.  races sorted by (addr, line). */
+int oracle_detect_global(const mckg_gaccess* ev, uint64_t n, mckg_grace* races, uint64_t capacity,
+                         uint64_t* n_races, uint64_t* line_first);
+void oracle_gen_c5(mckg_gaccess* ev, uint32_t blk0, uint32_t n_blocks, uint32_t n_total, uint64_t seed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,8 @@ TS_NONE = 0xFFFFFFFFFFFFFFFF
 C3_EVENTS_PER_BLOCK = 1024
 C3_SHMEM = 4096
 C3_SEED = 0x12116193
+C5_EVENTS_PER_BLOCK = 4096
+C5_RANGE = 65536
 
 STATUS_OVERFLOW = 1
 STATUS_RANGE = 2
@@ -38,6 +40,9 @@ EXPORTS = [
     "mckg_sort_triples",
     "mckg_scan_stuck",
     "mckg_gen_c3",
+    "mckg_gen_c5",
+    "mckg_partition_global",
+    "mckg_detect_global",
     "mck_run_source",
     "mck_disassemble",
     "mck_free",
@@ -104,6 +109,9 @@ def load():
     lib.mckg_sort_triples.argtypes = [vp, u64, u32, vp, vp]
     lib.mckg_scan_stuck.argtypes = [vp, u32, u32, u32, vp, vp, vp, vp]
     lib.mckg_gen_c3.argtypes = [vp, vp, u32, u32, u64, vp]
+    lib.mckg_gen_c5.argtypes = [vp, u32, u32, u32, u64, vp]
+    lib.mckg_partition_global.argtypes = [vp, u64, u32, u64, vp, vp, vp]
+    lib.mckg_detect_global.argtypes = [vp, u64, u64, vp, u64, vp, vp, vp, vp]
     _lib = lib
     return lib
 

@@ -73,6 +73,11 @@ def port():
                                             ctypes.POINTER(ctypes.c_uint32)]
         _port.oracle_gen_c3.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
                                         ctypes.c_uint32, ctypes.c_uint64]
+        _port.oracle_gen_c5.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32,
+                                        ctypes.c_uint32, ctypes.c_uint64]
+        _port.oracle_detect_global.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                               ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64),
+                                               ctypes.c_void_p]
     return _port
 
 
@@ -97,6 +102,35 @@ def gen_c3(blk0, n_blocks, seed=C3_SEED):
     bs = np.zeros(n_blocks + 1, dtype=np.uint64)
     port().oracle_gen_c3(ev.ctypes.data, bs.ctypes.data, blk0, n_blocks, seed)
     return ev, bs
+
+
+GACCESS_DTYPE = np.dtype([("a", "<u8"), ("sweep", "<u4"), ("b", "<u4")])
+GRACE_DTYPE = np.dtype([("addr", "<u8"), ("line", "<i4"), ("pad", "<i4")])
+C5_EVENTS_PER_BLOCK = 4096
+
+
+def make_gaccess(addr, length, write, tid, bid, line, sweep):
+    a = ((addr & 0xFFFFFFFFFF) | ((length & 0xF) << 40) | ((1 if write else 0) << 44)
+         | ((tid & 0x7FF) << 45) | ((line & 0xFF) << 56))
+    return (a, sweep, (bid & 0xFFFFFF) | (((line >> 8) & 0xFF) << 24))
+
+
+def gen_c5(blk0, n_blocks, n_total, seed=C3_SEED):
+    ev = np.zeros(n_blocks * C5_EVENTS_PER_BLOCK, dtype=GACCESS_DTYPE)
+    port().oracle_gen_c5(ev.ctypes.data, blk0, n_blocks, n_total, seed)
+    return ev
+
+
+def port_detect_global(ev, capacity=None):
+    ev = np.ascontiguousarray(ev, dtype=GACCESS_DTYPE)
+    if capacity is None:
+        capacity = 4 * len(ev) + 16
+    races = np.zeros(capacity, dtype=GRACE_DTYPE)
+    n = ctypes.c_uint64(0)
+    lf = np.full(MAX_LINES, TS_NONE, dtype=np.uint64)
+    rc = port().oracle_detect_global(ev.ctypes.data, len(ev), races.ctypes.data, capacity, ctypes.byref(n),
+                                     lf.ctypes.data)
+    return rc, races[: min(n.value, capacity)], n.value, lf
 
 
 def make_trace(events, block_start, shmem_bytes, obj_base=1, bid_base=0, gid=1):

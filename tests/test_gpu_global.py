@@ -1,0 +1,93 @@
+"""K3/K6 (global-race extension, BASELINE config 5) against the CPU checker
+oracle/global_detector.c: identical (byte, line) race sets and per-line
+first-detection keys; parity with the reference itself is unpinned (the
+reference has no global-race semantics)."""
+import numpy as np
+import pytest
+
+import oracle_bind as ob
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(ev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(ev).view(np.int32).reshape(-1, 4).copy()).cuda()
+
+
+def _detect(ev, addr_lo=0, capacity=None):
+    from paper_1211_6193_b200 import global_race as gr
+    t = _dev(ev)
+    out = gr.GlobalOut(capacity if capacity is not None else 4 * len(ev) + 16)
+    gr.detect(t, addr_lo, out.reset())
+    races, n, lf, st = gr.fetch(out)
+    order = np.lexsort((races["line"], races["addr"]))
+    return races[order], n, lf, st
+
+
+def _check(ev):
+    races, n, lf, st = _detect(ev)
+    rc, want, wn, wlf = ob.port_detect_global(ev)
+    assert rc == 0 and st == 0
+    assert n == wn
+    assert np.array_equal(races["addr"], want["addr"]) and np.array_equal(races["line"], want["line"])
+    assert np.array_equal(lf, wlf)
+    return n
+
+
+def test_gen_c5_matches_cpu_copy():
+    from paper_1211_6193_b200 import global_race as gr
+    ev = gr.gen_c5(3, 5, 40).cpu().numpy().view(ob.GACCESS_DTYPE).reshape(-1)
+    assert np.array_equal(ev, ob.gen_c5(3, 5, 40))
+
+
+def test_c5_sample():
+    n = _check(ob.gen_c5(0, 64, 64))
+    assert n > 0
+
+
+def _random(seed, n=20000, nblocks=12, span=4096):
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        length = int(rng.choice([1, 2, 4, 8]))
+        addr = int(rng.integers(0, span)) if rng.random() < 0.7 else int(rng.integers(0, 64))
+        rows.append(ob.make_gaccess(addr, length, rng.random() < 0.4, int(rng.integers(0, 64)),
+                                    int(rng.integers(0, nblocks)), int(rng.integers(10, 40)),
+                                    int(rng.integers(0, 500))))
+    return np.array(rows, dtype=ob.GACCESS_DTYPE)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_global_traces(seed):
+    _check(_random(seed))
+
+
+def test_two_owner_emulation_on_one_gpu():
+    """The multi-GPU split: partition by owner, detect each part with its
+    address base, union == single detection."""
+    import torch
+    from paper_1211_6193_b200 import global_race as gr
+    ev = ob.gen_c5(0, 32, 32)
+    space = 32 * 65536
+    grouped, counts = gr.partition(_dev(ev), 2, space)
+    torch.cuda.synchronize()
+    c = counts.cpu().tolist()
+    assert sum(c) == len(ev)
+    allr, lfs = [], []
+    off = 0
+    for r in range(2):
+        part = grouped[off:off + c[r]]
+        off += c[r]
+        lo, hi = gr.addr_range(r, 2, space)
+        out = gr.GlobalOut(4 * len(ev))
+        gr.detect(part, lo, out.reset())
+        races, n, lf, st = gr.fetch(out)
+        assert st == 0
+        a = races["addr"]
+        assert np.all((a >= lo) & (a < hi))
+        allr += list(zip(a.tolist(), races["line"].tolist()))
+        lfs.append(lf)
+    rc, want, wn, wlf = ob.port_detect_global(ev)
+    assert sorted(allr) == sorted(zip(want["addr"].tolist(), want["line"].tolist()))
+    assert np.array_equal(np.minimum(lfs[0], lfs[1]), wlf)
