@@ -259,6 +259,11 @@ def run_ours(args):
     k1 = None
     if rank == 0 and ws == 1 and not args.no_k1:
         k1 = run_k1(args)
+    c5 = None
+    if not args.no_c5:
+        ev = bs = tr = out = None  # free the C3 trace before C5
+        torch.cuda.empty_cache()
+        c5 = run_c5(args, args.c5_blocks if args.c5_blocks else (1 << 16) * ws, dev, ws, rank)
     e2e = None
     if rank == 0 and ws == 1 and args.e2e_blocks > 0:
         e2e = run_e2e(args, torch, race, _abi)
@@ -286,10 +291,65 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "k1": k1,
+            "c5": c5,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def run_c5(args, blocks, dev, ws, rank):
+    """C5 (configs[4]): cross-block global races over `blocks` simulated blocks
+    sharded over the ranks: K3 partition -> NCCL all-to-all -> K6 detect ->
+    MIN-all-reduce of the line table.  Device-timed (CUDA events), max over
+    ranks.  Returns the c5 object of the JSON line (rank 0)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1211_6193_b200 import global_race as gr
+    space = blocks * 65536
+    b0, b1 = gr.shard(blocks, rank, ws)
+    ev = gr.gen_c5(b0, b1 - b0, blocks, device=dev)
+    lo, _ = gr.addr_range(rank, ws, space)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        grouped, counts = gr.partition(ev, ws, space, stream)
+        mine = gr.exchange(grouped, counts) if ws > 1 else grouped
+        out = gr.GlobalOut(max(1, mine.shape[0] // 8), device=dev)
+        gr.detect(mine, lo, out.reset(), stream)
+        if ws > 1:
+            gr.min_allreduce_u64(out.line_first)
+        return out, mine.shape[0]
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 5))
+    t0.record(stream)
+    for _ in range(steps):
+        out, recv = step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    n_races = int(out.n.item())
+    status = int(out.status.item())
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([ev.shape[0], n_races, recv], dtype=torch.int64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms = float(t[0])
+    events = int(tot[0])
+    sent = ev.shape[0] * 16 * (ws - 1) / max(1, ws)  # bytes leaving this rank (uniform partition)
+    return {"workload": f"C5: {events} global 4-byte accesses, {blocks} blocks, 1% cross-block, "
+                        f"address-range all-to-all over {ws} GPU(s)",
+            "events_per_s": events / (ms / 1e3), "ms_per_step": ms, "races_reported": int(tot[1]),
+            "status": status, "nvlink_bytes_per_rank": sent,
+            "nvlink_GBps_per_rank": sent / (ms / 1e3) / 1e9 if ws > 1 else None,
+            "parity": "unpinned (no reference semantics); checker oracle/global_detector.c"}
 
 
 def run_k1(args):
@@ -364,6 +424,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-k1", action="store_true")
     ap.add_argument("--k1-racy", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--c5-blocks", type=int, default=0,
+                    help="C5 blocks in total (default 2^16 per GPU; BASELINE: 2^20 over 8 GPUs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
