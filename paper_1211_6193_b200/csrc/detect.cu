@@ -35,12 +35,19 @@
 
 #include "common.cuh"
 
+#ifndef MCKG_K2_NSTAGE
+#define MCKG_K2_NSTAGE 3
+#endif
+#ifndef MCKG_K2_MINB
+#define MCKG_K2_MINB 3
+#endif
+
 namespace mckg {
 namespace {
 
 constexpr int NT = 256;
 constexpr int NWARP = NT / 32;
-constexpr int NSTAGE = 3;
+constexpr int NSTAGE = MCKG_K2_NSTAGE;
 constexpr int EPT_MAX = 16;     // records per thread kept in registers (cap <= 4096)
 constexpr uint32_t HS = 512;    // (byte, line) dedup set entries
 constexpr uint32_t TBN = 256;   // staged triples before a global flush
@@ -472,7 +479,7 @@ __device__ void process_block(const Lay& L, const Params& P, const uint4* src, u
 constexpr int NTHREADS = NT + 32;
 
 template <int EPT>
-__global__ void __launch_bounds__(NTHREADS, EPT <= 4 ? 3 : (EPT <= 8 ? 2 : 1))
+__global__ void __launch_bounds__(NTHREADS, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 1))
     race_detect_kernel(Params P) {
   const Lay L = layout(P.cap, P.wpad);
   const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31u;

@@ -749,14 +749,31 @@ __device__ void finish_request(TS& t, const KP& P, Thread& th, const Req& rq, co
   }
 }
 
+__device__ __forceinline__ mck_ins ldg_ins(const mck_ins* p) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  mck_ins in;
+  in.op = (uint8_t)(v.x & 0xFF);
+  in.t = (uint8_t)((v.x >> 8) & 0xFF);
+  in.f = (uint8_t)((v.x >> 16) & 0xFF);
+  in.pad = 0;
+  in.a = (int32_t)v.y;
+  in.b = (int32_t)v.z;
+  in.line = (int32_t)v.w;
+  return in;
+}
+
+__device__ __forceinline__ void bar_named(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // One small step of thread `t`.  Returns 1 when a shared/global request is
 // pending (rq/pd filled), else 0.
-__device__ __noinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req& rq, Pend& pd, BlockShared& bs, uint32_t nthreads) {
+__device__ __forceinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req& rq, Pend& pd, BlockShared& bs, uint32_t nthreads) {
   const mck_ins* code = P.code;
-  mck_ins in = code[t.pc];
+  mck_ins in = ldg_ins(code + t.pc);
   while (in.op == OP_JMP) {
     t.pc = in.a;
-    in = code[t.pc];
+    in = ldg_ins(code + t.pc);
   }
   ++t.pc;
   ++t.steps;
@@ -1054,91 +1071,44 @@ __device__ __forceinline__ int ht_insert(unsigned long long* keys, uint32_t* val
 }
 
 
-// Runs sweeps for one warp while every other thread of the block is waiting
-// at a barrier or finished (the caller checked it).  Returns after the sweep
-// in which a lane arrives at a barrier, or when no lane is READY any more.
-__device__ void solo_sweeps(TS& t, const KP& P, Ctx& c, Thread& th, BlockShared& bs, const SmemLay& L,
-                            uint32_t E, uint32_t& sweep, uint32_t& lastStep,
-                            unsigned long long& sharedEvents, uint32_t n) {
-  const uint32_t lane = threadIdx.x & 31;
-  const bool active = threadIdx.x < n;
-  while (true) {
-    if (!__any_sync(0xFFFFFFFFu, active && th.state == S_READY)) return;
-    ++sweep;
-    if (sweep >= P.maxSweeps) {
-      set_error(P, ERR_SWEEPS, 0);
-      return;
-    }
-    c.sweep = sweep;
-    c.sub = 0;
-    Req rq;
-    Pend pd;
-    rq.kind = 0;
-    int pending = 0;
-    const bool run = active && th.state == S_READY && sweep >= th.readyAt;
-    if (run) {
-      lastStep = sweep;
-      pending = step(t, P, c, th, rq, pd, bs, n);
-      if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
-    }
-    const uint32_t req = __ballot_sync(0xFFFFFFFFu, pending);
-    const uint32_t wreq = __ballot_sync(0xFFFFFFFFu, pending && rq.kind == 2);
-    if (req) {
-      if ((req & (req - 1)) == 0 || wreq == 0) {
-        // one request, or reads only: no order dependence
-        if (pending) {
-          do_request(P, c, th, rq, L, E & 0xFF, c.bid, sharedEvents);
-          finish_request(t, P, th, rq, pd);
-          if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
-        }
-      } else {
-        for (uint32_t l = 0; l < 32; ++l) {
-          if (lane == l && pending) {
-            do_request(P, c, th, rq, L, E & 0xFF, c.bid, sharedEvents);
-            finish_request(t, P, th, rq, pd);
-            if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
-          }
-          __syncwarp();
-        }
-      }
-    }
-    if (__any_sync(0xFFFFFFFFu, active && th.state == S_WAIT && run)) return;
-  }
-}
-
 // ================= the kernel =================
-__global__ void __launch_bounds__(1024) grid_kernel(KP P) {
+// K simulated threads per GPU thread: simulated tid = k * CT + threadIdx.x
+// (CT = blockDim.x, a multiple of 32).  Smaller CTAs let more simulated
+// blocks stay resident, which is what long serial stretches (one live thread
+// per block) need; inside a sweep the K sub-threads step in tid order.
+template <int K>
+__global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kernel(KP P) {
   const uint32_t bid = blockIdx.x;
-  const uint32_t tid = threadIdx.x;
+  const uint32_t g = threadIdx.x;
+  const uint32_t CT = blockDim.x;
+  const uint32_t SLOTS = CT * K;
   const uint32_t n = (uint32_t)P.blockDim;
-  const bool active = tid < n;
   const SmemLay L = smemLayout(P.shmem, P.raceCheck, P.htBits);
   __shared__ BlockShared bs;
 
   // ---- block init ----
-  for (uint32_t i = tid; i < (uint32_t)P.shmem; i += blockDim.x) {
+  for (uint32_t i = g; i < (uint32_t)P.shmem; i += CT) {
     smem[L.bytes + i] = 0;
     smem[L.meta + i] = 0;
   }
   if (P.raceCheck) {
     uint32_t* sh = (uint32_t*)(smem + L.shadow);
-    for (uint32_t i = tid; i < (uint32_t)P.shmem; i += blockDim.x) sh[i] = shadow_empty(0);
+    for (uint32_t i = g; i < (uint32_t)P.shmem; i += CT) sh[i] = shadow_empty(0);
     unsigned long long* rs = (unsigned long long*)(smem + L.raceSet);
-    for (uint32_t i = tid; i < RACE_SET; i += blockDim.x) rs[i] = 0;
+    for (uint32_t i = g; i < RACE_SET; i += CT) rs[i] = 0;
   }
-  {
-    unsigned long long* hk = (unsigned long long*)(smem + L.htKey);
-    uint32_t* hv = (uint32_t*)(smem + L.htVal);
-    for (uint32_t i = tid; i < (1u << P.htBits); i += blockDim.x) {
-      hk[i] = 0;
-      hv[i] = 0;
-    }
+  unsigned long long* hk = (unsigned long long*)(smem + L.htKey);
+  uint32_t* hv = (uint32_t*)(smem + L.htVal);
+  const uint32_t hmask = (1u << P.htBits) - 1;
+  for (uint32_t i = g; i <= hmask; i += CT) {
+    hk[i] = 0;
+    hv[i] = 0;
   }
-  if (tid == 0) {
+  if (g == 0) {
     bs.wait[0] = bs.wait[1] = 0;
     bs.nz[0] = bs.nz[1] = 0;
     bs.allc[0] = bs.allc[1] = 0;
-    bs.fin = (int)(blockDim.x - n);  // padding lanes count as finished
+    bs.fin = (int)(SLOTS - n);  // padding sub-threads count as finished
     bs.conflict = 0;
     bs.steps = 0;
     bs.allocs = 0;
@@ -1147,54 +1117,62 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
     bs.busy[0] = bs.busy[1] = 0xFFFFFFFFu;
     bs.soloSweep = 0;
   }
+  __syncthreads();
 
-  TS t;
-  Thread th;
-  th.state = active ? S_READY : S_FIN;
-  th.readyAt = 1;
-  th.E = 0;
-  th.syncKind = 0;
-  th.operand = 0;
-  t.pc = 0;
-  t.nv = t.nscope = t.nowned = t.nframe = t.npobj = t.ptop = 0;
-  t.steps = t.allocs = 0;
-  for (int i = 0; i < POBJ; ++i) t.pobj[i].gen = 0;
-  for (int i = 0; i < BINDS; ++i) t.binds[i] = 0;
+  TS t[K];
+  Thread th[K];
+  Req rq[K];
+  Pend pd[K];
   Ctx c;
   c.bid = bid;
-  c.tid = tid;
   c.sub = 0;
   c.sweep = 0;
-  if (active) {
+#pragma unroll 1
+  for (int k = 0; k < K; ++k) {
+    const uint32_t tid = (uint32_t)k * CT + g;
+    const bool active = tid < n;
+    TS& tk = t[k];
+    Thread& hk_ = th[k];
+    hk_.state = active ? S_READY : S_FIN;
+    hk_.readyAt = 1;
+    hk_.E = 0;
+    hk_.syncKind = 0;
+    hk_.operand = 0;
+    tk.pc = 0;
+    tk.nv = tk.nscope = tk.nowned = tk.nframe = tk.npobj = tk.ptop = 0;
+    tk.steps = tk.allocs = 0;
+    for (int i = 0; i < POBJ; ++i) tk.pobj[i].gen = 0;
+    for (int i = 0; i < BINDS; ++i) tk.binds[i] = 0;
+    if (!active) continue;
     // spawnGrid (device.cpp:40-57): params are objects owned by the spawn
     // scope, the dynamic shared array is bound, k = [CallFrame, body]
     const mck_fn& kf = P.fns[P.kernel];
-    t.frames[0].retPc = -1;
-    t.frames[0].bindBase = 0;
-    t.frames[0].fn = P.kernel;
-    t.frames[0].scopeDepth = 0;
-    t.frames[0].valueDepth = 0;
-    t.nframe = 1;
-    t.scopeMark[0] = 0;
-    t.nscope = 1;
+    tk.frames[0].retPc = -1;
+    tk.frames[0].bindBase = 0;
+    tk.frames[0].fn = P.kernel;
+    tk.frames[0].scopeDepth = 0;
+    tk.frames[0].valueDepth = 0;
+    tk.nframe = 1;
+    tk.scopeMark[0] = 0;
+    tk.nscope = 1;
     for (int i = 0; i < P.nargs; ++i) {
       const mck_local& pl = P.locals[kf.local_base + i];
       uint32_t id;
-      if (!priv_alloc(t, P, pl.size, pl.name, id)) {
-        th.state = S_FIN;
+      if (!priv_alloc(tk, P, pl.size, pl.name, id)) {
+        hk_.state = S_FIN;
         break;
       }
-      priv_poke(t, t.pobj[id & 0xFFFFF], 0, pl.type, P.args[i]);
-      t.binds[i] = id;
+      priv_poke(tk, tk.pobj[id & 0xFFFFF], 0, pl.type, P.args[i]);
+      tk.binds[i] = id;
     }
-    t.allocs = 0;  // spawn-time params are accounted for by the host
-    if (kf.dyn_shared_slot >= 0) t.binds[kf.dyn_shared_slot] = P.sharedBase + bid;
-    t.pc = kf.entry;
-    if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+    tk.allocs = 0;  // spawn-time params are accounted for by the host
+    if (kf.dyn_shared_slot >= 0) tk.binds[kf.dyn_shared_slot] = P.sharedBase + bid;
+    tk.pc = kf.entry;
+    if (hk_.state == S_FIN) atomicAdd(&bs.fin, 1);
   }
   __syncthreads();
 
-  uint32_t E = 0;           // completed episodes (uniform)
+  uint32_t E = 0;  // completed episodes (uniform)
   // barrier counters are cumulative per episode parity: episode j (parity
   // j & 1) completes when wait[j & 1] reaches need[j & 1]
   int need[2] = {(int)n, (int)n};
@@ -1205,112 +1183,157 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
   unsigned long long sharedEvents = 0;
   uint32_t lastStep = 0;
   const uint32_t Lt = n - 1;
-  unsigned long long* hk = (unsigned long long*)(smem + L.htKey);
-  uint32_t* hv = (uint32_t*)(smem + L.htVal);
-  const uint32_t hmask = (1u << P.htBits) - 1;
   bool justSolo = true;  // the busy mask is valid only after a full sweep
   unsigned long long soloSweeps = 0;
   long long soloCycles = 0;
   const long long kStart = clock64();
+  bool solo = false;  // this warp is running sweeps alone (see below)
+  uint32_t soloS0 = 0;
+  long long soloC0 = 0;
+  const uint32_t myWarp = g >> 5, lane = g & 31;
+
+  auto anyReady = [&]() {
+    bool r = false;
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) r |= th[k].state == S_READY;
+    return r;
+  };
 
   while (true) {
-    // ---- barrier protocol in closed form (Appendix A); counters cover
-    // every step up to and including `sweep` ----
-    const int p = (E + 1) & 1;
-    const int arrived = bs.wait[p] - (need[p] - (int)n);
-    const int nfin = bs.fin;
-    if (arrived == (int)n) {
-      // episode E+1 completed in sweep T = `sweep` (the last arrival): the
-      // up-sweep chain, Turnaround (epoch clear) and Down(L) fire in T, one
-      // Down per sweep after that, FinalRelease(0) in T + L
-      const uint32_t T = sweep;
-      const int nz = bs.nz[p] - nzPrev[p], allc = bs.allc[p] - allcPrev[p];
-      nzPrev[p] += nz;
-      allcPrev[p] += allc;
-      need[p] += (int)n;  // the next episode of this parity is E + 3
-      if (active) {
-        th.state = S_READY;
-        th.readyAt = tid == 0 ? T + Lt + 1 : T + (Lt - tid) + 1;
-        th.E = E + 1;
-        Val res;
-        switch (th.syncKind) {
-          case MCK_SYNC_AND: res = v_int(allc == (int)n ? 1 : 0); break;
-          case MCK_SYNC_OR: res = v_int(nz > 0 ? 1 : 0); break;
-          case MCK_SYNC_COUNT: res = v_int(nz); break;
-          default: res = v_void(); break;
+    if (!solo) {
+      // ---- barrier protocol in closed form (Appendix A); counters cover
+      // every step up to and including `sweep` ----
+      const int p = (E + 1) & 1;
+      const int arrived = bs.wait[p] - (need[p] - (int)n);
+      const int nfin = bs.fin;
+      if (arrived == (int)n) {
+        // episode E+1 completed in sweep T = `sweep` (the last arrival): the
+        // up-sweep chain, Turnaround (epoch clear) and Down(L) fire in T, one
+        // Down per sweep after that, FinalRelease(0) in T + L
+        const uint32_t T = sweep;
+        const int nz = bs.nz[p] - nzPrev[p], allc = bs.allc[p] - allcPrev[p];
+        nzPrev[p] += nz;
+        allcPrev[p] += allc;
+        need[p] += (int)n;  // the next episode of this parity is E + 3
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) {
+          const uint32_t tid = (uint32_t)k * CT + g;
+          if (tid >= n) continue;
+          Thread& x = th[k];
+          x.state = S_READY;
+          x.readyAt = tid == 0 ? T + Lt + 1 : T + (Lt - tid) + 1;
+          x.E = E + 1;
+          Val res;
+          switch (x.syncKind) {
+            case MCK_SYNC_AND: res = v_int(allc == (int)n ? 1 : 0); break;
+            case MCK_SYNC_OR: res = v_int(nz > 0 ? 1 : 0); break;
+            case MCK_SYNC_COUNT: res = v_int(nz); break;
+            default: res = v_void(); break;
+          }
+          push(t[k], P, res);
         }
-        push(t, P, res);
+        rules += 2ull * n;
+        ++E;
+        if (P.raceCheck && (E & 0xFF) == 0) {  // stamp wrap: clear the shadow
+          uint32_t* sh = (uint32_t*)(smem + L.shadow);
+          for (uint32_t i = g; i < (uint32_t)P.shmem; i += CT) sh[i] = shadow_empty(0);
+          __syncthreads();
+        }
+      } else if (nfin == (int)SLOTS) {
+        break;  // every thread finished
+      } else if (arrived + nfin == (int)SLOTS) {
+        // quiescent with waiters: barrier deadlock (deadlock.cpp:15-34)
+        deadlocked = true;
+        break;
       }
-      rules += 2ull * n;
-      ++E;
-      if (P.raceCheck && (E & 0xFF) == 0) {  // stamp wrap: clear the shadow
-        uint32_t* sh = (uint32_t*)(smem + L.shadow);
-        for (uint32_t i = tid; i < (uint32_t)P.shmem; i += blockDim.x) sh[i] = shadow_empty(0);
-        __syncthreads();
-      }
-    } else if (nfin == (int)blockDim.x) {
-      break;  // every thread finished
-    } else if (arrived + nfin == (int)blockDim.x) {
-      // quiescent with waiters: barrier deadlock (deadlock.cpp:15-34)
-      deadlocked = true;
-      break;
-    }
-    // ---- solo mode: when a single warp holds every READY thread, no other
-    // thread can move until that warp arrives at a barrier or finishes, so it
-    // runs sweeps alone with warp-level synchronisation ----
-    {
+      // ---- solo mode: when a single warp holds every READY thread, no other
+      // thread can move until that warp arrives at a barrier or finishes, so
+      // it runs sweeps alone with warp-level synchronisation while the other
+      // warps park on named barrier 1 ----
       const uint32_t busy = justSolo ? 0xFFFFFFFFu : bs.busy[sweep & 1];
       justSolo = false;
       if (busy && (busy & (busy - 1)) == 0) {
         const uint32_t sw = (uint32_t)__ffs(busy) - 1;
-        const uint32_t s0 = sweep;
-        const long long c0 = clock64();
-        if ((tid >> 5) == sw) {
-          solo_sweeps(t, P, c, th, bs, L, E, sweep, lastStep, sharedEvents, n);
-          if ((tid & 31) == 0) bs.soloSweep = sweep;
+        if (myWarp != sw) {
+          const long long c0 = clock64();
+          const uint32_t s0 = sweep;
+          bar_named(1, CT);  // until the solo warp is done
+          soloCycles += clock64() - c0;
+          sweep = bs.soloSweep;
+          soloSweeps += sweep - s0;
+          justSolo = true;
+          if (sweep >= P.maxSweeps) break;
+          continue;
         }
-        __syncthreads();
-        soloCycles += clock64() - c0;
-        soloSweeps += bs.soloSweep - s0;
-        sweep = bs.soloSweep;
-        justSolo = true;
-        if (sweep >= P.maxSweeps) break;
-        continue;
+        solo = true;
+        soloS0 = sweep;
+        soloC0 = clock64();
       }
+    }
+    if (solo && !__any_sync(0xFFFFFFFFu, anyReady())) {
+      // nothing left to run in this warp: hand back to the block
+      if (lane == 0) bs.soloSweep = sweep;
+      solo = false;
+      soloCycles += clock64() - soloC0;
+      soloSweeps += sweep - soloS0;
+      bar_named(1, CT);
+      justSolo = true;
+      continue;
     }
     ++sweep;
     if (sweep >= P.maxSweeps) {
       set_error(P, ERR_SWEEPS, 0);
+      if (solo) {
+        if (lane == 0) bs.soloSweep = sweep;
+        bar_named(1, CT);
+      }
       break;
     }
     c.sweep = sweep;
-    c.sub = 0;
-    // ---- phase 1: one step per runnable thread; shared/global requests
-    // are registered in the conflict hash (word granularity) ----
-    Req rq;
-    Pend pd;
-    rq.kind = 0;
-    int pending = 0;
+    // ---- phase 1: one step per runnable sub-thread (tid order k-major) ----
+    uint32_t pendMask = 0, runMask = 0;
+    bool anyWrite = false;
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+      const uint32_t tid = (uint32_t)k * CT + g;
+      rq[k].kind = 0;
+      if (tid < n && th[k].state == S_READY && sweep >= th[k].readyAt) {
+        runMask |= 1u << k;
+        lastStep = sweep;
+        c.tid = tid;
+        c.sub = 0;
+        const int pending = step(t[k], P, c, th[k], rq[k], pd[k], bs, n);
+        if (th[k].state == S_FIN) atomicAdd(&bs.fin, 1);
+        if (pending) {
+          pendMask |= 1u << k;
+          anyWrite |= rq[k].kind == 2;
+        }
+      }
+    }
     bool conflict = false;
-    int slots[3] = {-1, -1, -1};
-    int ns = 0;
-    const bool run = active && th.state == S_READY && sweep >= th.readyAt;
-    if (run) {
-      lastStep = sweep;
-      pending = step(t, P, c, th, rq, pd, bs, n);
-      if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
-      if (pending) {
-        const int len = (int)t_scalar(rq.ty);
-        const unsigned long long addr = rq.space == R_OK_SHARED
-                                            ? (unsigned long long)rq.off
-                                            : (1ull << 40) | (rq.base + (unsigned long long)rq.off);
-        const bool wr = rq.kind == 2;
-        for (unsigned long long w = addr >> 2; w <= (addr + len - 1) >> 2 && ns < 3; ++w) {
+    if (solo) {
+      // warp-local memory phase: the other warps are parked
+      uint32_t nreq = 0;
+#pragma unroll 1
+      for (int k = 0; k < K; ++k) nreq += __popc(__ballot_sync(0xFFFFFFFFu, (pendMask >> k) & 1u));
+      conflict = nreq > 1 && __any_sync(0xFFFFFFFFu, anyWrite);
+    } else {
+      // word-level overlap with a write among this sweep's requests (one
+      // pass: the later inserter of an overlapping pair sees it)
+#pragma unroll 1
+      for (int k = 0; k < K; ++k) {
+        if (!((pendMask >> k) & 1u)) continue;
+        const Req& r = rq[k];
+        const int len = (int)t_scalar(r.ty);
+        const unsigned long long addr =
+            r.space == R_OK_SHARED ? (unsigned long long)r.off : (1ull << 40) | (r.base + (unsigned long long)r.off);
+        const bool wr = r.kind == 2;
+        for (unsigned long long w = addr >> 2; w <= (addr + len - 1) >> 2; ++w) {
           const unsigned long long key = w + 1;
           uint32_t h = (uint32_t)mix64(key) & hmask;
           int slot = -1;
           for (uint32_t probe = 0; probe <= hmask; ++probe) {
-            unsigned long long old = atomicCAS(hk + h, 0ull, key);
+            const unsigned long long old = atomicCAS(hk + h, 0ull, key);
             if (old == 0ull || old == key) {
               slot = (int)h;
               break;
@@ -1322,71 +1345,121 @@ __global__ void __launch_bounds__(1024) grid_kernel(KP P) {
             continue;
           }
           const uint32_t old = atomicAdd(hv + slot, wr ? 0x10001u : 1u);
-          // overlap with a write: some earlier inserter, and one side writes
           if ((old & 0xFFFF) != 0 && (wr || (old >> 16) != 0)) conflict = true;
-          slots[ns++] = slot;
         }
       }
+      if (__any_sync(0xFFFFFFFFu, anyReady()) && lane == 0) atomicOr(&bs.busy[sweep & 1], 1u << myWarp);
+      conflict = __syncthreads_or(conflict);
+      if (g == 0) bs.busy[(sweep + 1) & 1] = 0;
     }
-    if (__any_sync(0xFFFFFFFFu, active && th.state == S_READY) && (tid & 31) == 0)
-      atomicOr(&bs.busy[sweep & 1], 1u << (tid >> 5));
-    conflict = __syncthreads_or(conflict);
-    if (tid == 0) bs.busy[(sweep + 1) & 1] = 0;
+    // ---- memory phase: parallel, or replayed in tid order ----
     if (!conflict) {
-      if (pending) {
-        do_request(P, c, th, rq, L, E & 0xFF, bid, sharedEvents);
-        finish_request(t, P, th, rq, pd);
-        if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+#pragma unroll 1
+      for (int k = 0; k < K; ++k) {
+        if (!((pendMask >> k) & 1u)) continue;
+        c.tid = (uint32_t)k * CT + g;
+        c.sub = 1;
+        do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents);
+        finish_request(t[k], P, th[k], rq[k], pd[k]);
+        if (th[k].state == S_FIN) atomicAdd(&bs.fin, 1);
       }
     } else {
-      // replay the memory phase in tid order (round-robin order)
-      const uint32_t warp = tid >> 5, lane = tid & 31;
-      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
-        if (warp == w) {
-          for (uint32_t l = 0; l < 32; ++l) {
-            if (lane == l && pending) {
-              do_request(P, c, th, rq, L, E & 0xFF, bid, sharedEvents);
-              finish_request(t, P, th, rq, pd);
-              if (th.state == S_FIN) atomicAdd(&bs.fin, 1);
+      const uint32_t nw = solo ? 1u : (CT >> 5);
+#pragma unroll 1
+      for (int k = 0; k < K; ++k) {
+        for (uint32_t w = 0; w < nw; ++w) {
+          if (solo || myWarp == w) {
+            for (uint32_t l = 0; l < 32; ++l) {
+              if (lane == l && ((pendMask >> k) & 1u)) {
+                c.tid = (uint32_t)k * CT + g;
+                c.sub = 1;
+                do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents);
+                finish_request(t[k], P, th[k], rq[k], pd[k]);
+                if (th[k].state == S_FIN) atomicAdd(&bs.fin, 1);
+              }
+              __syncwarp();
             }
-            __syncwarp();
           }
+          if (!solo) __syncthreads();
         }
-        __syncthreads();
       }
     }
-    for (int i = 0; i < ns; ++i) {
-      hk[slots[i]] = 0ull;
-      hv[slots[i]] = 0u;
+    if (solo) {
+      bool arrivedNow = false;
+#pragma unroll 1
+      for (int k = 0; k < K; ++k) arrivedNow |= ((runMask >> k) & 1u) && th[k].state == S_WAIT;
+      if (__any_sync(0xFFFFFFFFu, arrivedNow)) {
+        // a lane arrived at a barrier: the block decides what happens next
+        if (lane == 0) bs.soloSweep = sweep;
+        solo = false;
+        soloCycles += clock64() - soloC0;
+        soloSweeps += sweep - soloS0;
+        bar_named(1, CT);
+        justSolo = true;
+      }
+      continue;
+    }
+    // clear the hash slots of this sweep (every inserter clears its keys)
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+      if (!((pendMask >> k) & 1u)) continue;
+      const Req& r = rq[k];
+      const int len = (int)t_scalar(r.ty);
+      const unsigned long long addr =
+          r.space == R_OK_SHARED ? (unsigned long long)r.off : (1ull << 40) | (r.base + (unsigned long long)r.off);
+      for (unsigned long long w = addr >> 2; w <= (addr + len - 1) >> 2; ++w) {
+        const unsigned long long key = w + 1;
+        uint32_t h = (uint32_t)mix64(key) & hmask;
+        for (uint32_t probe = 0; probe <= hmask; ++probe) {
+          const unsigned long long cur = hk[h];
+          if (cur == key) {
+            hk[h] = 0ull;
+            hv[h] = 0u;
+            break;
+          }
+          if (cur == 0ull) break;
+          h = (h + 1) & hmask;
+        }
+      }
     }
     __syncthreads();
   }
 
   // ---- block outputs ----
-  const uint32_t warp = tid >> 5, lane = tid & 31;
   const uint32_t words = (n + 31) / 32;
-  if (deadlocked) {
-    bool waiting = active && th.state == S_WAIT;
-    uint32_t m = __ballot_sync(0xFFFFFFFFu, waiting);
-    if (lane == 0 && warp < words) P.waitMask[(size_t)bid * words + warp] = m;
-    // up-sweep rules of the stuck episode: from tid 0 along the waiting prefix
-    // (device.cpp:111-141): p - 1 rules where p = first non-waiting tid
+  unsigned long long steps = 0, allocs = 0;
+#pragma unroll 1
+  for (int k = 0; k < K; ++k) {
+    steps += t[k].steps;
+    allocs += t[k].allocs;
+    if (deadlocked) {
+      const uint32_t tid = (uint32_t)k * CT + g;
+      const bool waiting = tid < n && th[k].state == S_WAIT;
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, waiting);
+      const uint32_t word = ((uint32_t)k * CT + (myWarp << 5)) >> 5;
+      if (lane == 0 && word < words) P.waitMask[(size_t)bid * words + word] = m;
+    }
   }
-  atomicAdd(&bs.steps, (unsigned long long)t.steps);
-  atomicAdd(&bs.allocs, (unsigned long long)t.allocs);
+  atomicAdd(&bs.steps, steps);
+  atomicAdd(&bs.allocs, allocs);
   atomicAdd(&bs.sharedEvents, sharedEvents);
   atomicMax(&bs.lastSweep, lastStep);
   __syncthreads();
   if (deadlocked) {
-    // first non-waiting tid
+    // up-sweep rules of the stuck episode (device.cpp:111-141): the token ran
+    // from tid 0 along the waiting prefix: p - 1 rules, p = first non-waiting tid
     __shared__ uint32_t firstNot;
-    if (tid == 0) firstNot = n;
+    if (g == 0) firstNot = n;
     __syncthreads();
-    if (active && th.state != S_WAIT) atomicMin(&firstNot, tid);
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+      const uint32_t tid = (uint32_t)k * CT + g;
+      if (tid < n && th[k].state != S_WAIT) atomicMin(&firstNot, tid);
+    }
     __syncthreads();
-    if (tid == 0 && firstNot >= 1) rules += firstNot - 1;
+    if (g == 0 && firstNot >= 1) rules += firstNot - 1;
   }
-  if (tid == 0) {
+  if (g == 0) {
     BlockOut& o = P.blocks[bid];
     o.sweeps = sweep;
     o.soloSweeps = soloSweeps;
@@ -1438,6 +1511,12 @@ struct DBuf {
     return true;
   }
 };
+
+// MCKG_K1_K=<1|2|4|8> forces the multiplexing factor (experiments).
+static int kForceK = [] {
+  const char* e = getenv("MCKG_K1_K");
+  return e ? atoi(e) : 0;
+}();
 
 class CudaEngine final : public DeviceEngine {
  public:
@@ -1536,9 +1615,16 @@ class CudaEngine final : public DeviceEngine {
       if (!upload(code_, P.code, err) || !upload(fns_, P.fns, err) || !upload(locals_, P.locals, err)) return false;
       progCached_ = &P;
     }
-    const int threads = (int)((g.blockDim + 31) / 32 * 32);
+    // K simulated threads per GPU thread: CTAs of 64-128 threads keep up to
+    // 32 simulated blocks resident per SM (serial stretches need residency)
+    // measured (round 1): C4 1024-thread blocks 33 -> 20 ms with K = 4; the
+    // 256-thread C2 blocks are fastest with K = 1 (local-memory bound)
+    int K = g.blockDim > 256 ? 4 : 1;
+    if (kForceK > 0) K = kForceK;
+    if (K > 1 && (g.blockDim + K - 1) / K > 256) K = 4;  // K >= 2 kernels take <= 256 threads
+    const int threads = (int)(((g.blockDim + K - 1) / K + 31) / 32 * 32);
     int htBits = 1;
-    while ((1 << htBits) < 4 * threads) ++htBits;
+    while ((1 << htBits) < 4 * threads * K) ++htBits;
     const SmemLay L = smemLayout(g.shmemBytes, g.raceCheck ? 1 : 0, htBits);
     if (L.end > 200 * 1024) {
       out.error = "the block's shared array (" + std::to_string(g.shmemBytes) +
@@ -1618,13 +1704,14 @@ class CudaEngine final : public DeviceEngine {
     kp.waitMask = dWait.p;
     kp.error = dErr.p;
     kp.errorInfo = dErr.p + 1;
-    CK(cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.end));
+    void (*kern)(KP) = K == 1 ? grid_kernel<1> : K == 2 ? grid_kernel<2> : K == 4 ? grid_kernel<4> : grid_kernel<8>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.end));
     init_diag_ts(dDiag.p, diagN, stream_);  // ts := +inf
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, stream_);
-    grid_kernel<<<(unsigned)nb, threads, L.end, stream_>>>(kp);
+    kern<<<(unsigned)nb, threads, L.end, stream_>>>(kp);
     cudaEventRecord(e1, stream_);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(stream_));
