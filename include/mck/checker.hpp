@@ -43,6 +43,7 @@ struct Diagnostic {
   DiagCategory category = DiagCategory::UndefinedBehavior;
   std::string message;
   SourceLoc loc;
+  uint64_t sweep = 0;  // B200 extension: round-robin sweep of the first occurrence
 };
 
 struct FrontendError {

@@ -1234,6 +1234,7 @@ __global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kern
         }
         rules += 2ull * n;
         ++E;
+        justSolo = true;  // the busy mask predates these releases
         if (P.raceCheck && (E & 0xFF) == 0) {  // stamp wrap: clear the shadow
           uint32_t* sh = (uint32_t*)(smem + L.shadow);
           for (uint32_t i = g; i < (uint32_t)P.shmem; i += CT) sh[i] = shadow_empty(0);

@@ -54,7 +54,8 @@ extern "C" int mck_run_source(const char* src, const char* filename, const mck_r
       const auto& d = r.diagnostics[i];
       o += std::string(i ? "," : "") + "{\"cat\":" + js(mck::categoryName(d.category)) + ",\"sev\":" +
            (d.severity == mck::Severity::Error ? "\"error\"" : "\"warning\"") + ",\"msg\":" + js(d.message) +
-           ",\"line\":" + std::to_string(d.loc.line) + "}";
+           ",\"line\":" + std::to_string(d.loc.line) +
+           (getenv("MCK_DIAG_SWEEP") ? ",\"sweep\":" + std::to_string(d.sweep) : std::string()) + "}";
     }
     o += "],\"stuck_reports\":[";
     for (size_t i = 0; i < r.stuckReports.size(); ++i) {

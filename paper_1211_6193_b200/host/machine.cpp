@@ -1598,7 +1598,10 @@ mck::RunResult HostMachine::run() {
   });
   std::set<std::pair<int, std::string>> seen;
   for (const DiagEv& e : diags_)
-    if (seen.insert({static_cast<int>(e.d.category), e.d.message}).second) r.diagnostics.push_back(e.d);
+    if (seen.insert({static_cast<int>(e.d.category), e.d.message}).second) {
+      r.diagnostics.push_back(e.d);
+      r.diagnostics.back().sweep = e.sweep;
+    }
   r.steps = steps_;
   if (r.stuck)
     r.exitCode = 3;

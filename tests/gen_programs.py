@@ -200,3 +200,103 @@ int main(void) {{
 }}
 """
     return src
+
+
+def random_kernel2(seed):
+    """Richer random device programs (test infrastructure): device functions
+    (with recursion), __syncthreads_and/or/count, local arrays and pointer
+    arithmetic, intra-block global-memory conflicts, UB that halts a thread,
+    two launches on two streams and a host that prints the results.
+    Cross-BLOCK global conflicts are avoided (the B200 engine does not order
+    different blocks inside a sweep; SURVEY Appendix E covers them)."""
+    rng = random.Random(10_000 + seed)
+    nb = rng.choice([1, 2, 3])
+    nt = rng.choice([1, 2, 4, 7, 16, 32, 33, 48])
+    sh = 4 * rng.choice([8, 16, 64])
+    m = sh // 4
+    body = []
+    for _ in range(rng.randint(4, 12)):
+        r = rng.randrange(16)
+        k = rng.randrange(1, 7)
+        if r == 0:
+            body.append(f"s[(t * {k}) % {m}] = f(t + {k}, {rng.randrange(4)});")
+        elif r == 1:
+            body.append(f"x += s[(t + {k}) % {m}] * {rng.randrange(1, 4)};")
+        elif r == 2:
+            body.append(f"x += __syncthreads_count(t % {k} == 0);")
+        elif r == 3:
+            body.append(f"x += __syncthreads_or(x > {rng.randrange(20)}) + 2 * __syncthreads_and(t < {rng.randrange(1, 40)});")
+        elif r == 4:
+            body.append(f"loc[t % 4] = x; p = loc + (t % 3); x += *p + p[1];")
+        elif r == 5:
+            body.append(f"g[b * 64 + (t % 64)] += x;")  # block-private global slice; intra-block conflicts
+        elif r == 6:
+            body.append(f"j = 0; while (j < t % {k + 1}) {{ if (j == {k}) break; x = x * 3 - j; j++; }}")
+        elif r == 7:
+            body.append(f"for (j = 0; j < {k}; ++j) {{ if (j % 2) continue; c[(t + j) % {sh}] = (char)(x + j); }}")
+        elif r == 8:
+            body.append(f"x = (t & 1) ? x + c[(t * 5) % {sh}] : x - {k};")
+        elif r == 9:
+            body.append(f"if (t == {rng.randrange(nt + 2)}) {{ x = x / (t - t); }}")  # UB halt in one thread
+        elif r == 10:
+            body.append(f"x += fact(t % 6);")
+        elif r == 11:
+            body.append(f"s[(t + 1) % {m}] = x; __syncthreads(); x += s[t % {m}];")
+        elif r == 12:
+            body.append(f"if (t % {k + 1} == 0) {{ __syncthreads(); }}")  # may deadlock
+        elif r == 13:
+            body.append(f"x = (x << {rng.randrange(3)}) ^ (x >> 1) | {k};")
+        elif r == 14:
+            body.append(f"y = (long)x * {rng.choice([3, 100000, 2147483647])}; x = (int)(y % 1000);")
+        else:
+            body.append(f"g[b * 64 + ((t + {k}) % 64)] = g[b * 64 + (t % 64)] + 1;")
+    code = "\n  ".join(body)
+    k2 = rng.choice([1, 2])
+    return f"""#include <stdio.h>
+__device__ int f(int a, int d) {{
+  if (d <= 0) return a % 7;
+  return f(a * 3 + 1, d - 1) - d;
+}}
+__device__ long fact(int n) {{
+  if (n < 2) return 1;
+  return n * fact(n - 1);
+}}
+__global__ void k(int* g) {{
+  extern __shared__ int s[];
+  char* c;
+  int t, j, x, b, loc[4], *p;
+  long y;
+  c = (char*)s;
+  t = threadIdx.x;
+  b = blockIdx.x;
+  x = t;
+  j = 0;
+  for (j = 0; j < {m}; ++j) {{ if (j % {nt if nt > 0 else 1} == t) s[j] = j; }}
+  __syncthreads();
+  {code}
+  g[b * 64 + (t % 64)] = x;
+}}
+__global__ void k2(int* g, int* out) {{
+  int t = threadIdx.x, i, acc = 0;
+  for (i = 0; i < {k2}; ++i) {{
+    acc += g[(t * 5 + i) % {nb * 64}];
+  }}
+  out[t] = acc;
+}}
+int main(void) {{
+  int *g, *out, h[16], i;
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  cudaMalloc(&g, {nb * 64} * sizeof(int));
+  cudaMalloc(&out, 16 * sizeof(int));
+  cudaMemset(g, 0, {nb * 64} * sizeof(int));
+  k<<<{nb}, {nt}, {sh}>>>(g);
+  cudaDeviceSynchronize();
+  k2<<<1, 16, 0, st>>>(g, out);
+  cudaMemcpyAsync(h, out, 16 * sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  for (i = 0; i < 16; ++i) printf("%d ", h[i]);
+  printf("\\n");
+  return 0;
+}}
+"""

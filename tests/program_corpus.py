@@ -22,6 +22,8 @@ def corpus():
     ]
     for i in range(300):
         out.append((f"rand{i}", f"rand{i}.cu", gp.random_kernel(i)))
+    for i in range(200):
+        out.append((f"rich{i}", f"rich{i}.cu", gp.random_kernel2(i)))
     return out
 
 

@@ -51,3 +51,10 @@ def test_divergent_barrier_deadlock(name):
 @pytest.mark.parametrize("seed", range(300))
 def test_random_racy_kernels(seed):
     _check(f"rand{seed}")
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_rich_random_programs(seed):
+    """Device functions + recursion, __syncthreads_and/or/count, local arrays,
+    intra-block global conflicts, UB halts, deadlocks, two streams."""
+    _check(f"rich{seed}")
