@@ -6,6 +6,8 @@ by the unmodified reference (oracle/_ref/libmckref.so, Machine::run under
 tests/golden/programs.json, so the GPU box needs no reference build."""
 import gen_programs as gp
 
+RICH = 500
+
 
 def corpus():
     out = [
@@ -22,7 +24,7 @@ def corpus():
     ]
     for i in range(300):
         out.append((f"rand{i}", f"rand{i}.cu", gp.random_kernel(i)))
-    for i in range(200):
+    for i in range(RICH):
         out.append((f"rich{i}", f"rich{i}.cu", gp.random_kernel2(i)))
     return out
 

@@ -9,7 +9,7 @@ import os
 
 import pytest
 
-from program_corpus import corpus, project
+from program_corpus import RICH, corpus, project
 
 pytestmark = pytest.mark.gpu
 
@@ -53,8 +53,23 @@ def test_random_racy_kernels(seed):
     _check(f"rand{seed}")
 
 
-@pytest.mark.parametrize("seed", range(200))
+@pytest.mark.parametrize("seed", range(RICH))
 def test_rich_random_programs(seed):
     """Device functions + recursion, __syncthreads_and/or/count, local arrays,
     intra-block global conflicts, UB halts, deadlocks, two streams."""
     _check(f"rich{seed}")
+
+
+SEED0 = json.load(open(os.path.join(HERE, "golden", "programs_seed0.json")))
+
+
+@pytest.mark.parametrize("name", sorted(SEED0))
+def test_matches_reference_default_schedule(name):
+    """The reference CLI's default policy is seeded-random (seed 0); on the
+    BASELINE program families its RunResult equals the round-robin one
+    (SURVEY F4), so the engine matches the default run too."""
+    from paper_1211_6193_b200 import checker
+    fname, src = CORPUS[name]
+    got = project(checker.run_source(src, filename=fname))
+    for k, v in SEED0[name].items():
+        assert got[k] == v, (name, k)
