@@ -313,8 +313,11 @@ def run_c5(args, blocks, dev, ws, rank):
     stream = torch.cuda.current_stream()
 
     def step():
-        grouped, counts = gr.partition(ev, ws, space, stream)
-        mine = gr.exchange(grouped, counts) if ws > 1 else grouped
+        if ws > 1:
+            grouped, counts = gr.partition(ev, ws, space, stream)
+            mine = gr.exchange(grouped, counts)
+        else:
+            mine = ev  # one owner: nothing to partition or exchange
         out = gr.GlobalOut(max(1, mine.shape[0] // 8), device=dev)
         gr.detect(mine, lo, out.reset(), stream)
         if ws > 1:

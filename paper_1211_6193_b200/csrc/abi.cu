@@ -45,6 +45,20 @@ int sm_count() {
   return sms;
 }
 
+void keep_pool_memory() {
+  static thread_local int done_dev = -1;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done_dev = d;
+}
+
 }  // namespace mckg
 
 using namespace mckg;

@@ -12,6 +12,9 @@ void set_error(const char* what, cudaError_t e = cudaSuccess);
 void note_launch(uint32_t kernels, uint32_t grid, uint32_t block, uint32_t smem);
 void add_launches(uint32_t kernels);
 int sm_count();
+// Keeps freed stream-ordered allocations in the device's default memory pool
+// (release threshold = max): the detectors allocate multi-GB scratch per call.
+void keep_pool_memory();
 
 #define MCKG_CUDA_TRY(expr)                                  \
   do {                                                       \

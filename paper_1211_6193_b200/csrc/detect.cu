@@ -713,6 +713,7 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
 extern "C" int mckg_sort_triples(mckg_race_triple* triples, uint64_t n, uint32_t obj_base,
                                  unsigned long long* n_unique, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_memory();
   if (n == 0) {
     if (n_unique) MCKG_CUDA_TRY(cudaMemsetAsync(n_unique, 0, sizeof(unsigned long long), s));
     return MCKG_OK;

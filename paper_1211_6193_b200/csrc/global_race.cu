@@ -61,24 +61,39 @@ __global__ void gen_c5_kernel(mckg_gaccess* ev, uint32_t blk0, uint32_t n_blocks
 }
 
 // ---- K3: owner partition ----
+__device__ __forceinline__ uint32_t owner_of(uint64_t a, uint32_t P, unsigned long long space) {
+  const uint32_t o = (uint32_t)((ga_addr(a) * P) / space);
+  return o < P ? o : P - 1;
+}
+
+constexpr uint32_t TILE = 4096;  // records per scatter tile (256 threads x 16)
+
 __global__ void owner_hist_kernel(const mckg_gaccess* ev, uint64_t n, uint32_t P, unsigned long long space,
                                   unsigned long long* counts) {
-  __shared__ unsigned long long h[64];
+  __shared__ unsigned int h[64];
   for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t o = (uint32_t)((ga_addr(ev[i].a) * P) / space);
-    atomicAdd(&h[o < P ? o : P - 1], 1ull);
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < n; i0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    const uint32_t o = i < n ? owner_of(ev[i].a, P, space) : 0xFFFFFFFFu;
+    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, o);  // warp-aggregated
+    if (o != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(grp) - 1)) atomicAdd(&h[o], (unsigned)__popc(grp));
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < P; i += blockDim.x)
-    if (h[i]) atomicAdd(counts + i, h[i]);
+    if (h[i]) atomicAdd(counts + i, (unsigned long long)h[i]);
 }
 
+// One tile of TILE records per CTA iteration: per-owner tile counts in shared
+// memory (warp-aggregated), one global reservation per (tile, owner), then
+// every record lands at base + its rank inside the tile.
 __global__ void owner_scatter_kernel(const mckg_gaccess* ev, uint64_t n, uint32_t P, unsigned long long space,
                                      const unsigned long long* counts, unsigned long long* cursor,
                                      mckg_gaccess* out) {
   __shared__ unsigned long long base[64];
+  __shared__ unsigned long long tbase[64];
+  __shared__ unsigned int tcnt[64];
   if (threadIdx.x == 0) {
     unsigned long long s = 0;
     for (uint32_t r = 0; r < P; ++r) {
@@ -86,25 +101,33 @@ __global__ void owner_scatter_kernel(const mckg_gaccess* ev, uint64_t n, uint32_
       s += counts[r];
     }
   }
-  __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
-  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < n; i0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = i0 + threadIdx.x;
-    const bool in = i < n;
-    mckg_gaccess g{};
-    uint32_t o = 0xFFFFFFFFu;
-    if (in) {
-      g = ev[i];
-      o = (uint32_t)((ga_addr(g.a) * P) / space);
-      if (o >= P) o = P - 1;
+  constexpr uint32_t PER = TILE / 256;
+  for (uint64_t t0 = blockIdx.x * (uint64_t)TILE; t0 < n; t0 += (uint64_t)gridDim.x * TILE) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) tcnt[i] = 0;
+    __syncthreads();
+    uint32_t o[PER], pos[PER];
+#pragma unroll
+    for (uint32_t k = 0; k < PER; ++k) {
+      const uint64_t i = t0 + (uint64_t)k * 256 + threadIdx.x;
+      o[k] = i < n ? owner_of(ev[i].a, P, space) : 0xFFFFFFFFu;
+      const uint32_t grp = __match_any_sync(0xFFFFFFFFu, o[k]);
+      const int leader = __ffs(grp) - 1;
+      uint32_t b = 0;
+      if (o[k] != 0xFFFFFFFFu && lane == (uint32_t)leader) b = atomicAdd(&tcnt[o[k]], (unsigned)__popc(grp));
+      b = __shfl_sync(0xFFFFFFFFu, b, leader);
+      pos[k] = b + __popc(grp & ((1u << lane) - 1u));
     }
-    // warp-aggregated reservation per owner
-    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, o);
-    const int leader = __ffs(grp) - 1;
-    unsigned long long pos = 0;
-    if (in && lane == (uint32_t)leader) pos = atomicAdd(cursor + o, (unsigned long long)__popc(grp));
-    pos = __shfl_sync(0xFFFFFFFFu, pos, leader);
-    if (in) out[base[o] + pos + __popc(grp & ((1u << lane) - 1u))] = g;
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < P; r += blockDim.x)
+      tbase[r] = tcnt[r] ? atomicAdd(cursor + r, (unsigned long long)tcnt[r]) : 0ull;
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < PER; ++k) {
+      const uint64_t i = t0 + (uint64_t)k * 256 + threadIdx.x;
+      if (i < n) out[base[o[k]] + tbase[o[k]] + pos[k]] = ev[i];
+    }
   }
 }
 
@@ -150,6 +173,9 @@ __global__ void scan_runs_kernel(const mckg_gaccess* ev, const unsigned long lon
     const uint64_t e = e0 + threadIdx.x;
     if (e < m) {
       const unsigned long long w = keys[e];
+      // a word touched by one access only cannot race: skip without loading
+      const bool single = (e == 0 || keys[e - 1] != w) && (e + 1 >= m || keys[e + 1] != w);
+      if (single) continue;
       const mckg_gaccess X = ev[vals[e]];
       const uint32_t xbid = X.b & 0xFFFFFFu, xtid = ga_tid(X.a);
       const unsigned long long xts = ts_key(X.sweep, xbid, xtid);
@@ -252,6 +278,7 @@ extern "C" int mckg_partition_global(const mckg_gaccess* events, uint64_t n, uin
     return MCKG_E_ARG;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_memory();
   unsigned long long* cursor = nullptr;
   MCKG_CUDA_TRY(cudaMemsetAsync(counts, 0, n_ranks * sizeof(uint64_t), s));
   MCKG_CUDA_TRY(cudaMallocAsync(&cursor, n_ranks * sizeof(unsigned long long), s));
@@ -259,8 +286,10 @@ extern "C" int mckg_partition_global(const mckg_gaccess* events, uint64_t n, uin
   if (n) {
     const uint32_t g = grid_for(n);
     owner_hist_kernel<<<g, 256, 0, s>>>(events, n, n_ranks, addr_space, (unsigned long long*)counts);
-    owner_scatter_kernel<<<g, 256, 0, s>>>(events, n, n_ranks, addr_space, (const unsigned long long*)counts,
-                                           cursor, out);
+    const uint64_t tiles = (n + TILE - 1) / TILE;
+    const uint32_t gs = (uint32_t)(tiles < (uint64_t)sm_count() * 8 ? tiles : (uint64_t)sm_count() * 8);
+    owner_scatter_kernel<<<gs, 256, 0, s>>>(events, n, n_ranks, addr_space, (const unsigned long long*)counts,
+                                            cursor, out);
     MCKG_CUDA_TRY(cudaGetLastError());
   }
   cudaFreeAsync(cursor, s);
@@ -280,6 +309,7 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
     return MCKG_E_RANGE;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_memory();
   MCKG_CUDA_TRY(cudaMemsetAsync(n_races, 0, sizeof(unsigned long long), s));
   if (n == 0) return MCKG_OK;
   uint32_t *nw = nullptr, *off = nullptr, *vals = nullptr, *vals2 = nullptr;

@@ -60,6 +60,7 @@ extern "C" int mckg_scan_stuck(const uint32_t* arrivals, uint32_t n_blocks, uint
     return MCKG_E_ARG;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_memory();
   if (n_blocks == 0) {
     MCKG_CUDA_TRY(cudaMemsetAsync(n_dl, 0, sizeof(uint32_t), s));
     return MCKG_OK;
