@@ -78,6 +78,7 @@ struct Frame {
 struct TS {
   int pc;
   int nv, nscope, nowned, nframe, npobj, ptop;
+  int bb, fn;  // bind base and function of the current frame (cached)
   uint32_t steps, allocs;
   Val vals[VS];
   uint8_t scopeMark[SCOPES];
@@ -85,8 +86,8 @@ struct TS {
   Frame frames[FRAMES];
   uint32_t binds[BINDS];
   PObj pobj[POBJ];
-  uint8_t pbytes[PB];
-  uint8_t pmeta[PB];
+  alignas(8) uint8_t pbytes[PB];
+  alignas(8) uint8_t pmeta[PB];
 };
 
 struct DevDiagRec {
@@ -245,19 +246,20 @@ __device__ __forceinline__ uint32_t priv_id(int idx, uint16_t gen) {
 }
 
 __device__ bool priv_alloc(TS& t, const KP& P, int size, int name, uint32_t& id) {
-  if (t.npobj >= POBJ || t.ptop + size > PB || size < 0 || t.nowned >= OWNED) {
+  const int base = (t.ptop + 7) & ~7;  // 8-byte aligned objects: word-wide scalar access
+  if (t.npobj >= POBJ || base + size > PB || size < 0 || t.nowned >= OWNED) {
     set_error(P, ERR_PRIV, size);
     return false;
   }
   int idx = t.npobj++;
   PObj& o = t.pobj[idx];
   o.gen = (uint16_t)(o.gen + 1);
-  o.off = (uint16_t)t.ptop;
+  o.off = (uint16_t)base;
   o.size = (uint16_t)size;
   o.live = 1;
   o.name = name;
-  for (int i = 0; i < size; ++i) t.pmeta[t.ptop + i] = 0;
-  t.ptop += size;
+  for (int i = 0; i < size; i += 8) *reinterpret_cast<uint64_t*>(t.pmeta + base + i) = 0ull;
+  t.ptop = base + size;
   t.owned[t.nowned++] = (uint8_t)idx;
   ++t.allocs;
   id = priv_id(idx, o.gen);
@@ -282,6 +284,31 @@ __device__ void pop_scopes(TS& t, int depth) {
 __device__ void priv_poke(TS& t, const PObj& o, int64_t off, uint8_t ty, const Val& v) {
   int len = (int)t_scalar(ty);
   int base = o.off;
+  const int a = base + (int)off;
+  if ((len == 4 && (a & 3) == 0) || (len == 8 && (a & 7) == 0)) {
+    // aligned scalar: word-wide; pointer slots near it are cleared only if present
+    const int lo = base + (off - 7 < 0 ? 0 : (int)off - 7), hi = base + (off + len < o.size ? (int)off + len : o.size);
+    uint64_t any = 0;
+    for (int wb = lo & ~7; wb < hi; wb += 8) {
+      const uint64_t w = *reinterpret_cast<const uint64_t*>(t.pmeta + wb);
+      const int s0 = lo - wb > 0 ? lo - wb : 0, s1 = hi - wb < 8 ? hi - wb : 8;
+      const uint64_t msk = (s1 >= 8 ? ~0ull : ((1ull << (8 * s1)) - 1)) & ~((1ull << (8 * s0)) - 1);
+      any |= w & msk & 0x0202020202020202ull;
+    }
+    if (any)
+      for (int64_t s = off - 7 < 0 ? 0 : off - 7; s < off + len && s < o.size; ++s)
+        t.pmeta[base + s] &= (uint8_t)~META_PTR;
+    const uint64_t raw = encode_scalar(v, ty);
+    const bool ptr = v.kind == MCK_K_PTR && v.obj != 0;
+    if (len == 4) {
+      *reinterpret_cast<uint32_t*>(t.pbytes + a) = (uint32_t)raw;
+      *reinterpret_cast<uint32_t*>(t.pmeta + a) |= 0x01010101u * META_DEF;
+    } else {
+      *reinterpret_cast<uint64_t*>(t.pbytes + a) = raw;
+      *reinterpret_cast<uint64_t*>(t.pmeta + a) |= 0x0101010101010101ull * META_DEF | (ptr ? (uint64_t)META_PTR : 0ull);
+    }
+    return;
+  }
   for (int64_t s = off - 7 < 0 ? 0 : off - 7; s < off + len && s < o.size; ++s)
     if (s + 8 > off) t.pmeta[base + s] &= (uint8_t)~META_PTR;
   uint64_t raw = encode_scalar(v, ty);
@@ -571,6 +598,8 @@ __device__ bool enter_fn(TS& t, const KP& P, int fn, int retPc) {
   }
   t.frames[t.nframe++] = f;
   t.scopeMark[t.nscope++] = (uint8_t)t.nowned;
+  t.bb = f.bindBase;
+  t.fn = fn;
   return true;
 }
 
@@ -599,6 +628,8 @@ __device__ bool leave_fn(TS& t, const KP& P, Ctx& c, const Val* v, int line, boo
   }
   push(t, P, out);
   t.pc = f.retPc;
+  t.bb = t.frames[t.nframe - 1].bindBase;
+  t.fn = t.frames[t.nframe - 1].fn;
   return true;
 }
 
@@ -618,7 +649,21 @@ __device__ int mem_read(TS& t, const KP& P, Ctx& c, Thread& th, uint32_t obj, in
   }
   if (r.kind == R_OK_PRIV) {
     bool undef, ps;
-    uint64_t raw = load_raw(t.pbytes + r.base + off, len, undef, t.pmeta + r.base + off, ps);
+    uint64_t raw;
+    const int64_t a = (int64_t)r.base + off;
+    if (len == 4 && (a & 3) == 0) {
+      raw = *reinterpret_cast<const uint32_t*>(t.pbytes + a);
+      const uint32_t m = *reinterpret_cast<const uint32_t*>(t.pmeta + a);
+      undef = (m & 0x01010101u) != 0x01010101u;
+      ps = (m & META_PTR) != 0;
+    } else if (len == 8 && (a & 7) == 0) {
+      raw = *reinterpret_cast<const uint64_t*>(t.pbytes + a);
+      const uint64_t m = *reinterpret_cast<const uint64_t*>(t.pmeta + a);
+      undef = (m & 0x0101010101010101ull) != 0x0101010101010101ull;
+      ps = (m & META_PTR) != 0;
+    } else {
+      raw = load_raw(t.pbytes + a, len, undef, t.pmeta + a, ps);
+    }
     rq.kind = 0;
     rq.ok = true;
     if (MCK_T_PTR(ty) > 0) {
@@ -794,7 +839,7 @@ __device__ __forceinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req&
       push(t, P, mk(MCK_K_FLOAT, in.t, 0, (int64_t)(((uint64_t)(uint32_t)in.b << 32) | (uint32_t)in.a)));
       break;
     case OP_PUSH_LOCAL: {
-      uint32_t o = t.binds[t.frames[t.nframe - 1].bindBase + in.a];
+      uint32_t o = t.binds[t.bb + in.a];
       if (!o) {
         emit_diag(P, c, MCK_D_FIXED_UB, L, MCK_UB_UNBOUND, 0, 0, 0, in.b);
         th.state = S_FIN;
@@ -986,7 +1031,7 @@ __device__ __forceinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req&
       const int argBase = t.nv;
       // args stay in vals[argBase .. argBase+n) until bound (the frame records nv)
       if (!enter_fn(t, P, in.a, t.pc)) { th.state = S_FIN; break; }
-      const int bb = t.frames[t.nframe - 1].bindBase;
+      const int bb = t.bb;
       for (int i = 0; i < n; ++i) {
         const mck_local& pl = local_of(P, in.a, i);
         Val cv;
@@ -1019,8 +1064,8 @@ __device__ __forceinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req&
       break;
     }
     case OP_DECL: {
-      const int fn = t.frames[t.nframe - 1].fn;
-      const int bb = t.frames[t.nframe - 1].bindBase;
+      const int fn = t.fn;
+      const int bb = t.bb;
       if (in.f) {  // extern __shared__: bind the block's array
         t.binds[bb + in.a] = P.sharedBase + c.bid;
         break;
@@ -1036,7 +1081,7 @@ __device__ __forceinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req&
       bool ok = convert(v, in.t, r, d);
       emit_ops(P, c, d, L);
       if (!ok) { th.state = S_FIN; break; }
-      const uint32_t o = t.binds[t.frames[t.nframe - 1].bindBase + in.a];
+      const uint32_t o = t.binds[t.bb + in.a];
       pd.op = OP_INITSTORE;
       pd.postfix = false;
       if (mem_write(t, P, c, th, o, 0, in.t, r, L, rq)) {
@@ -1155,6 +1200,8 @@ __global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kern
     tk.nframe = 1;
     tk.scopeMark[0] = 0;
     tk.nscope = 1;
+    tk.bb = 0;
+    tk.fn = P.kernel;
     for (int i = 0; i < P.nargs; ++i) {
       const mck_local& pl = P.locals[kf.local_base + i];
       uint32_t id;
