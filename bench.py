@@ -184,10 +184,17 @@ def run_ours(args):
     from paper_1211_6193_b200 import _abi, race
 
     ws, rank, local = dist_env()
+    # MCKG_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo -- a functional
+    # dry run of the multi-rank paths on a one-GPU box (not a performance mode)
+    shared = os.environ.get("MCKG_BENCH_SHARED_GPU") == "1"
+    local = 0 if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     blocks = args.blocks
     b0 = blocks * rank // ws
     b1 = blocks * (rank + 1) // ws
@@ -209,7 +216,7 @@ def run_ours(args):
         if ws > 1:
             lf = out.line_first
             lf.bitwise_xor_(-(1 << 63))  # unsigned order -> signed order
-            dist.all_reduce(lf, op=dist.ReduceOp.MIN)
+            _all_reduce(lf, dist.ReduceOp.MIN)
             lf.bitwise_xor_(-(1 << 63))
 
     for _ in range(args.warmup):
@@ -239,8 +246,8 @@ def run_ours(args):
     t = torch.tensor([ms, statistics.mean(k_ms)], dtype=torch.float64, device=dev)
     tot = torch.tensor([nb * EVENTS_PER_BLOCK, n_tri], dtype=torch.int64, device=dev)
     if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        _all_reduce(t, dist.ReduceOp.MAX)
+        _all_reduce(tot, dist.ReduceOp.SUM)
     ms, k_avg = float(t[0]), float(t[1])
     total_events = int(tot[0])
     total_tri = int(tot[1])
@@ -298,6 +305,17 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _all_reduce(t, op):
+    """all_reduce that also works for CUDA tensors on the gloo dry-run backend."""
+    import torch.distributed as dist
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+
+
 def run_c5(args, blocks, dev, ws, rank):
     """C5 (configs[4]): cross-block global races over `blocks` simulated blocks
     sharded over the ranks: K3 partition -> NCCL all-to-all -> K6 detect ->
@@ -321,7 +339,9 @@ def run_c5(args, blocks, dev, ws, rank):
         out = gr.GlobalOut(max(1, mine.shape[0] // 8), device=dev)
         gr.detect(mine, lo, out.reset(), stream)
         if ws > 1:
-            gr.min_allreduce_u64(out.line_first)
+            out.line_first.bitwise_xor_(-(1 << 63))
+            _all_reduce(out.line_first, dist.ReduceOp.MIN)
+            out.line_first.bitwise_xor_(-(1 << 63))
         return out, mine.shape[0]
 
     for _ in range(max(1, args.warmup // 2)):
@@ -342,8 +362,8 @@ def run_c5(args, blocks, dev, ws, rank):
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     tot = torch.tensor([ev.shape[0], n_races, recv], dtype=torch.int64, device=dev)
     if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        _all_reduce(t, dist.ReduceOp.MAX)
+        _all_reduce(tot, dist.ReduceOp.SUM)
     ms = float(t[0])
     events = int(tot[0])
     sent = ev.shape[0] * 16 * (ws - 1) / max(1, ws)  # bytes leaving this rank (uniform partition)

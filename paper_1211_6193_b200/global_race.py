@@ -66,15 +66,21 @@ def exchange(grouped, counts, group=None):
     tensors (gloo)."""
     import torch.distributed as dist
     ws = dist.get_world_size(group)
+    # gloo (CPU tests, one-GPU dry runs) moves host tensors; NCCL moves HBM
+    host = dist.get_backend(group) == "gloo"
+    dev = grouped.device
     send = counts.to(torch.int64)
+    if host:
+        send = send.cpu()
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
     s_list = [int(x) for x in send.cpu().tolist()]
     r_list = [int(x) for x in recv.cpu().tolist()]
-    out = torch.empty((sum(r_list), 4), dtype=grouped.dtype, device=grouped.device)
+    src = grouped.contiguous().cpu() if host else grouped.contiguous()
+    out = torch.empty((sum(r_list), 4), dtype=grouped.dtype, device=src.device)
     assert len(s_list) == ws
-    dist.all_to_all_single(out, grouped.contiguous(), r_list, s_list, group=group)
-    return out
+    dist.all_to_all_single(out, src, r_list, s_list, group=group)
+    return out.to(dev) if host else out
 
 
 class GlobalOut:
