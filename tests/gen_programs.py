@@ -300,3 +300,122 @@ int main(void) {{
   return 0;
 }}
 """
+
+
+def concurrency_program(seed):
+    """Host/device concurrency: two or three kernels on
+    different streams in flight at once, async copies, events, and host loops
+    that poll cudaStreamQuery / cudaEventQuery -- their iteration counts depend
+    on the exact round-robin timing of the grids against the host thread."""
+    rng = random.Random(20_000 + seed)
+    nb1, nt1 = rng.choice([1, 2]), rng.choice([1, 3, 8, 17])
+    nb2, nt2 = rng.choice([1, 2, 3]), rng.choice([2, 5, 16])
+    loops1, loops2 = rng.randint(1, 12), rng.randint(1, 8)
+    poll = rng.choice(["stream", "event", "both"])
+    use_sync = rng.random() < 0.5
+    return f"""#include <stdio.h>
+__global__ void busy(int* g, int n) {{
+  int t = threadIdx.x + blockIdx.x * blockDim.x, i, acc = t;
+  for (i = 0; i < n; ++i) {{ acc = acc * 3 + i; }}
+  g[t] = acc % 1000;
+}}
+__global__ void other(int* g, int off) {{
+  extern __shared__ int s[];
+  int t = threadIdx.x;
+  s[t] = t + off;
+  __syncthreads();
+  g[off + blockIdx.x * blockDim.x + t] = s[(t + 1) % blockDim.x];
+}}
+int main(void) {{
+  int *g, h[128], i, polls = 0, epolls = 0;
+  cudaStream_t s1, s2;
+  cudaEvent_t e1;
+  cudaStreamCreate(&s1);
+  cudaStreamCreate(&s2);
+  cudaEventCreate(&e1);
+  cudaMalloc(&g, 128 * sizeof(int));
+  cudaMemset(g, 0, 128 * sizeof(int));
+  busy<<<{nb1}, {nt1}, 0, s1>>>(g, {loops1});
+  cudaEventRecord(e1, s1);
+  other<<<{nb2}, {nt2}, {nt2} * sizeof(int), s2>>>(g, 64);
+  busy<<<1, 4, 0, s2>>>(g + 100, {loops2});
+  {"while (cudaStreamQuery(s1) != cudaSuccess) { polls++; }" if poll in ("stream", "both") else ""}
+  {"while (cudaEventQuery(e1) == cudaErrorNotReady) { epolls++; }" if poll in ("event", "both") else ""}
+  {"cudaStreamSynchronize(s2);" if use_sync else "cudaDeviceSynchronize();"}
+  cudaMemcpyAsync(h, g, 128 * sizeof(int), cudaMemcpyDeviceToHost, s1);
+  cudaStreamSynchronize(s1);
+  printf("polls=%d epolls=%d\\n", polls, epolls);
+  for (i = 0; i < 128; i += 7) printf("%d ", h[i]);
+  printf("\\n");
+  return 0;
+}}
+"""
+
+
+def numeric_program(seed):
+    """Device-side numerics and memory model: float/double arithmetic and
+    conversions, __device__ globals, __host__ __device__ helpers called from
+    both sides, unsigned / char / long wrap-around, shifts, pointer casts,
+    compound assignments, ternaries, loops with break/continue."""
+    rng = random.Random(30_000 + seed)
+    nt = rng.choice([1, 2, 5, 8, 32])
+    ops = []
+    for _ in range(rng.randint(5, 14)):
+        r = rng.randrange(12)
+        c = rng.randint(1, 9)
+        if r == 0:
+            ops.append(f"f = f * {c}.5f - (float)t;")
+        elif r == 1:
+            ops.append(f"d = d / ({c} + t) + f;")
+        elif r == 2:
+            ops.append(f"u = u * {rng.choice([3, 65537, 2654435761])}u + t; u ^= u >> {c};")
+        elif r == 3:
+            ops.append(f"ch = (char)(ch + {c * 37}); acc += ch;")
+        elif r == 4:
+            ops.append(f"acc += twice(t + {c}) + (int)mix(d, {c});")
+        elif r == 5:
+            ops.append(f"gcount += t; acc += gcount % {c + 1};")
+        elif r == 6:
+            ops.append(f"l = l * {rng.choice([1000003, 7, -5])} + acc; acc = (int)(l % 1000);")
+        elif r == 7:
+            ops.append(f"acc = acc > {c * 10} ? acc - (int)f : acc + (int)d;")
+        elif r == 8:
+            ops.append(f"for (i = 0; i < {c}; ++i) {{ if (i == t) continue; if (i > 6) break; acc += i << (t % 4); }}")
+        elif r == 9:
+            ops.append(f"cp = (char*)&acc; acc += cp[{c % 4}];")
+        elif r == 10:
+            ops.append(f"acc %= {c + 2}; acc -= {c}; acc *= -{c};")
+        else:
+            ops.append(f"f = (float)(int)d; d = (double)u / {c}.0;")
+    body = "\n  ".join(ops)
+    return f"""#include <stdio.h>
+__device__ int gcount;
+__host__ __device__ int twice(int x) {{ return x + x; }}
+__device__ double mix(double a, int b) {{ return a * b - b; }}
+__global__ void k(int* out, float* fo, double* dout) {{
+  int t = threadIdx.x, acc = t, i;
+  unsigned u = 7u;
+  char ch = 'a', *cp;
+  long l = 1;
+  float f = 1.25f;
+  double d = 0.5;
+  {body}
+  out[t] = acc;
+  fo[t] = f;
+  dout[t] = d;
+}}
+int main(void) {{
+  int *o, h[32], i;
+  float *fo, hf[32];
+  double *dd, hd[32];
+  cudaMalloc(&o, 32 * sizeof(int));
+  cudaMalloc(&fo, 32 * sizeof(float));
+  cudaMalloc(&dd, 32 * sizeof(double));
+  k<<<1, {nt}>>>(o, fo, dd);
+  cudaMemcpy(h, o, {nt} * sizeof(int), cudaMemcpyDeviceToHost);
+  cudaMemcpy(hf, fo, {nt} * sizeof(float), cudaMemcpyDeviceToHost);
+  cudaMemcpy(hd, dd, {nt} * sizeof(double), cudaMemcpyDeviceToHost);
+  for (i = 0; i < {nt}; ++i) printf("%d %f %f %d\\n", h[i], hf[i], hd[i], twice(h[i]));
+  return 0;
+}}
+"""

@@ -7,6 +7,8 @@ tests/golden/programs.json, so the GPU box needs no reference build."""
 import gen_programs as gp
 
 RICH = 500
+CONC = 100
+NUMS = 150
 
 
 def corpus():
@@ -26,6 +28,10 @@ def corpus():
         out.append((f"rand{i}", f"rand{i}.cu", gp.random_kernel(i)))
     for i in range(RICH):
         out.append((f"rich{i}", f"rich{i}.cu", gp.random_kernel2(i)))
+    for i in range(CONC):
+        out.append((f"conc{i}", f"conc{i}.cu", gp.concurrency_program(i)))
+    for i in range(NUMS):
+        out.append((f"num{i}", f"num{i}.cu", gp.numeric_program(i)))
     return out
 
 

@@ -9,7 +9,7 @@ import os
 
 import pytest
 
-from program_corpus import RICH, corpus, project
+from program_corpus import CONC, NUMS, RICH, corpus, project
 
 pytestmark = pytest.mark.gpu
 
@@ -73,3 +73,18 @@ def test_matches_reference_default_schedule(name):
     got = project(checker.run_source(src, filename=fname))
     for k, v in SEED0[name].items():
         assert got[k] == v, (name, k)
+
+
+@pytest.mark.parametrize("seed", range(CONC))
+def test_concurrent_streams_and_polling(seed):
+    """Kernels on several streams in flight together, async copies, events, and
+    host loops polling cudaStreamQuery / cudaEventQuery: the poll counts
+    depend on the exact sweep timing of the grids against the host thread."""
+    _check(f"conc{seed}")
+
+
+@pytest.mark.parametrize("seed", range(NUMS))
+def test_device_numerics(seed):
+    """float / double / unsigned / char / long arithmetic and conversions in
+    device code, __device__ globals, __host__ __device__ helpers, pointer casts."""
+    _check(f"num{seed}")
