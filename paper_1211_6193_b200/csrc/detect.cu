@@ -68,7 +68,7 @@ struct Params {
   unsigned long long* n_tri;
   unsigned long long* line_first;
   uint32_t* status;
-  uint32_t debug;  // experiments only: bit0 skip exact pass, bit1 skip filter
+  uint32_t debug;  // experiments only (MCKG_DEBUG): 1 skip exact, 2 skip filter, 8/16 stop early (bisection)
 };
 
 extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -407,7 +407,12 @@ __device__ void process_block(const Lay& L, const Params& P, const uint4* src, u
   }
   if (t == 0) *clcount = 0;
   fsync();
+  if (P.debug & 8u) return;   // experiment: load + bitmap + first P1 only
   if (warp == 0) build_segments(L, n);
+  if (P.debug & 16u) {        // experiment: + epoch segmentation
+    fsync();
+    return;
+  }
   uint32_t cur = cur0;
   uint32_t sidx = 0;
   while (true) {
