@@ -264,8 +264,8 @@ def run_ours(args):
     launches = 2 * args.steps
 
     k1 = None
-    if rank == 0 and ws == 1 and not args.no_k1:
-        k1 = run_k1(args)
+    if not args.no_k1:
+        k1 = run_k1(args, ws, rank, local, shared)
     c5 = None
     if not args.no_c5:
         ev = bs = tr = out = None  # free the C3 trace before C5
@@ -375,26 +375,69 @@ def run_c5(args, blocks, dev, ws, rank):
             "parity": "unpinned (no reference semantics); checker oracle/global_detector.c"}
 
 
-def run_k1(args):
-    """C2 (configs[1]) through the whole checker: K1 thread-steps/s."""
+def _k1_run(src, name, ws, rank, dev, shared):
+    """One whole-checker run; with ws > 1 every rank runs its block range of
+    each grid (NCCL transport; host transport in the shared-GPU dry run)."""
+    from paper_1211_6193_b200 import checker
+    kw = {}
+    if ws > 1:
+        import torch.distributed as dist
+        kw = dict(rank=rank, world=ws, device=dev)
+        if shared:
+            kw["allgather"] = checker.torch_allgather()
+        else:
+            obj = [checker.comm_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            kw["comm"] = obj[0]
+    t0 = time.perf_counter()
+    r = checker.run_source(src, name, step_limit=8_000_000_000, **kw)
+    return r, time.perf_counter() - t0
+
+
+def run_k1(args, ws=1, rank=0, dev=0, shared=False):
+    """C2 (configs[1]) and C4 (configs[3]) through the whole checker: K1
+    thread-steps/s (device steps / max-over-ranks grid time)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import gen_programs as gp
-    from paper_1211_6193_b200 import checker
     src = gp.scaled(1 << 24, 256, racy=args.k1_racy)
-    t0 = time.perf_counter()
-    r = checker.run_source(src, "c2.cu", step_limit=8_000_000_000)
-    wall = time.perf_counter() - t0
+    r, wall = _k1_run(src, "c2.cu", ws, rank, dev, shared)
     st = r["stats"]
     gs = st["grid_ms"] / 1e3
     ok = (r["output"] == "OUTPUT: 830472184\n" and r["exit"] == 0) if not args.k1_racy else r["exit"] == 1
-    return {"workload": "C2: Fig. 1 reduction, 2^24 ints, 65536 blocks x 256 threads"
-                        + (" (racy variant)" if args.k1_racy else ""),
-            "thread_steps_per_s": st["device_steps"] / gs, "shared_events_per_s": st["shared_events"] / gs,
-            "grid_ms": st["grid_ms"], "device_steps": st["device_steps"], "barrier_rules": st["barrier_rules"],
-            "shared_events": st["shared_events"], "total_steps": r["steps"], "host_steps": st["host_steps"],
-            "wall_s_end_to_end": wall, "output_ok": ok, "engine_error": r.get("engine_error", ""),
-            "kernel_launches": st["kernel_launches"],
-            "note": "reference CPU checker is quadratic in threads here (SURVEY F1: ~25 years extrapolated)"}
+    out = {"workload": "C2: Fig. 1 reduction, 2^24 ints, 65536 blocks x 256 threads"
+                       + (" (racy variant)" if args.k1_racy else ""),
+           "parallelism": f"block-range shard over {ws} rank(s)",
+           "thread_steps_per_s": st["device_steps"] / gs, "shared_events_per_s": st["shared_events"] / gs,
+           "grid_ms": st["grid_ms"], "device_steps": st["device_steps"], "barrier_rules": st["barrier_rules"],
+           "shared_events": st["shared_events"], "total_steps": r["steps"], "host_steps": st["host_steps"],
+           "wall_s_end_to_end": wall, "output_ok": ok, "engine_error": r.get("engine_error", ""),
+           "kernel_launches": st["kernel_launches"],
+           "note": "reference CPU checker is quadratic in threads here (SURVEY F1: ~25 years extrapolated)"}
+    if not args.no_c4:
+        nb = 1 << 16
+        r4, wall4 = _k1_run(gp.divergent_barrier_gen(nb, 1024, 0), "c4.cu", ws, rank, dev, shared)
+        st4 = r4["stats"]
+        stuck = [s for s in r4["stuck_reports"] if s["kind"] == "barrier"]
+        # closed form: blocks b % 3 == 1 are all-odd (no deadlock), b % 3 == 0
+        # all-even; b % 3 == 2 mixes parities -> deadlocked
+        import numpy as np
+        i = np.arange(nb * 1024, dtype=np.int64).reshape(nb, 1024)
+        b = np.arange(nb, dtype=np.int64)[:, None]
+        v = np.where(b % 3 == 0, 2 * i, np.where(b % 3 == 1, 2 * i + 1, (i * 3 + b) % 7))
+        odd = (v % 2) == 1
+        mixed = odd.any(1) & ~odd.all(1)
+        exp_bids = np.nonzero(mixed)[0].tolist()
+        got_bids = [s["bid"] for s in stuck]
+        ok4 = r4["exit"] == 3 and got_bids == exp_bids and all(
+            s["waiting"] == np.nonzero(odd[s["bid"]])[0].tolist() for s in stuck[:64])
+        out["c4"] = {"workload": "C4: divergent-barrier deadlock sweep, 2^16 blocks x 1024 threads",
+                     "deadlocks_ok": bool(ok4),
+                     "thread_steps_per_s": st4["device_steps"] / (st4["grid_ms"] / 1e3),
+                     "grid_ms": st4["grid_ms"], "device_steps": st4["device_steps"],
+                     "barrier_rules": st4["barrier_rules"], "deadlocked_blocks": len(stuck),
+                     "wall_s_end_to_end": wall4, "exit": r4["exit"],
+                     "engine_error": r4.get("engine_error", ""), "kernel_launches": st4["kernel_launches"]}
+    return out if rank == 0 else None
 
 
 def run_e2e(args, torch, race, _abi):
@@ -447,6 +490,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-k1", action="store_true")
     ap.add_argument("--k1-racy", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the K1 C4 deadlock-sweep leg")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--c5-blocks", type=int, default=0,
                     help="C5 blocks in total (default 2^16 per GPU; BASELINE: 2^20 over 8 GPUs)")

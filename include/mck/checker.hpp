@@ -78,6 +78,12 @@ struct RunOptions {
   ArchParams arch;
   // B200 extensions (not in the reference):
   int device = 0;             // CUDA device ordinal of the grid engine
+  std::vector<int> devices;   // several devices: each grid's blocks are split across them
+  int rank = 0, world = 1;    // one process per GPU: this rank runs its share of every grid's
+  std::vector<uint8_t> commId;  // blocks; 128-byte NCCL id from mck::makeCommId on rank 0
+  // host transport instead of NCCL (gather n bytes per rank, rank order; 0 = ok)
+  int (*allgather)(void* ctx, const void* send, uint64_t n, void* recv) = nullptr;
+  void* allgatherCtx = nullptr;
   bool globalRaceCheck = false;  // SURVEY Appendix E (off: reference-identical output)
 };
 
@@ -150,6 +156,10 @@ class Machine {
   RunOptions opts_;
   std::unique_ptr<MachineImpl> impl_;
 };
+
+// A fresh 128-byte communicator id for RunOptions::commId (rank 0 makes it,
+// the launcher broadcasts it).  Empty on failure.
+std::vector<uint8_t> makeCommId();
 
 std::string formatStuckReports(const std::vector<StuckReport>& reports);
 

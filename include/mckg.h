@@ -305,7 +305,19 @@ typedef struct mck_run_opts {
   int32_t round_robin;        /* 1 = SchedulePolicy::RoundRobin (the engine's schedule) */
   int32_t device;             /* CUDA device ordinal                                    */
   int32_t max_threads_per_block; /* ArchParams::maxThreadsPerBlock, 0 = 1024           */
+  int32_t n_devices;          /* > 0: split every grid over devices[0 .. n_devices)    */
+  int32_t devices[8];         /* CUDA ordinals; repeating one = virtual devices (tests) */
+  int32_t rank;               /* world > 1: one process per GPU; this rank runs blocks  */
+  int32_t world;              /*   [gridDim*rank/world, gridDim*(rank+1)/world)          */
+  uint8_t comm_id[128];       /* from mckg_comm_id() on rank 0, broadcast by the caller  */
+  /* optional host transport instead of NCCL (ranks sharing a GPU, tests):
+   * gather n bytes from every rank into recv[world*n] in rank order, 0 = ok */
+  int (*allgather)(void* ctx, const void* send, uint64_t n, void* recv);
+  void* allgather_ctx;
 } mck_run_opts;
+
+/* A fresh NCCL communicator id for mck_run_opts.comm_id. */
+int mckg_comm_id(uint8_t out[128]);
 
 /* JSON keys: exit, output, steps, stuck, main_return, diags[{cat,sev,msg,line}],
  * stuck_reports[{kind,gid,bid,waiting,missing,reason}], report_text,

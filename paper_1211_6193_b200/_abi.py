@@ -43,6 +43,7 @@ EXPORTS = [
     "mckg_gen_c5",
     "mckg_partition_global",
     "mckg_detect_global",
+    "mckg_comm_id",
     "mck_run_source",
     "mck_disassemble",
     "mck_free",

@@ -31,6 +31,7 @@
 // Triples (obj, byte, line) are deduplicated per block and appended; the
 // first racing timestamp per line is atomicMin'ed into a line table.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -128,6 +129,8 @@ struct KP {
   uint8_t* gmeta;
   int raceCheck;
   int htBits;                 // conflict hash size = 1 << htBits
+  uint32_t bidBase;           // first simulated block of this launch (multi-device split)
+  int markDirty;              // record global writes in META_DIRTY (replicated memory)
   uint32_t maxSweeps;         // < 2^26; each sweep takes >= 1 step (step limit)
   // outputs
   unsigned long long* lineFirst;
@@ -258,7 +261,11 @@ __device__ bool priv_alloc(TS& t, const KP& P, int size, int name, uint32_t& id)
   o.size = (uint16_t)size;
   o.live = 1;
   o.name = name;
-  for (int i = 0; i < size; i += 8) *reinterpret_cast<uint64_t*>(t.pmeta + base + i) = 0ull;
+  // fresh objects read as zero bytes, undefined (MemObject::bytes.resize, memory.cpp:30)
+  for (int i = 0; i < size; i += 8) {
+    *reinterpret_cast<uint64_t*>(t.pmeta + base + i) = 0ull;
+    *reinterpret_cast<uint64_t*>(t.pbytes + base + i) = 0ull;
+  }
   t.ptop = base + size;
   t.owned[t.nowned++] = (uint8_t)idx;
   ++t.allocs;
@@ -750,8 +757,11 @@ __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq
   if (rq.kind == 2) {
     if (rq.space == R_OK_SHARED)
       store_raw(smem + L.bytes, smem + L.meta, rq.size, rq.off, len, rq.raw, rq.ptr);
-    else
+    else {
       store_raw(P.gbytes + rq.base, P.gmeta + rq.base, rq.size, rq.off, len, rq.raw, rq.ptr);
+      if (P.markDirty)
+        for (int i = 0; i < len; ++i) meta_or(P.gmeta + rq.base, rq.off + i, META_DIRTY);
+    }
     rq.ok = true;
     return;
   }
@@ -1123,7 +1133,8 @@ __device__ __forceinline__ int ht_insert(unsigned long long* keys, uint32_t* val
 // per block) need; inside a sweep the K sub-threads step in tid order.
 template <int K>
 __global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kernel(KP P) {
-  const uint32_t bid = blockIdx.x;
+  const uint32_t bid = blockIdx.x + P.bidBase;  // simulated block
+  const uint32_t lb = blockIdx.x;               // index into this launch's outputs
   const uint32_t g = threadIdx.x;
   const uint32_t CT = blockDim.x;
   const uint32_t SLOTS = CT * K;
@@ -1485,7 +1496,7 @@ __global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kern
       const bool waiting = tid < n && th[k].state == S_WAIT;
       const uint32_t m = __ballot_sync(0xFFFFFFFFu, waiting);
       const uint32_t word = ((uint32_t)k * CT + (myWarp << 5)) >> 5;
-      if (lane == 0 && word < words) P.waitMask[(size_t)bid * words + word] = m;
+      if (lane == 0 && word < words) P.waitMask[(size_t)lb * words + word] = m;
     }
   }
   atomicAdd(&bs.steps, steps);
@@ -1508,7 +1519,7 @@ __global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kern
     if (g == 0 && firstNot >= 1) rules += firstNot - 1;
   }
   if (g == 0) {
-    BlockOut& o = P.blocks[bid];
+    BlockOut& o = P.blocks[lb];
     o.sweeps = sweep;
     o.soloSweeps = soloSweeps;
     o.cycles = (unsigned long long)(clock64() - kStart);
@@ -1566,17 +1577,149 @@ static int kForceK = [] {
   return e ? atoi(e) : 0;
 }();
 
+__global__ void init_ts_kernel(k1::DevDiagRec* p, uint32_t n) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i].ts = ~0ull;
+}
+
+// dst <- src for every byte src wrote in the grid (META_DIRTY)
+__global__ void merge_dirty_kernel(uint8_t* db, uint8_t* dm, const uint8_t* sb, const uint8_t* sm, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t m = sm[i];
+    if (m & META_DIRTY) {
+      db[i] = sb[i];
+      dm[i] = m;
+    }
+  }
+}
+
+__global__ void clear_dirty_kernel(uint8_t* m, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    m[i] &= (uint8_t)~META_DIRTY;
+}
+
+// [lo, hi) of the bytes written by the grid (lohi = {lo, ~hi}, both atomicMin)
+__global__ void dirty_range_kernel(const uint8_t* m, uint64_t n, unsigned long long* lohi) {
+  unsigned long long lo = ~0ull, nhi = ~0ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (m[i] & META_DIRTY) {
+      lo = min(lo, (unsigned long long)i);
+      nhi = min(nhi, ~(unsigned long long)(i + 1));
+    }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    nhi = min(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+  }
+  if ((threadIdx.x & 31) == 0 && lo != ~0ull) {
+    atomicMin(lohi, lo);
+    atomicMin(lohi + 1, nhi);
+  }
+}
+
+// one 32-bit word per byte: written ? (rank+1)<<16 | meta<<8 | byte : 0, so
+// an all-reduce MAX picks the highest rank's write (the same rule as the
+// local replica merge: a later block range wins)
+__global__ void pack_dirty_kernel(const uint8_t* b, const uint8_t* m, uint64_t lo, uint64_t n, uint32_t* w,
+                                  uint32_t tag) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t mm = m[lo + i];
+    w[i] = (mm & META_DIRTY) ? (tag << 16 | (uint32_t)mm << 8 | b[lo + i]) : 0u;
+  }
+}
+
+__global__ void unpack_dirty_kernel(uint8_t* b, uint8_t* m, uint64_t lo, uint64_t n, const uint32_t* w) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = w[i];
+    if (v) {
+      b[lo + i] = (uint8_t)v;
+      m[lo + i] = (uint8_t)(v >> 8);
+    }
+  }
+}
+
+// One replica of device-global memory and the per-launch buffers of one
+// device.  Several replicas may share a physical device ("virtual devices",
+// used to test the multi-device split on one GPU).
+struct Replica {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  uint8_t* bytes = nullptr;
+  uint8_t* meta = nullptr;
+  uint64_t cap = 0;
+  const Program* prog = nullptr;
+  DBuf<mck_ins> code;
+  DBuf<mck_fn> fns;
+  DBuf<mck_local> locals;
+  DBuf<uint32_t> ids, glob, ranges, wait;
+  DBuf<DevObjInfo> objs;
+  DBuf<mck_core::Val> args;
+  DBuf<unsigned long long> line, ntri;
+  DBuf<int32_t> tri;
+  DBuf<k1::DevDiagRec> diag;
+  DBuf<k1::BlockOut> blocks;
+  DBuf<int> err;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  uint32_t b0 = 0, nb = 0;
+};
+
 class CudaEngine final : public DeviceEngine {
  public:
-  explicit CudaEngine(int dev) : dev_(dev) {}
+  CudaEngine(std::vector<int> devs, const EngineComm& comm) : devs_(std::move(devs)), comm_(comm) {}
   ~CudaEngine() override {
-    if (bytes_) cudaFree(bytes_);
-    if (meta_) cudaFree(meta_);
-    if (stream_) cudaStreamDestroy(stream_);
+    if (nccl_) ncclCommDestroy(nccl_);
+    for (auto& r : reps_) {
+      cudaSetDevice(r.dev);
+      if (r.bytes) cudaFree(r.bytes);
+      if (r.meta) cudaFree(r.meta);
+      if (r.e0) cudaEventDestroy(r.e0);
+      if (r.e1) cudaEventDestroy(r.e1);
+      if (r.stream) cudaStreamDestroy(r.stream);
+    }
   }
   bool init(std::string& err) {
-    CK(cudaSetDevice(dev_));
-    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    reps_.resize(devs_.size());
+    for (size_t i = 0; i < devs_.size(); ++i) {
+      Replica& r = reps_[i];
+      r.dev = devs_[i];
+      CK(cudaSetDevice(r.dev));
+      CK(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
+      CK(cudaEventCreate(&r.e0));
+      CK(cudaEventCreate(&r.e1));
+    }
+    // peer access between distinct physical devices (NVLink / NVSwitch)
+    for (size_t i = 0; i < devs_.size(); ++i)
+      for (size_t j = 0; j < devs_.size(); ++j) {
+        if (devs_[i] == devs_[j]) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, devs_[i], devs_[j]);
+        if (!can) {
+          err = "devices " + std::to_string(devs_[i]) + " and " + std::to_string(devs_[j]) + " have no peer access";
+          return false;
+        }
+        cudaSetDevice(devs_[i]);
+        cudaError_t e = cudaDeviceEnablePeerAccess(devs_[j], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          err = std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e);
+          return false;
+        }
+        cudaGetLastError();
+      }
+    if (comm_.world > 1 && !comm_.allgather) {
+      if (comm_.rank < 0 || comm_.rank >= comm_.world) {
+        err = "rank outside 0..world-1";
+        return false;
+      }
+      ncclUniqueId id;
+      static_assert(sizeof(id.internal) == 128, "ncclUniqueId");
+      std::memcpy(id.internal, comm_.id.data(), 128);
+      CK(cudaSetDevice(reps_[0].dev));
+      ncclResult_t r = ncclCommInitRank(&nccl_, comm_.world, id, comm_.rank);
+      if (r != ncclSuccess) {
+        err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+        nccl_ = nullptr;
+        return false;
+      }
+    }
     return true;
   }
   bool hasDevice() const override { return true; }
@@ -1584,25 +1727,37 @@ class CudaEngine final : public DeviceEngine {
   uint64_t alloc(int64_t size) override {
     uint64_t b = (top_ + 15) & ~15ull;
     uint64_t need = b + (uint64_t)size;
-    if (need > cap_) grow(need);
+    for (auto& r : reps_)
+      if (need > r.cap) grow(r, need);
     top_ = need;
     return b;
   }
   void write(uint64_t base, const uint8_t* b, const uint8_t* m, int64_t n) override {
-    cudaMemcpy(bytes_ + base, b, (size_t)n, cudaMemcpyHostToDevice);
-    cudaMemcpy(meta_ + base, m, (size_t)n, cudaMemcpyHostToDevice);
+    for (auto& r : reps_) {
+      cudaSetDevice(r.dev);
+      cudaMemcpy(r.bytes + base, b, (size_t)n, cudaMemcpyHostToDevice);
+      cudaMemcpy(r.meta + base, m, (size_t)n, cudaMemcpyHostToDevice);
+    }
   }
   void read(uint64_t base, uint8_t* b, uint8_t* m, int64_t n) override {
-    cudaMemcpy(b, bytes_ + base, (size_t)n, cudaMemcpyDeviceToHost);
-    cudaMemcpy(m, meta_ + base, (size_t)n, cudaMemcpyDeviceToHost);
+    Replica& r = reps_[0];
+    cudaSetDevice(r.dev);
+    cudaMemcpy(b, r.bytes + base, (size_t)n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(m, r.meta + base, (size_t)n, cudaMemcpyDeviceToHost);
   }
   void copy(uint64_t dst, uint64_t src, int64_t n) override {
-    cudaMemcpy(bytes_ + dst, bytes_ + src, (size_t)n, cudaMemcpyDeviceToDevice);
-    cudaMemcpy(meta_ + dst, meta_ + src, (size_t)n, cudaMemcpyDeviceToDevice);
+    for (auto& r : reps_) {
+      cudaSetDevice(r.dev);
+      cudaMemcpy(r.bytes + dst, r.bytes + src, (size_t)n, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(r.meta + dst, r.meta + src, (size_t)n, cudaMemcpyDeviceToDevice);
+    }
   }
   void fill(uint64_t base, uint8_t v, uint8_t m, int64_t n) override {
-    cudaMemset(bytes_ + base, v, (size_t)n);
-    cudaMemset(meta_ + base, m, (size_t)n);
+    for (auto& r : reps_) {
+      cudaSetDevice(r.dev);
+      cudaMemset(r.bytes + base, v, (size_t)n);
+      cudaMemset(r.meta + base, m, (size_t)n);
+    }
   }
   bool runGrid(const GridSpec& g, GridResult& out) override {
     std::string err;
@@ -1612,32 +1767,32 @@ class CudaEngine final : public DeviceEngine {
   }
 
  private:
-  int dev_;
-  cudaStream_t stream_ = nullptr;
-  uint8_t* bytes_ = nullptr;
-  uint8_t* meta_ = nullptr;
-  uint64_t cap_ = 0, top_ = 0;
-  const Program* progCached_ = nullptr;
-  DBuf<mck_ins> code_;
-  DBuf<mck_fn> fns_;
-  DBuf<mck_local> locals_;
+  std::vector<int> devs_;
+  EngineComm comm_;
+  ncclComm_t nccl_ = nullptr;
+  std::vector<Replica> reps_;
+  uint64_t top_ = 0;
+  DBuf<unsigned long long> lohi_;
+  DBuf<uint32_t> packed_;
+  DBuf<uint8_t> blobs_;
 
-  void grow(uint64_t need) {
-    uint64_t nc = std::max<uint64_t>(need, std::max<uint64_t>(cap_ * 2, 1ull << 20));
+  void grow(Replica& r, uint64_t need) {
+    cudaSetDevice(r.dev);
+    uint64_t nc = std::max<uint64_t>(need, std::max<uint64_t>(r.cap * 2, 1ull << 20));
     uint8_t *nb = nullptr, *nm = nullptr;
     cudaMalloc(&nb, nc);
     cudaMalloc(&nm, nc);
     cudaMemset(nb, 0, nc);
     cudaMemset(nm, 0, nc);
-    if (bytes_) {
-      cudaMemcpy(nb, bytes_, top_, cudaMemcpyDeviceToDevice);
-      cudaMemcpy(nm, meta_, top_, cudaMemcpyDeviceToDevice);
-      cudaFree(bytes_);
-      cudaFree(meta_);
+    if (r.bytes) {
+      cudaMemcpy(nb, r.bytes, top_, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(nm, r.meta, top_, cudaMemcpyDeviceToDevice);
+      cudaFree(r.bytes);
+      cudaFree(r.meta);
     }
-    bytes_ = nb;
-    meta_ = nm;
-    cap_ = nc;
+    r.bytes = nb;
+    r.meta = nm;
+    r.cap = nc;
   }
 
   template <typename T>
@@ -1647,7 +1802,7 @@ class CudaEngine final : public DeviceEngine {
     return true;
   }
 
-  bool run(const GridSpec& g, GridResult& out, std::string& err) {
+  bool runLocal(const GridSpec& g, GridResult& out, std::string& err) {
     using namespace k1;
     const Program& P = *g.prog;
     if (g.blockDim > 1024) {
@@ -1658,13 +1813,6 @@ class CudaEngine final : public DeviceEngine {
       out.error = "gridDim > 2^26 is not supported by the B200 engine";
       return false;
     }
-    CK(cudaSetDevice(dev_));
-    if (progCached_ != &P) {
-      if (!upload(code_, P.code, err) || !upload(fns_, P.fns, err) || !upload(locals_, P.locals, err)) return false;
-      progCached_ = &P;
-    }
-    // K simulated threads per GPU thread: CTAs of 64-128 threads keep up to
-    // 32 simulated blocks resident per SM (serial stretches need residency)
     // measured (round 1): C4 1024-thread blocks 33 -> 20 ms with K = 4; the
     // 256-thread C2 blocks are fastest with K = 1 (local-memory bound)
     int K = g.blockDim > 256 ? 4 : 1;
@@ -1679,203 +1827,514 @@ class CudaEngine final : public DeviceEngine {
                   " bytes) exceeds the engine's on-chip shadow capacity";
       return false;
     }
-    // tables
+    void (*kern)(KP) = K == 1 ? grid_kernel<1> : K == 2 ? grid_kernel<2> : K == 4 ? grid_kernel<4> : grid_kernel<8>;
+    const size_t total = (size_t)g.gridDim;
+    const size_t D = reps_.size();
+    const uint32_t words = (uint32_t)((g.blockDim + 31) / 32);
+    const uint32_t diagN = 1u << 18;
     std::vector<uint32_t> ids;
     for (const auto& o : g.objects) ids.push_back(o.id);
-    DBuf<uint32_t> dIds, dGlob, dRanges;
-    DBuf<DevObjInfo> dObjs;
-    DBuf<Val> dArgs;
-    if (!upload(dIds, ids, err) || !upload(dObjs, g.objects, err) || !upload(dGlob, g.globalIds, err) ||
-        !upload(dArgs, g.args, err))
-      return false;
     std::vector<uint32_t> rng;
     for (const auto& r : g.sharedRanges) rng.insert(rng.end(), r.begin(), r.end());
-    if (!upload(dRanges, rng, err)) return false;
-    // outputs
-    const size_t nb = (size_t)g.gridDim;
-    const uint32_t words = (uint32_t)((g.blockDim + 31) / 32);
-    DBuf<unsigned long long> dLine, dNTri;
-    DBuf<int32_t> dTri;
-    DBuf<DevDiagRec> dDiag;
-    DBuf<BlockOut> dBlocks;
-    DBuf<uint32_t> dWait;
-    DBuf<int> dErr;
-    // racy grids report up to ~shmem bytes x lines per block (C2 racy: 508/block)
-    const unsigned long long triCap =
-        g.raceCheck ? std::min<unsigned long long>(1ull << 28, std::max<unsigned long long>(1ull << 22, nb * 1024ull))
-                    : 1;
-    const uint32_t diagN = 1u << 18;
-    if (!dLine.ensure(LINES, err) || !dNTri.ensure(1, err) || !dTri.ensure(3 * triCap, err) ||
-        !dDiag.ensure(diagN, err) || !dBlocks.ensure(nb, err) || !dWait.ensure(nb * words, err) ||
-        !dErr.ensure(2, err))
-      return false;
-    CK(cudaMemsetAsync(dLine.p, 0xFF, LINES * sizeof(unsigned long long), stream_));
-    CK(cudaMemsetAsync(dNTri.p, 0, sizeof(unsigned long long), stream_));
-    CK(cudaMemsetAsync(dDiag.p, 0, diagN * sizeof(DevDiagRec), stream_));
-    CK(cudaMemsetAsync(dWait.p, 0, nb * words * sizeof(uint32_t), stream_));
-    CK(cudaMemsetAsync(dErr.p, 0, 2 * sizeof(int), stream_));
-    KP kp;
-    kp.code = code_.p;
-    kp.fns = fns_.p;
-    kp.locals = locals_.p;
-    kp.kernel = g.kernel;
-    kp.nargs = (int)g.args.size();
-    kp.args = dArgs.p;
-    kp.gid = g.gid;
-    kp.sharedBase = g.sharedBase;
-    kp.nextId = g.nextId;
-    kp.gridDim = g.gridDim;
-    kp.blockDim = g.blockDim;
-    kp.shmem = g.shmemBytes;
     const mck_fn& kf = P.fns[(size_t)g.kernel];
-    kp.sharedName = kf.dyn_shared_slot >= 0 ? P.locals[(size_t)(kf.local_base + kf.dyn_shared_slot)].name
-                                            : P.sharedDefaultName;
-    kp.warpSize = g.warpSize;
-    kp.objIds = dIds.p;
-    kp.objs = dObjs.p;
-    kp.nobjs = (int)g.objects.size();
-    kp.globalIds = dGlob.p;
-    kp.shRanges = dRanges.p;
-    kp.nranges = (int)g.sharedRanges.size();
-    kp.gbytes = bytes_;
-    kp.gmeta = meta_;
-    kp.raceCheck = g.raceCheck ? 1 : 0;
-    kp.htBits = htBits;
-    kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
-    kp.lineFirst = dLine.p;
-    kp.triples = dTri.p;
-    kp.tripleCap = triCap;
-    kp.nTriples = dNTri.p;
-    kp.diags = dDiag.p;
-    kp.diagMask = diagN - 1;
-    kp.blocks = dBlocks.p;
-    kp.waitMask = dWait.p;
-    kp.error = dErr.p;
-    kp.errorInfo = dErr.p + 1;
-    void (*kern)(KP) = K == 1 ? grid_kernel<1> : K == 2 ? grid_kernel<2> : K == 4 ? grid_kernel<4> : grid_kernel<8>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.end));
-    init_diag_ts(dDiag.p, diagN, stream_);  // ts := +inf
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, stream_);
-    kern<<<(unsigned)nb, threads, L.end, stream_>>>(kp);
-    cudaEventRecord(e1, stream_);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(stream_));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    out.ms = ms;
-    out.launches = 2;
-    int herr[2];
-    CK(cudaMemcpy(herr, dErr.p, sizeof herr, cudaMemcpyDeviceToHost));
-    if (herr[0]) {
-      static const char* why[] = {"", "thread value/scope/frame stack overflow", "private memory of a thread exceeds the engine limit",
-                                  "a pointer to a thread-private object was stored to shared or global memory",
-                                  "too many distinct diagnostics", "too many reported race triples",
-                                  "source line outside 0..65535", "sweep budget exhausted (step limit or 2^26 sweeps)", "bad opcode"};
-      out.error = std::string("B200 engine limitation: ") + why[herr[0] < 9 ? herr[0] : 0] + " (info " +
-                  std::to_string(herr[1]) + ")";
-      return false;
+    std::vector<unsigned long long> triCaps(D);
+    // host-issued copies/memsets run on the legacy stream, which does not
+    // order against the engine's non-blocking streams
+    for (const auto& R : reps_) {
+      CK(cudaSetDevice(R.dev));
+      CK(cudaStreamSynchronize(nullptr));
     }
-    // block outcomes
-    std::vector<BlockOut> bo(nb);
-    CK(cudaMemcpy(bo.data(), dBlocks.p, nb * sizeof(BlockOut), cudaMemcpyDeviceToHost));
-    std::vector<uint32_t> wm;
-    bool anyDl = false;
-    for (const auto& b : bo) {
-      out.sweeps += b.sweeps;
-      out.soloSweeps += b.soloSweeps;
-      out.blockCycles += b.cycles;
-      out.soloCycles += b.soloCycles;
-      out.deviceSteps += b.steps;
-      out.barrierRules += b.rules;
-      out.allocs += b.allocs;
-      out.sharedEvents += b.sharedEvents;
-      out.duration = std::max(out.duration, b.lastSweep);
-      if (b.deadlocked) anyDl = true;
+    // ---- launch every replica's block range ----
+    // this rank's block range (one process per GPU under torchrun), split
+    // again over the local replicas
+    const size_t G0 = total * (size_t)comm_.rank / (size_t)comm_.world;
+    const size_t GN = total * (size_t)(comm_.rank + 1) / (size_t)comm_.world - G0;
+    for (size_t ri = 0; ri < D; ++ri) {
+      Replica& R = reps_[ri];
+      R.b0 = (uint32_t)(G0 + GN * ri / D);
+      R.nb = (uint32_t)(G0 + GN * (ri + 1) / D) - R.b0;
+      if (R.nb == 0) continue;
+      CK(cudaSetDevice(R.dev));
+      if (R.prog != &P) {
+        if (!upload(R.code, P.code, err) || !upload(R.fns, P.fns, err) || !upload(R.locals, P.locals, err))
+          return false;
+        R.prog = &P;
+      }
+      if (!upload(R.ids, ids, err) || !upload(R.objs, g.objects, err) || !upload(R.glob, g.globalIds, err) ||
+          !upload(R.args, g.args, err) || !upload(R.ranges, rng, err))
+        return false;
+      const size_t nb = R.nb;
+      // racy grids report up to ~shmem bytes x lines per block (C2 racy: 508/block)
+      triCaps[ri] = g.raceCheck ? std::min<unsigned long long>(1ull << 28, std::max<unsigned long long>(1ull << 22, nb * 1024ull))
+                                : 1;
+      if (!R.line.ensure(LINES, err) || !R.ntri.ensure(1, err) || !R.tri.ensure(3 * triCaps[ri], err) ||
+          !R.diag.ensure(diagN, err) || !R.blocks.ensure(nb, err) || !R.wait.ensure(nb * words, err) ||
+          !R.err.ensure(2, err))
+        return false;
+      CK(cudaMemsetAsync(R.line.p, 0xFF, LINES * sizeof(unsigned long long), R.stream));
+      CK(cudaMemsetAsync(R.ntri.p, 0, sizeof(unsigned long long), R.stream));
+      CK(cudaMemsetAsync(R.diag.p, 0, diagN * sizeof(DevDiagRec), R.stream));
+      CK(cudaMemsetAsync(R.wait.p, 0, nb * words * sizeof(uint32_t), R.stream));
+      CK(cudaMemsetAsync(R.err.p, 0, 2 * sizeof(int), R.stream));
+      init_ts_kernel<<<(diagN + 255) / 256, 256, 0, R.stream>>>(R.diag.p, diagN);
+      KP kp;
+      kp.code = R.code.p;
+      kp.fns = R.fns.p;
+      kp.locals = R.locals.p;
+      kp.kernel = g.kernel;
+      kp.nargs = (int)g.args.size();
+      kp.args = R.args.p;
+      kp.gid = g.gid;
+      kp.sharedBase = g.sharedBase;
+      kp.nextId = g.nextId;
+      kp.gridDim = g.gridDim;
+      kp.blockDim = g.blockDim;
+      kp.shmem = g.shmemBytes;
+      kp.sharedName = kf.dyn_shared_slot >= 0 ? P.locals[(size_t)(kf.local_base + kf.dyn_shared_slot)].name
+                                              : P.sharedDefaultName;
+      kp.warpSize = g.warpSize;
+      kp.objIds = R.ids.p;
+      kp.objs = R.objs.p;
+      kp.nobjs = (int)g.objects.size();
+      kp.globalIds = R.glob.p;
+      kp.shRanges = R.ranges.p;
+      kp.nranges = (int)g.sharedRanges.size();
+      kp.gbytes = R.bytes;
+      kp.gmeta = R.meta;
+      kp.raceCheck = g.raceCheck ? 1 : 0;
+      kp.htBits = htBits;
+      kp.bidBase = R.b0;
+      kp.markDirty = (D > 1 || comm_.world > 1) ? 1 : 0;
+      kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
+      kp.lineFirst = R.line.p;
+      kp.triples = R.tri.p;
+      kp.tripleCap = triCaps[ri];
+      kp.nTriples = R.ntri.p;
+      kp.diags = R.diag.p;
+      kp.diagMask = diagN - 1;
+      kp.blocks = R.blocks.p;
+      kp.waitMask = R.wait.p;
+      kp.error = R.err.p;
+      kp.errorInfo = R.err.p + 1;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.end));
+      cudaEventRecord(R.e0, R.stream);
+      kern<<<(unsigned)nb, threads, L.end, R.stream>>>(kp);
+      cudaEventRecord(R.e1, R.stream);
+      CK(cudaGetLastError());
     }
-    out.deadlocked = anyDl;
-    if (anyDl) {
-      wm.resize(nb * words);
-      CK(cudaMemcpy(wm.data(), dWait.p, wm.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-      for (size_t b = 0; b < nb; ++b) {
-        if (!bo[b].deadlocked) continue;
-        GridResult::Stuck s;
-        s.bid = (uint32_t)b;
-        for (uint32_t t = 0; t < (uint32_t)g.blockDim; ++t)
-          if ((wm[b * words + t / 32] >> (t % 32)) & 1u) s.waiting.push_back((int)t);
-        out.stuck.push_back(std::move(s));
+    // ---- collect ----
+    std::vector<unsigned long long> lfAll(LINES, ~0ull);
+    std::vector<std::array<int64_t, 3>> tris;
+    out.launches = 0;
+    for (size_t ri = 0; ri < D; ++ri) {
+      Replica& R = reps_[ri];
+      if (R.nb == 0) continue;
+      CK(cudaSetDevice(R.dev));
+      CK(cudaStreamSynchronize(R.stream));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, R.e0, R.e1);
+      out.ms = std::max<double>(out.ms, ms);
+      out.launches += 2;
+      int herr[2];
+      CK(cudaMemcpy(herr, R.err.p, sizeof herr, cudaMemcpyDeviceToHost));
+      if (herr[0]) {
+        static const char* why[] = {"", "thread value/scope/frame stack overflow",
+                                    "private memory of a thread exceeds the engine limit",
+                                    "a pointer to a thread-private object was stored to shared or global memory",
+                                    "too many distinct diagnostics", "too many reported race triples",
+                                    "source line outside 0..65535",
+                                    "sweep budget exhausted (step limit or 2^26 sweeps)", "bad opcode"};
+        out.error = std::string("B200 engine limitation: ") + why[herr[0] < 9 ? herr[0] : 0] + " (info " +
+                    std::to_string(herr[1]) + ")";
+        return false;
+      }
+      const size_t nb = R.nb;
+      std::vector<BlockOut> bo(nb);
+      CK(cudaMemcpy(bo.data(), R.blocks.p, nb * sizeof(BlockOut), cudaMemcpyDeviceToHost));
+      bool anyDl = false;
+      for (const auto& b : bo) {
+        out.sweeps += b.sweeps;
+        out.soloSweeps += b.soloSweeps;
+        out.blockCycles += b.cycles;
+        out.soloCycles += b.soloCycles;
+        out.deviceSteps += b.steps;
+        out.barrierRules += b.rules;
+        out.allocs += b.allocs;
+        out.sharedEvents += b.sharedEvents;
+        out.duration = std::max(out.duration, b.lastSweep);
+        if (b.deadlocked) anyDl = true;
+      }
+      if (anyDl) {
+        out.deadlocked = true;
+        std::vector<uint32_t> wm(nb * words);
+        CK(cudaMemcpy(wm.data(), R.wait.p, wm.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        for (size_t b = 0; b < nb; ++b) {
+          if (!bo[b].deadlocked) continue;
+          GridResult::Stuck st;
+          st.bid = R.b0 + (uint32_t)b;
+          for (uint32_t t = 0; t < (uint32_t)g.blockDim; ++t)
+            if ((wm[b * words + t / 32] >> (t % 32)) & 1u) st.waiting.push_back((int)t);
+          out.stuck.push_back(std::move(st));
+        }
+      }
+      std::vector<DevDiagRec> dr(diagN);
+      CK(cudaMemcpy(dr.data(), R.diag.p, diagN * sizeof(DevDiagRec), cudaMemcpyDeviceToHost));
+      for (const auto& r : dr)
+        if (r.hkey) {
+          DevDiag d;
+          d.key = r.ts;
+          d.code = r.code;
+          d.line = r.line;
+          for (int i = 0; i < 4; ++i) d.p[i] = r.p[i];
+          d.name = r.name;
+          out.diags.push_back(d);
+        }
+      std::vector<unsigned long long> lf(LINES);
+      CK(cudaMemcpy(lf.data(), R.line.p, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      for (int l = 0; l < LINES; ++l) lfAll[(size_t)l] = std::min(lfAll[(size_t)l], lf[(size_t)l]);
+      unsigned long long ntri = 0;
+      CK(cudaMemcpy(&ntri, R.ntri.p, sizeof ntri, cudaMemcpyDeviceToHost));
+      if (ntri) {
+        std::vector<int32_t> tri(3 * std::min<unsigned long long>(ntri, triCaps[ri]));
+        CK(cudaMemcpy(tri.data(), R.tri.p, tri.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < tri.size(); i += 3)
+          tris.push_back({(int64_t)(uint32_t)tri[i], (int64_t)(uint32_t)tri[i + 1], (int64_t)tri[i + 2]});
       }
     }
-    // diagnostics
-    std::vector<DevDiagRec> dr(diagN);
-    CK(cudaMemcpy(dr.data(), dDiag.p, diagN * sizeof(DevDiagRec), cudaMemcpyDeviceToHost));
-    for (const auto& r : dr)
-      if (r.hkey) {
-        DevDiag d;
-        d.key = r.ts;
-        d.code = r.code;
-        d.line = r.line;
-        for (int i = 0; i < 4; ++i) d.p[i] = r.p[i];
-        d.name = r.name;
-        out.diags.push_back(d);
-      }
-    std::vector<unsigned long long> lf(LINES);
-    CK(cudaMemcpy(lf.data(), dLine.p, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     for (int l = 0; l < LINES; ++l)
-      if (lf[(size_t)l] != ~0ull) {
+      if (lfAll[(size_t)l] != ~0ull) {
         DevDiag d;
-        d.key = lf[(size_t)l];
+        d.key = lfAll[(size_t)l];
         d.code = MCK_D_RACE;
         d.line = l;
         d.p[0] = d.p[1] = d.p[2] = d.p[3] = 0;
         d.name = -1;
         out.diags.push_back(d);
       }
-    unsigned long long ntri = 0;
-    CK(cudaMemcpy(&ntri, dNTri.p, sizeof ntri, cudaMemcpyDeviceToHost));
-    if (ntri) {
-      std::vector<int32_t> tri(3 * std::min<unsigned long long>(ntri, triCap));
-      CK(cudaMemcpy(tri.data(), dTri.p, tri.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-      std::vector<std::array<int64_t, 3>> v;
-      v.reserve(tri.size() / 3);
-      for (size_t i = 0; i < tri.size(); i += 3)
-        v.push_back({(int64_t)(uint32_t)tri[i], (int64_t)(uint32_t)tri[i + 1], (int64_t)tri[i + 2]});
-      std::sort(v.begin(), v.end());
-      v.erase(std::unique(v.begin(), v.end()), v.end());
-      out.reported = std::move(v);
+    std::sort(tris.begin(), tris.end());
+    tris.erase(std::unique(tris.begin(), tris.end()), tris.end());
+    out.reported = std::move(tris);
+    std::sort(out.stuck.begin(), out.stuck.end(),
+              [](const GridResult::Stuck& a, const GridResult::Stuck& b) { return a.bid < b.bid; });
+    return true;
+  }
+
+  // ---- replicated global memory: merge every replica's writes into
+  // replica 0 in block-range order (a later range wins a cross-block
+  // conflict) ----
+  bool mergeLocal(GridResult& out, std::string& err) {
+    const size_t D = reps_.size();
+    if (D == 1 || top_ == 0) return true;
+    Replica& R0 = reps_[0];
+    CK(cudaSetDevice(R0.dev));
+    for (size_t ri = 1; ri < D; ++ri) {
+      if (reps_[ri].nb == 0) continue;
+      merge_dirty_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.bytes, R0.meta, reps_[ri].bytes, reps_[ri].meta, top_);
+      ++out.launches;
+    }
+    CK(cudaStreamSynchronize(R0.stream));
+    return true;
+  }
+
+  // clear the dirty bits of replica 0, then copy it to the other replicas
+  bool finishMemory(GridResult& out, std::string& err) {
+    const size_t D = reps_.size();
+    if ((D == 1 && comm_.world == 1) || top_ == 0) return true;
+    Replica& R0 = reps_[0];
+    CK(cudaSetDevice(R0.dev));
+    clear_dirty_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.meta, top_);
+    out.launches += 1;
+    CK(cudaStreamSynchronize(R0.stream));
+    for (size_t ri = 1; ri < D; ++ri) {
+      CK(cudaMemcpyPeer(reps_[ri].bytes, reps_[ri].dev, R0.bytes, R0.dev, top_));
+      CK(cudaMemcpyPeer(reps_[ri].meta, reps_[ri].dev, R0.meta, R0.dev, top_));
+    }
+    for (const auto& R : reps_) {
+      CK(cudaSetDevice(R.dev));
+      CK(cudaDeviceSynchronize());
     }
     return true;
   }
 
-  static void init_diag_ts(k1::DevDiagRec* p, uint32_t n, cudaStream_t s);
+  // ---- ranks: every rank holds the same global image before the grid;
+  // the bytes each rank's blocks wrote are combined by one all-reduce(MAX)
+  // over the union of the written ranges ----
+  // host transport: gather `n` bytes from every rank (rank order)
+  bool hostGather(const void* send, size_t n, std::vector<uint8_t>& all, std::string& err) {
+    all.assign(n * (size_t)comm_.world, 0);
+    if (comm_.allgather(comm_.ctx, send, n, all.data()) != 0) {
+      err = "host allgather callback failed";
+      return false;
+    }
+    return true;
+  }
+
+  bool exchangeMemoryHost(GridResult& out, std::string& err) {
+    Replica& R0 = reps_[0];
+    CK(cudaSetDevice(R0.dev));
+    if (!lohi_.ensure(2, err)) return false;
+    CK(cudaMemsetAsync(lohi_.p, 0xFF, 2 * sizeof(unsigned long long), R0.stream));
+    if (top_ > 0) {
+      dirty_range_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.meta, top_, lohi_.p);
+      ++out.launches;
+    }
+    unsigned long long mine[2];
+    CK(cudaMemcpyAsync(mine, lohi_.p, sizeof mine, cudaMemcpyDeviceToHost, R0.stream));
+    CK(cudaStreamSynchronize(R0.stream));
+    std::vector<uint8_t> all;
+    if (!hostGather(mine, sizeof mine, all, err)) return false;
+    unsigned long long lo = ~0ull, nhi = ~0ull;
+    for (int r = 0; r < comm_.world; ++r) {
+      unsigned long long v[2];
+      std::memcpy(v, all.data() + r * sizeof v, sizeof v);
+      lo = std::min(lo, v[0]);
+      nhi = std::min(nhi, v[1]);
+    }
+    const uint64_t hi = ~nhi;
+    if (lo == ~0ull || hi <= lo) return true;
+    const uint64_t n = hi - lo;
+    if (!packed_.ensure(n, err)) return false;
+    pack_dirty_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.bytes, R0.meta, lo, n, packed_.p,
+                                                        (uint32_t)comm_.rank + 1);
+    std::vector<uint32_t> w(n);
+    CK(cudaMemcpyAsync(w.data(), packed_.p, n * 4, cudaMemcpyDeviceToHost, R0.stream));
+    CK(cudaStreamSynchronize(R0.stream));
+    if (!hostGather(w.data(), n * 4, all, err)) return false;
+    for (int r = 0; r < comm_.world; ++r) {
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(all.data() + (size_t)r * n * 4);
+      for (uint64_t i = 0; i < n; ++i) w[i] = std::max(w[i], q[i]);
+    }
+    CK(cudaMemcpyAsync(packed_.p, w.data(), n * 4, cudaMemcpyHostToDevice, R0.stream));
+    unpack_dirty_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.bytes, R0.meta, lo, n, packed_.p);
+    out.launches += 2;
+    CK(cudaStreamSynchronize(R0.stream));
+    return true;
+  }
+
+  bool exchangeMemory(GridResult& out, std::string& err) {
+    if (comm_.allgather) return exchangeMemoryHost(out, err);
+    Replica& R0 = reps_[0];
+    CK(cudaSetDevice(R0.dev));
+    if (!lohi_.ensure(2, err)) return false;
+    CK(cudaMemsetAsync(lohi_.p, 0xFF, 2 * sizeof(unsigned long long), R0.stream));
+    if (top_ > 0) {
+      dirty_range_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.meta, top_, lohi_.p);
+      ++out.launches;
+    }
+    if (ncclAllReduce(lohi_.p, lohi_.p, 2, ncclUint64, ncclMin, nccl_, R0.stream) != ncclSuccess) {
+      err = "ncclAllReduce (dirty range) failed";
+      return false;
+    }
+    unsigned long long lohi[2];
+    CK(cudaMemcpyAsync(lohi, lohi_.p, sizeof lohi, cudaMemcpyDeviceToHost, R0.stream));
+    CK(cudaStreamSynchronize(R0.stream));
+    const uint64_t lo = lohi[0], hi = ~lohi[1];
+    if (lo == ~0ull || hi <= lo) return true;  // nobody wrote device memory
+    const uint64_t n = hi - lo;
+    if (!packed_.ensure(n, err)) return false;
+    pack_dirty_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.bytes, R0.meta, lo, n, packed_.p,
+                                                        (uint32_t)comm_.rank + 1);
+    if (ncclAllReduce(packed_.p, packed_.p, n, ncclUint32, ncclMax, nccl_, R0.stream) != ncclSuccess) {
+      err = "ncclAllReduce (written bytes) failed";
+      return false;
+    }
+    unpack_dirty_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.bytes, R0.meta, lo, n, packed_.p);
+    out.launches += 2;
+    CK(cudaStreamSynchronize(R0.stream));
+    return true;
+  }
+
+  // ---- ranks: gather every rank's partial GridResult (in rank order) ----
+  struct BlobHdr {
+    uint64_t ok, deviceSteps, barrierRules, allocs, sharedEvents, sweeps, soloSweeps, blockCycles, soloCycles;
+    uint64_t duration, deadlocked, nDiag, nStuck, nTids, nTri, errLen, launches;
+    double ms;
+  };
+
+  static void serialize(const GridResult& r, bool ok, std::vector<uint8_t>& b) {
+    BlobHdr h{};
+    h.ok = ok;
+    h.deviceSteps = r.deviceSteps;
+    h.barrierRules = r.barrierRules;
+    h.allocs = r.allocs;
+    h.sharedEvents = r.sharedEvents;
+    h.sweeps = r.sweeps;
+    h.soloSweeps = r.soloSweeps;
+    h.blockCycles = r.blockCycles;
+    h.soloCycles = r.soloCycles;
+    h.duration = r.duration;
+    h.deadlocked = r.deadlocked;
+    h.nDiag = r.diags.size();
+    h.nStuck = r.stuck.size();
+    for (const auto& s : r.stuck) h.nTids += s.waiting.size();
+    h.nTri = r.reported.size();
+    h.errLen = r.error.size();
+    h.launches = r.launches;
+    h.ms = r.ms;
+    auto put = [&b](const void* p, size_t n) {
+      const uint8_t* c = static_cast<const uint8_t*>(p);
+      b.insert(b.end(), c, c + n);
+    };
+    put(&h, sizeof h);
+    if (!r.diags.empty()) put(r.diags.data(), r.diags.size() * sizeof(DevDiag));
+    for (const auto& s : r.stuck) {
+      uint64_t v[2] = {s.bid, s.waiting.size()};
+      put(v, sizeof v);
+      if (!s.waiting.empty()) put(s.waiting.data(), s.waiting.size() * sizeof(int));
+    }
+    if (!r.reported.empty()) put(r.reported.data(), r.reported.size() * sizeof(r.reported[0]));
+    put(r.error.data(), r.error.size());
+  }
+
+  static void deserializeInto(const uint8_t* p, GridResult& r, bool& ok) {
+    BlobHdr h;
+    std::memcpy(&h, p, sizeof h);
+    p += sizeof h;
+    ok = ok && h.ok;
+    r.deviceSteps += h.deviceSteps;
+    r.barrierRules += h.barrierRules;
+    r.allocs += h.allocs;
+    r.sharedEvents += h.sharedEvents;
+    r.sweeps += h.sweeps;
+    r.soloSweeps += h.soloSweeps;
+    r.blockCycles += h.blockCycles;
+    r.soloCycles += h.soloCycles;
+    r.duration = std::max<uint32_t>(r.duration, (uint32_t)h.duration);
+    r.deadlocked = r.deadlocked || h.deadlocked;
+    r.ms = std::max(r.ms, h.ms);
+    for (uint64_t i = 0; i < h.nDiag; ++i, p += sizeof(DevDiag)) {
+      DevDiag d;
+      std::memcpy(&d, p, sizeof d);
+      r.diags.push_back(d);
+    }
+    for (uint64_t i = 0; i < h.nStuck; ++i) {
+      uint64_t v[2];
+      std::memcpy(v, p, sizeof v);
+      p += sizeof v;
+      GridResult::Stuck s;
+      s.bid = (uint32_t)v[0];
+      s.waiting.resize(v[1]);
+      if (v[1]) std::memcpy(s.waiting.data(), p, v[1] * sizeof(int));
+      p += v[1] * sizeof(int);
+      r.stuck.push_back(std::move(s));
+    }
+    for (uint64_t i = 0; i < h.nTri; ++i, p += sizeof(std::array<int64_t, 3>)) {
+      std::array<int64_t, 3> t;
+      std::memcpy(&t, p, sizeof t);
+      r.reported.push_back(t);
+    }
+    if (h.errLen && r.error.empty()) r.error.assign(reinterpret_cast<const char*>(p), h.errLen);
+  }
+
+  bool exchangeResults(GridResult& out, bool& ok, std::string& err) {
+    Replica& R0 = reps_[0];
+    CK(cudaSetDevice(R0.dev));
+    std::vector<uint8_t> mine;
+    serialize(out, ok, mine);
+    const int W = comm_.world;
+    std::vector<uint8_t> all;
+    size_t slot = 0;
+    if (comm_.allgather) {
+      unsigned long long sz = mine.size();
+      if (!hostGather(&sz, sizeof sz, all, err)) return false;
+      unsigned long long mx = 0;
+      for (int r = 0; r < W; ++r) {
+        unsigned long long v;
+        std::memcpy(&v, all.data() + r * sizeof v, sizeof v);
+        mx = std::max(mx, v);
+      }
+      slot = ((size_t)mx + 15) & ~(size_t)15;
+      mine.resize(slot, 0);
+      if (!hostGather(mine.data(), slot, all, err)) return false;
+    } else if (!gatherNccl(mine, all, slot, err)) {
+      return false;
+    }
+    GridResult m;
+    bool allOk = true;
+    for (int r = 0; r < W; ++r) deserializeInto(all.data() + slot * r, m, allOk);
+    std::sort(m.reported.begin(), m.reported.end());
+    m.reported.erase(std::unique(m.reported.begin(), m.reported.end()), m.reported.end());
+    std::sort(m.stuck.begin(), m.stuck.end(),
+              [](const GridResult::Stuck& a, const GridResult::Stuck& b) { return a.bid < b.bid; });
+    m.launches = out.launches;
+    out = std::move(m);
+    ok = allOk;
+    if (!ok && out.error.empty()) out.error = "B200 engine: a peer rank failed this grid";
+    return true;
+  }
+
+  bool gatherNccl(std::vector<uint8_t>& mine, std::vector<uint8_t>& all, size_t& slot, std::string& err) {
+    Replica& R0 = reps_[0];
+    const int W = comm_.world;
+    // sizes
+    if (!lohi_.ensure((size_t)W + 1, err)) return false;
+    unsigned long long sz = mine.size();
+    CK(cudaMemcpyAsync(lohi_.p + W, &sz, sizeof sz, cudaMemcpyHostToDevice, R0.stream));
+    if (ncclAllGather(lohi_.p + W, lohi_.p, 1, ncclUint64, nccl_, R0.stream) != ncclSuccess) {
+      err = "ncclAllGather (result sizes) failed";
+      return false;
+    }
+    std::vector<unsigned long long> sizes(W);
+    CK(cudaMemcpyAsync(sizes.data(), lohi_.p, W * sizeof(unsigned long long), cudaMemcpyDeviceToHost, R0.stream));
+    CK(cudaStreamSynchronize(R0.stream));
+    const size_t mx = (size_t)*std::max_element(sizes.begin(), sizes.end());
+    slot = (mx + 15) & ~(size_t)15;
+    if (!blobs_.ensure(slot * (W + 1), err)) return false;
+    mine.resize(slot, 0);
+    uint8_t* send = blobs_.p + slot * W;
+    CK(cudaMemcpyAsync(send, mine.data(), slot, cudaMemcpyHostToDevice, R0.stream));
+    if (ncclAllGather(send, blobs_.p, slot, ncclUint8, nccl_, R0.stream) != ncclSuccess) {
+      err = "ncclAllGather (results) failed";
+      return false;
+    }
+    all.assign(slot * W, 0);
+    CK(cudaMemcpyAsync(all.data(), blobs_.p, all.size(), cudaMemcpyDeviceToHost, R0.stream));
+    CK(cudaStreamSynchronize(R0.stream));
+    return true;
+  }
+
+  bool run(const GridSpec& g, GridResult& out, std::string& err) {
+    bool ok = runLocal(g, out, err) && mergeLocal(out, err);
+    if (comm_.world > 1) {
+      if (!ok && out.error.empty()) out.error = err.empty() ? "B200 engine error" : err;
+      if (!exchangeResults(out, ok, err)) return false;
+      if (ok && !exchangeMemory(out, err)) return false;
+    }
+    if (!finishMemory(out, err)) return false;
+    return ok;
+  }
 };
-
-__global__ void init_ts_kernel(k1::DevDiagRec* p, uint32_t n) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i].ts = ~0ull;
-}
-
-void CudaEngine::init_diag_ts(k1::DevDiagRec* p, uint32_t n, cudaStream_t s) {
-  init_ts_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, n);
-}
 
 }  // namespace
 
-std::unique_ptr<DeviceEngine> makeCudaEngine(int device, std::string& why) {
+std::unique_ptr<DeviceEngine> makeCudaEngine(const std::vector<int>& devices, const EngineComm& comm,
+                                             std::string& why) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
-  if (e != cudaSuccess || n <= device) {
-    why = e != cudaSuccess ? cudaGetErrorString(e) : "no such device";
+  if (e != cudaSuccess || n == 0) {
+    why = e != cudaSuccess ? cudaGetErrorString(e) : "no CUDA device";
     cudaGetLastError();
     return nullptr;
   }
-  std::unique_ptr<CudaEngine> eng(new CudaEngine(device));
+  for (int d : devices)
+    if (d < 0 || d >= n) {
+      why = "no such device " + std::to_string(d);
+      return nullptr;
+    }
+  std::unique_ptr<CudaEngine> eng(new CudaEngine(devices, comm));
   if (!eng->init(why)) return nullptr;
   return std::unique_ptr<DeviceEngine>(eng.release());
+}
+
+bool makeCommId(std::array<uint8_t, 128>& id, std::string& why) {
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) {
+    why = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+    return false;
+  }
+  std::memcpy(id.data(), u.internal, 128);
+  return true;
 }
 
 }  // namespace mckb

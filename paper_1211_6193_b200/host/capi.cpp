@@ -40,6 +40,14 @@ extern "C" int mck_run_source(const char* src, const char* filename, const mck_r
     ro.policy = opts->round_robin ? mck::SchedulePolicy::RoundRobin : mck::SchedulePolicy::SeededRandom;
     ro.seed = opts->seed;
     if (opts->max_threads_per_block > 0) ro.arch.maxThreadsPerBlock = opts->max_threads_per_block;
+    for (int i = 0; i < opts->n_devices && i < 8; ++i) ro.devices.push_back(opts->devices[i]);
+    if (opts->world > 1) {
+      ro.rank = opts->rank;
+      ro.world = opts->world;
+      ro.commId.assign(opts->comm_id, opts->comm_id + 128);
+      ro.allgather = opts->allgather;
+      ro.allgatherCtx = opts->allgather_ctx;
+    }
   }
   std::string o;
   try {
@@ -106,3 +114,10 @@ extern "C" int mck_disassemble(const char* src, const char* filename, char** tex
 }
 
 extern "C" void mck_free(char* p) { std::free(p); }
+
+extern "C" int mckg_comm_id(uint8_t out[128]) {
+  std::vector<uint8_t> id = mck::makeCommId();
+  if (id.size() != 128) return MCKG_E_CUDA;
+  std::memcpy(out, id.data(), 128);
+  return MCKG_OK;
+}

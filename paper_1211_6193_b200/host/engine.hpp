@@ -22,6 +22,7 @@ namespace mckb {
 // Per-byte metadata of every memory object (host and device):
 constexpr uint8_t META_DEF = 1;  // byte defined (MemByte::defined, machine.hpp:33-37)
 constexpr uint8_t META_PTR = 2;  // a pointer slot starts here (MemObject::ptrs, machine.hpp:45)
+constexpr uint8_t META_DIRTY = 4;  // written by the running grid (replica merge; cleared after)
 
 // A device-global object as the engine sees it.
 struct DevObjInfo {
@@ -91,8 +92,26 @@ class DeviceEngine {
   virtual bool runGrid(const GridSpec& spec, GridResult& out) = 0;
 };
 
-// The B200 engine; returns nullptr (with `why`) when no CUDA device is usable.
-std::unique_ptr<DeviceEngine> makeCudaEngine(int device, std::string& why);
+// Rank sharding (one process per GPU): rank r runs blocks
+// [gridDim*r/world, gridDim*(r+1)/world) of every grid; the written global
+// bytes and the partial results are combined over NCCL after each grid.
+struct EngineComm {
+  int rank = 0, world = 1;
+  std::array<uint8_t, 128> id{};  // ncclUniqueId made by rank 0
+  // host transport instead of NCCL (ranks sharing one GPU, gloo tests):
+  // gather n bytes from every rank into recv[world * n], rank order; 0 = ok
+  int (*allgather)(void* ctx, const void* send, uint64_t n, void* recv) = nullptr;
+  void* ctx = nullptr;
+};
+
+// The B200 engine over one or more devices (a grid's blocks are split into
+// contiguous ranges, one per device; device-global memory is replicated and
+// merged after each grid).  A device may be listed twice ("virtual devices").
+// Returns nullptr (with `why`) when no CUDA device is usable.
+std::unique_ptr<DeviceEngine> makeCudaEngine(const std::vector<int>& devices, const EngineComm& comm,
+                                             std::string& why);
+// a fresh ncclUniqueId (rank 0 makes it; the launcher broadcasts it)
+bool makeCommId(std::array<uint8_t, 128>& id, std::string& why);
 // Storage-only stand-in used when no GPU is present: device allocations and
 // copies work, launching a grid fails loudly (there is no CPU execution path).
 std::unique_ptr<DeviceEngine> makeStorageOnlyEngine(const std::string& why);

@@ -1460,7 +1460,14 @@ std::vector<mck::StuckReport> HostMachine::scanStuck() const {
 // ======================= run =======================
 
 mck::RunResult HostMachine::run() {
-  eng_ = makeCudaEngine(o_.device, engWhy_);
+  std::vector<int> devs = o_.devices.empty() ? std::vector<int>{o_.device} : o_.devices;
+  EngineComm comm;
+  comm.rank = o_.rank;
+  comm.world = std::max(1, o_.world);
+  if (o_.commId.size() == comm.id.size()) std::copy(o_.commId.begin(), o_.commId.end(), comm.id.begin());
+  comm.allgather = o_.allgather;
+  comm.ctx = o_.allgatherCtx;
+  eng_ = makeCudaEngine(devs, comm, engWhy_);
   if (!eng_) eng_ = makeStorageOnlyEngine(engWhy_);
   // globals (machine.cpp:57-68)
   for (const GlobalInfo& g : P_->globals) {
@@ -1651,6 +1658,13 @@ Machine::~Machine() = default;
 RunResult Machine::run() {
   impl_->m.reset(new mckb::HostMachine(prog_, opts_));
   return impl_->m->run();
+}
+
+std::vector<uint8_t> makeCommId() {
+  std::array<uint8_t, 128> id;
+  std::string why;
+  if (!mckb::makeCommId(id, why)) return {};
+  return std::vector<uint8_t>(id.begin(), id.end());
 }
 
 std::string formatStuckReports(const std::vector<StuckReport>& reports) {
