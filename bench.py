@@ -261,7 +261,8 @@ def run_ours(args):
         peak_src = "measured"
     except (OSError, ValueError, KeyError):
         peak, peak_src = 6650.0, "fallback"
-    launches = 2 * args.steps
+    # per step: mckg_race_out_reset (1) + the kernels of the last detect call
+    launches = args.steps * (1 + _abi.launch_stats().kernels)
 
     k1 = None
     if not args.no_k1:

@@ -46,18 +46,20 @@ namespace mckg {
 namespace {
 
 constexpr int NT = 256;
-constexpr int NWARP = NT / 32;
 constexpr int NSTAGE = MCKG_K2_NSTAGE;
 constexpr int EPT_MAX = 16;     // records per thread kept in registers (cap <= 4096)
-constexpr uint32_t HS = 512;    // (byte, line) dedup set entries
-constexpr uint32_t TBN = 256;   // staged triples before a global flush
+constexpr uint32_t HS = 512;    // (word, line) -> reported byte mask, per block
+constexpr uint32_t TBN = 256;   // staged triples per buffer before the global append
 constexpr uint32_t LTN = 32;    // line-first local table entries
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t INV = 0xFFFFFFFFu;
 constexpr uint32_t ST_OVERFLOW = MCKG_ST_OVERFLOW, ST_RANGE = MCKG_ST_RANGE,
                    ST_ORDER = MCKG_ST_ORDER, ST_DUP = MCKG_ST_DUP;
-// misc[] slots
-constexpr int M_TBN = 0, M_CLN = 1, M_NSEG = 2, M_BASE_LO = 3, M_BASE_HI = 4, M_FLAGS = 5;
+// NSLOT epochs are filtered at once, each in its own word arrays: tag[slot][w]
+// (some accessing tid, u16) and ma[slot][w] = {multi, any-write} 16-bit unit
+// stamps.  A stale stamp that wraps to the current one only adds a candidate
+// (the exact pass removes it): the filter never misses a race.
+constexpr uint32_t NSLOT = 2;
 
 struct Params {
   const mckg_access* ev;
@@ -68,34 +70,39 @@ struct Params {
   unsigned long long* n_tri;
   unsigned long long* line_first;
   uint32_t* status;
-  uint32_t debug;  // experiments only (MCKG_DEBUG): 1 skip exact, 2 skip filter, 8/16 stop early (bisection)
+  uint32_t debug;  // experiments only (MCKG_DEBUG): 1 skip the exact pass, 2 skip filter + exact
+  // two-kernel mode: the filter writes each block's candidate list (<= CMAX
+  // record indices) for exact_kernel; a longer list sets *cflag and the fused
+  // kernel (filter + exact in one pass) redoes the launch
+  uint32_t mode;       // 0 fused, 1 filter -> candidate lists
+  uint32_t gate;       // fused kernel: 1 = run only if *cflag is set
+  uint16_t* ccount;    // [n_blocks]
+  uint16_t* cidx;      // [n_blocks * CMAX]
+  uint32_t* cflag;
 };
+constexpr uint32_t CMAX = 64;
 
 extern __shared__ __align__(128) uint8_t smem_raw[];
 // fixed-size per-CTA state (static shared memory: compile-time addresses)
 __shared__ unsigned long long s_hset[HS];
 __shared__ unsigned long long s_lt_ts[LTN];
-__shared__ mckg_race_triple s_tbuf[TBN];
+__shared__ mckg_race_triple s_tbuf[2][TBN];
 __shared__ uint32_t s_lt_line[LTN];
-__shared__ uint32_t s_misc[16];
-__shared__ uint32_t s_info[2][4];  // per cl buffer: n, b, m
-__shared__ uint64_t s_full_cl[2], s_free_cl[2];
+__shared__ uint32_t s_cnt[4];    // [0..1] candidates per cl buffer, [2..3] staged triples
+__shared__ uint32_t s_flags;
 __shared__ uint64_t s_mbar[NSTAGE];
 
 // Byte offsets of the size-dependent state in the dynamic shared memory.
 struct Lay {
-  uint32_t tag, multi, anyw, bitmap, cl, seg, stage, end;
+  uint32_t ma, tag, cl, stage, end;
 };
 
 __host__ __device__ inline Lay layout(uint32_t cap, uint32_t wpad) {
   Lay L;
   uint32_t p = 0;
-  L.tag = p;     p += wpad * 4;
-  L.multi = p;   p += wpad * 4;
-  L.anyw = p;    p += wpad * 4;
-  L.bitmap = p;  p += (cap / 32 + 1) * 4;
+  L.ma = p;      p += NSLOT * wpad * 4;
+  L.tag = p;     p += NSLOT * wpad * 2;
   L.cl = p;      p += 2 * cap * 2;
-  L.seg = p;     p += (cap + 2) * 2;
   p = (p + 127u) & ~127u;
   L.stage = p;   p += NSTAGE * cap * 16;
   L.end = p;
@@ -109,41 +116,60 @@ __device__ __forceinline__ T* sp(uint32_t off) {
 
 __device__ __forceinline__ uint32_t sw(uint32_t w) { return w ^ ((w >> 5) & 31u); }
 
-__device__ __forceinline__ bool valid_ev(uint32_t w0, int32_t line, uint32_t shm) {
-  uint32_t off = acc_off(w0), len = acc_len(w0);
-  return len != 0 && len <= MCKG_MAX_LEN && off + len <= shm && (uint32_t)line < MCKG_MAX_LINES;
+// ---- shared-window accessors (plain LDS/STS, predicated stores) ----
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n}" ::"r"(a),
+      "h"((uint16_t)v), "r"((uint32_t)p)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
 }
 
-// 1 = inserted, 0 = already present, 2 = probe limit (caller flags ST_DUP)
-__device__ int hset_insert(const Lay& L, unsigned long long key, unsigned long long bstamp) {
-  unsigned long long* hs = s_hset;
-  uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 40) & (HS - 1);
-  for (uint32_t probe = 0; probe < 64; ++probe) {
-    unsigned long long cur = hs[h];
-    while ((cur >> 40) != bstamp) {  // stale slot: claim it
-      unsigned long long old = atomicCAS(hs + h, cur, key);
-      if (old == cur) return 1;
-      cur = old;
+// Barrier among the NT threads.
+__device__ __forceinline__ void fsync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+
+// Rare path: the 2nd/3rd word of an access spanning several 4-byte words
+// (tag_slot / ma_slot: the slot's arrays).
+__device__ __noinline__ bool extra_words(uint32_t tag_slot, uint32_t ma_slot, uint32_t w0, uint32_t tid,
+                                         int phase, uint32_t st) {
+  const uint32_t off = acc_off(w0), len = acc_len(w0);
+  const bool wr = acc_write(w0);
+  bool cand = false;
+  for (uint32_t w = (off >> 2) + 1; w <= (off + len - 1u) >> 2; ++w) {
+    const uint32_t a = tag_slot + sw(w) * 2u, m = ma_slot + sw(w) * 4u;
+    if (phase == 1) {
+      sts16_if(true, a, tid);
+    } else if (phase == 2) {
+      sts16_if(lds16(a) != tid, m, st);
+      sts16_if(wr, m + 2u, st);
+    } else {
+      cand |= lds32(m) == (st | (st << 16));
     }
-    if (cur == key) return 0;
-    h = (h + 1) & (HS - 1);
   }
-  return 2;
+  return cand;
 }
 
-__device__ void line_note(const Lay& L, const Params& P, int32_t line, unsigned long long ts) {
-  uint32_t* lt_line = s_lt_line;
-  unsigned long long* lt_ts = s_lt_ts;
-  uint32_t l = (uint32_t)line;
+// First racing timestamp per line: a CTA table, global atomicMin on overflow.
+__device__ void line_note(const Params& P, int32_t line, unsigned long long ts) {
+  const uint32_t l = (uint32_t)line;
   uint32_t h = l & (LTN - 1);
   for (uint32_t probe = 0; probe < LTN; ++probe) {
-    uint32_t v = lt_line[h];
+    uint32_t v = s_lt_line[h];
     if (v == INF) {
-      uint32_t old = atomicCAS(lt_line + h, INF, l);
+      const uint32_t old = atomicCAS(s_lt_line + h, INF, l);
       v = old == INF ? l : old;
     }
     if (v == l) {
-      atomicMin(lt_ts + h, ts);
+      atomicMin(s_lt_ts + h, ts);
       return;
     }
     h = (h + 1) & (LTN - 1);
@@ -151,90 +177,416 @@ __device__ void line_note(const Lay& L, const Params& P, int32_t line, unsigned 
   atomicMin(P.line_first + l, ts);
 }
 
-
-
-// ---- 32-bit shared-window accessors (plain LDS/STS, predicated stores) ----
-__device__ __forceinline__ uint32_t lds(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts_if(bool p, uint32_t a, uint32_t v) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n}" ::"r"(a),
-      "r"(v), "r"((uint32_t)p)
-      : "memory");
-}
-
-// Barrier among the NT filter threads only (the exact warp runs decoupled).
-__device__ __forceinline__ void fsync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
-
-// Rare path: the 2nd/3rd word of an access spanning several 4-byte words.
-__device__ __noinline__ bool extra_words(uint32_t tag_base, uint32_t d1, uint32_t d2, uint32_t w0,
-                                         uint32_t tid, int phase, uint32_t st) {
-  const uint32_t off = acc_off(w0), len = acc_len(w0);
-  const bool wr = acc_write(w0);
-  bool cand = false;
-  for (uint32_t w = (off >> 2) + 1; w <= (off + len - 1u) >> 2; ++w) {
-    const uint32_t a = tag_base + sw(w) * 4u;
-    if (phase == 1) {
-      sts_if(true, a, tid);
-    } else if (phase == 2) {
-      sts_if(lds(a) != tid, a + d1, st);
-      sts_if(wr, a + d2, st);
-    } else {
-      cand |= lds(a + d1) == st && lds(a + d2) == st;
+// The block's reported set, per (word, line): slot = bstamp:24 | word:18 |
+// line:16 | byte mask:4.  Returns the bytes of `mask` not reported before,
+// or 0x10 | mask when the probe limit is hit (caller flags ST_DUP).
+__device__ uint32_t hset_or(unsigned long long bstamp, uint32_t word, uint32_t line, uint32_t mask) {
+  const unsigned long long want = (bstamp << 40) | ((unsigned long long)(word & 0x3FFFFu) << 22) |
+                                  ((unsigned long long)(line & 0xFFFFu) << 6);
+  uint32_t h = (uint32_t)(((want >> 6) * 0x9E3779B97F4A7C15ull) >> 40) & (HS - 1);
+  for (uint32_t probe = 0; probe < 64; ++probe) {
+    unsigned long long cur = s_hset[h];
+    while ((cur >> 40) != bstamp) {  // stale slot (an earlier block): claim it
+      const unsigned long long old = atomicCAS(s_hset + h, cur, want | mask);
+      if (old == cur) return mask;
+      cur = old;
     }
-  }
-  return cand;
-}
-
-// Epoch segment starts from the start bitmap, in order (warp 0 only).
-__device__ void build_segments(const Lay& L, uint32_t n) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t* bitmap = sp<uint32_t>(L.bitmap);
-  uint16_t* seg = sp<uint16_t>(L.seg);
-  const uint32_t nwords = (n + 31u) / 32u;
-  uint32_t total = 0;
-  for (uint32_t base = 0; base < nwords; base += 32) {
-    uint32_t word = base + lane < nwords ? bitmap[base + lane] : 0u;
-    const uint32_t c = __popc(word);
-    uint32_t incl = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-      if (lane >= (uint32_t)d) incl += v;
+    if ((cur & ~0x3Full) == want) {
+      const unsigned long long old = atomicOr(s_hset + h, (unsigned long long)mask);
+      return mask & ~(uint32_t)old & 0xFu;
     }
-    uint32_t pos = total + incl - c;
-    while (word) {
-      const uint32_t b = __ffs(word) - 1u;
-      seg[pos++] = (uint16_t)((base + lane) * 32u + b);
-      word &= word - 1u;
-    }
-    total += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    h = (h + 1) & (HS - 1);
   }
-  if (lane == 0) {
-    seg[total] = (uint16_t)n;
-    s_misc[M_NSEG] = total;
-  }
+  return 0x10u | mask;
 }
-
-// Per-lane cache of first racing timestamps by line (exact warp only; lane l
-// owns one entry), flushed to the global line table on eviction / at exit.
-struct ExactState {
-  uint32_t lc_line;
-  unsigned long long lc_ts;
-  uint32_t lc_next;  // uniform: next slot to allocate
-  uint32_t tbn;      // uniform: staged triples in s_tbuf
-};
 
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
   return ((unsigned long long)__shfl_sync(0xFFFFFFFFu, (uint32_t)(v >> 32), src) << 32) |
          __shfl_sync(0xFFFFFFFFu, (uint32_t)v, src);
 }
 
-__device__ void line_cache_put(ExactState& E, const Params& P, bool leader, uint32_t line,
-                               unsigned long long ts) {
+// Exact pass of one block over its m candidates, by all NT threads: group
+// of C lanes per candidate X, each lane scanning every C-th candidate Y, the
+// lanes' racing bytes OR-reduced.  X races on the bytes it shares with an
+// earlier candidate Y of the same epoch and another thread where X or Y
+// writes -- the reference predicate (racecheck.cpp:24-32) verbatim.  The
+// racing bytes are reported once per (obj, byte, line) and the line's first
+// racing timestamp is min-reduced.
+__device__ void exact_block(const Params& P, const uint4* src, const uint16_t* cl, uint32_t m, int q,
+                            uint32_t obj, uint32_t bid, unsigned long long bstamp) {
+  const uint32_t t = threadIdx.x, warp = t >> 5;
+  // as few warps as possible (instruction count): W = ceil(m / 32) warps,
+  // C lanes per candidate with m * C <= 32 * W
+  const uint32_t W = min((m + 31u) >> 5, (uint32_t)NT / 32u);
+  uint32_t C = 32;
+  while (C > 1 && C * m > 32u * W) C >>= 1;
+  const uint32_t groups = 32u * W / C;
+  if (warp >= W) return;
+  const uint32_t sub = t & (C - 1u);
+  for (uint32_t xb = 0; xb < m; xb += groups) {
+    const uint32_t i = xb + t / C;
+    const bool act = i < m;
+    const uint32_t xi = act ? cl[i] : 0u;
+    const uint4 X = act ? src[xi] : make_uint4(0, 0, 0, 0);
+    const uint32_t xoff = acc_off(X.x), xend = xoff + acc_len(X.x);
+    const uint32_t xtid = acc_tid(X.y), xep = acc_epoch(X.y);
+    const bool xw = acc_write(X.x);
+    uint32_t bits = 0;
+    if (act) {
+      for (uint32_t j = sub; j < m; j += C) {
+        const uint32_t yi = cl[j];
+        const uint2 Y = *reinterpret_cast<const uint2*>(src + yi);
+        const uint32_t yoff = acc_off(Y.x), yend = yoff + acc_len(Y.x);
+        const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
+        const bool hit = yi < xi && acc_epoch(Y.y) == xep && acc_tid(Y.y) != xtid &&
+                         (xw || acc_write(Y.x)) && lo < hi;
+        if (hit) bits |= ((1u << (hi - lo)) - 1u) << (lo - xoff);
+      }
+    }
+    for (uint32_t d = 1; d < C; d <<= 1) bits |= __shfl_xor_sync(0xFFFFFFFFu, bits, d);
+    const bool racing = sub == 0 && bits != 0;
+    const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
+    if (!rm) continue;
+    const uint32_t lane = t & 31u;
+    const int32_t line = (int32_t)X.z;
+    // first racing timestamp per line: min over the warp's lanes of a line
+    const unsigned long long ts = ts_key(X.w, bid, xtid);
+    const uint32_t gm = __match_any_sync(0xFFFFFFFFu, racing ? (uint32_t)line : (0x80000000u | lane));
+    unsigned long long mn = ts;
+    for (uint32_t tmp = rm; tmp; tmp &= tmp - 1u) {
+      const int s = __ffs(tmp) - 1;
+      const unsigned long long v = shfl64(ts, s);
+      if ((gm >> s) & 1u) mn = v < mn ? v : mn;
+    }
+    if (racing && lane == (uint32_t)(__ffs(gm) - 1)) line_note(P, line, mn);
+    // reported set: bytes of (word, line) not reported before in this block
+    uint32_t fresh[3] = {0u, 0u, 0u};
+    uint32_t k = 0;
+    if (racing) {
+      const uint64_t ab = (uint64_t)bits << (xoff & 3u);  // bit j = byte (xoff & ~3) + j
+      for (uint32_t w = 0; w < 3u && (xoff >> 2) + w <= (xend - 1u) >> 2; ++w) {
+        const uint32_t wm = (uint32_t)(ab >> (4u * w)) & 0xFu;
+        if (!wm) continue;
+        uint32_t f = hset_or(bstamp, (xoff >> 2) + w, (uint32_t)line, wm);
+        if (f & 0x10u) {
+          atomicOr(&s_flags, ST_DUP);
+          f &= 0xFu;
+        }
+        fresh[w] = f;
+        k += __popc(f);
+      }
+    }
+    // one staging-buffer reservation per warp
+    uint32_t incl = k;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= (uint32_t)d) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (!total) continue;
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(s_cnt + 2 + q, total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 31);
+    uint32_t pos = base + incl - k;
+    for (uint32_t w = 0; w < 3u; ++w)
+      for (uint32_t f = fresh[w]; f; f &= f - 1u, ++pos) {
+        const mckg_race_triple tr{obj, ((xoff >> 2) + w) * 4u + (__ffs(f) - 1u), line};
+        if (pos < TBN) {
+          s_tbuf[q][pos] = tr;
+        } else {  // staging buffer full: straight to the global array
+          const unsigned long long g = atomicAdd(P.n_tri, 1ull);
+          if (g < P.capacity)
+            P.tri[g] = tr;
+          else
+            atomicOr(&s_flags, ST_OVERFLOW);
+        }
+      }
+  }
+}
+
+// Appends the staged triples of buffer q to the global array (warp 0).
+__device__ void flush_triples(const Params& P, int q) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t n = min(s_cnt[2 + q], TBN);
+  if (n == 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(P.n_tri, (unsigned long long)n);
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  for (uint32_t i = lane; i < n; i += 32) {
+    if (base + i < P.capacity)
+      P.tri[base + i] = s_tbuf[q][i];
+    else
+      atomicOr(&s_flags, ST_OVERFLOW);
+  }
+}
+
+// One CTA of NT threads streams simulated blocks b = blockIdx.x + k * grid.
+// A unit is (block, round): the block's epochs [ws, ws + NSLOT) relative to
+// its first epoch (one round unless the block spans more epochs).  Per unit
+//   (a) | P2: multi / any-write stamps; exact pass of the previous block
+//   (b) | P3: candidates -> cl; P1 (tag <- tid) of the next unit;
+//         append the previous block's triples; release its TMA stage
+// P3 reads only ma[], P1 writes only tag[]; the exact pass reads the stage
+// and cl of the previous block, which nothing else touches until (b).
+template <int EPT>
+__global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 1))
+    race_detect_kernel(Params P) {
+  if (P.gate && *(volatile uint32_t*)P.cflag == 0) return;  // the two-kernel path succeeded
+  const Lay L = layout(P.cap, P.wpad);
+  const uint32_t t = threadIdx.x, lane = t & 31u;
+  uint64_t* mbar = s_mbar;
+  uint4* stage = sp<uint4>(L.stage);
+  uint16_t* clbuf = sp<uint16_t>(L.cl);  // 2 x cap
+  for (uint32_t i = t; i < HS; i += NT) s_hset[i] = 0ull;
+  for (uint32_t i = t; i < LTN; i += NT) {
+    s_lt_line[i] = INF;
+    s_lt_ts[i] = ~0ull;
+  }
+  for (uint32_t i = t; i < 3 * NSLOT * P.wpad / 2; i += NT) sp<uint32_t>(L.ma)[i] = 0u;
+  if (t < 4) s_cnt[t] = 0u;
+  if (t == 0) {
+    s_flags = 0;
+    for (int k = 0; k < NSTAGE; ++k) mbar_init(mbar + k, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const uint32_t G = gridDim.x;
+  auto nev = [&](uint32_t b) { return P.bstart[b + 1] - P.bstart[b]; };
+  auto issue = [&](uint32_t b, int st) {  // one thread
+    const uint64_t n = nev(b);
+    if (n == 0 || n > P.cap) return;
+    const uint64_t s0 = P.bstart[b];
+    const uint32_t bytes = (uint32_t)(n * 16);
+    mbar_expect_tx(mbar + st, bytes);
+    bulk_g2s(stage + (size_t)st * P.cap, P.ev + s0, bytes, mbar + st);
+  };
+  if (t == 0)
+    for (int k = 0; k < NSTAGE; ++k) {
+      const uint32_t b = blockIdx.x + (uint32_t)k * G;
+      if (b < P.n_blocks) issue(b, k);
+    }
+
+  const uint32_t tag_base = smem_u32(smem_raw) + L.tag;
+  const uint32_t ma_delta = smem_u32(smem_raw) + L.ma - 2u * tag_base;  // ma = 2 * tag + delta
+  const uint32_t slotw = P.wpad;
+  uint32_t erel[EPT], wsw[EPT], xa[EPT], meta[EPT];
+  uint32_t sphase = 0, stamp = 0, flags = 0;
+  int it = 0;
+  uint32_t b = blockIdx.x;
+  uint32_t n = 0, ws = 0, elast = 0;
+  bool wmw = false;
+  const uint4* src = stage;
+  bool live = b < P.n_blocks;
+  // the previous block, whose exact pass runs in the next interval
+  bool pend = false;
+  int pit = 0;
+  uint32_t pb = 0, pn = 0;
+  unsigned long long bstamp = 0;
+
+  // P1 of the unit starting at relative epoch `ws` (xa computed for the unit)
+  auto p1 = [&](uint32_t st) {
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const uint32_t slot = erel[k] - ws;
+      xa[k] = tag_base + (slot < NSLOT ? (slot * slotw + wsw[k]) << 1 : 0u);  // loads stay in range
+      sts16_if(slot < NSLOT, xa[k], meta[k] & 0x7FFu);
+    }
+    if (wmw) {
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t slot = erel[k] - ws;
+        if (slot < NSLOT && (meta[k] & 0x1000u))
+          extra_words(tag_base + slot * slotw * 2u, 2u * (tag_base + slot * slotw * 2u) + ma_delta,
+                      src[k * NT + t].x, meta[k] & 0x7FFu, 1, st);
+      }
+    }
+  };
+  auto load_block = [&]() {
+    const uint64_t n_all = nev(b);
+    n = n_all <= P.cap ? (uint32_t)n_all : 0u;
+    if (n_all > P.cap) flags |= ST_RANGE;  // exceeds the staging capacity
+    const int sti = it % NSTAGE;
+    src = stage + (size_t)sti * P.cap;
+    if (n > 0) {
+      mbar_wait(mbar + sti, (sphase >> sti) & 1u);
+      sphase ^= 1u << sti;
+    }
+    if (P.debug & 2u) n = 0;  // experiment: TMA stream only
+    const uint32_t e0 = n > 0 ? acc_epoch(src[0].y) : 0u;
+    elast = n > 0 ? acc_epoch(src[n - 1].y) - e0 : 0u;
+    ws = 0;
+    uint32_t mw = 0;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const uint32_t i = (uint32_t)k * NT + t;
+      const bool in = i < n;
+      const uint4 r = in ? src[i] : make_uint4(0, 0, 0, 0);
+      const uint32_t e = acc_epoch(r.y);
+      uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, e, 1);
+      if (lane == 0 && in && i > 0) prev = acc_epoch(src[i - 1].y);
+      if (in && i > 0 && e < prev) flags |= ST_ORDER;
+      const uint32_t off = acc_off(r.x), len = acc_len(r.x);
+      const bool ok = in && (len - 1u) < MCKG_MAX_LEN && off + len <= P.shmem_bytes &&
+                      ((uint32_t)r.z >> 16) == 0u && e >= e0;
+      if (in && !ok && e >= e0) flags |= ST_RANGE;
+      erel[k] = ok ? e - e0 : INV;
+      wsw[k] = sw(off >> 2);
+      const uint32_t spans = ok && ((off & 3u) + len) > 4u;
+      meta[k] = acc_tid(r.y) | (acc_write(r.x) << 11) | (spans << 12);
+      mw |= spans;
+    }
+    wmw = __any_sync(0xFFFFFFFFu, mw);
+  };
+
+  if (live) {
+    load_block();
+    p1(++stamp & 0xFFFFu);
+  }
+  while (true) {
+    fsync();  // (a) P1 of this unit and P3 of the previous one are complete
+    const bool doexact = pend;
+    const int pq = pit & 1;
+    pend = false;
+    if (doexact) {
+      ++bstamp;
+      const uint32_t m = pn > 0 ? s_cnt[pq] : 0u;
+      if (P.mode == 1) {
+        // hand the candidate list to exact_kernel
+        if (t < 32) {
+          const uint16_t* cl = clbuf + (size_t)pq * P.cap;
+          if (m <= CMAX) {
+            for (uint32_t i = lane; i < m; i += 32) P.cidx[(size_t)pb * CMAX + i] = cl[i];
+            if (lane == 0) P.ccount[pb] = (uint16_t)m;
+          } else if (lane == 0) {
+            P.ccount[pb] = 0;
+            atomicOr(P.cflag, 1u);
+          }
+        }
+      } else if (m > 0 && !(P.debug & 1u)) {
+        exact_block(P, stage + (size_t)(pit % NSTAGE) * P.cap, clbuf + (size_t)pq * P.cap, m, pq,
+                    P.obj_base + pb, P.bid_base + pb, bstamp);
+      }
+    }
+    const uint32_t st = stamp & 0xFFFFu;
+    if (live) {
+      // P2: words seen by a second thread; written words
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const bool a = erel[k] - ws < NSLOT;
+        const uint32_t tg = lds16(xa[k]);
+        const uint32_t mm = 2u * xa[k] + ma_delta;
+        sts16_if(a && tg != (meta[k] & 0x7FFu), mm, st);
+        sts16_if(a && (meta[k] & 0x800u), mm + 2u, st);
+      }
+      if (wmw) {
+        for (int k = 0; k < EPT; ++k) {
+          const uint32_t slot = erel[k] - ws;
+          if (slot < NSLOT && (meta[k] & 0x1000u))
+            extra_words(tag_base + slot * slotw * 2u, 2u * (tag_base + slot * slotw * 2u) + ma_delta,
+                        src[k * NT + t].x, meta[k] & 0x7FFu, 2, st);
+        }
+      }
+    }
+    fsync();  // (b)
+    if (doexact) {
+      // the previous block is done: append its triples, free its stage
+      if (t < 32) {
+        flush_triples(P, pq);
+        __syncwarp();
+        if (t == 0) s_cnt[2 + pq] = 0;
+      }
+      if (t == 0) {
+        s_cnt[pq] = 0;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t nb = pb + (uint32_t)NSTAGE * G;
+        if (nb < P.n_blocks) issue(nb, pit % NSTAGE);
+      }
+    }
+    if (!live) break;
+    // P3: candidates -> the block's list (warp-aggregated compaction)
+    const int p = it & 1;
+    uint16_t* cl = clbuf + (size_t)p * P.cap;
+    uint32_t cmask = 0;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const uint32_t v = lds32(2u * xa[k] + ma_delta);
+      if (erel[k] - ws < NSLOT && v == (st | (st << 16))) cmask |= 1u << k;
+    }
+    if (wmw) {
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t slot = erel[k] - ws;
+        if (slot < NSLOT && (meta[k] & 0x1000u) &&
+            extra_words(tag_base + slot * slotw * 2u, 2u * (tag_base + slot * slotw * 2u) + ma_delta,
+                        src[k * NT + t].x, meta[k] & 0x7FFu, 3, st))
+          cmask |= 1u << k;
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, cmask)) {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const bool cand = (cmask >> k) & 1u;
+        const uint32_t bm = __ballot_sync(0xFFFFFFFFu, cand);
+        if (bm) {
+          const uint32_t leader = __ffs(bm) - 1u;
+          uint32_t base = 0;
+          if (lane == leader) base = atomicAdd(s_cnt + p, (uint32_t)__popc(bm));
+          base = __shfl_sync(0xFFFFFFFFu, base, leader);
+          if (cand) cl[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)((uint32_t)k * NT + t);
+        }
+      }
+    }
+    // next unit: the next round of this block, or the next block
+    if (ws + NSLOT <= elast) {
+      // first record past the window (records are in epoch order)
+      const uint32_t e0 = acc_epoch(src[0].y), lim = e0 + ws + NSLOT;
+      uint32_t lo = 0, hi = n;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (acc_epoch(src[mid].y) < lim) lo = mid + 1; else hi = mid;
+      }
+      ws = lo < n ? acc_epoch(src[lo].y) - e0 : elast + 1;
+      p1(++stamp & 0xFFFFu);
+    } else {
+      pend = true;
+      pit = it;
+      pb = b;
+      pn = n;
+      b += G;
+      ++it;
+      live = b < P.n_blocks;
+      if (live) {
+        load_block();
+        p1(++stamp & 0xFFFFu);
+      }
+    }
+  }
+  flags = __reduce_or_sync(0xFFFFFFFFu, flags);
+  if (lane == 0 && flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+  if (t < LTN && s_lt_line[t] != INF) atomicMin(P.line_first + s_lt_line[t], s_lt_ts[t]);
+  if (t == 0 && s_flags) atomicOr(P.status, s_flags);
+}
+
+// ---------------- exact_kernel: the exact pass of the two-kernel mode ----
+// One warp per simulated block with candidates (grid-stride), lane per X,
+// the Y's by shuffle; the candidate records are read from the trace in
+// global memory (16 B each, ~1.5 % of the records on C3).  Per warp: a
+// lane-owned line-first cache, a (word, line) reported-set table and a
+// triple staging buffer, all contention-free.
+constexpr uint32_t XW = 8;     // warps per CTA
+constexpr uint32_t XHS = 128;  // reported-set slots per warp
+constexpr uint32_t XTB = 64;   // staged triples per warp
+
+struct WarpOut {
+  uint32_t lc_line;          // lane-owned line cache entry
+  unsigned long long lc_ts;
+  uint32_t lc_next;          // uniform: next slot to allocate
+  uint32_t tbn;              // uniform: staged triples
+  uint32_t flags;
+};
+
+__device__ void wo_line(WarpOut& E, const Params& P, bool leader, uint32_t line, unsigned long long ts) {
   const uint32_t lane = threadIdx.x & 31u;
   for (uint32_t lm = __ballot_sync(0xFFFFFFFFu, leader); lm; lm &= lm - 1u) {
     const int src = __ffs(lm) - 1;
@@ -254,8 +606,7 @@ __device__ void line_cache_put(ExactState& E, const Params& P, bool leader, uint
   }
 }
 
-// Flushes the staged triples (exact warp only).
-__device__ void flush_tbuf(ExactState& E, const Params& P) {
+__device__ void wo_flush(WarpOut& E, const Params& P, mckg_race_triple* tb) {
   const uint32_t lane = threadIdx.x & 31u;
   __syncwarp();
   const uint32_t n = E.tbn;
@@ -265,63 +616,74 @@ __device__ void flush_tbuf(ExactState& E, const Params& P) {
   base = __shfl_sync(0xFFFFFFFFu, base, 0);
   for (uint32_t i = lane; i < n; i += 32) {
     if (base + i < P.capacity)
-      P.tri[base + i] = s_tbuf[i];
+      P.tri[base + i] = tb[i];
     else
-      atomicOr(s_misc + M_FLAGS, ST_OVERFLOW);
+      E.flags |= ST_OVERFLOW;
   }
   __syncwarp();
   E.tbn = 0;
 }
 
-// Appends k (warp-uniform) triples per `emit` lane: bytes b0..b0+k-1.
-__device__ void append_triples(ExactState& E, const Params& P, bool emit, uint32_t obj,
-                               uint32_t b0, uint32_t k, int32_t line) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t em = __ballot_sync(0xFFFFFFFFu, emit);
-  if (!em) return;
-  const uint32_t need = k * __popc(em);
-  if (E.tbn + need > TBN) flush_tbuf(E, P);
-  const uint32_t pre = k * __popc(em & ((1u << lane) - 1u));
-  if (emit)
-    for (uint32_t q = 0; q < k; ++q) s_tbuf[E.tbn + pre + q] = mckg_race_triple{obj, b0 + q, line};
-  __syncwarp();
-  E.tbn += need;
+// the (word, line) reported-set table of one warp (see hset_or)
+__device__ uint32_t whset_or(unsigned long long* hs, unsigned long long bstamp, uint32_t word, uint32_t line,
+                             uint32_t mask) {
+  const unsigned long long want = (bstamp << 40) | ((unsigned long long)(word & 0x3FFFFu) << 22) |
+                                  ((unsigned long long)(line & 0xFFFFu) << 6);
+  uint32_t h = (uint32_t)(((want >> 6) * 0x9E3779B97F4A7C15ull) >> 40) & (XHS - 1);
+  for (uint32_t probe = 0; probe < XHS; ++probe) {
+    unsigned long long cur = hs[h];
+    while ((cur >> 40) != bstamp) {
+      const unsigned long long old = atomicCAS(hs + h, cur, want | mask);
+      if (old == cur) return mask;
+      cur = old;
+    }
+    if ((cur & ~0x3Full) == want) {
+      const unsigned long long old = atomicOr(hs + h, (unsigned long long)mask);
+      return mask & ~(uint32_t)old & 0xFu;
+    }
+    h = (h + 1) & (XHS - 1);
+  }
+  return 0x10u | mask;
 }
 
-// Exact pass over a block's candidate list, run by the dedicated exact warp:
-// lane-per-X, each lane scans every candidate Y (broadcast loads).
-__device__ void exact_block(ExactState& E, const Lay& L, const Params& P, const uint4* src,
-                            const uint16_t* cl, uint32_t m, uint32_t obj, uint32_t bid,
-                            unsigned long long bstamp) {
+__device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const uint16_t* cl, uint32_t m,
+                           uint32_t obj, uint32_t bid, unsigned long long bstamp, unsigned long long* hs,
+                           mckg_race_triple* tb) {
   const uint32_t lane = threadIdx.x & 31u;
-  uint32_t* misc = s_misc;
   for (uint32_t xb = 0; xb < m; xb += 32u) {
-    const uint32_t xp = xb + lane;
-    const bool act = xp < m;
-    const uint32_t xi = act ? cl[xp] : 0u;
-    const uint4 X = src[xi];
-    const uint32_t xlen = acc_len(X.x);
-    const uint32_t xoff = acc_off(X.x), xend = xoff + xlen;
+    const bool act = xb + lane < m;
+    const uint32_t xi = act ? cl[xb + lane] : 0xFFFFu;
+    const uint4 X = act ? __ldg(src + xi) : make_uint4(0, 0, 0, 0);
+    const uint32_t xoff = acc_off(X.x), xend = xoff + acc_len(X.x);
     const uint32_t xtid = acc_tid(X.y), xep = acc_epoch(X.y);
     const bool xw = acc_write(X.x);
     uint32_t bits = 0;
-#pragma unroll 4
-    for (uint32_t j = 0; j < m; ++j) {
-      const uint32_t yi = cl[j];
-      const uint2 Y = *reinterpret_cast<const uint2*>(src + yi);
-      const uint32_t yoff = acc_off(Y.x), yend = yoff + acc_len(Y.x);
-      const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
-      const bool hit = yi < xi && acc_epoch(Y.y) == xep && acc_tid(Y.y) != xtid &&
-                       (xw || acc_write(Y.x)) && lo < hi;
-      if (hit) bits |= ((1u << (hi - lo)) - 1u) << (lo - xoff);
+    for (uint32_t yb = 0; yb < m; yb += 32u) {
+      uint32_t yi_l = xi, y0 = X.x, y1 = X.y;
+      if (yb != xb) {
+        const bool ya = yb + lane < m;
+        yi_l = ya ? cl[yb + lane] : 0xFFFFu;
+        const uint2 Yv = ya ? __ldg(reinterpret_cast<const uint2*>(src + yi_l)) : make_uint2(0, 0);
+        y0 = Yv.x;
+        y1 = Yv.y;
+      }
+      const uint32_t cnt = min(32u, m - yb);
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint32_t yi = __shfl_sync(0xFFFFFFFFu, yi_l, j);
+        const uint32_t Yx = __shfl_sync(0xFFFFFFFFu, y0, j);
+        const uint32_t Yy = __shfl_sync(0xFFFFFFFFu, y1, j);
+        const uint32_t yoff = acc_off(Yx), yend = yoff + acc_len(Yx);
+        const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
+        const bool hit = yi < xi && acc_epoch(Yy) == xep && acc_tid(Yy) != xtid &&
+                         (xw || acc_write(Yx)) && lo < hi;
+        if (hit) bits |= ((1u << (hi - lo)) - 1u) << (lo - xoff);
+      }
     }
-    if (!act) bits = 0;
-    const bool racing = bits != 0;
-    if (!__any_sync(0xFFFFFFFFu, racing)) continue;
+    const bool racing = act && bits != 0;
+    const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
+    if (!rm) continue;
     const int32_t line = (int32_t)X.z;
     const unsigned long long ts = ts_key(X.w, bid, xtid);
-    // first racing timestamp per line: min within the warp, then the cache
-    const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
     const uint32_t gm = __match_any_sync(0xFFFFFFFFu, racing ? (uint32_t)line : (0x80000000u | lane));
     unsigned long long mn = ts;
     for (uint32_t tmp = rm; tmp; tmp &= tmp - 1u) {
@@ -329,270 +691,73 @@ __device__ void exact_block(ExactState& E, const Lay& L, const Params& P, const 
       const unsigned long long v = shfl64(ts, s);
       if ((gm >> s) & 1u) mn = v < mn ? v : mn;
     }
-    line_cache_put(E, P, racing && lane == (uint32_t)(__ffs(gm) - 1), (uint32_t)line, mn);
-    // reported triples, deduplicated per block
-    const bool simple = m <= 32u &&
-        __all_sync(0xFFFFFFFFu, !racing || (xlen == 4u && (xoff & 3u) == 0u && bits == 0xFu));
-    if (simple) {
-      // whole aligned words: (word, line) identifies the 4 bytes exactly
-      const uint32_t km = __match_any_sync(0xFFFFFFFFu, racing ? ((xoff >> 2) | ((uint32_t)line << 18))
-                                                                : (0xFFFFFFFFu - lane));
-      const bool lead = racing && lane == (uint32_t)(__ffs(km) - 1);
-      append_triples(E, P, lead, obj, xoff, 4u, line);
-    } else {
-      for (uint32_t q = 0; q < MCKG_MAX_LEN; ++q) {
-        bool fresh = false;
-        if ((bits >> q) & 1u) {
-          const uint32_t byte = xoff + q;
-          const unsigned long long key = (bstamp << 40) |
-                                         ((unsigned long long)(byte & 0xFFFFFu) << 16) |
-                                         ((uint32_t)line & 0xFFFFu);
-          const int r = hset_insert(L, key, bstamp);
-          if (r == 2) atomicOr(misc + M_FLAGS, ST_DUP);
-          fresh = r != 0;
+    wo_line(E, P, racing && lane == (uint32_t)(__ffs(gm) - 1), (uint32_t)line, mn);
+    // fresh bytes per word of X (at most 3 words)
+    uint32_t fresh[3] = {0u, 0u, 0u};
+    uint32_t k = 0;
+    if (racing) {
+      const uint64_t ab = (uint64_t)bits << (xoff & 3u);
+      for (uint32_t w = 0; w < 3u && (xoff >> 2) + w <= (xend - 1u) >> 2; ++w) {
+        const uint32_t wm = (uint32_t)(ab >> (4u * w)) & 0xFu;
+        if (!wm) continue;
+        uint32_t f = whset_or(hs, bstamp, (xoff >> 2) + w, (uint32_t)line, wm);
+        if (f & 0x10u) {
+          E.flags |= ST_DUP;
+          f &= 0xFu;
         }
-        append_triples(E, P, fresh, obj, xoff + q, 1u, line);
+        fresh[w] = f;
+        k += __popc(f);
       }
     }
+    uint32_t incl = k;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= (uint32_t)d) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (E.tbn + total > XTB) wo_flush(E, P, tb);
+    uint32_t pos = E.tbn + incl - k;
+    for (uint32_t w = 0; w < 3u; ++w)
+      for (uint32_t f = fresh[w]; f; f &= f - 1u, ++pos) {
+        const mckg_race_triple tr{obj, ((xoff >> 2) + w) * 4u + (__ffs(f) - 1u), line};
+        if (pos < XTB) {
+          tb[pos] = tr;
+        } else {  // more than a buffer in one step: straight to global memory
+          const unsigned long long g = atomicAdd(P.n_tri, 1ull);
+          if (g < P.capacity)
+            P.tri[g] = tr;
+          else
+            E.flags |= ST_OVERFLOW;
+        }
+      }
+    __syncwarp();
+    E.tbn = min(E.tbn + total, XTB);
   }
 }
 
-template <int EPT>
-__device__ void process_block(const Lay& L, const Params& P, const uint4* src, uint32_t n,
-                              uint16_t* cl, uint32_t* clcount, uint32_t& stamp) {
-  const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
-  const uint32_t shm = P.shmem_bytes;
-  const uint32_t tag_base = smem_u32(smem_raw) + L.tag;
-  const uint32_t d1 = L.multi - L.tag, d2 = L.anyw - L.tag;
-  uint32_t* bitmap = sp<uint32_t>(L.bitmap);
-  const uint16_t* seg = sp<uint16_t>(L.seg);
-  uint32_t* misc = s_misc;
-  // Per owned record i = k*NT + t: epoch (INV = absent or invalid), shared
-  // address of its first word's tag, meta = tid | write << 11 | spans << 12.
-  uint32_t ep[EPT], xa[EPT], meta[EPT];
-  uint32_t flags = 0, mw = 0;
-  const uint32_t cur0 = acc_epoch(src[0].y);
-#pragma unroll
-  for (int k = 0; k < EPT; ++k) {
-    const uint32_t i = (uint32_t)k * NT + t;
-    const bool in = i < n;
-    const uint4 r = in ? src[i] : make_uint4(0, 0, 0, 0);
-    const uint32_t e = acc_epoch(r.y);
-    uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, e, 1);
-    if (lane == 0 && in && i > 0) prev = acc_epoch(src[i - 1].y);
-    const bool start = in && (i == 0 || e != prev);
-    if (in && i > 0 && e < prev) flags |= ST_ORDER;
-    const uint32_t off = acc_off(r.x), len = acc_len(r.x);
-    const bool ok = in && (len - 1u) < MCKG_MAX_LEN && off + len <= shm &&
-                    ((uint32_t)r.z >> 16) == 0u;
-    if (in && !ok) flags |= ST_RANGE;
-    ep[k] = ok ? e : INV;
-    xa[k] = tag_base + (ok ? sw(off >> 2) * 4u : 0u);
-    const uint32_t spans = ok && ((off & 3u) + len) > 4u;
-    meta[k] = acc_tid(r.y) | (acc_write(r.x) << 11) | (spans << 12);
-    mw |= spans;
-    const uint32_t bm = __ballot_sync(0xFFFFFFFFu, start);
-    if (lane == 0 && (uint32_t)k * NT < n) bitmap[(uint32_t)k * NWARP + warp] = bm;
-    // P1 of the first epoch, fused with the load
-    sts_if(ep[k] == cur0, xa[k], meta[k] & 0x7FFu);
+__global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
+  __shared__ unsigned long long hs_all[XW][XHS];
+  __shared__ mckg_race_triple tb_all[XW][XTB];
+  if (*(volatile uint32_t*)P.cflag) return;  // a list overflowed: the fused kernel redoes the launch
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  unsigned long long* hs = hs_all[warp];
+  mckg_race_triple* tb = tb_all[warp];
+  for (uint32_t i = lane; i < XHS; i += 32) hs[i] = 0ull;
+  __syncwarp();
+  WarpOut E{INF, ~0ull, 0u, 0u, 0u};
+  unsigned long long bstamp = 0;
+  for (uint32_t b = blockIdx.x * XW + warp; b < P.n_blocks; b += gridDim.x * XW) {
+    const uint32_t m = P.ccount[b];
+    if (m == 0) continue;
+    ++bstamp;
+    exact_warp(E, P, reinterpret_cast<const uint4*>(P.ev + P.bstart[b]), P.cidx + (size_t)b * CMAX, m,
+               P.obj_base + b, P.bid_base + b, bstamp, hs, tb);
   }
-  flags = __reduce_or_sync(0xFFFFFFFFu, flags);
-  if (lane == 0 && flags) atomicOr(misc + M_FLAGS, flags);
-  const bool wmw = __any_sync(0xFFFFFFFFu, mw);  // warp has multi-word accesses
-  uint32_t st = ++stamp;
-  if (wmw) {
-    for (int k = 0; k < EPT; ++k)
-      if (ep[k] == cur0 && (meta[k] & 0x1000u))
-        extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 1, st);
-  }
-  if (t == 0) *clcount = 0;
-  fsync();
-  if (P.debug & 8u) return;   // experiment: load + bitmap + first P1 only
-  if (warp == 0) build_segments(L, n);
-  if (P.debug & 16u) {        // experiment: + epoch segmentation
-    fsync();
-    return;
-  }
-  uint32_t cur = cur0;
-  uint32_t sidx = 0;
-  while (true) {
-    // P2: words seen by a second thread; written words
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const bool a = ep[k] == cur;
-      const uint32_t tg = lds(xa[k]);
-      sts_if(a && tg != (meta[k] & 0x7FFu), xa[k] + d1, st);
-      sts_if(a && (meta[k] & 0x800u), xa[k] + d2, st);
-    }
-    if (wmw) {
-      for (int k = 0; k < EPT; ++k)
-        if (ep[k] == cur && (meta[k] & 0x1000u))
-          extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 2, st);
-    }
-    fsync();
-    const uint32_t e = seg[sidx + 1];
-    // P3: candidates -> block list cl (warp-aggregated compaction)
-    uint32_t cmask = 0;  // bit k: record k is a candidate
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const uint32_t mv = lds(xa[k] + d1), av = lds(xa[k] + d2);
-      if (ep[k] == cur && mv == st && av == st) cmask |= 1u << k;
-    }
-    if (wmw) {
-      for (int k = 0; k < EPT; ++k)
-        if (ep[k] == cur && (meta[k] & 0x1000u) &&
-            extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 3, st))
-          cmask |= 1u << k;
-    }
-    if (__any_sync(0xFFFFFFFFu, cmask)) {
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        const bool cand = (cmask >> k) & 1u;
-        const uint32_t bm = __ballot_sync(0xFFFFFFFFu, cand);
-        if (bm) {
-          const uint32_t leader = __ffs(bm) - 1u;
-          uint32_t base = 0;
-          if (lane == leader) base = atomicAdd(clcount, (uint32_t)__popc(bm));
-          base = __shfl_sync(0xFFFFFFFFu, base, leader);
-          if (cand) cl[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)((uint32_t)k * NT + t);
-        }
-      }
-    }
-    const bool more = e < n;
-    if (more) {  // P1 of the next epoch shares this barrier interval
-      cur = acc_epoch(src[e].y);
-      st = ++stamp;
-      ++sidx;
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) sts_if(ep[k] == cur, xa[k], meta[k] & 0x7FFu);
-      if (wmw) {
-        for (int k = 0; k < EPT; ++k)
-          if (ep[k] == cur && (meta[k] & 0x1000u))
-            extra_words(tag_base, d1, d2, src[k * NT + t].x, meta[k] & 0x7FFu, 1, st);
-      }
-    }
-    fsync();
-    if (!more) break;
-  }
-}
-
-// One CTA = 8 filter warps + 1 exact warp (warp specialised).  Filter warps
-// run the epoch filter of block b+1 while the exact warp finishes block b;
-// they hand candidate lists over through two mbarrier-guarded buffers.  The
-// exact warp also owns the report state and re-issues the TMA load into the
-// stage it has just released.
-constexpr int NTHREADS = NT + 32;
-
-template <int EPT>
-__global__ void __launch_bounds__(NTHREADS, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 1))
-    race_detect_kernel(Params P) {
-  const Lay L = layout(P.cap, P.wpad);
-  const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31u;
-  uint32_t* misc = s_misc;
-  uint64_t* mbar = s_mbar;
-  uint4* stage = sp<uint4>(L.stage);
-  uint16_t* clbuf = sp<uint16_t>(L.cl);  // 2 x cap
-  for (uint32_t i = t; i < HS; i += NTHREADS) s_hset[i] = 0ull;
-  for (uint32_t i = t; i < LTN; i += NTHREADS) {
-    s_lt_line[i] = INF;
-    s_lt_ts[i] = ~0ull;
-  }
-  for (uint32_t i = t; i < 3 * P.wpad; i += NTHREADS) sp<uint32_t>(L.tag)[i] = 0u;
-  if (t < 16) misc[t] = 0u;
-  if (t == 0) {
-    for (int k = 0; k < NSTAGE; ++k) mbar_init(mbar + k, 1);
-    for (int k = 0; k < 2; ++k) {
-      mbar_init(s_full_cl + k, 1);
-      mbar_init(s_free_cl + k, 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const uint32_t G = gridDim.x;
-  auto nev = [&](uint32_t b) { return P.bstart[b + 1] - P.bstart[b]; };
-  auto issue = [&](uint32_t b, int st) {  // one thread
-    const uint64_t n = nev(b);
-    if (n == 0 || n > P.cap) return;
-    const uint64_t s0 = P.bstart[b];
-    const uint32_t bytes = (uint32_t)(n * 16);
-    mbar_expect_tx(mbar + st, bytes);
-    bulk_g2s(stage + (size_t)st * P.cap, P.ev + s0, bytes, mbar + st);
-  };
-
-  if (warp < NT / 32) {
-    // ---------------- filter warps ----------------
-    uint32_t sphase = 0, stamp = 0;
-    int it = 0;
-    for (uint32_t b = blockIdx.x; b < P.n_blocks; b += G, ++it) {
-      const int st = it % NSTAGE;
-      const int p = it & 1;
-      const uint32_t u = (uint32_t)(it >> 1);
-      mbar_wait(s_free_cl + p, (u & 1u) ^ 1u);  // exact warp done with this buffer
-      const uint64_t n_all = nev(b);
-      const uint32_t n = n_all <= P.cap ? (uint32_t)n_all : 0u;
-      uint32_t* clcount = misc + 8 + p;
-      if (n > 0 && (P.debug & 2u)) {
-        mbar_wait(mbar + st, (sphase >> st) & 1u);
-        sphase ^= 1u << st;
-        if (t == 0) *clcount = 0;
-        fsync();
-      } else if (n > 0) {
-        mbar_wait(mbar + st, (sphase >> st) & 1u);
-        sphase ^= 1u << st;
-        process_block<EPT>(L, P, stage + (size_t)st * P.cap, n, clbuf + (size_t)p * P.cap,
-                           clcount, stamp);
-      } else {
-        if (t == 0) {
-          *clcount = 0;
-          if (n_all > 0) atomicOr(misc + M_FLAGS, ST_RANGE);  // exceeds the staging capacity
-        }
-        fsync();
-      }
-      if (t == 0) {
-        s_info[p][0] = n;
-        s_info[p][1] = b;
-        s_info[p][2] = *clcount;
-        mbar_arrive(s_full_cl + p);
-      }
-    }
-  } else {
-    // ---------------- exact / report warp ----------------
-    if (lane == 0)
-      for (int k = 0; k < NSTAGE; ++k) {
-        const uint32_t b = blockIdx.x + (uint32_t)k * G;
-        if (b < P.n_blocks) issue(b, k);
-      }
-    unsigned long long bstamp = 0;
-    ExactState E{INF, ~0ull, 0u, 0u};
-    int it = 0;
-    for (uint32_t b = blockIdx.x; b < P.n_blocks; b += G, ++it) {
-      const int st = it % NSTAGE;
-      const int p = it & 1;
-      const uint32_t u = (uint32_t)(it >> 1);
-      mbar_wait(s_full_cl + p, u & 1u);
-      const uint32_t n = s_info[p][0], m = s_info[p][2];
-      ++bstamp;
-      if (n > 0 && m > 0 && !(P.debug & 1u))
-        exact_block(E, L, P, stage + (size_t)st * P.cap, clbuf + (size_t)p * P.cap, m,
-                    P.obj_base + b, P.bid_base + b, bstamp);
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(s_free_cl + p);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t nb = b + (uint32_t)NSTAGE * G;
-        if (nb < P.n_blocks) issue(nb, st);
-      }
-    }
-    flush_tbuf(E, P);
-    if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
-  }
-  __syncthreads();
-  if (t == 0 && misc[M_FLAGS]) atomicOr(P.status, misc[M_FLAGS]);
-  if (t == 0 && (P.debug & 12u)) {
-    atomicAdd(P.status + 1, misc[12]);
-    atomicAdd(P.status + 2, misc[13]);
-  }
+  wo_flush(E, P, tb);
+  if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
+  const uint32_t f = __reduce_or_sync(0xFFFFFFFFu, E.flags);
+  if (lane == 0 && f) atomicOr(P.status, f);
 }
 
 __global__ void reset_kernel(unsigned long long* n_tri, unsigned long long* line_first,
@@ -687,7 +852,7 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     configured[ki] = smem;
   }
   int per_sm = 0;
-  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTHREADS, smem));
+  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
   if (per_sm < 1) per_sm = 1;
   uint32_t grid = (uint32_t)sm_count() * (uint32_t)per_sm;
   if (grid > tr->n_blocks) grid = tr->n_blocks;
@@ -709,9 +874,48 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     const char* dbg = getenv("MCKG_DEBUG");
     P.debug = dbg ? (uint32_t)atoi(dbg) : 0u;
   }
-  kern<<<grid, NTHREADS, smem, (cudaStream_t)stream>>>(P);
+  P.mode = 0;
+  P.gate = 0;
+  P.ccount = nullptr;
+  P.cidx = nullptr;
+  P.cflag = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (P.debug & 32u) {  // MCKG_DEBUG=32: the fused kernel alone (tests cover both paths)
+    kern<<<grid, NT, smem, s>>>(P);
+    MCKG_CUDA_TRY(cudaGetLastError());
+    note_launch(1, grid, NT, (uint32_t)smem);
+    return MCKG_OK;
+  }
+  // two-kernel path: filter -> candidate lists -> exact_kernel; the fused
+  // kernel (gated on *cflag) redoes the launch if a block has > CMAX candidates
+  keep_pool_memory();
+  MCKG_CUDA_TRY(cudaMallocAsync(&P.ccount, (size_t)tr->n_blocks * sizeof(uint16_t), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&P.cidx, (size_t)tr->n_blocks * CMAX * sizeof(uint16_t), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&P.cflag, sizeof(uint32_t), s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(P.cflag, 0, sizeof(uint32_t), s));
+  P.mode = 1;
+  kern<<<grid, NT, smem, s>>>(P);
+  uint32_t launched = 1;
+  if (!(P.debug & 1u)) {
+    static int xper = 0;
+    if (!xper) {
+      MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, exact_kernel, XW * 32, 0));
+      if (xper < 1) xper = 1;
+    }
+    uint32_t xgrid = (uint32_t)sm_count() * (uint32_t)xper;
+    const uint32_t need = (tr->n_blocks + XW - 1) / XW;
+    if (xgrid > need) xgrid = need;
+    exact_kernel<<<xgrid, XW * 32, 0, s>>>(P);
+    P.mode = 0;
+    P.gate = 1;
+    kern<<<grid, NT, smem, s>>>(P);
+    launched += 2;
+  }
   MCKG_CUDA_TRY(cudaGetLastError());
-  note_launch(1, grid, NTHREADS, (uint32_t)smem);
+  cudaFreeAsync(P.ccount, s);
+  cudaFreeAsync(P.cidx, s);
+  cudaFreeAsync(P.cflag, s);
+  note_launch(launched, grid, NT, (uint32_t)smem);
   return MCKG_OK;
 }
 

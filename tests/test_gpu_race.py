@@ -1,6 +1,10 @@
 """K2 (mckg_detect_shared) parity against the CPU oracle: bit-exact reported
 triples (RaceState::reported, machine.hpp:91), bit-exact first-detection
-timestamps per line (the Race diagnostic order, machine.cpp:41-46)."""
+timestamps per line (the Race diagnostic order, machine.cpp:41-46).
+
+Every test runs on both K2 paths: the default two-kernel path (filter ->
+per-block candidate lists -> exact_kernel, with the fused kernel redoing a
+launch whose lists overflow) and the fused kernel alone (MCKG_DEBUG=32)."""
 import numpy as np
 import pytest
 
@@ -8,6 +12,15 @@ import oracle_bind as ob
 from tracegen_py import random_trace
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, params=["two_kernel", "fused"])
+def k2_path(request, monkeypatch):
+    if request.param == "fused":
+        monkeypatch.setenv("MCKG_DEBUG", "32")
+    else:
+        monkeypatch.delenv("MCKG_DEBUG", raising=False)
+    return request.param
 
 
 def _gpu(ev, bs, shmem, capacity=None, obj_base=1, bid_base=0):
