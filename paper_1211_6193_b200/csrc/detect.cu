@@ -32,21 +32,30 @@
 //      racing timestamp per line is min-reduced in shared memory, then
 //      globally.
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include "common.cuh"
 
+// TMA stages and CTAs/SM: the fused kernel (report state in static shared
+// memory) 3 / 3; the filter of the two-kernel path 2 / 4
 #ifndef MCKG_K2_NSTAGE
 #define MCKG_K2_NSTAGE 3
 #endif
 #ifndef MCKG_K2_MINB
 #define MCKG_K2_MINB 3
 #endif
+#ifndef MCKG_K2F_NSTAGE
+#define MCKG_K2F_NSTAGE 3
+#endif
+#ifndef MCKG_K2F_MINB
+#define MCKG_K2F_MINB 3
+#endif
 
 namespace mckg {
 namespace {
 
 constexpr int NT = 256;
-constexpr int NSTAGE = MCKG_K2_NSTAGE;
+constexpr int NSTAGE_MAX = 3;
 constexpr int EPT_MAX = 16;     // records per thread kept in registers (cap <= 4096)
 constexpr uint32_t HS = 512;    // (word, line) -> reported byte mask, per block
 constexpr uint32_t TBN = 256;   // staged triples per buffer before the global append
@@ -90,21 +99,22 @@ __shared__ mckg_race_triple s_tbuf[2][TBN];
 __shared__ uint32_t s_lt_line[LTN];
 __shared__ uint32_t s_cnt[4];    // [0..1] candidates per cl buffer, [2..3] staged triples
 __shared__ uint32_t s_flags;
-__shared__ uint64_t s_mbar[NSTAGE];
+__shared__ uint64_t s_mbar[NSTAGE_MAX];
+__shared__ uint32_t s_n[NSTAGE_MAX];  // events of the block in each stage (0: none loaded)
 
 // Byte offsets of the size-dependent state in the dynamic shared memory.
 struct Lay {
   uint32_t ma, tag, cl, stage, end;
 };
 
-__host__ __device__ inline Lay layout(uint32_t cap, uint32_t wpad) {
+__host__ __device__ inline Lay layout(uint32_t cap, uint32_t wpad, uint32_t nstage) {
   Lay L;
   uint32_t p = 0;
   L.ma = p;      p += NSLOT * wpad * 4;
   L.tag = p;     p += NSLOT * wpad * 2;
   L.cl = p;      p += 2 * cap * 2;
   p = (p + 127u) & ~127u;
-  L.stage = p;   p += NSTAGE * cap * 16;
+  L.stage = p;   p += nstage * cap * 16;
   L.end = p;
   return L;
 }
@@ -136,6 +146,17 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 
 // Barrier among the NT threads.
 __device__ __forceinline__ void fsync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+// ... that also returns the OR of p over the threads.
+__device__ __forceinline__ bool fsync_or(bool p) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred a, b;\n\tsetp.ne.u32 a, %1, 0;\n\t"
+      "barrier.cta.red.or.pred b, 1, %2, a;\n\tselp.u32 %0, 1, 0, b;\n}"
+      : "=r"(r)
+      : "r"((uint32_t)p), "n"(NT)
+      : "memory");
+  return r != 0;
+}
 
 // Rare path: the 2nd/3rd word of an access spanning several 4-byte words
 // (tag_slot / ma_slot: the slot's arrays).
@@ -329,50 +350,55 @@ __device__ void flush_triples(const Params& P, int q) {
 //         append the previous block's triples; release its TMA stage
 // P3 reads only ma[], P1 writes only tag[]; the exact pass reads the stage
 // and cl of the previous block, which nothing else touches until (b).
-template <int EPT>
-__global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 1))
+template <int EPT, bool FUSED>
+__global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2F_MINB) : (EPT <= 8 ? 2 : 1))
     race_detect_kernel(Params P) {
+  constexpr int NSTAGE = FUSED ? MCKG_K2_NSTAGE : MCKG_K2F_NSTAGE;
   if (P.gate && *(volatile uint32_t*)P.cflag == 0) return;  // the two-kernel path succeeded
-  const Lay L = layout(P.cap, P.wpad);
+  const Lay L = layout(P.cap, P.wpad, NSTAGE);
   const uint32_t t = threadIdx.x, lane = t & 31u;
   uint64_t* mbar = s_mbar;
   uint4* stage = sp<uint4>(L.stage);
   uint16_t* clbuf = sp<uint16_t>(L.cl);  // 2 x cap
-  for (uint32_t i = t; i < HS; i += NT) s_hset[i] = 0ull;
-  for (uint32_t i = t; i < LTN; i += NT) {
-    s_lt_line[i] = INF;
-    s_lt_ts[i] = ~0ull;
+  if constexpr (FUSED) {
+    for (uint32_t i = t; i < HS; i += NT) s_hset[i] = 0ull;
+    for (uint32_t i = t; i < LTN; i += NT) {
+      s_lt_line[i] = INF;
+      s_lt_ts[i] = ~0ull;
+    }
   }
   for (uint32_t i = t; i < 3 * NSLOT * P.wpad / 2; i += NT) sp<uint32_t>(L.ma)[i] = 0u;
   if (t < 4) s_cnt[t] = 0u;
-  if (t == 0) {
-    s_flags = 0;
-    for (int k = 0; k < NSTAGE; ++k) mbar_init(mbar + k, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
+  uint32_t flags = 0;
   const uint32_t G = gridDim.x;
-  auto nev = [&](uint32_t b) { return P.bstart[b + 1] - P.bstart[b]; };
-  auto issue = [&](uint32_t b, int st) {  // one thread
-    const uint64_t n = nev(b);
-    if (n == 0 || n > P.cap) return;
-    const uint64_t s0 = P.bstart[b];
+  // one thread: stream block b into stage st; s_n[st] = its event count
+  // (0 when empty or beyond the staging capacity -- flagged, skipped)
+  auto issue = [&](uint32_t b, int st) {
+    const uint64_t s0 = P.bstart[b], n = P.bstart[b + 1] - s0;
+    if (n > P.cap) flags |= ST_RANGE;
+    const bool go = n > 0 && n <= P.cap;
+    s_n[st] = go ? (uint32_t)n : 0u;
+    if (!go) return;
     const uint32_t bytes = (uint32_t)(n * 16);
     mbar_expect_tx(mbar + st, bytes);
     bulk_g2s(stage + (size_t)st * P.cap, P.ev + s0, bytes, mbar + st);
   };
-  if (t == 0)
+  if (t == 0) {
+    s_flags = 0;
+    for (int k = 0; k < NSTAGE; ++k) mbar_init(mbar + k, 1);
+    fence_mbar_init();
     for (int k = 0; k < NSTAGE; ++k) {
       const uint32_t b = blockIdx.x + (uint32_t)k * G;
       if (b < P.n_blocks) issue(b, k);
     }
+  }
+  __syncthreads();
 
   const uint32_t tag_base = smem_u32(smem_raw) + L.tag;
   const uint32_t ma_delta = smem_u32(smem_raw) + L.ma - 2u * tag_base;  // ma = 2 * tag + delta
   const uint32_t slotw = P.wpad;
   uint32_t erel[EPT], wsw[EPT], xa[EPT], meta[EPT];
-  uint32_t sphase = 0, stamp = 0, flags = 0;
+  uint32_t sphase = 0, stamp = 0;
   int it = 0;
   uint32_t b = blockIdx.x;
   uint32_t n = 0, ws = 0, elast = 0;
@@ -381,6 +407,9 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
   bool live = b < P.n_blocks;
   // the previous block, whose exact pass runs in the next interval
   bool pend = false;
+  bool fresh = false;  // the current unit's block was loaded in the last interval
+  bool held = false;   // the current block still needs its stage after its first unit
+  bool pheld = false;
   int pit = 0;
   uint32_t pb = 0, pn = 0;
   unsigned long long bstamp = 0;
@@ -403,10 +432,8 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
     }
   };
   auto load_block = [&]() {
-    const uint64_t n_all = nev(b);
-    n = n_all <= P.cap ? (uint32_t)n_all : 0u;
-    if (n_all > P.cap) flags |= ST_RANGE;  // exceeds the staging capacity
     const int sti = it % NSTAGE;
+    n = s_n[sti];
     src = stage + (size_t)sti * P.cap;
     if (n > 0) {
       mbar_wait(mbar + sti, (sphase >> sti) & 1u);
@@ -417,41 +444,62 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
     elast = n > 0 ? acc_epoch(src[n - 1].y) - e0 : 0u;
     ws = 0;
     uint32_t mw = 0;
+    // decode; FULL (n == EPT * NT, the common case) drops the bounds predicates
+    auto decode = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const uint32_t i = (uint32_t)k * NT + t;
-      const bool in = i < n;
-      const uint4 r = in ? src[i] : make_uint4(0, 0, 0, 0);
-      const uint32_t e = acc_epoch(r.y);
-      uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, e, 1);
-      if (lane == 0 && in && i > 0) prev = acc_epoch(src[i - 1].y);
-      if (in && i > 0 && e < prev) flags |= ST_ORDER;
-      const uint32_t off = acc_off(r.x), len = acc_len(r.x);
-      const bool ok = in && (len - 1u) < MCKG_MAX_LEN && off + len <= P.shmem_bytes &&
-                      ((uint32_t)r.z >> 16) == 0u && e >= e0;
-      if (in && !ok && e >= e0) flags |= ST_RANGE;
-      erel[k] = ok ? e - e0 : INV;
-      wsw[k] = sw(off >> 2);
-      const uint32_t spans = ok && ((off & 3u) + len) > 4u;
-      meta[k] = acc_tid(r.y) | (acc_write(r.x) << 11) | (spans << 12);
-      mw |= spans;
-    }
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t i = (uint32_t)k * NT + t;
+        const bool in = FULL || i < n;
+        const uint4 r = in ? src[i] : make_uint4(0, 0, 0, 0);
+        const uint32_t e = acc_epoch(r.y);
+        uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, e, 1);
+        if (lane == 0) prev = i > 0 && in ? acc_epoch(src[i - 1].y) : 0u;
+        if (in && e < prev) flags |= ST_ORDER;
+        const uint32_t off = acc_off(r.x), len = acc_len(r.x);
+        const bool ok = in && (len - 1u) < MCKG_MAX_LEN && off + len <= P.shmem_bytes && (r.z >> 16) == 0u;
+        if (in && !ok) flags |= ST_RANGE;
+        erel[k] = ok ? e - e0 : INV;  // e < e0 only if unsorted (flagged): out of every window
+        wsw[k] = sw(off >> 2);
+        const uint32_t spans = ok && ((off & 3u) + len) > 4u;
+        meta[k] = (r.y & 0x7FFu) | ((r.x >> 13) & 0x800u) | (spans << 12);
+        mw |= spans;
+      }
+    };
+    if (n == (uint32_t)(EPT * NT))
+      decode(std::true_type{});
+    else
+      decode(std::false_type{});
     wmw = __any_sync(0xFFFFFFFFu, mw);
   };
 
   if (live) {
     load_block();
     p1(++stamp & 0xFFFFu);
+    fresh = true;
   }
   while (true) {
-    fsync();  // (a) P1 of this unit and P3 of the previous one are complete
+    // (a) P1 of this unit and P3 of the previous one are complete
+    const bool spans_any = fsync_or(fresh && wmw);
+    if (fresh) {
+      // two-kernel path: a one-round block without multi-word accesses never
+      // reads its stage again (records live in registers, the exact kernel
+      // reads global memory): stream the next block into it right away
+      held = FUSED || spans_any || elast >= NSLOT;
+      if (!held && t == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t nb = b + (uint32_t)NSTAGE * G;
+        if (nb < P.n_blocks) issue(nb, it % NSTAGE);
+      }
+      fresh = false;
+    }
     const bool doexact = pend;
     const int pq = pit & 1;
     pend = false;
     if (doexact) {
       ++bstamp;
       const uint32_t m = pn > 0 ? s_cnt[pq] : 0u;
-      if (P.mode == 1) {
+      if constexpr (!FUSED) {
         // hand the candidate list to exact_kernel
         if (t < 32) {
           const uint16_t* cl = clbuf + (size_t)pq * P.cap;
@@ -469,7 +517,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
       }
     }
     const uint32_t st = stamp & 0xFFFFu;
-    if (live) {
+    if (live && !(P.debug & 64u)) {
       // P2: words seen by a second thread; written words
 #pragma unroll
       for (int k = 0; k < EPT; ++k) {
@@ -491,16 +539,20 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
     fsync();  // (b)
     if (doexact) {
       // the previous block is done: append its triples, free its stage
-      if (t < 32) {
-        flush_triples(P, pq);
-        __syncwarp();
-        if (t == 0) s_cnt[2 + pq] = 0;
+      if constexpr (FUSED) {
+        if (t < 32) {
+          flush_triples(P, pq);
+          __syncwarp();
+          if (t == 0) s_cnt[2 + pq] = 0;
+        }
       }
       if (t == 0) {
         s_cnt[pq] = 0;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t nb = pb + (uint32_t)NSTAGE * G;
-        if (nb < P.n_blocks) issue(nb, pit % NSTAGE);
+        if (pheld) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const uint32_t nb = pb + (uint32_t)NSTAGE * G;
+          if (nb < P.n_blocks) issue(nb, pit % NSTAGE);
+        }
       }
     }
     if (!live) break;
@@ -510,6 +562,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
     uint32_t cmask = 0;
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
+      if (P.debug & 64u) break;  // experiment: decode + P1 + barriers only
       const uint32_t v = lds32(2u * xa[k] + ma_delta);
       if (erel[k] - ws < NSLOT && v == (st | (st << 16))) cmask |= 1u << k;
     }
@@ -549,6 +602,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
       p1(++stamp & 0xFFFFu);
     } else {
       pend = true;
+      pheld = held;
       pit = it;
       pb = b;
       pn = n;
@@ -558,13 +612,16 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
       if (live) {
         load_block();
         p1(++stamp & 0xFFFFu);
+        fresh = true;
       }
     }
   }
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if (lane == 0 && flags) atomicOr(&s_flags, flags);
   __syncthreads();
-  if (t < LTN && s_lt_line[t] != INF) atomicMin(P.line_first + s_lt_line[t], s_lt_ts[t]);
+  if constexpr (FUSED) {
+    if (t < LTN && s_lt_line[t] != INF) atomicMin(P.line_first + s_lt_line[t], s_lt_ts[t]);
+  }
   if (t == 0 && s_flags) atomicOr(P.status, s_flags);
 }
 
@@ -795,8 +852,8 @@ int detect_config(uint32_t cap, uint32_t shmem_bytes, size_t* smem, uint32_t* wp
   uint32_t words = (shmem_bytes + 3u) / 4u;
   *wpad = (words + 31u) & ~31u;
   if (*wpad == 0) *wpad = 32;
-  *smem = layout(cap, *wpad).end;
-  return *smem <= 227u * 1024u ? MCKG_OK : MCKG_E_RANGE;
+  *smem = layout(cap, *wpad, MCKG_K2_NSTAGE).end;  // the larger (fused) configuration
+  return *smem + 11u * 1024u <= 227u * 1024u ? MCKG_OK : MCKG_E_RANGE;
 }
 
 }  // namespace mckg
@@ -842,20 +899,30 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     set_error("mckg_detect_shared: shared object too large for the shared-memory filter");
     return MCKG_E_RANGE;
   }
-  void (*kern)(Params) = cap <= 4u * NT   ? race_detect_kernel<4>
-                         : cap <= 8u * NT ? race_detect_kernel<8>
-                                          : race_detect_kernel<16>;
   const int ki = cap <= 4u * NT ? 0 : cap <= 8u * NT ? 1 : 2;
-  static thread_local size_t configured[3] = {0, 0, 0};
-  if (smem > configured[ki]) {
-    MCKG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[ki] = smem;
+  void (*kf)(Params) = ki == 0 ? race_detect_kernel<4, true> : ki == 1 ? race_detect_kernel<8, true>
+                                                                      : race_detect_kernel<16, true>;
+  void (*kt)(Params) = ki == 0 ? race_detect_kernel<4, false> : ki == 1 ? race_detect_kernel<8, false>
+                                                                       : race_detect_kernel<16, false>;
+  const size_t smem_f = layout(cap, wpad, MCKG_K2_NSTAGE).end, smem_t = layout(cap, wpad, MCKG_K2F_NSTAGE).end;
+  static thread_local size_t configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  if (smem_f > configured[0][ki]) {
+    MCKG_CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+    configured[0][ki] = smem_f;
   }
-  int per_sm = 0;
-  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
-  if (per_sm < 1) per_sm = 1;
-  uint32_t grid = (uint32_t)sm_count() * (uint32_t)per_sm;
-  if (grid > tr->n_blocks) grid = tr->n_blocks;
+  if (smem_t > configured[1][ki]) {
+    MCKG_CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
+    configured[1][ki] = smem_t;
+  }
+  auto grid_of = [&](void (*k)(Params), size_t sm) -> uint32_t {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, sm) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    uint32_t g = (uint32_t)sm_count() * (uint32_t)per_sm;
+    return g > tr->n_blocks ? tr->n_blocks : g;
+  };
+  const uint32_t grid_f = grid_of(kf, smem_f), grid_t = grid_of(kt, smem_t);
+  (void)smem;
   Params P;
   P.ev = tr->events;
   P.bstart = tr->block_start;
@@ -881,9 +948,9 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.cflag = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   if (P.debug & 32u) {  // MCKG_DEBUG=32: the fused kernel alone (tests cover both paths)
-    kern<<<grid, NT, smem, s>>>(P);
+    kf<<<grid_f, NT, smem_f, s>>>(P);
     MCKG_CUDA_TRY(cudaGetLastError());
-    note_launch(1, grid, NT, (uint32_t)smem);
+    note_launch(1, grid_f, NT, (uint32_t)smem_f);
     return MCKG_OK;
   }
   // two-kernel path: filter -> candidate lists -> exact_kernel; the fused
@@ -894,7 +961,7 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   MCKG_CUDA_TRY(cudaMallocAsync(&P.cflag, sizeof(uint32_t), s));
   MCKG_CUDA_TRY(cudaMemsetAsync(P.cflag, 0, sizeof(uint32_t), s));
   P.mode = 1;
-  kern<<<grid, NT, smem, s>>>(P);
+  kt<<<grid_t, NT, smem_t, s>>>(P);
   uint32_t launched = 1;
   if (!(P.debug & 1u)) {
     static int xper = 0;
@@ -908,14 +975,14 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     exact_kernel<<<xgrid, XW * 32, 0, s>>>(P);
     P.mode = 0;
     P.gate = 1;
-    kern<<<grid, NT, smem, s>>>(P);
+    kf<<<grid_f, NT, smem_f, s>>>(P);
     launched += 2;
   }
   MCKG_CUDA_TRY(cudaGetLastError());
   cudaFreeAsync(P.ccount, s);
   cudaFreeAsync(P.cidx, s);
   cudaFreeAsync(P.cflag, s);
-  note_launch(launched, grid, NT, (uint32_t)smem);
+  note_launch(launched, grid_t, NT, (uint32_t)smem_t);
   return MCKG_OK;
 }
 
