@@ -703,17 +703,126 @@ __device__ uint32_t whset_or(unsigned long long* hs, unsigned long long bstamp, 
   return 0x10u | mask;
 }
 
+// one line's first racing timestamp into the lane-owned cache (uniform call)
+__device__ __forceinline__ void wo_line1(WarpOut& E, const Params& P, uint32_t L, unsigned long long T) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t own = __ballot_sync(0xFFFFFFFFu, E.lc_line == L);
+  if (own) {
+    if (lane == (uint32_t)(__ffs(own) - 1) && T < E.lc_ts) E.lc_ts = T;
+  } else {
+    if (lane == E.lc_next) {
+      if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
+      E.lc_line = L;
+      E.lc_ts = T;
+    }
+    E.lc_next = (E.lc_next + 1u) & 31u;
+  }
+}
+
+// X (lane-per-X, record R, index xi) races on `bits` (bit j = byte off(X)+j):
+// line-first per distinct line, then the bytes not reported before.
+__device__ void exact_report(WarpOut& E, const Params& P, bool act, const uint4& X, uint32_t bits, uint32_t obj,
+                             uint32_t bid, unsigned long long bstamp, unsigned long long* hs, mckg_race_triple* tb) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const bool racing = act && bits != 0;
+  const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
+  if (!rm) return;
+  const uint32_t line = X.z, xoff = acc_off(X.x), xend = xoff + acc_len(X.x);
+  const unsigned long long ts = ts_key(X.w, bid, acc_tid(X.y));
+  for (uint32_t left = rm; left;) {
+    const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, __ffs(left) - 1);
+    const bool in = racing && line == L;
+    const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, in ? (uint32_t)(ts >> 32) : ~0u);
+    const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, in && (uint32_t)(ts >> 32) == mh ? (uint32_t)ts : ~0u);
+    left &= ~__ballot_sync(0xFFFFFFFFu, in);
+    wo_line1(E, P, L, ((unsigned long long)mh << 32) | ml);
+  }
+  // fresh bytes per word of X (at most 3 words)
+  uint32_t fresh[3] = {0u, 0u, 0u};
+  uint32_t k = 0;
+  if (racing) {
+    const uint64_t ab = (uint64_t)bits << (xoff & 3u);
+    for (uint32_t w = 0; w < 3u && (xoff >> 2) + w <= (xend - 1u) >> 2; ++w) {
+      const uint32_t wm = (uint32_t)(ab >> (4u * w)) & 0xFu;
+      if (!wm) continue;
+      uint32_t f = whset_or(hs, bstamp, (xoff >> 2) + w, line, wm);
+      if (f & 0x10u) {
+        E.flags |= ST_DUP;
+        f &= 0xFu;
+      }
+      fresh[w] = f;
+      k += __popc(f);
+    }
+  }
+  uint32_t incl = k;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= (uint32_t)d) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  if (E.tbn + total > XTB) wo_flush(E, P, tb);
+  uint32_t pos = E.tbn + incl - k;
+  for (uint32_t w = 0; w < 3u; ++w)
+    for (uint32_t f = fresh[w]; f; f &= f - 1u, ++pos) {
+      const mckg_race_triple tr{obj, ((xoff >> 2) + w) * 4u + (__ffs(f) - 1u), (int32_t)line};
+      if (pos < XTB) {
+        tb[pos] = tr;
+      } else {  // more than a buffer in one step: straight to global memory
+        const unsigned long long g = atomicAdd(P.n_tri, 1ull);
+        if (g < P.capacity)
+          P.tri[g] = tr;
+        else
+          E.flags |= ST_OVERFLOW;
+      }
+    }
+  __syncwarp();
+  E.tbn = min(E.tbn + total, XTB);
+}
+
+__device__ __forceinline__ uint32_t hit_bits(uint32_t xi, uint32_t Xx, uint32_t Xy, uint32_t yi, uint32_t Yx,
+                                             uint32_t Yy) {
+  const uint32_t xoff = acc_off(Xx), xend = xoff + acc_len(Xx);
+  const uint32_t yoff = acc_off(Yx), yend = yoff + acc_len(Yx);
+  const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
+  const bool hit = yi < xi && acc_epoch(Yy) == acc_epoch(Xy) && acc_tid(Yy) != acc_tid(Xy) &&
+                   ((Xx | Yx) & (1u << 24)) && lo < hi;
+  return hit ? ((1u << (hi - lo)) - 1u) << (lo - xoff) : 0u;
+}
+
 __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const uint16_t* cl, uint32_t m,
                            uint32_t obj, uint32_t bid, unsigned long long bstamp, unsigned long long* hs,
                            mckg_race_triple* tb) {
   const uint32_t lane = threadIdx.x & 31u;
+  if (m <= 32u) {
+    // candidate j at lane j; C lanes per X, each scanning every C-th Y
+    const bool ya = lane < m;
+    const uint32_t yi_l = ya ? cl[lane] : 0xFFFFu;
+    const uint4 R = ya ? __ldg(src + yi_l) : make_uint4(0, 0, 0, 0);
+    uint32_t C = 32;
+    while (C > 1 && C * m > 32u) C >>= 1;
+    const uint32_t g = lane / C, sub = lane & (C - 1u);
+    const uint32_t xi = __shfl_sync(0xFFFFFFFFu, yi_l, g & 31u);
+    const uint32_t Xx = __shfl_sync(0xFFFFFFFFu, R.x, g & 31u);
+    const uint32_t Xy = __shfl_sync(0xFFFFFFFFu, R.y, g & 31u);
+    uint32_t bits = 0;
+    const uint32_t iters = (m + C - 1u) / C;
+    for (uint32_t it = 0; it < iters; ++it) {
+      const uint32_t j = sub + it * C;
+      const uint32_t yi = __shfl_sync(0xFFFFFFFFu, yi_l, j & 31u);
+      const uint32_t Yx = __shfl_sync(0xFFFFFFFFu, R.x, j & 31u);
+      const uint32_t Yy = __shfl_sync(0xFFFFFFFFu, R.y, j & 31u);
+      if (j < m) bits |= hit_bits(xi, Xx, Xy, yi, Yx, Yy);
+    }
+    for (uint32_t d = 1; d < C; d <<= 1) bits |= __shfl_xor_sync(0xFFFFFFFFu, bits, d);
+    bits = __shfl_sync(0xFFFFFFFFu, bits, (lane * C) & 31u);  // back to lane-per-X
+    exact_report(E, P, ya, R, bits, obj, bid, bstamp, hs, tb);
+    return;
+  }
   for (uint32_t xb = 0; xb < m; xb += 32u) {
     const bool act = xb + lane < m;
     const uint32_t xi = act ? cl[xb + lane] : 0xFFFFu;
     const uint4 X = act ? __ldg(src + xi) : make_uint4(0, 0, 0, 0);
-    const uint32_t xoff = acc_off(X.x), xend = xoff + acc_len(X.x);
-    const uint32_t xtid = acc_tid(X.y), xep = acc_epoch(X.y);
-    const bool xw = acc_write(X.x);
     uint32_t bits = 0;
     for (uint32_t yb = 0; yb < m; yb += 32u) {
       uint32_t yi_l = xi, y0 = X.x, y1 = X.y;
@@ -725,71 +834,11 @@ __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const 
         y1 = Yv.y;
       }
       const uint32_t cnt = min(32u, m - yb);
-      for (uint32_t j = 0; j < cnt; ++j) {
-        const uint32_t yi = __shfl_sync(0xFFFFFFFFu, yi_l, j);
-        const uint32_t Yx = __shfl_sync(0xFFFFFFFFu, y0, j);
-        const uint32_t Yy = __shfl_sync(0xFFFFFFFFu, y1, j);
-        const uint32_t yoff = acc_off(Yx), yend = yoff + acc_len(Yx);
-        const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
-        const bool hit = yi < xi && acc_epoch(Yy) == xep && acc_tid(Yy) != xtid &&
-                         (xw || acc_write(Yx)) && lo < hi;
-        if (hit) bits |= ((1u << (hi - lo)) - 1u) << (lo - xoff);
-      }
+      for (uint32_t j = 0; j < cnt; ++j)
+        bits |= hit_bits(xi, X.x, X.y, __shfl_sync(0xFFFFFFFFu, yi_l, j), __shfl_sync(0xFFFFFFFFu, y0, j),
+                         __shfl_sync(0xFFFFFFFFu, y1, j));
     }
-    const bool racing = act && bits != 0;
-    const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
-    if (!rm) continue;
-    const int32_t line = (int32_t)X.z;
-    const unsigned long long ts = ts_key(X.w, bid, xtid);
-    const uint32_t gm = __match_any_sync(0xFFFFFFFFu, racing ? (uint32_t)line : (0x80000000u | lane));
-    unsigned long long mn = ts;
-    for (uint32_t tmp = rm; tmp; tmp &= tmp - 1u) {
-      const int s = __ffs(tmp) - 1;
-      const unsigned long long v = shfl64(ts, s);
-      if ((gm >> s) & 1u) mn = v < mn ? v : mn;
-    }
-    wo_line(E, P, racing && lane == (uint32_t)(__ffs(gm) - 1), (uint32_t)line, mn);
-    // fresh bytes per word of X (at most 3 words)
-    uint32_t fresh[3] = {0u, 0u, 0u};
-    uint32_t k = 0;
-    if (racing) {
-      const uint64_t ab = (uint64_t)bits << (xoff & 3u);
-      for (uint32_t w = 0; w < 3u && (xoff >> 2) + w <= (xend - 1u) >> 2; ++w) {
-        const uint32_t wm = (uint32_t)(ab >> (4u * w)) & 0xFu;
-        if (!wm) continue;
-        uint32_t f = whset_or(hs, bstamp, (xoff >> 2) + w, (uint32_t)line, wm);
-        if (f & 0x10u) {
-          E.flags |= ST_DUP;
-          f &= 0xFu;
-        }
-        fresh[w] = f;
-        k += __popc(f);
-      }
-    }
-    uint32_t incl = k;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-      if (lane >= (uint32_t)d) incl += v;
-    }
-    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    if (E.tbn + total > XTB) wo_flush(E, P, tb);
-    uint32_t pos = E.tbn + incl - k;
-    for (uint32_t w = 0; w < 3u; ++w)
-      for (uint32_t f = fresh[w]; f; f &= f - 1u, ++pos) {
-        const mckg_race_triple tr{obj, ((xoff >> 2) + w) * 4u + (__ffs(f) - 1u), line};
-        if (pos < XTB) {
-          tb[pos] = tr;
-        } else {  // more than a buffer in one step: straight to global memory
-          const unsigned long long g = atomicAdd(P.n_tri, 1ull);
-          if (g < P.capacity)
-            P.tri[g] = tr;
-          else
-            E.flags |= ST_OVERFLOW;
-        }
-      }
-    __syncwarp();
-    E.tbn = min(E.tbn + total, XTB);
+    exact_report(E, P, act, X, act ? bits : 0u, obj, bid, bstamp, hs, tb);
   }
 }
 
