@@ -173,7 +173,8 @@ def load_traffic():
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("race_detect_kernel")
+            d = json.load(f)
+            return d.get("detect_call", d.get("race_detect_kernel"))
     except (OSError, ValueError):
         return None
 
@@ -291,7 +292,7 @@ def run_ours(args):
                        "l2": "inputs (16 GiB) >> L2 (126 MB); no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(),
-                         "kernel": "race_detect_kernel", "kernel_ms": k_avg,
+                         "kernel": "mckg_detect_shared: race_detect_kernel (filter) + exact_kernel, timed together", "kernel_ms": k_avg,
                          "peak_source": peak_src,
                          "algorithmic_bytes": "16 B/event + 8 B/block + 12 B/reported triple"},
             "clocks": clocks.summary(),

@@ -58,7 +58,7 @@ constexpr int NT = 256;
 constexpr int NSTAGE_MAX = 3;
 constexpr int EPT_MAX = 16;     // records per thread kept in registers (cap <= 4096)
 constexpr uint32_t HS = 512;    // (word, line) -> reported byte mask, per block
-constexpr uint32_t TBN = 256;   // staged triples per buffer before the global append
+constexpr uint32_t TBN = 128;   // staged triples per buffer before the global append
 constexpr uint32_t LTN = 32;    // line-first local table entries
 constexpr uint32_t INF = 0xFFFFFFFFu;
 constexpr uint32_t INV = 0xFFFFFFFFu;
@@ -111,7 +111,7 @@ __host__ __device__ inline Lay layout(uint32_t cap, uint32_t wpad, uint32_t nsta
   Lay L;
   uint32_t p = 0;
   L.ma = p;      p += NSLOT * wpad * 4;
-  L.tag = p;     p += NSLOT * wpad * 2;
+  L.tag = p;     p += NSLOT * wpad * 4;
   L.cl = p;      p += 2 * cap * 2;
   p = (p + 127u) & ~127u;
   L.stage = p;   p += nstage * cap * 16;
@@ -136,6 +136,12 @@ __device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n}" ::"r"(a),
       "h"((uint16_t)v), "r"((uint32_t)p)
+      : "memory");
+}
+__device__ __forceinline__ void sts32_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n}" ::"r"(a),
+      "r"(v), "r"((uint32_t)p)
       : "memory");
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -166,11 +172,11 @@ __device__ __noinline__ bool extra_words(uint32_t tag_slot, uint32_t ma_slot, ui
   const bool wr = acc_write(w0);
   bool cand = false;
   for (uint32_t w = (off >> 2) + 1; w <= (off + len - 1u) >> 2; ++w) {
-    const uint32_t a = tag_slot + sw(w) * 2u, m = ma_slot + sw(w) * 4u;
+    const uint32_t a = tag_slot + sw(w) * 4u, m = ma_slot + sw(w) * 4u;
     if (phase == 1) {
-      sts16_if(true, a, tid);
+      sts32_if(true, a, tid);
     } else if (phase == 2) {
-      sts16_if(lds16(a) != tid, m, st);
+      sts16_if(lds32(a) != tid, m, st);
       sts16_if(wr, m + 2u, st);
     } else {
       cand |= lds32(m) == (st | (st << 16));
@@ -367,7 +373,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
       s_lt_ts[i] = ~0ull;
     }
   }
-  for (uint32_t i = t; i < 3 * NSLOT * P.wpad / 2; i += NT) sp<uint32_t>(L.ma)[i] = 0u;
+  for (uint32_t i = t; i < 2 * NSLOT * P.wpad; i += NT) sp<uint32_t>(L.ma)[i] = 0u;
   if (t < 4) s_cnt[t] = 0u;
   uint32_t flags = 0;
   const uint32_t G = gridDim.x;
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
   __syncthreads();
 
   const uint32_t tag_base = smem_u32(smem_raw) + L.tag;
-  const uint32_t ma_delta = smem_u32(smem_raw) + L.ma - 2u * tag_base;  // ma = 2 * tag + delta
+  const uint32_t ma_delta = L.ma - L.tag;  // ma entry = tag entry + delta (both 4 B per word)
   const uint32_t slotw = P.wpad;
   uint32_t erel[EPT], wsw[EPT], xa[EPT], meta[EPT];
   uint32_t sphase = 0, stamp = 0;
@@ -419,14 +425,14 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       const uint32_t slot = erel[k] - ws;
-      xa[k] = tag_base + (slot < NSLOT ? (slot * slotw + wsw[k]) << 1 : 0u);  // loads stay in range
-      sts16_if(slot < NSLOT, xa[k], meta[k] & 0x7FFu);
+      xa[k] = tag_base + (slot < NSLOT ? (slot * slotw + wsw[k]) << 2 : 0u);  // loads stay in range
+      sts32_if(slot < NSLOT, xa[k], meta[k] & 0x7FFu);
     }
     if (wmw) {
       for (int k = 0; k < EPT; ++k) {
         const uint32_t slot = erel[k] - ws;
         if (slot < NSLOT && (meta[k] & 0x1000u))
-          extra_words(tag_base + slot * slotw * 2u, 2u * (tag_base + slot * slotw * 2u) + ma_delta,
+          extra_words(tag_base + slot * slotw * 4u, tag_base + slot * slotw * 4u + ma_delta,
                       src[k * NT + t].x, meta[k] & 0x7FFu, 1, st);
       }
     }
@@ -522,8 +528,8 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
 #pragma unroll
       for (int k = 0; k < EPT; ++k) {
         const bool a = erel[k] - ws < NSLOT;
-        const uint32_t tg = lds16(xa[k]);
-        const uint32_t mm = 2u * xa[k] + ma_delta;
+        const uint32_t tg = lds32(xa[k]);
+        const uint32_t mm = xa[k] + ma_delta;
         sts16_if(a && tg != (meta[k] & 0x7FFu), mm, st);
         sts16_if(a && (meta[k] & 0x800u), mm + 2u, st);
       }
@@ -531,7 +537,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
         for (int k = 0; k < EPT; ++k) {
           const uint32_t slot = erel[k] - ws;
           if (slot < NSLOT && (meta[k] & 0x1000u))
-            extra_words(tag_base + slot * slotw * 2u, 2u * (tag_base + slot * slotw * 2u) + ma_delta,
+            extra_words(tag_base + slot * slotw * 4u, tag_base + slot * slotw * 4u + ma_delta,
                         src[k * NT + t].x, meta[k] & 0x7FFu, 2, st);
         }
       }
@@ -563,14 +569,14 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       if (P.debug & 64u) break;  // experiment: decode + P1 + barriers only
-      const uint32_t v = lds32(2u * xa[k] + ma_delta);
+      const uint32_t v = lds32(xa[k] + ma_delta);
       if (erel[k] - ws < NSLOT && v == (st | (st << 16))) cmask |= 1u << k;
     }
     if (wmw) {
       for (int k = 0; k < EPT; ++k) {
         const uint32_t slot = erel[k] - ws;
         if (slot < NSLOT && (meta[k] & 0x1000u) &&
-            extra_words(tag_base + slot * slotw * 2u, 2u * (tag_base + slot * slotw * 2u) + ma_delta,
+            extra_words(tag_base + slot * slotw * 4u, tag_base + slot * slotw * 4u + ma_delta,
                         src[k * NT + t].x, meta[k] & 0x7FFu, 3, st))
           cmask |= 1u << k;
       }

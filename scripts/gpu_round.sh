@@ -12,9 +12,9 @@ timeout 600 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_ou
 cat gpurun_out/bench.json
 if [ -z "$NO_NCU" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --e2e-blocks 0 \
+  --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-k1 --no-c5 --e2e-blocks 0 \
   > gpurun_out/ncu_launch_bench.log 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:race_detect -s 2 -c 1 \
-  -o gpurun_out/prof_detect python bench.py --steps 3 --warmup 3 --no-cpu --e2e-blocks 0 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"race_detect|exact_kernel" -s 6 -c 2 \
+  -o gpurun_out/prof_detect python bench.py --steps 3 --warmup 3 --no-cpu --no-k1 --no-c5 --e2e-blocks 0 \
   > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
