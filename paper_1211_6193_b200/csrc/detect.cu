@@ -81,14 +81,17 @@ struct Params {
   uint32_t* status;
   uint32_t debug;  // experiments only (MCKG_DEBUG): 1 skip the exact pass, 2 skip filter + exact
   // two-kernel mode: the filter writes each block's candidate list (<= CMAX
-  // record indices) for exact_kernel; a longer list sets *cflag and the fused
-  // kernel (filter + exact in one pass) redoes the launch
+  // record indices) for exact_kernel; a block with a longer list is appended
+  // to olist and redone by the fused kernel (filter + exact in one pass)
   uint32_t mode;       // 0 fused, 1 filter -> candidate lists
-  uint32_t gate;       // fused kernel: 1 = run only if *cflag is set
-  uint16_t* ccount;    // [n_blocks]
+  uint32_t gate;       // fused kernel: 1 = only the blocks of olist
+  uint16_t* ccount;    // [n_blocks]; OVERFLOWED = in olist
   uint16_t* cidx;      // [n_blocks * CMAX]
-  uint32_t* cflag;
+  uint32_t* ocount;    // [0] blocks in olist, [1] exact_kernel's next block
+  uint32_t* olist;     // [n_blocks]
 };
+constexpr uint16_t PENDING = 0xFFFFu;     // ccount before the filter publishes it
+constexpr uint16_t OVERFLOWED = 0xFFFEu;
 constexpr uint32_t CMAX = 64;
 
 extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -360,7 +363,11 @@ template <int EPT, bool FUSED>
 __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2F_MINB) : (EPT <= 8 ? 2 : 1))
     race_detect_kernel(Params P) {
   constexpr int NSTAGE = FUSED ? MCKG_K2_NSTAGE : MCKG_K2F_NSTAGE;
-  if (P.gate && *(volatile uint32_t*)P.cflag == 0) return;  // the two-kernel path succeeded
+  // the blocks this launch covers: all, or (gated fused pass) the overflow list
+  const uint32_t nblk = P.gate ? *(volatile uint32_t*)P.ocount : P.n_blocks;
+  if (nblk == 0) return;
+  if constexpr (!FUSED) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  auto blk = [&](uint32_t j) { return P.gate ? P.olist[j] : j; };
   const Lay L = layout(P.cap, P.wpad, NSTAGE);
   const uint32_t t = threadIdx.x, lane = t & 31u;
   uint64_t* mbar = s_mbar;
@@ -379,7 +386,8 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
   const uint32_t G = gridDim.x;
   // one thread: stream block b into stage st; s_n[st] = its event count
   // (0 when empty or beyond the staging capacity -- flagged, skipped)
-  auto issue = [&](uint32_t b, int st) {
+  auto issue = [&](uint32_t j, int st) {  // j: position in the launch's block sequence
+    const uint32_t b = blk(j);
     const uint64_t s0 = P.bstart[b], n = P.bstart[b + 1] - s0;
     if (n > P.cap) flags |= ST_RANGE;
     const bool go = n > 0 && n <= P.cap;
@@ -394,8 +402,8 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
     for (int k = 0; k < NSTAGE; ++k) mbar_init(mbar + k, 1);
     fence_mbar_init();
     for (int k = 0; k < NSTAGE; ++k) {
-      const uint32_t b = blockIdx.x + (uint32_t)k * G;
-      if (b < P.n_blocks) issue(b, k);
+      const uint32_t j = blockIdx.x + (uint32_t)k * G;
+      if (j < nblk) issue(j, k);
     }
   }
   __syncthreads();
@@ -406,18 +414,18 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
   uint32_t erel[EPT], wsw[EPT], xa[EPT], meta[EPT];
   uint32_t sphase = 0, stamp = 0;
   int it = 0;
-  uint32_t b = blockIdx.x;
+  uint32_t j = blockIdx.x, b = j < nblk ? blk(j) : 0u;
   uint32_t n = 0, ws = 0, elast = 0;
   bool wmw = false;
   const uint4* src = stage;
-  bool live = b < P.n_blocks;
+  bool live = j < nblk;
   // the previous block, whose exact pass runs in the next interval
   bool pend = false;
   bool fresh = false;  // the current unit's block was loaded in the last interval
   bool held = false;   // the current block still needs its stage after its first unit
   bool pheld = false;
   int pit = 0;
-  uint32_t pb = 0, pn = 0;
+  uint32_t pb = 0, pj = 0, pn = 0;
   unsigned long long bstamp = 0;
 
   // P1 of the unit starting at relative epoch `ws` (xa computed for the unit)
@@ -494,8 +502,8 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
       held = FUSED || spans_any || elast >= NSLOT;
       if (!held && t == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t nb = b + (uint32_t)NSTAGE * G;
-        if (nb < P.n_blocks) issue(nb, it % NSTAGE);
+        const uint32_t nj = j + (uint32_t)NSTAGE * G;
+        if (nj < nblk) issue(nj, it % NSTAGE);
       }
       fresh = false;
     }
@@ -509,13 +517,14 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
         // hand the candidate list to exact_kernel
         if (t < 32) {
           const uint16_t* cl = clbuf + (size_t)pq * P.cap;
+          // publish the list and its count; exact_kernel runs concurrently and
+          // polls both (every slot starts PENDING), so no fence is needed
           if (m <= CMAX) {
             for (uint32_t i = lane; i < m; i += 32) P.cidx[(size_t)pb * CMAX + i] = cl[i];
-            if (lane == 0) P.ccount[pb] = (uint16_t)m;
-          } else if (lane == 0) {
-            P.ccount[pb] = 0;
-            atomicOr(P.cflag, 1u);
+          } else if (lane == 0) {  // too many candidates: the fused pass redoes this block
+            P.olist[atomicAdd(P.ocount, 1u)] = pb;
           }
+          if (lane == 0) *(volatile uint16_t*)(P.ccount + pb) = m <= CMAX ? (uint16_t)m : OVERFLOWED;
         }
       } else if (m > 0 && !(P.debug & 1u)) {
         exact_block(P, stage + (size_t)(pit % NSTAGE) * P.cap, clbuf + (size_t)pq * P.cap, m, pq,
@@ -556,8 +565,8 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
         s_cnt[pq] = 0;
         if (pheld) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          const uint32_t nb = pb + (uint32_t)NSTAGE * G;
-          if (nb < P.n_blocks) issue(nb, pit % NSTAGE);
+          const uint32_t nj = pj + (uint32_t)NSTAGE * G;
+          if (nj < nblk) issue(nj, pit % NSTAGE);
         }
       }
     }
@@ -611,10 +620,12 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
       pheld = held;
       pit = it;
       pb = b;
+      pj = j;
       pn = n;
-      b += G;
+      j += G;
       ++it;
-      live = b < P.n_blocks;
+      live = j < nblk;
+      if (live) b = blk(j);
       if (live) {
         load_block();
         p1(++stamp & 0xFFFFu);
@@ -637,7 +648,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
 // global memory (16 B each, ~1.5 % of the records on C3).  Per warp: a
 // lane-owned line-first cache, a (word, line) reported-set table and a
 // triple staging buffer, all contention-free.
-constexpr uint32_t XW = 8;     // warps per CTA
+constexpr uint32_t XW = 4;     // warps per CTA (one CTA fits beside 3 filter CTAs per SM)
 constexpr uint32_t XHS = 128;  // reported-set slots per warp
 constexpr uint32_t XTB = 64;   // staged triples per warp
 
@@ -803,7 +814,7 @@ __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const 
   if (m <= 32u) {
     // candidate j at lane j; C lanes per X, each scanning every C-th Y
     const bool ya = lane < m;
-    const uint32_t yi_l = ya ? cl[lane] : 0xFFFFu;
+    const uint32_t yi_l = ya ? __ldcg(cl + lane) : 0xFFFFu;
     const uint4 R = ya ? __ldg(src + yi_l) : make_uint4(0, 0, 0, 0);
     uint32_t C = 32;
     while (C > 1 && C * m > 32u) C >>= 1;
@@ -827,14 +838,14 @@ __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const 
   }
   for (uint32_t xb = 0; xb < m; xb += 32u) {
     const bool act = xb + lane < m;
-    const uint32_t xi = act ? cl[xb + lane] : 0xFFFFu;
+    const uint32_t xi = act ? __ldcg(cl + xb + lane) : 0xFFFFu;
     const uint4 X = act ? __ldg(src + xi) : make_uint4(0, 0, 0, 0);
     uint32_t bits = 0;
     for (uint32_t yb = 0; yb < m; yb += 32u) {
       uint32_t yi_l = xi, y0 = X.x, y1 = X.y;
       if (yb != xb) {
         const bool ya = yb + lane < m;
-        yi_l = ya ? cl[yb + lane] : 0xFFFFu;
+        yi_l = ya ? __ldcg(cl + yb + lane) : 0xFFFFu;
         const uint2 Yv = ya ? __ldg(reinterpret_cast<const uint2*>(src + yi_l)) : make_uint2(0, 0);
         y0 = Yv.x;
         y1 = Yv.y;
@@ -851,7 +862,6 @@ __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const 
 __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
   __shared__ unsigned long long hs_all[XW][XHS];
   __shared__ mckg_race_triple tb_all[XW][XTB];
-  if (*(volatile uint32_t*)P.cflag) return;  // a list overflowed: the fused kernel redoes the launch
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   unsigned long long* hs = hs_all[warp];
   mckg_race_triple* tb = tb_all[warp];
@@ -859,12 +869,33 @@ __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
   __syncwarp();
   WarpOut E{INF, ~0ull, 0u, 0u, 0u};
   unsigned long long bstamp = 0;
-  for (uint32_t b = blockIdx.x * XW + warp; b < P.n_blocks; b += gridDim.x * XW) {
-    const uint32_t m = P.ccount[b];
-    if (m == 0) continue;
+  // blocks are claimed in order from a global counter; this kernel may run
+  // beside the filter (programmatic dependent launch) and waits for each
+  // block's published count
+  constexpr uint32_t CHUNK = 16;  // blocks per claim
+  uint32_t b = 0, bend = 0;
+  while (true) {
+    if (b == bend) {
+      if (lane == 0) b = atomicAdd(P.ocount + 1, CHUNK);
+      b = __shfl_sync(0xFFFFFFFFu, b, 0);
+      bend = min(b + CHUNK, P.n_blocks);
+    }
+    if (b >= P.n_blocks) break;
+    const uint32_t bb = b++;
+    uint32_t m = *(volatile uint16_t*)(P.ccount + bb);
+    while (m == PENDING) {
+      __nanosleep(1000);
+      m = *(volatile uint16_t*)(P.ccount + bb);
+    }
+    if (m == 0 || m == OVERFLOWED) continue;  // none / redone by the fused pass
+    // the entries are published independently of the count: wait for them too
+    // (olist / ocount are read only by the fused pass, after this kernel)
+    for (uint32_t i = lane; i < m; i += 32)
+      while (*(volatile uint16_t*)(P.cidx + (size_t)bb * CMAX + i) == PENDING) __nanosleep(100);
+    __syncwarp();
     ++bstamp;
-    exact_warp(E, P, reinterpret_cast<const uint4*>(P.ev + P.bstart[b]), P.cidx + (size_t)b * CMAX, m,
-               P.obj_base + b, P.bid_base + b, bstamp, hs, tb);
+    exact_warp(E, P, reinterpret_cast<const uint4*>(P.ev + P.bstart[bb]), P.cidx + (size_t)bb * CMAX, m,
+               P.obj_base + bb, P.bid_base + bb, bstamp, hs, tb);
   }
   wo_flush(E, P, tb);
   if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
@@ -1000,7 +1031,8 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.gate = 0;
   P.ccount = nullptr;
   P.cidx = nullptr;
-  P.cflag = nullptr;
+  P.ocount = nullptr;
+  P.olist = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   if (P.debug & 32u) {  // MCKG_DEBUG=32: the fused kernel alone (tests cover both paths)
     kf<<<grid_f, NT, smem_f, s>>>(P);
@@ -1009,12 +1041,15 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     return MCKG_OK;
   }
   // two-kernel path: filter -> candidate lists -> exact_kernel; the fused
-  // kernel (gated on *cflag) redoes the launch if a block has > CMAX candidates
+  // kernel (gated) redoes only the blocks with more than CMAX candidates
   keep_pool_memory();
   MCKG_CUDA_TRY(cudaMallocAsync(&P.ccount, (size_t)tr->n_blocks * sizeof(uint16_t), s));
   MCKG_CUDA_TRY(cudaMallocAsync(&P.cidx, (size_t)tr->n_blocks * CMAX * sizeof(uint16_t), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&P.cflag, sizeof(uint32_t), s));
-  MCKG_CUDA_TRY(cudaMemsetAsync(P.cflag, 0, sizeof(uint32_t), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&P.ocount, 2 * sizeof(uint32_t), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&P.olist, (size_t)tr->n_blocks * sizeof(uint32_t), s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(P.ocount, 0, 2 * sizeof(uint32_t), s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(P.ccount, 0xFF, (size_t)tr->n_blocks * sizeof(uint16_t), s));  // PENDING
+  MCKG_CUDA_TRY(cudaMemsetAsync(P.cidx, 0xFF, (size_t)tr->n_blocks * CMAX * sizeof(uint16_t), s));
   P.mode = 1;
   kt<<<grid_t, NT, smem_t, s>>>(P);
   uint32_t launched = 1;
@@ -1027,7 +1062,19 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     uint32_t xgrid = (uint32_t)sm_count() * (uint32_t)xper;
     const uint32_t need = (tr->n_blocks + XW - 1) / XW;
     if (xgrid > need) xgrid = need;
-    exact_kernel<<<xgrid, XW * 32, 0, s>>>(P);
+    // programmatic dependent launch: exact_kernel starts once every filter CTA
+    // is resident and consumes the candidate lists as they are published
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(xgrid);
+    cfg.blockDim = dim3(XW * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = (P.debug & 128u) ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MCKG_CUDA_TRY(cudaLaunchKernelEx(&cfg, exact_kernel, P));
     P.mode = 0;
     P.gate = 1;
     kf<<<grid_f, NT, smem_f, s>>>(P);
@@ -1036,7 +1083,8 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   MCKG_CUDA_TRY(cudaGetLastError());
   cudaFreeAsync(P.ccount, s);
   cudaFreeAsync(P.cidx, s);
-  cudaFreeAsync(P.cflag, s);
+  cudaFreeAsync(P.ocount, s);
+  cudaFreeAsync(P.olist, s);
   note_launch(launched, grid_t, NT, (uint32_t)smem_t);
   return MCKG_OK;
 }
