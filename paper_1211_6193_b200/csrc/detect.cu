@@ -10,27 +10,29 @@
 //
 // Design (one CTA streams many simulated blocks; blocks never
 // interact because each owns its shared object, device.cpp:33-38):
-//   1. stage: the block's 16-byte records are pulled into shared memory by
-//      the TMA engine (cp.async.bulk + mbarrier), NSTAGE blocks in flight;
-//      each thread keeps its EPT records (decoded) in registers.
-//   2. epochs: a per-block start bitmap (shfl_up + ballot) splits the records
-//      into epoch segments (epochs are non-decreasing in timestamp order).
-//   3. filter, per epoch, on 4-byte words: P1 tag[w] = some accessing tid;
-//      P2 mark words seen by a second tid / written; P3 an event is a
-//      candidate iff one of its words is both.  A byte can race only if its
-//      word passes, so the filter has no false negatives (a byte has a racing
-//      access iff >= 2 threads touch it in the epoch and one writes).  P3 of
-//      epoch k and P1 of epoch k+1 share a barrier interval.
-//   4. exact pass, once per block over the (rare) candidates, byte-exact and
-//      warp-cooperative: X races on the bytes it shares with an earlier
-//      candidate Y of the same epoch and another thread where X or Y writes --
-//      the reference predicate verbatim, restricted to the bytes that can
-//      matter.  Lanes hold the Y's; one __reduce_or_sync gives X's racing bytes.
-//   5. report: racing (byte, line) pairs are deduplicated per block in a
-//      shared hash set (the reported set is per object), staged in shared
-//      memory and appended to the global triple array in chunks; the first
-//      racing timestamp per line is min-reduced in shared memory, then
-//      globally.
+//   1. stage: each block's 16-byte records are pulled into shared memory by
+//      the TMA engine (cp.async.bulk + mbarrier, 3 stages); every thread keeps
+//      EPT records decoded in registers, so a one-round block releases its
+//      stage to the next TMA load right after the decode.
+//   2. filter, on 4-byte words, NSLOT epochs at once in per-slot arrays (a
+//      "unit" = block x epoch window; one unit per block unless a block spans
+//      more epochs): P1 tag[w] = some accessing tid | barrier | P2 stamp the
+//      words seen by a second tid / written | barrier | P3 an event is a
+//      candidate iff one of its words is both -- fused with P1 of the next
+//      unit.  Two barriers per block.  A byte can race only if its word
+//      passes, so the filter has no false negatives.
+//   3. exact pass over the (rare) candidates -- the reference predicate
+//      verbatim, byte-exact: X races on the bytes it shares with an earlier
+//      candidate Y of the same epoch and another thread where X or Y writes.
+//      Default (two-kernel) path: the filter publishes each block's candidate
+//      list; exact_kernel, launched programmatically beside the filter
+//      (PDL), polls the lists and runs one warp per block (C lanes per
+//      candidate, Y's by shuffle).  A block with more than CMAX candidates is
+//      redone by the fused kernel variant (filter + exact on all threads).
+//   4. report: racing (byte, line) pairs are deduplicated per block through a
+//      (word, line) -> byte-mask table, staged per warp and appended to the
+//      global triple array; the first racing timestamp per line is
+//      min-reduced per warp (lane-owned line cache), then globally.
 #include <cub/cub.cuh>
 #include <type_traits>
 
