@@ -1704,7 +1704,10 @@ class CudaEngine final : public DeviceEngine {
         }
         cudaGetLastError();
       }
-    if (comm_.world > 1 && !comm_.allgather) {
+    // MCKG_K1_FORCE_EXCHANGE=1: run the rank exchange even for world == 1 (a
+    // one-rank NCCL communicator) -- exercises the NCCL path on one GPU
+    exch_ = comm_.world > 1 || getenv("MCKG_K1_FORCE_EXCHANGE") != nullptr;
+    if (exch_ && !comm_.allgather) {
       if (comm_.rank < 0 || comm_.rank >= comm_.world) {
         err = "rank outside 0..world-1";
         return false;
@@ -1712,6 +1715,10 @@ class CudaEngine final : public DeviceEngine {
       ncclUniqueId id;
       static_assert(sizeof(id.internal) == 128, "ncclUniqueId");
       std::memcpy(id.internal, comm_.id.data(), 128);
+      if (comm_.world == 1 && ncclGetUniqueId(&id) != ncclSuccess) {
+        err = "ncclGetUniqueId failed";
+        return false;
+      }
       CK(cudaSetDevice(reps_[0].dev));
       ncclResult_t r = ncclCommInitRank(&nccl_, comm_.world, id, comm_.rank);
       if (r != ncclSuccess) {
@@ -1769,6 +1776,7 @@ class CudaEngine final : public DeviceEngine {
  private:
   std::vector<int> devs_;
   EngineComm comm_;
+  bool exch_ = false;  // rank exchange after every grid
   ncclComm_t nccl_ = nullptr;
   std::vector<Replica> reps_;
   uint64_t top_ = 0;
@@ -1904,7 +1912,7 @@ class CudaEngine final : public DeviceEngine {
       kp.raceCheck = g.raceCheck ? 1 : 0;
       kp.htBits = htBits;
       kp.bidBase = R.b0;
-      kp.markDirty = (D > 1 || comm_.world > 1) ? 1 : 0;
+      kp.markDirty = (D > 1 || exch_) ? 1 : 0;
       kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
       kp.lineFirst = R.line.p;
       kp.triples = R.tri.p;
@@ -2039,7 +2047,7 @@ class CudaEngine final : public DeviceEngine {
   // clear the dirty bits of replica 0, then copy it to the other replicas
   bool finishMemory(GridResult& out, std::string& err) {
     const size_t D = reps_.size();
-    if ((D == 1 && comm_.world == 1) || top_ == 0) return true;
+    if ((D == 1 && !exch_) || top_ == 0) return true;
     Replica& R0 = reps_[0];
     CK(cudaSetDevice(R0.dev));
     clear_dirty_kernel<<<148u * 8u, 256, 0, R0.stream>>>(R0.meta, top_);
@@ -2295,7 +2303,7 @@ class CudaEngine final : public DeviceEngine {
 
   bool run(const GridSpec& g, GridResult& out, std::string& err) {
     bool ok = runLocal(g, out, err) && mergeLocal(out, err);
-    if (comm_.world > 1) {
+    if (exch_) {
       if (!ok && out.error.empty()) out.error = err.empty() ? "B200 engine error" : err;
       if (!exchangeResults(out, ok, err)) return false;
       if (ok && !exchangeMemory(out, err)) return false;

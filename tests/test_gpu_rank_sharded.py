@@ -53,3 +53,19 @@ def test_ranks_nccl_transport(tmp_path):
     if n < 2:
         pytest.skip("NCCL transport needs one GPU per rank")
     _compare(_run(min(n, 4), "nccl", PICK, 29640, tmp_path))
+
+
+def test_nccl_exchange_path_one_rank(monkeypatch):
+    """MCKG_K1_FORCE_EXCHANGE=1 runs the full NCCL exchange (dirty-range
+    all-reduce, packed-byte all-reduce(MAX), result all-gather) on a
+    one-rank communicator: the NCCL code path on a one-GPU box."""
+    from paper_1211_6193_b200 import checker
+    from program_corpus import project
+    monkeypatch.setenv("MCKG_K1_FORCE_EXCHANGE", "1")
+    progs = {n: (f, s) for n, f, s in corpus()}
+    res = {}
+    for n in PICK[::6]:  # a communicator per run (~1 s of NCCL setup each)
+        fname, src = progs[n]
+        r = checker.run_source(src, filename=fname)
+        res[n] = dict(project(r), engine_error=r.get("engine_error", ""))
+    _compare(res)
