@@ -87,13 +87,14 @@ struct Params {
   // to olist and redone by the fused kernel (filter + exact in one pass)
   uint32_t mode;       // 0 fused, 1 filter -> candidate lists
   uint32_t gate;       // fused kernel: 1 = only the blocks of olist
-  uint16_t* ccount;    // [n_blocks]; OVERFLOWED = in olist
-  uint16_t* cidx;      // [n_blocks * CMAX]
+  // per block, wpb 64-bit words {candidate bits of 32 records, 1}: word
+  // k * 8 + warp covers records k * NT + warp * 32 + lane (0 = not published)
+  unsigned long long* cbits;  // [n_blocks * wpb]
+  uint32_t wpb;
   uint32_t* ocount;    // [0] blocks in olist, [1] exact_kernel's next block
   uint32_t* olist;     // [n_blocks]
 };
-constexpr uint16_t PENDING = 0xFFFFu;     // ccount before the filter publishes it
-constexpr uint16_t OVERFLOWED = 0xFFFEu;
+
 constexpr uint32_t CMAX = 64;
 
 extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -132,11 +133,6 @@ __device__ __forceinline__ T* sp(uint32_t off) {
 __device__ __forceinline__ uint32_t sw(uint32_t w) { return w ^ ((w >> 5) & 31u); }
 
 // ---- shared-window accessors (plain LDS/STS, predicated stores) ----
-__device__ __forceinline__ uint32_t lds16(uint32_t a) {
-  uint16_t v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-}
 __device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n}" ::"r"(a),
@@ -415,6 +411,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
   const uint32_t slotw = P.wpad;
   uint32_t erel[EPT], wsw[EPT], xa[EPT], meta[EPT];
   uint32_t sphase = 0, stamp = 0;
+  uint32_t cacc = 0;  // candidate bits of the current block (two-kernel path)
   int it = 0;
   uint32_t j = blockIdx.x, b = j < nblk ? blk(j) : 0u;
   uint32_t n = 0, ws = 0, elast = 0;
@@ -516,18 +513,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
       ++bstamp;
       const uint32_t m = pn > 0 ? s_cnt[pq] : 0u;
       if constexpr (!FUSED) {
-        // hand the candidate list to exact_kernel
-        if (t < 32) {
-          const uint16_t* cl = clbuf + (size_t)pq * P.cap;
-          // publish the list and its count; exact_kernel runs concurrently and
-          // polls both (every slot starts PENDING), so no fence is needed
-          if (m <= CMAX) {
-            for (uint32_t i = lane; i < m; i += 32) P.cidx[(size_t)pb * CMAX + i] = cl[i];
-          } else if (lane == 0) {  // too many candidates: the fused pass redoes this block
-            P.olist[atomicAdd(P.ocount, 1u)] = pb;
-          }
-          if (lane == 0) *(volatile uint16_t*)(P.ccount + pb) = m <= CMAX ? (uint16_t)m : OVERFLOWED;
-        }
+        (void)m;  // published in P3 of the block's last unit
       } else if (m > 0 && !(P.debug & 1u)) {
         exact_block(P, stage + (size_t)(pit % NSTAGE) * P.cap, clbuf + (size_t)pq * P.cap, m, pq,
                     P.obj_base + pb, P.bid_base + pb, bstamp);
@@ -592,7 +578,9 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
           cmask |= 1u << k;
       }
     }
-    if (__any_sync(0xFFFFFFFFu, cmask)) {
+    if constexpr (!FUSED) {
+      cacc |= cmask;
+    } else if (__any_sync(0xFFFFFFFFu, cmask)) {
 #pragma unroll
       for (int k = 0; k < EPT; ++k) {
         const bool cand = (cmask >> k) & 1u;
@@ -618,6 +606,20 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
       ws = lo < n ? acc_epoch(src[lo].y) - e0 : elast + 1;
       p1(++stamp & 0xFFFFu);
     } else {
+      if constexpr (!FUSED) {
+        // publish this warp's candidate bits of the block (exact_kernel polls)
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          const uint32_t bm = __ballot_sync(0xFFFFFFFFu, (cacc >> k) & 1u);
+          if (lane == (uint32_t)k) mine = bm;
+        }
+        if (lane < (uint32_t)EPT) {
+          unsigned long long* w = P.cbits + (size_t)b * P.wpb + lane * (NT / 32) + (t >> 5);
+          *(volatile unsigned long long*)w = (1ull << 32) | mine;
+        }
+        cacc = 0;
+      }
       pend = true;
       pheld = held;
       pit = it;
@@ -662,25 +664,6 @@ struct WarpOut {
   uint32_t flags;
 };
 
-__device__ void wo_line(WarpOut& E, const Params& P, bool leader, uint32_t line, unsigned long long ts) {
-  const uint32_t lane = threadIdx.x & 31u;
-  for (uint32_t lm = __ballot_sync(0xFFFFFFFFu, leader); lm; lm &= lm - 1u) {
-    const int src = __ffs(lm) - 1;
-    const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, src);
-    const unsigned long long T = shfl64(ts, src);
-    const uint32_t own = __ballot_sync(0xFFFFFFFFu, E.lc_line == L);
-    if (own) {
-      if (lane == (uint32_t)(__ffs(own) - 1) && T < E.lc_ts) E.lc_ts = T;
-    } else {
-      if (lane == E.lc_next) {
-        if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
-        E.lc_line = L;
-        E.lc_ts = T;
-      }
-      E.lc_next = (E.lc_next + 1u) & 31u;
-    }
-  }
-}
 
 __device__ void wo_flush(WarpOut& E, const Params& P, mckg_race_triple* tb) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -816,7 +799,7 @@ __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const 
   if (m <= 32u) {
     // candidate j at lane j; C lanes per X, each scanning every C-th Y
     const bool ya = lane < m;
-    const uint32_t yi_l = ya ? __ldcg(cl + lane) : 0xFFFFu;
+    const uint32_t yi_l = ya ? cl[lane] : 0xFFFFu;
     const uint4 R = ya ? __ldg(src + yi_l) : make_uint4(0, 0, 0, 0);
     uint32_t C = 32;
     while (C > 1 && C * m > 32u) C >>= 1;
@@ -840,14 +823,14 @@ __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const 
   }
   for (uint32_t xb = 0; xb < m; xb += 32u) {
     const bool act = xb + lane < m;
-    const uint32_t xi = act ? __ldcg(cl + xb + lane) : 0xFFFFu;
+    const uint32_t xi = act ? cl[xb + lane] : 0xFFFFu;
     const uint4 X = act ? __ldg(src + xi) : make_uint4(0, 0, 0, 0);
     uint32_t bits = 0;
     for (uint32_t yb = 0; yb < m; yb += 32u) {
       uint32_t yi_l = xi, y0 = X.x, y1 = X.y;
       if (yb != xb) {
         const bool ya = yb + lane < m;
-        yi_l = ya ? __ldcg(cl + yb + lane) : 0xFFFFu;
+        yi_l = ya ? cl[yb + lane] : 0xFFFFu;
         const uint2 Yv = ya ? __ldg(reinterpret_cast<const uint2*>(src + yi_l)) : make_uint2(0, 0);
         y0 = Yv.x;
         y1 = Yv.y;
@@ -864,9 +847,11 @@ __device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const 
 __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
   __shared__ unsigned long long hs_all[XW][XHS];
   __shared__ mckg_race_triple tb_all[XW][XTB];
+  __shared__ uint16_t cl_all[XW][CMAX];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   unsigned long long* hs = hs_all[warp];
   mckg_race_triple* tb = tb_all[warp];
+  uint16_t* cl = cl_all[warp];
   for (uint32_t i = lane; i < XHS; i += 32) hs[i] = 0ull;
   __syncwarp();
   WarpOut E{INF, ~0ull, 0u, 0u, 0u};
@@ -884,20 +869,48 @@ __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
     }
     if (b >= P.n_blocks) break;
     const uint32_t bb = b++;
-    uint32_t m = *(volatile uint16_t*)(P.ccount + bb);
-    while (m == PENDING) {
-      __nanosleep(1000);
-      m = *(volatile uint16_t*)(P.ccount + bb);
+    // the block's candidate bits (published by the filter; 0 = not yet)
+    uint32_t mk[4] = {0u, 0u, 0u, 0u};
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t q = (uint32_t)r * 32u + lane;
+      if (q < P.wpb) {
+        const volatile unsigned long long* w = P.cbits + (size_t)bb * P.wpb + q;
+        unsigned long long v = *w;
+        while ((v >> 32) == 0) {
+          __nanosleep(500);
+          v = *w;
+        }
+        mk[r] = (uint32_t)v;
+        cnt += __popc(mk[r]);
+      }
     }
-    if (m == 0 || m == OVERFLOWED) continue;  // none / redone by the fused pass
-    // the entries are published independently of the count: wait for them too
-    // (olist / ocount are read only by the fused pass, after this kernel)
-    for (uint32_t i = lane; i < m; i += 32)
-      while (*(volatile uint16_t*)(P.cidx + (size_t)bb * CMAX + i) == PENDING) __nanosleep(100);
+    const uint32_t m = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (m == 0) continue;
+    if (m > CMAX) {  // too many candidates: the fused pass redoes this block
+      if (lane == 0) P.olist[atomicAdd(P.ocount, 1u)] = bb;
+      continue;
+    }
+    // candidate list: record (word q) * 32 + bit
+    uint32_t base = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t c = __popc(mk[r]);
+      uint32_t incl = c;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= (uint32_t)d) incl += v;
+      }
+      uint32_t pos = base + incl - c;
+      for (uint32_t f = mk[r]; f; f &= f - 1u) cl[pos++] = (uint16_t)(((uint32_t)r * 32u + lane) * 32u + (__ffs(f) - 1u));
+      base += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
     __syncwarp();
     ++bstamp;
-    exact_warp(E, P, reinterpret_cast<const uint4*>(P.ev + P.bstart[bb]), P.cidx + (size_t)bb * CMAX, m,
-               P.obj_base + bb, P.bid_base + bb, bstamp, hs, tb);
+    exact_warp(E, P, reinterpret_cast<const uint4*>(P.ev + P.bstart[bb]), cl, m, P.obj_base + bb, P.bid_base + bb,
+               bstamp, hs, tb);
+    __syncwarp();
   }
   wo_flush(E, P, tb);
   if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
@@ -1031,8 +1044,8 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   }
   P.mode = 0;
   P.gate = 0;
-  P.ccount = nullptr;
-  P.cidx = nullptr;
+  P.cbits = nullptr;
+  P.wpb = cap / 32u;
   P.ocount = nullptr;
   P.olist = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1045,13 +1058,12 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   // two-kernel path: filter -> candidate lists -> exact_kernel; the fused
   // kernel (gated) redoes only the blocks with more than CMAX candidates
   keep_pool_memory();
-  MCKG_CUDA_TRY(cudaMallocAsync(&P.ccount, (size_t)tr->n_blocks * sizeof(uint16_t), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&P.cidx, (size_t)tr->n_blocks * CMAX * sizeof(uint16_t), s));
+  P.wpb = (uint32_t)(ki == 0 ? 4 : ki == 1 ? 8 : 16) * (NT / 32);  // EPT * warps
+  MCKG_CUDA_TRY(cudaMallocAsync(&P.cbits, (size_t)tr->n_blocks * P.wpb * sizeof(unsigned long long), s));
   MCKG_CUDA_TRY(cudaMallocAsync(&P.ocount, 2 * sizeof(uint32_t), s));
   MCKG_CUDA_TRY(cudaMallocAsync(&P.olist, (size_t)tr->n_blocks * sizeof(uint32_t), s));
   MCKG_CUDA_TRY(cudaMemsetAsync(P.ocount, 0, 2 * sizeof(uint32_t), s));
-  MCKG_CUDA_TRY(cudaMemsetAsync(P.ccount, 0xFF, (size_t)tr->n_blocks * sizeof(uint16_t), s));  // PENDING
-  MCKG_CUDA_TRY(cudaMemsetAsync(P.cidx, 0xFF, (size_t)tr->n_blocks * CMAX * sizeof(uint16_t), s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(P.cbits, 0, (size_t)tr->n_blocks * P.wpb * sizeof(unsigned long long), s));
   P.mode = 1;
   kt<<<grid_t, NT, smem_t, s>>>(P);
   uint32_t launched = 1;
@@ -1083,8 +1095,7 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     launched += 2;
   }
   MCKG_CUDA_TRY(cudaGetLastError());
-  cudaFreeAsync(P.ccount, s);
-  cudaFreeAsync(P.cidx, s);
+  cudaFreeAsync(P.cbits, s);
   cudaFreeAsync(P.ocount, s);
   cudaFreeAsync(P.olist, s);
   note_launch(launched, grid_t, NT, (uint32_t)smem_t);
