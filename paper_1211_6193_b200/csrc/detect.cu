@@ -362,10 +362,10 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
     race_detect_kernel(Params P) {
   constexpr int NSTAGE = FUSED ? MCKG_K2_NSTAGE : MCKG_K2F_NSTAGE;
   // the blocks this launch covers: all, or (gated fused pass) the overflow list
-  const uint32_t nblk = P.gate ? *(volatile uint32_t*)P.ocount : P.n_blocks;
+  const uint32_t nblk = FUSED && P.gate ? *(volatile uint32_t*)P.ocount : P.n_blocks;
   if (nblk == 0) return;
   if constexpr (!FUSED) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  auto blk = [&](uint32_t j) { return P.gate ? P.olist[j] : j; };
+  auto blk = [&](uint32_t j) { return FUSED && P.gate ? P.olist[j] : j; };
   const Lay L = layout(P.cap, P.wpad, NSTAGE);
   const uint32_t t = threadIdx.x, lane = t & 31u;
   uint64_t* mbar = s_mbar;
@@ -609,10 +609,12 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
       if constexpr (!FUSED) {
         // publish this warp's candidate bits of the block (exact_kernel polls)
         uint32_t mine = 0;
+        if (__any_sync(0xFFFFFFFFu, cacc != 0u)) {
 #pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-          const uint32_t bm = __ballot_sync(0xFFFFFFFFu, (cacc >> k) & 1u);
-          if (lane == (uint32_t)k) mine = bm;
+          for (int k = 0; k < EPT; ++k) {
+            const uint32_t bm = __ballot_sync(0xFFFFFFFFu, (cacc >> k) & 1u);
+            if (lane == (uint32_t)k) mine = bm;
+          }
         }
         if (lane < (uint32_t)EPT) {
           unsigned long long* w = P.cbits + (size_t)b * P.wpb + lane * (NT / 32) + (t >> 5);
