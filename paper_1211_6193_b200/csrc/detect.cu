@@ -50,7 +50,7 @@
 #define MCKG_K2F_NSTAGE 3
 #endif
 #ifndef MCKG_K2F_MINB
-#define MCKG_K2F_MINB 3
+#define MCKG_K2F_MINB 4
 #endif
 
 namespace mckg {
@@ -877,6 +877,7 @@ __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const uint32_t q = (uint32_t)r * 32u + lane;
+      if ((uint32_t)r * 32u >= P.wpb) break;
       if (q < P.wpb) {
         const volatile unsigned long long* w = P.cbits + (size_t)bb * P.wpb + q;
         unsigned long long v = *w;
@@ -896,8 +897,10 @@ __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
     }
     // candidate list: record (word q) * 32 + bit
     uint32_t base = 0;
+    const int rounds = (int)((P.wpb + 31u) >> 5);
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
+      if (r >= rounds) break;
       const uint32_t c = __popc(mk[r]);
       uint32_t incl = c;
       for (int d = 1; d < 32; d <<= 1) {
