@@ -138,6 +138,7 @@ struct RunResult {
   std::vector<RaceTriple> reported;  // RaceState::reported, std::set order
   EngineStats stats;
   std::string engineError;           // non-empty: the run was abandoned by the engine
+  std::vector<std::string> trace;    // RunOptions::trace: the Machine::trace lines, in order
 };
 
 class MachineImpl;

@@ -314,6 +314,7 @@ typedef struct mck_run_opts {
    * gather n bytes from every rank into recv[world*n] in rank order, 0 = ok */
   int (*allgather)(void* ctx, const void* send, uint64_t n, void* recv);
   void* allgather_ctx;
+  int32_t trace;              /* RunOptions::trace: JSON "trace" = the --trace lines  */
 } mck_run_opts;
 
 /* A fresh NCCL communicator id for mck_run_opts.comm_id. */

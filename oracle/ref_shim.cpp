@@ -161,7 +161,10 @@ int mckref_run(const char* src, const char* filename, int policy, uint64_t seed,
     ro.seed = seed;
     ro.stepLimit = step_limit;
     ro.raceCheck = race_check != 0;
+    ro.trace = (capture & 2) != 0;  // bit 1: the --trace lines
     Machine m(prog, ro);
+    std::vector<std::string> traceLines;
+    m.onTrace = [&](const std::string& line) { traceLines.push_back(line); };
 
     std::vector<CapEvent> ev;
     std::map<ThreadKey, uint32_t> epochOf;
@@ -171,7 +174,7 @@ int mckref_run(const char* src, const char* filename, int policy, uint64_t seed,
     size_t stepMark = 0;
     uint64_t devSteps = 0, barrierRules = 0, hostSteps = 0, dispatches = 0;
     m.onMemAccess = [&](const MemAccessInfo& a) {
-        if (!capture || !a.allowed || a.space.kind != SpaceKind::DeviceShared) return;
+        if (!(capture & 1) || !a.allowed || a.space.kind != SpaceKind::DeviceShared) return;
         const Configuration& cfg = m.config();
         if (!cfg.race.enabled) return;
         auto it = cfg.memory.objects.find(a.object);
@@ -270,7 +273,9 @@ int mckref_run(const char* src, const char* filename, int policy, uint64_t seed,
             o << "]";
         }
     }
-    o << "},\"events\":[";
+    o << "},\"trace\":[";
+    for (size_t i = 0; i < traceLines.size(); ++i) o << (i ? "," : "") << jsonStr(traceLines[i]);
+    o << "],\"events\":[";
     for (size_t i = 0; i < ev.size(); ++i) {
         const CapEvent& e = ev[i];
         o << (i ? "," : "") << "[" << e.gid << "," << e.bid << "," << e.tid << "," << e.obj << ","

@@ -28,6 +28,7 @@ class RunOpts(ctypes.Structure):
         ("comm_id", ctypes.c_uint8 * 128),
         ("allgather", ctypes.c_void_p),
         ("allgather_ctx", ctypes.c_void_p),
+        ("trace", ctypes.c_int32),
     ]
 
 
@@ -71,7 +72,8 @@ def torch_allgather(group=None):
 
 
 def run_source(src, filename="test.cu", step_limit=0, race_check=True, device=0,
-               round_robin=True, seed=0, devices=None, rank=0, world=1, comm=None, allgather=None):
+               round_robin=True, seed=0, devices=None, rank=0, world=1, comm=None, allgather=None,
+               trace=False):
     """Machine::run on a source program -> dict (keys: see include/mckg.h).
 
     devices: list of CUDA ordinals to split every grid over (a repeated
@@ -95,7 +97,7 @@ def run_source(src, filename="test.cu", step_limit=0, race_check=True, device=0,
                 return 1
         cb = ALLGATHER(_cb)
     o = RunOpts(step_limit, seed, 1 if race_check else 0, 1 if round_robin else 0, device, 0, len(devs), arr,
-                rank, world, cid, ctypes.cast(cb, ctypes.c_void_p) if cb else None, None)
+                rank, world, cid, ctypes.cast(cb, ctypes.c_void_p) if cb else None, None, 1 if trace else 0)
     out = ctypes.c_void_p()
     rc = lib.mck_run_source(src.encode(), filename.encode(), ctypes.byref(o), ctypes.byref(out))
     _abi.check(rc, "mck_run_source")

@@ -56,6 +56,7 @@ constexpr int FRAMES = 16;
 constexpr int BINDS = 96;
 constexpr int POBJ = 48;
 constexpr int PB = 768;      // private bytes (locals and params of all frames)
+constexpr int TEP = TRACE_EPISODES;
 
 constexpr uint32_t PRIV = 0x80000000u;
 constexpr uint32_t NONE_TID = 0x7FFu;
@@ -106,6 +107,8 @@ struct BlockOut {
   unsigned long long sharedEvents;
   uint32_t lastSweep;
   uint32_t deadlocked;
+  uint32_t episodes;  // completed barrier episodes
+  uint32_t pad;
 };
 
 struct KP {
@@ -130,6 +133,7 @@ struct KP {
   int raceCheck;
   int htBits;                 // conflict hash size = 1 << htBits
   uint32_t bidBase;           // first simulated block of this launch (multi-device split)
+  uint32_t* tarr;             // trace mode: [block][episode < TEP][tid] arrival sweep + 1
   int markDirty;              // record global writes in META_DIRTY (replicated memory)
   uint32_t maxSweeps;         // < 2^26; each sweep takes >= 1 step (step limit)
   // outputs
@@ -1066,6 +1070,8 @@ __device__ __forceinline__ int step(TS& t, const KP& P, Ctx& c, Thread& th, Req&
       th.state = S_WAIT;
       th.syncKind = in.f;
       th.operand = operand;
+      if (P.tarr && th.E < TEP)  // --trace: arrival sweeps give the barrier-rule timeline
+        P.tarr[((size_t)(c.bid - P.bidBase) * TEP + th.E) * (size_t)P.blockDim + c.tid] = c.sweep + 1;
       const int p = (th.E + 1) & 1;
       const bool nz = operand != 0;
       atomicAdd(&bs.wait[p], 1);
@@ -1530,6 +1536,7 @@ __global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kern
     o.sharedEvents = bs.sharedEvents;
     o.lastSweep = bs.lastSweep;
     o.deadlocked = deadlocked ? 1 : 0;
+    o.episodes = E;
   }
 }
 
@@ -1657,6 +1664,7 @@ struct Replica {
   DBuf<int32_t> tri;
   DBuf<k1::DevDiagRec> diag;
   DBuf<k1::BlockOut> blocks;
+  DBuf<uint32_t> tarr;
   DBuf<int> err;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   uint32_t b0 = 0, nb = 0;
@@ -1837,6 +1845,10 @@ class CudaEngine final : public DeviceEngine {
     }
     void (*kern)(KP) = K == 1 ? grid_kernel<1> : K == 2 ? grid_kernel<2> : K == 4 ? grid_kernel<4> : grid_kernel<8>;
     const size_t total = (size_t)g.gridDim;
+    if (g.trace && (exch_ || total * (size_t)TEP * (size_t)g.blockDim > (1ull << 26))) {
+      out.error = exch_ ? "--trace is single-rank" : "--trace supports grids up to 2^20 threads";
+      return false;
+    }
     const size_t D = reps_.size();
     const uint32_t words = (uint32_t)((g.blockDim + 31) / 32);
     const uint32_t diagN = 1u << 18;
@@ -1877,6 +1889,7 @@ class CudaEngine final : public DeviceEngine {
                                 : 1;
       if (!R.line.ensure(LINES, err) || !R.ntri.ensure(1, err) || !R.tri.ensure(3 * triCaps[ri], err) ||
           !R.diag.ensure(diagN, err) || !R.blocks.ensure(nb, err) || !R.wait.ensure(nb * words, err) ||
+          (g.trace && !R.tarr.ensure(nb * TEP * (size_t)g.blockDim, err)) ||
           !R.err.ensure(2, err))
         return false;
       CK(cudaMemsetAsync(R.line.p, 0xFF, LINES * sizeof(unsigned long long), R.stream));
@@ -1884,6 +1897,7 @@ class CudaEngine final : public DeviceEngine {
       CK(cudaMemsetAsync(R.diag.p, 0, diagN * sizeof(DevDiagRec), R.stream));
       CK(cudaMemsetAsync(R.wait.p, 0, nb * words * sizeof(uint32_t), R.stream));
       CK(cudaMemsetAsync(R.err.p, 0, 2 * sizeof(int), R.stream));
+      if (g.trace) CK(cudaMemsetAsync(R.tarr.p, 0, nb * TEP * (size_t)g.blockDim * sizeof(uint32_t), R.stream));
       init_ts_kernel<<<(diagN + 255) / 256, 256, 0, R.stream>>>(R.diag.p, diagN);
       KP kp;
       kp.code = R.code.p;
@@ -1912,6 +1926,7 @@ class CudaEngine final : public DeviceEngine {
       kp.raceCheck = g.raceCheck ? 1 : 0;
       kp.htBits = htBits;
       kp.bidBase = R.b0;
+      kp.tarr = g.trace ? R.tarr.p : nullptr;
       kp.markDirty = (D > 1 || exch_) ? 1 : 0;
       kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
       kp.lineFirst = R.line.p;
@@ -1925,6 +1940,14 @@ class CudaEngine final : public DeviceEngine {
       kp.error = R.err.p;
       kp.errorInfo = R.err.p + 1;
       CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.end));
+      {
+        // shared-memory carveout: experiments (MCKG_K1_CARVEOUT=<percent>)
+        static int carve = [] {
+          const char* e = getenv("MCKG_K1_CARVEOUT");
+          return e ? atoi(e) : -1;
+        }();
+        if (carve >= 0) CK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      }
       cudaEventRecord(R.e0, R.stream);
       kern<<<(unsigned)nb, threads, L.end, R.stream>>>(kp);
       cudaEventRecord(R.e1, R.stream);
@@ -1959,6 +1982,15 @@ class CudaEngine final : public DeviceEngine {
       const size_t nb = R.nb;
       std::vector<BlockOut> bo(nb);
       CK(cudaMemcpy(bo.data(), R.blocks.p, nb * sizeof(BlockOut), cudaMemcpyDeviceToHost));
+      if (g.trace) {
+        if (out.episodes.empty()) {
+          out.episodes.assign(total, 0);
+          out.arrivals.assign(total * TEP * (size_t)g.blockDim, 0);
+        }
+        for (size_t b = 0; b < nb; ++b) out.episodes[R.b0 + b] = bo[b].episodes;
+        CK(cudaMemcpy(out.arrivals.data() + (size_t)R.b0 * TEP * (size_t)g.blockDim, R.tarr.p,
+                      nb * TEP * (size_t)g.blockDim * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+      }
       bool anyDl = false;
       for (const auto& b : bo) {
         out.sweeps += b.sweeps;

@@ -41,6 +41,7 @@ extern "C" int mck_run_source(const char* src, const char* filename, const mck_r
     ro.seed = opts->seed;
     if (opts->max_threads_per_block > 0) ro.arch.maxThreadsPerBlock = opts->max_threads_per_block;
     for (int i = 0; i < opts->n_devices && i < 8; ++i) ro.devices.push_back(opts->devices[i]);
+    ro.trace = opts->trace != 0;
     if (opts->world > 1) {
       ro.rank = opts->rank;
       ro.world = opts->world;
@@ -82,6 +83,8 @@ extern "C" int mck_run_source(const char* src, const char* filename, const mck_r
     for (size_t i = 0; i < r.reported.size(); ++i)
       o += std::string(i ? "," : "") + "[" + std::to_string(r.reported[i].object) + "," +
            std::to_string(r.reported[i].byte) + "," + std::to_string(r.reported[i].line) + "]";
+    o += "],\"trace\":[";
+    for (size_t i = 0; i < r.trace.size(); ++i) o += std::string(i ? "," : "") + js(r.trace[i]);
     const auto& st = r.stats;
     o += "],\"stats\":{\"host_steps\":" + std::to_string(st.hostSteps) + ",\"device_steps\":" +
          std::to_string(st.deviceSteps) + ",\"barrier_rules\":" + std::to_string(st.barrierRules) +

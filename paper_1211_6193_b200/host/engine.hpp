@@ -22,7 +22,8 @@ namespace mckb {
 // Per-byte metadata of every memory object (host and device):
 constexpr uint8_t META_DEF = 1;  // byte defined (MemByte::defined, machine.hpp:33-37)
 constexpr uint8_t META_PTR = 2;  // a pointer slot starts here (MemObject::ptrs, machine.hpp:45)
-constexpr uint8_t META_DIRTY = 4;  // written by the running grid (replica merge; cleared after)
+constexpr uint8_t META_DIRTY = 4;
+constexpr int TRACE_EPISODES = 64;  // --trace: barrier episodes recorded per block  // written by the running grid (replica merge; cleared after)
 
 // A device-global object as the engine sees it.
 struct DevObjInfo {
@@ -49,6 +50,7 @@ struct GridSpec {
   std::vector<uint32_t> globalIds;  // object id of every TU global (host or device)
   // shared arrays of earlier grids (for memBoundary messages): (first id, count, gid)
   std::vector<std::array<uint32_t, 3>> sharedRanges;
+  bool trace = false;               // record barrier arrivals (GridResult::arrivals)
 };
 
 struct DevDiag {
@@ -78,6 +80,10 @@ struct GridResult {
   double ms = 0;
   uint32_t launches = 0;
   std::string error;            // engine limitation hit: run abandoned
+  // trace mode: per block, completed barrier episodes, and the local arrival
+  // sweep + 1 of every thread in its first TRACE_EPISODES episodes (0 = none)
+  std::vector<uint32_t> episodes;   // [gridDim]
+  std::vector<uint32_t> arrivals;   // [gridDim][TRACE_EPISODES][blockDim]
 };
 
 class DeviceEngine {

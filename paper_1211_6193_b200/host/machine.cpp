@@ -117,6 +117,16 @@ struct DiagEv {
   mck::Diagnostic d;
 };
 
+// A --trace line with its execution timestamp (Machine::trace, machine.cpp:52;
+// lines from device.cpp:63,163-195,215 and streams.cpp:49-61).
+struct TraceEv {
+  uint64_t sweep;
+  int phase;  // 1 device step (grid completed), 2 barrier rule, 3 dispatch
+  uint64_t k1, k2;
+  uint64_t seq;
+  std::string text;
+};
+
 enum class WaitKind { None, Device, Stream, Event };
 
 }  // namespace
@@ -166,6 +176,11 @@ class HostMachine {
   int lastApiError_ = 0;
   std::string output_;
   std::vector<DiagEv> diags_;
+  std::vector<TraceEv> traces_;
+  void traceLine(uint64_t sweep, int phase, uint64_t k1, uint64_t k2, std::string text) {
+    if (o_.trace) traces_.push_back(TraceEv{sweep, phase, k1, k2, seq_++, std::move(text)});
+  }
+  void traceBarriers(uint32_t gid, const GridRec& rec, uint64_t spawn);
   std::vector<mck::RaceTriple> reported_;
   mck::EngineStats stats_;
   std::string engineError_;
@@ -1324,6 +1339,7 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   g.stepBudget = o_.stepLimit > steps_ ? o_.stepLimit - steps_ : 0;
   g.globalIds = globalIds_;
   g.sharedRanges = sharedRanges_;
+  g.trace = o_.trace;
   const int nparams = P_->fns[static_cast<size_t>(l.kernel)].n_params;
   // spawnGrid allocates gridDim shared objects, then nparams objects per thread
   const uint64_t reserve = static_cast<uint64_t>(l.grid) + static_cast<uint64_t>(l.grid) * l.block * nparams;
@@ -1348,6 +1364,16 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   sharedRanges_.push_back({g.sharedBase, static_cast<uint32_t>(l.grid), g.gid});
   rec.endSweep = rec.res.deadlocked ? NEVER : sweep_ + rec.res.duration;
   if (rec.endSweep != NEVER) ++runningGrids_;
+  traceLine(sweep_, 3, 0, 0,
+            "stream sid=" + std::to_string(sid) + " dispatch=launch gid=" + std::to_string(g.gid) +
+                " kernel=" + P_->fnNames[static_cast<size_t>(l.kernel)]);
+  if (o_.trace && engineError_.empty()) {
+    traceBarriers(g.gid, rec, sweep_);
+    // finishThread of the grid's last thread (device.cpp:215)
+    if (rec.endSweep != NEVER)
+      traceLine(rec.endSweep, 1, (static_cast<uint64_t>(g.gid) << 32) | 0xFFFFFFFFu, 0,
+                "grid gid=" + std::to_string(g.gid) + " completed");
+  }
   ++stats_.grids;
   stats_.gridMs += rec.res.ms;
   stats_.kernelLaunches += rec.res.launches;
@@ -1383,18 +1409,70 @@ void HostMachine::dispatch(uint32_t sid) {
   StreamItem item = s.q.front();
   s.q.pop_front();
   --queued_;
+  const std::string pre = "stream sid=" + std::to_string(sid) + " dispatch=";
   switch (item.kind) {
     case ItemKind::Launch: spawnGrid(sid, item.launch); break;
-    case ItemKind::Copy: performCopy(item.copy, sid); break;
+    case ItemKind::Copy:
+      performCopy(item.copy, sid);
+      traceLine(sweep_, 3, 0, 0, pre + "memcpy n=" + std::to_string(item.copy.n));
+      break;
     case ItemKind::EventRecord: {
       auto e = events_.find(item.eid);
       if (e != events_.end()) e->second = EvStatus::Recorded;
+      traceLine(sweep_, 3, 0, 0, pre + "event-record eid=" + std::to_string(item.eid));
       break;
     }
-    case ItemKind::WaitEvent: break;
+    case ItemKind::WaitEvent: traceLine(sweep_, 3, 0, 0, pre + "wait-event eid=" + std::to_string(item.eid)); break;
   }
   StreamRec& s2 = streams_.at(sid);
   if (s2.destroyed && s2.idle()) streams_.erase(sid);
+}
+
+// Barrier-rule trace lines from the recorded arrival sweeps (device.cpp:
+// 111-198 under round robin): up(t -> t+1) fires in the
+// first sweep where threads 0..t+1 have all arrived (the chain cascades in
+// key order), Turnaround and Down(L) in the last arrival's sweep T, Down(t)
+// in T + L - t, FinalRelease in T + L.  A deadlocked episode runs its up
+// chain up to the first thread that never arrives.
+void HostMachine::traceBarriers(uint32_t gid, const GridRec& rec, uint64_t spawn) {
+  const GridResult& r = rec.res;
+  if (r.episodes.empty()) return;
+  const int64_t B = rec.blockDim, L = B - 1;
+  std::vector<char> stuck(static_cast<size_t>(rec.gridDim), 0);
+  for (const auto& s : r.stuck) stuck[s.bid] = 1;
+  enum { UP = 0, TURN = 1, DOWN = 2, REL = 3 };
+  for (int64_t b = 0; b < rec.gridDim; ++b) {
+    const uint32_t done = r.episodes[static_cast<size_t>(b)];
+    const uint32_t eps = done + (stuck[static_cast<size_t>(b)] ? 1u : 0u);
+    if (eps > static_cast<uint32_t>(TRACE_EPISODES)) {
+      engineError_ = "--trace records at most " + std::to_string(TRACE_EPISODES) + " barrier episodes per block";
+      return;
+    }
+    const uint64_t k1 = (static_cast<uint64_t>(gid) << 32) | static_cast<uint64_t>(b);
+    const std::string head = "sync gid=" + std::to_string(gid) + " bid=" + std::to_string(b) + " rule=";
+    for (uint32_t e = 0; e < eps; ++e) {
+      const uint32_t* a = r.arrivals.data() + (static_cast<size_t>(b) * TRACE_EPISODES + e) * static_cast<size_t>(B);
+      auto rule = [&](uint64_t lsweep, int64_t keyTid, int kind, const std::string& text) {
+        traceLine(spawn + lsweep, 2, k1, (static_cast<uint64_t>(keyTid) << 2) | static_cast<uint64_t>(kind), head + text);
+      };
+      if (a[0] == 0) continue;  // thread 0 never arrived: no rule fires
+      uint64_t U = a[0] - 1;
+      int64_t t = 0;
+      for (; t < L && a[t + 1] != 0; ++t) {
+        U = std::max<uint64_t>(U, a[t + 1] - 1);
+        rule(U, t, UP, "up tid=" + std::to_string(t + 1) + " token=1");
+      }
+      if (e >= done) continue;  // deadlocked: the chain stops at the first absent thread
+      const uint64_t T = U;
+      rule(T, L, TURN, "turn tid=" + std::to_string(L) + " token=2");
+      if (L == 0) {
+        rule(T, 0, REL, "release tid=0 token=0");
+        continue;
+      }
+      for (int64_t d = L; d >= 1; --d) rule(T + static_cast<uint64_t>(L - d), d, DOWN, "down tid=" + std::to_string(d) + " token=2");
+      rule(T + static_cast<uint64_t>(L), 0, REL, "release tid=0 token=0");
+    }
+  }
 }
 
 void HostMachine::completeGrids(uint64_t sweep) {
@@ -1619,6 +1697,14 @@ mck::RunResult HostMachine::run() {
   std::sort(reported_.begin(), reported_.end());
   r.reported = reported_;
   r.stats = stats_;
+  std::stable_sort(traces_.begin(), traces_.end(), [](const TraceEv& a, const TraceEv& b) {
+    if (a.sweep != b.sweep) return a.sweep < b.sweep;
+    if (a.phase != b.phase) return a.phase < b.phase;
+    if (a.k1 != b.k1) return a.k1 < b.k1;
+    if (a.k2 != b.k2) return a.k2 < b.k2;
+    return a.seq < b.seq;
+  });
+  for (const TraceEv& e : traces_) r.trace.push_back(e.text);
   return r;
 }
 
@@ -1710,6 +1796,7 @@ FileRunOutcome runSourceText(const std::string& source, const std::string& filen
   Machine m(prog, ro);
   out.run = m.run();
   out.stdoutText = out.run.output;
+  for (const std::string& t : out.run.trace) out.stderrText += "cudak: trace: " + t + "\n";
   for (const Diagnostic& d : out.run.diagnostics) out.stderrText += "cudak: " + d.message + "\n";
   if (!out.run.engineError.empty()) {
     out.stderrText += "cudak: engine error: " + out.run.engineError + "\n";

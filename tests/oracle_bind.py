@@ -172,12 +172,12 @@ def port_scan_stuck(arrivals, n_blocks, block_dim, bid_base=0):
 
 
 def ref_run(src, filename="test.cu", policy="rr", seed=0, step_limit=50_000_000, race_check=True,
-            capture=True):
+            capture=True, trace=False):
     """Machine::run of the reference on a source program -> dict (see ref_shim.cpp)."""
     lib = ref()
     out = ctypes.c_void_p()
     lib.mckref_run(src.encode(), filename.encode(), 1 if policy == "rr" else 0, seed, step_limit,
-                   1 if race_check else 0, 1 if capture else 0, ctypes.byref(out))
+                   1 if race_check else 0, (1 if capture else 0) | (2 if trace else 0), ctypes.byref(out))
     s = ctypes.string_at(out.value).decode()
     lib.mckref_free(out)
     return json.loads(s)

@@ -85,3 +85,17 @@ def test_deadlock_port_closed_form():
         assert (b in dl.tolist()) == mixed
         got = [t for t in range(bd) if (wm[b * words + t // 32] >> (t % 32)) & 1]
         assert got == (odd if mixed else [])
+
+
+def test_trace_golden_is_the_reference():
+    """tests/golden/traces.json was produced by the reference (oracle/_ref)."""
+    import json
+    import os
+    if ob.ref() is None:
+        pytest.skip("reference library not built here")
+    from program_corpus import corpus
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "traces.json")))
+    progs = {n: (f, s) for n, f, s in corpus()}
+    for n in sorted(gold)[:10]:
+        f, s = progs[n]
+        assert ob.ref_run(s, f, capture=False, trace=True)["trace"] == gold[n]

@@ -5,7 +5,7 @@
 // reference exit codes (0 clean, 1 diagnostics, 2 frontend error, 3 stuck).
 //
 //   mckb [--no-race-check] [--schedule roundrobin|random] [--seed N]
-//        [--step-limit N] [--report FILE] [--stats] file.cu
+//        [--step-limit N] [--report FILE] [--trace] [--stats] file.cu
 //
 // Device grids run on the B200 engine; the schedule is round-robin (the
 // engine's exact schedule; --schedule random is accepted and noted).
@@ -35,10 +35,11 @@ int main(int argc, char** argv) {
     } else if (a == "--seed") o.seed = std::strtoull(next().c_str(), nullptr, 10);
     else if (a == "--step-limit") o.stepLimit = std::strtoull(next().c_str(), nullptr, 10);
     else if (a == "--report") o.reportPath = next();
+    else if (a == "--trace") o.trace = true;
     else if (a == "--stats") stats = true;
     else if (a == "-h" || a == "--help") {
       std::printf("usage: mckb [--no-race-check] [--schedule roundrobin|random] [--seed N] "
-                  "[--step-limit N] [--report FILE] [--stats] file.cu\n");
+                  "[--step-limit N] [--report FILE] [--trace] [--stats] file.cu\n");
       return 0;
     } else if (!a.empty() && a[0] == '-') {
       std::fprintf(stderr, "mckb: unknown option %s\n", a.c_str());
