@@ -1138,7 +1138,10 @@ __device__ __forceinline__ int ht_insert(unsigned long long* keys, uint32_t* val
 // blocks stay resident, which is what long serial stretches (one live thread
 // per block) need; inside a sweep the K sub-threads step in tid order.
 template <int K>
-__global__ void __launch_bounds__(K == 1 ? 1024 : 256, K == 1 ? 1 : 4) grid_kernel(KP P) {
+#ifndef MCKG_K1_MINB
+#define MCKG_K1_MINB 4  // K = 1 serves blocks of <= 256 threads
+#endif
+__global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP P) {
   const uint32_t bid = blockIdx.x + P.bidBase;  // simulated block
   const uint32_t lb = blockIdx.x;               // index into this launch's outputs
   const uint32_t g = threadIdx.x;
@@ -1834,6 +1837,7 @@ class CudaEngine final : public DeviceEngine {
     int K = g.blockDim > 256 ? 4 : 1;
     if (kForceK > 0) K = kForceK;
     if (K > 1 && (g.blockDim + K - 1) / K > 256) K = 4;  // K >= 2 kernels take <= 256 threads
+    if (K == 1 && g.blockDim > 256) K = 4;               // so does K = 1
     const int threads = (int)(((g.blockDim + K - 1) / K + 31) / 32 * 32);
     int htBits = 1;
     while ((1 << htBits) < 4 * threads * K) ++htBits;
