@@ -2,6 +2,9 @@
 // entry point mckg_detect_shared_host, which streams a host-resident trace to
 // the device in chunks on two CUDA streams so that the PCIe copies of chunk
 // c+1 overlap the detection of chunk c.
+#include <array>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -108,9 +111,25 @@ extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* t
     max_ev = std::max<uint64_t>(max_ev, hbs[cuts[c + 1]] - hbs[cuts[c]]);
     max_nb = std::max<uint32_t>(max_nb, cuts[c + 1] - cuts[c]);
   }
+  // two pipeline streams per device, created once (the detector keeps
+  // per-stream scratch, so stable stream handles keep that scratch bounded)
+  static std::mutex smu;
+  static std::map<int, std::array<cudaStream_t, 2>> sstreams;
   cudaStream_t st[2];
-  MCKG_CUDA_TRY(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
-  MCKG_CUDA_TRY(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+  {
+    int dev = 0;
+    MCKG_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(smu);
+    auto it = sstreams.find(dev);
+    if (it == sstreams.end()) {
+      std::array<cudaStream_t, 2> a{};
+      MCKG_CUDA_TRY(cudaStreamCreateWithFlags(&a[0], cudaStreamNonBlocking));
+      MCKG_CUDA_TRY(cudaStreamCreateWithFlags(&a[1], cudaStreamNonBlocking));
+      it = sstreams.emplace(dev, a).first;
+    }
+    st[0] = it->second[0];
+    st[1] = it->second[1];
+  }
   mckg_access* dev_ev[2] = {nullptr, nullptr};
   uint64_t* dev_bs[2] = {nullptr, nullptr};
   uint64_t* pin_bs = nullptr;
@@ -227,8 +246,6 @@ extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* t
   cudaFree(out.n_triples);
   cudaFree(out.line_first);
   cudaFree(out.status);
-  cudaStreamDestroy(st[0]);
-  cudaStreamDestroy(st[1]);
   add_launches(launches);
   return rc;
 }

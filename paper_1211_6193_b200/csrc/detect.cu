@@ -34,6 +34,8 @@
 //      global triple array; the first racing timestamp per line is
 //      min-reduced per warp (lane-owned line cache), then globally.
 #include <cub/cub.cuh>
+#include <map>
+#include <mutex>
 #include <type_traits>
 
 #include "common.cuh"
@@ -89,8 +91,9 @@ struct Params {
   uint32_t gate;       // fused kernel: 1 = only the blocks of olist
   // per block, wpb 64-bit words {candidate bits of 32 records, 1}: word
   // k * 8 + warp covers records k * NT + warp * 32 + lane (0 = not published)
-  unsigned long long* cbits;  // [n_blocks * wpb]
+  unsigned long long* cbits;  // [n_blocks * wpb]; high word = ctag when published
   uint32_t wpb;
+  uint32_t ctag;              // this call's publication tag (never 0)
   uint32_t* ocount;    // [0] blocks in olist, [1] exact_kernel's next block
   uint32_t* olist;     // [n_blocks]
 };
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
         }
         if (lane < (uint32_t)EPT) {
           unsigned long long* w = P.cbits + (size_t)b * P.wpb + lane * (NT / 32) + (t >> 5);
-          *(volatile unsigned long long*)w = (1ull << 32) | mine;
+          *(volatile unsigned long long*)w = ((unsigned long long)P.ctag << 32) | mine;
         }
         cacc = 0;
       }
@@ -881,7 +884,7 @@ __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
       if (q < P.wpb) {
         const volatile unsigned long long* w = P.cbits + (size_t)bb * P.wpb + q;
         unsigned long long v = *w;
-        while ((v >> 32) == 0) {
+        while ((uint32_t)(v >> 32) != P.ctag) {
           __nanosleep(500);
           v = *w;
         }
@@ -1051,6 +1054,7 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.gate = 0;
   P.cbits = nullptr;
   P.wpb = cap / 32u;
+  P.ctag = 0;
   P.ocount = nullptr;
   P.olist = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1064,11 +1068,40 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   // kernel (gated) redoes only the blocks with more than CMAX candidates
   keep_pool_memory();
   P.wpb = (uint32_t)(ki == 0 ? 4 : ki == 1 ? 8 : 16) * (NT / 32);  // EPT * warps
-  MCKG_CUDA_TRY(cudaMallocAsync(&P.cbits, (size_t)tr->n_blocks * P.wpb * sizeof(unsigned long long), s));
+  // candidate bitmaps: a buffer per stream that only this path writes,
+  // cleared once; words carry the call's tag, so stale words never match
+  {
+    struct CBuf {
+      unsigned long long* p = nullptr;
+      size_t words = 0;
+      uint32_t tag = 0;
+      int dev = -1;
+    };
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, CBuf> bufs;
+    int dev = 0;
+    MCKG_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    CBuf& cb = bufs[{dev, s}];
+    const size_t need = (size_t)tr->n_blocks * P.wpb;
+    if (cb.words < need || cb.tag == 0xFFFFFFFFu) {
+      if (cb.p) {
+        MCKG_CUDA_TRY(cudaStreamSynchronize(s));
+        MCKG_CUDA_TRY(cudaFree(cb.p));
+        cb.p = nullptr;
+      }
+      const size_t words = std::max(need, cb.words);
+      MCKG_CUDA_TRY(cudaMalloc(&cb.p, words * sizeof(unsigned long long)));
+      MCKG_CUDA_TRY(cudaMemsetAsync(cb.p, 0, words * sizeof(unsigned long long), s));
+      cb.words = words;
+      cb.tag = 0;
+    }
+    P.cbits = cb.p;
+    P.ctag = ++cb.tag;
+  }
   MCKG_CUDA_TRY(cudaMallocAsync(&P.ocount, 2 * sizeof(uint32_t), s));
   MCKG_CUDA_TRY(cudaMallocAsync(&P.olist, (size_t)tr->n_blocks * sizeof(uint32_t), s));
   MCKG_CUDA_TRY(cudaMemsetAsync(P.ocount, 0, 2 * sizeof(uint32_t), s));
-  MCKG_CUDA_TRY(cudaMemsetAsync(P.cbits, 0, (size_t)tr->n_blocks * P.wpb * sizeof(unsigned long long), s));
   P.mode = 1;
   kt<<<grid_t, NT, smem_t, s>>>(P);
   uint32_t launched = 1;
@@ -1100,7 +1133,6 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     launched += 2;
   }
   MCKG_CUDA_TRY(cudaGetLastError());
-  cudaFreeAsync(P.cbits, s);
   cudaFreeAsync(P.ocount, s);
   cudaFreeAsync(P.olist, s);
   note_launch(launched, grid_t, NT, (uint32_t)smem_t);
