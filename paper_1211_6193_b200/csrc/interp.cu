@@ -1273,12 +1273,17 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       const int p = (E + 1) & 1;
       const int arrived = bs.wait[p] - (need[p] - (int)n);
       const int nfin = bs.fin;
+      const int nzNow = bs.nz[p], allcNow = bs.allc[p];
+      // every warp reads the counters before any warp's next step phase can
+      // change them (a fast warp would otherwise let a slow one see arrivals
+      // of the next sweep)
+      __syncthreads();
       if (arrived == (int)n) {
         // episode E+1 completed in sweep T = `sweep` (the last arrival): the
         // up-sweep chain, Turnaround (epoch clear) and Down(L) fire in T, one
         // Down per sweep after that, FinalRelease(0) in T + L
         const uint32_t T = sweep;
-        const int nz = bs.nz[p] - nzPrev[p], allc = bs.allc[p] - allcPrev[p];
+        const int nz = nzNow - nzPrev[p], allc = allcNow - allcPrev[p];
         nzPrev[p] += nz;
         allcPrev[p] += allc;
         need[p] += (int)n;  // the next episode of this parity is E + 3
