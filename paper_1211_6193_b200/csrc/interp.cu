@@ -180,7 +180,7 @@ struct BlockShared {
   unsigned long long allocs;
   unsigned long long sharedEvents;
   uint32_t lastSweep;
-  uint32_t busy[2];    // warps holding READY threads, by sweep parity
+  uint32_t nextRun[2][32];  // per warp: first sweep a thread of it can step (~0u: none), by sweep parity
   uint32_t soloSweep;  // sweep reached by a solo warp
 };
 
@@ -1179,7 +1179,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
     bs.allocs = 0;
     bs.sharedEvents = 0;
     bs.lastSweep = 0;
-    bs.busy[0] = bs.busy[1] = 0xFFFFFFFFu;
+    for (int w = 0; w < 32; ++w) bs.nextRun[0][w] = bs.nextRun[1][w] = 0u;
     bs.soloSweep = 0;
   }
   __syncthreads();
@@ -1250,7 +1250,10 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
   unsigned long long sharedEvents = 0;
   uint32_t lastStep = 0;
   const uint32_t Lt = n - 1;
-  bool justSolo = true;  // the busy mask is valid only after a full sweep
+  bool justSolo = true;  // the next-run table is valid only after a full sweep
+  bool released = false;  // an episode completed at the loop top (closed-form release)
+  uint32_t relT = 0;
+  uint32_t soloH = ~0u;   // solo: the first sweep another warp can step
   unsigned long long soloSweeps = 0;
   long long soloCycles = 0;
   const long long kStart = clock64();
@@ -1306,7 +1309,8 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
         }
         rules += 2ull * n;
         ++E;
-        justSolo = true;  // the busy mask predates these releases
+        released = true;  // next-run sweeps follow the closed form below
+        relT = T;
         if (P.raceCheck && (E & 0xFF) == 0) {  // stamp wrap: clear the shadow
           uint32_t* sh = (uint32_t*)(smem + L.shadow);
           for (uint32_t i = g; i < (uint32_t)P.shmem; i += CT) sh[i] = shadow_empty(0);
@@ -1323,10 +1327,28 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       // thread can move until that warp arrives at a barrier or finishes, so
       // it runs sweeps alone with warp-level synchronisation while the other
       // warps park on named barrier 1 ----
-      const uint32_t busy = justSolo ? 0xFFFFFFFFu : bs.busy[sweep & 1];
+      // which warps can step in sweep + 1, and from when the others can
+      const uint32_t nw_all = (CT + 31u) >> 5;
+      uint32_t nr = ~0u;  // lane w: warp w's first runnable sweep
+      if (lane < nw_all) {
+        if (released) {
+          // closed form: thread t >= 1 runs from T + L - t + 1, thread 0 from T + L + 1
+          int64_t maxTid = -1;
+          for (int k = K - 1; k >= 0 && maxTid < 0; --k) {
+            const int64_t base = (int64_t)k * CT + 32 * (int64_t)lane;
+            if (base < (int64_t)n) maxTid = base + 31 < (int64_t)n - 1 ? base + 31 : (int64_t)n - 1;
+          }
+          if (maxTid >= 0) nr = maxTid == 0 ? relT + Lt + 1 : relT + Lt - (uint32_t)maxTid + 1;
+        } else {
+          nr = justSolo ? 0u : bs.nextRun[sweep & 1][lane];
+        }
+      }
+      released = false;
       justSolo = false;
+      const uint32_t busy = __ballot_sync(0xFFFFFFFFu, nr <= sweep + 1);
       if (busy && (busy & (busy - 1)) == 0) {
         const uint32_t sw = (uint32_t)__ffs(busy) - 1;
+        soloH = __reduce_min_sync(0xFFFFFFFFu, lane == sw ? ~0u : nr);
         if (myWarp != sw) {
           const long long c0 = clock64();
           const uint32_t s0 = sweep;
@@ -1343,8 +1365,9 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
         soloC0 = clock64();
       }
     }
-    if (solo && !__any_sync(0xFFFFFFFFu, anyReady())) {
-      // nothing left to run in this warp: hand back to the block
+    if (solo && (sweep + 1 >= soloH || !__any_sync(0xFFFFFFFFu, anyReady()))) {
+      // another warp can step from the next sweep on, or nothing is left to
+      // run in this warp: hand back to the block
       if (lane == 0) bs.soloSweep = sweep;
       solo = false;
       soloCycles += clock64() - soloC0;
@@ -1421,9 +1444,15 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
           if ((old & 0xFFFF) != 0 && (wr || (old >> 16) != 0)) conflict = true;
         }
       }
-      if (__any_sync(0xFFFFFFFFu, anyReady()) && lane == 0) atomicOr(&bs.busy[sweep & 1], 1u << myWarp);
+      {
+        uint32_t mine = ~0u;
+#pragma unroll 1
+        for (int k = 0; k < K; ++k)
+          if (th[k].state == S_READY) mine = min(mine, max(th[k].readyAt, sweep + 1));
+        mine = __reduce_min_sync(0xFFFFFFFFu, mine);
+        if (lane == 0) bs.nextRun[sweep & 1][myWarp] = mine;
+      }
       conflict = __syncthreads_or(conflict);
-      if (g == 0) bs.busy[(sweep + 1) & 1] = 0;
     }
     // ---- memory phase: parallel, or replayed in tid order ----
     if (!conflict) {
