@@ -187,4 +187,16 @@ struct FileRunOutcome {
 FileRunOutcome runFile(const CliOptions& opts, bool live = false);
 FileRunOutcome runSourceText(const std::string& source, const std::string& filename, const CliOptions& opts);
 
+// Architecture-parameter file, one `key = integer` per line (driver.hpp:37-41);
+// throws std::runtime_error with file:line on malformed input.
+ArchParams loadArchFile(const std::string& path);
+
+struct CorpusOutcome {
+  int passed = 0;
+  int failed = 0;
+  std::string table;  // one PASS/FAIL line per fixture
+};
+// Every .cu file of a directory against its .expect sidecar (driver.hpp:43-57).
+CorpusOutcome runCorpus(const std::string& directory);
+
 }  // namespace mck

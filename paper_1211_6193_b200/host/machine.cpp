@@ -1806,7 +1806,9 @@ FileRunOutcome runSourceText(const std::string& source, const std::string& filen
   }
   if (out.run.stuck && !opts.reportPath.empty()) {
     if (FILE* f = std::fopen(opts.reportPath.c_str(), "w")) {
-      std::string t = formatStuckReports(out.run.stuckReports);
+      // driver.cpp:152-158; the configuration dump is not modelled
+      std::string t = "stuck-state report for " + filename + "\n\n" + formatStuckReports(out.run.stuckReports) +
+                      "\nfinal configuration:\n(not modelled by the B200 engine)\n";
       std::fwrite(t.data(), 1, t.size(), f);
       std::fclose(f);
     }

@@ -52,4 +52,34 @@ def test_cli_fig1_family(tmp_path, name):
     assert out.stdout == want["output"]
     assert out.stderr == "".join("cudak: " + d["msg"] + "\n" for d in want["diags"])
     if want["exit"] == 3:
-        assert (tmp_path / "report.txt").read_text() == want["report_text"]
+        # driver.cpp:152-158: header, the stuck reports, then the configuration dump
+        text = (tmp_path / "report.txt").read_text()
+        head = "stuck-state report for " + fname + "\n\n" + want["report_text"] + "\nfinal configuration:\n"
+        assert text.startswith(head)
+
+
+@needs_cli
+def test_cli_arch_file_and_corpus(tmp_path):
+    """--arch (loadArchFile, driver.cpp:39-84) and --run-corpus (runCorpus,
+    driver.cpp:280-340) on host-only fixtures (no GPU needed)."""
+    (tmp_path / "arch.txt").write_text("# B200-ish\nwarpSize = 32\nmaxThreadsPerBlock = 512\n")
+    src = "int main(void) { return 0; }\n"
+    out = _run(tmp_path, "a.cu", src, "--arch", "arch.txt")
+    assert out.returncode == 0, out.stderr
+    (tmp_path / "bad.txt").write_text("warpSize = x\n")
+    out = _run(tmp_path, "a.cu", src, "--arch", "bad.txt")
+    assert out.returncode == 2 and "bad.txt:1: 'x' is not an integer" in out.stderr
+    corp = tmp_path / "corpus"
+    corp.mkdir()
+    (corp / "ok.cu").write_text('#include <stdio.h>\nint main(void) { printf("hi %d\\n", 7); return 0; }\n')
+    (corp / "ok.expect").write_text("exit 0\nstdout<<EOF\nhi 7\nEOF\n")
+    (corp / "ret.cu").write_text("int main(void) { return 5; }\n")
+    (corp / "ret.expect").write_text("exit 4\n")
+    (corp / "nosidecar.cu").write_text("int main(void) { return 0; }\n")
+    r = subprocess.run([MCKB, "--run-corpus", str(corp)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 1
+    lines = r.stdout.splitlines()
+    assert lines[0].startswith("FAIL nosidecar.cu (missing sidecar")
+    assert lines[1] == "PASS ok.cu"
+    assert lines[2] == "FAIL ret.cu (exit code 5, expected 4)"
+    assert lines[3] == "1 passed, 2 failed"

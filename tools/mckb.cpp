@@ -5,13 +5,18 @@
 // reference exit codes (0 clean, 1 diagnostics, 2 frontend error, 3 stuck).
 //
 //   mckb [--no-race-check] [--schedule roundrobin|random] [--seed N]
-//        [--step-limit N] [--report FILE] [--trace] [--stats] file.cu
+//        [--step-limit N] [--report FILE] [--trace] [--arch FILE] [--stats] file.cu
+//   mckb --run-corpus DIR        (every DIR/*.cu against its .expect sidecar)
+//
+// On a stuck run the report file (default: <file>.cudak-report.txt, as the
+// reference CLI) receives the stuck reports.
 //
 // Device grids run on the B200 engine; the schedule is round-robin (the
 // engine's exact schedule; --schedule random is accepted and noted).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <string>
 
 #include "mck/checker.hpp"
@@ -19,6 +24,8 @@
 int main(int argc, char** argv) {
   mck::CliOptions o;
   bool stats = false;
+  bool reportSet = false;
+  std::string corpusDir;
   for (int i = 1; i < argc; ++i) {
     std::string a = argv[i];
     auto next = [&]() -> std::string {
@@ -34,12 +41,17 @@ int main(int argc, char** argv) {
       o.schedule = v == "roundrobin" ? mck::SchedulePolicy::RoundRobin : mck::SchedulePolicy::SeededRandom;
     } else if (a == "--seed") o.seed = std::strtoull(next().c_str(), nullptr, 10);
     else if (a == "--step-limit") o.stepLimit = std::strtoull(next().c_str(), nullptr, 10);
-    else if (a == "--report") o.reportPath = next();
+    else if (a == "--report") {
+      o.reportPath = next();
+      reportSet = true;
+    } else if (a == "--arch") o.archFile = next();
+    else if (a == "--run-corpus") corpusDir = next();
     else if (a == "--trace") o.trace = true;
     else if (a == "--stats") stats = true;
     else if (a == "-h" || a == "--help") {
       std::printf("usage: mckb [--no-race-check] [--schedule roundrobin|random] [--seed N] "
-                  "[--step-limit N] [--report FILE] [--trace] [--stats] file.cu\n");
+                  "[--step-limit N] [--report FILE] [--trace] [--arch FILE] [--stats] file.cu\n"
+                  "       mckb --run-corpus DIR\n");
       return 0;
     } else if (!a.empty() && a[0] == '-') {
       std::fprintf(stderr, "mckb: unknown option %s\n", a.c_str());
@@ -48,9 +60,23 @@ int main(int argc, char** argv) {
       o.inputPath = a;
     }
   }
+  if (!corpusDir.empty()) {
+    const mck::CorpusOutcome c = mck::runCorpus(corpusDir);
+    std::printf("%s%d passed, %d failed\n", c.table.c_str(), c.passed, c.failed);
+    return c.failed == 0 ? 0 : 1;
+  }
   if (o.inputPath.empty()) {
     std::fprintf(stderr, "mckb: no input file\n");
     return 2;
+  }
+  if (!reportSet) o.reportPath = o.inputPath + ".cudak-report.txt";
+  if (!o.archFile.empty()) {
+    try {
+      o.arch = mck::loadArchFile(o.archFile);
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "cudak: %s\n", e.what());
+      return 2;
+    }
   }
   mck::FileRunOutcome out = mck::runFile(o);
   std::fwrite(out.stdoutText.data(), 1, out.stdoutText.size(), stdout);
