@@ -130,6 +130,35 @@ extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* t
     st[0] = it->second[0];
     st[1] = it->second[1];
   }
+  // device staging, pinned block starts and the outputs are kept per device
+  // and grown on demand (large cudaMalloc / cudaMallocHost calls cost
+  // milliseconds); one call at a time per device
+  struct HostPathScratch {
+    std::mutex mu;
+    mckg_access* ev[2] = {nullptr, nullptr};
+    uint64_t ev_cap = 0;
+    uint64_t* bs[2] = {nullptr, nullptr};
+    uint64_t bs_cap = 0;
+    uint64_t* pin_bs = nullptr;
+    uint64_t pin_cap = 0;
+    mckg_race_triple* tri = nullptr;
+    uint64_t tri_cap = 0;
+    unsigned long long* n_tri = nullptr;
+    unsigned long long* line_first = nullptr;
+    uint32_t* status = nullptr;
+  };
+  static std::mutex scr_mu;
+  static std::map<int, HostPathScratch*> scratch;
+  HostPathScratch* S = nullptr;
+  {
+    int dev = 0;
+    MCKG_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(scr_mu);
+    HostPathScratch*& e = scratch[dev];
+    if (!e) e = new HostPathScratch();
+    S = e;
+  }
+  std::lock_guard<std::mutex> call_lock(S->mu);
   mckg_access* dev_ev[2] = {nullptr, nullptr};
   uint64_t* dev_bs[2] = {nullptr, nullptr};
   uint64_t* pin_bs = nullptr;
@@ -142,32 +171,75 @@ extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* t
   };
   do {
     cudaError_t e;
-    for (int k = 0; k < 2 && n_chunks; ++k) {
-      if ((e = cudaMalloc(&dev_ev[k], std::max<uint64_t>(1, max_ev) * sizeof(mckg_access)))) {
+    const uint64_t need_ev = std::max<uint64_t>(1, max_ev), need_bs = max_nb + 1ull;
+    if (S->ev_cap < need_ev) {
+      for (int k = 0; k < 2; ++k) {
+        cudaFree(S->ev[k]);
+        S->ev[k] = nullptr;
+      }
+      S->ev_cap = 0;
+      for (int k = 0; k < 2; ++k)
+        if ((e = cudaMalloc(&S->ev[k], need_ev * sizeof(mckg_access)))) break;
+      if (e) {
         fail("cudaMalloc(events)", e);
         break;
       }
-      if ((e = cudaMalloc(&dev_bs[k], (max_nb + 1ull) * sizeof(uint64_t)))) {
+      S->ev_cap = need_ev;
+    }
+    if (S->bs_cap < need_bs) {
+      for (int k = 0; k < 2; ++k) {
+        cudaFree(S->bs[k]);
+        S->bs[k] = nullptr;
+      }
+      S->bs_cap = 0;
+      for (int k = 0; k < 2; ++k)
+        if ((e = cudaMalloc(&S->bs[k], need_bs * sizeof(uint64_t)))) break;
+      if (e) {
         fail("cudaMalloc(block_start)", e);
         break;
       }
+      S->bs_cap = need_bs;
     }
-    if (rc) break;
-    if ((e = cudaMallocHost(&pin_bs, (tr->n_blocks + n_chunks + 1ull) * sizeof(uint64_t)))) {
-      fail("cudaMallocHost", e);
-      break;
+    const uint64_t need_pin = tr->n_blocks + n_chunks + 1ull;
+    if (S->pin_cap < need_pin) {
+      cudaFreeHost(S->pin_bs);
+      S->pin_bs = nullptr;
+      S->pin_cap = 0;
+      if ((e = cudaMallocHost(&S->pin_bs, need_pin * sizeof(uint64_t)))) {
+        fail("cudaMallocHost", e);
+        break;
+      }
+      S->pin_cap = need_pin;
     }
-    if ((e = cudaMalloc(&out.triples, std::max<uint64_t>(1, capacity) * sizeof(mckg_race_triple)))) {
-      fail("cudaMalloc(triples)", e);
-      break;
+    const uint64_t need_tri = std::max<uint64_t>(1, capacity);
+    if (S->tri_cap < need_tri) {
+      cudaFree(S->tri);
+      S->tri = nullptr;
+      S->tri_cap = 0;
+      if ((e = cudaMalloc(&S->tri, need_tri * sizeof(mckg_race_triple)))) {
+        fail("cudaMalloc(triples)", e);
+        break;
+      }
+      S->tri_cap = need_tri;
     }
+    if (!S->n_tri) {
+      if ((e = cudaMalloc(&S->n_tri, sizeof(unsigned long long))) ||
+          (e = cudaMalloc(&S->line_first, MCKG_MAX_LINES * sizeof(unsigned long long))) ||
+          (e = cudaMalloc(&S->status, sizeof(uint32_t)))) {
+        fail("cudaMalloc(outputs)", e);
+        break;
+      }
+    }
+    for (int k = 0; k < 2; ++k) {
+      dev_ev[k] = S->ev[k];
+      dev_bs[k] = S->bs[k];
+    }
+    pin_bs = S->pin_bs;
+    out.triples = S->tri;
     out.capacity = capacity;
-    if ((e = cudaMalloc(&out.n_triples, sizeof(unsigned long long))) ||
-        (e = cudaMalloc(&out.line_first, MCKG_MAX_LINES * sizeof(unsigned long long))) ||
-        (e = cudaMalloc(&out.status, sizeof(uint32_t)))) {
-      fail("cudaMalloc(outputs)", e);
-      break;
-    }
+    out.n_triples = S->n_tri;
+    out.line_first = S->line_first;
+    out.status = S->status;
     if ((rc = mckg_race_out_reset(&out, st[0]))) break;
     ++launches;
     if ((e = cudaStreamSynchronize(st[0]))) {
@@ -237,15 +309,6 @@ extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* t
     }
     if (n > capacity) rc = MCKG_E_OVERFLOW;
   } while (0);
-  for (int k = 0; k < 2; ++k) {
-    cudaFree(dev_ev[k]);
-    cudaFree(dev_bs[k]);
-  }
-  cudaFreeHost(pin_bs);
-  cudaFree(out.triples);
-  cudaFree(out.n_triples);
-  cudaFree(out.line_first);
-  cudaFree(out.status);
   add_launches(launches);
   return rc;
 }
