@@ -108,6 +108,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -164,7 +175,7 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": f"cpu{thr}",
                                         "sample_events_per_step": total_events // args.steps},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": kind,
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -243,6 +254,18 @@ def run_ours(args):
     n_tri = int(out.n_triples.item())
     status = int(out.status.item())
     assert status == 0, f"detector status {status}"
+    # the run's own result, sorted into RaceState::reported order on the
+    # device, kept on the host for the full-size parity check (cpu leg)
+    gpu_res = None
+    if (rank == 0 and ws == 1 and not args.no_cpu) or args.dump:
+        gpu_res = race.fetch(out, obj_base=1 + b0)
+    if args.dump:  # this rank's reported set + the reduced line table (multi-rank set tests)
+        import numpy as np
+        os.makedirs(args.dump, exist_ok=True)
+        np.savez(os.path.join(args.dump, f"c3_r{rank}.npz"), triples=gpu_res.triples,
+                 line_first=gpu_res.line_first, n=gpu_res.n_triples)
+    if not (rank == 0 and ws == 1 and not args.no_cpu):
+        gpu_res = None
     # max over ranks
     t = torch.tensor([ms, statistics.mean(k_ms)], dtype=torch.float64, device=dev)
     tot = torch.tensor([nb * EVENTS_PER_BLOCK, n_tri], dtype=torch.int64, device=dev)
@@ -279,12 +302,24 @@ def run_ours(args):
     e2e = None
     if rank == 0 and ws == 1 and args.e2e_blocks > 0:
         e2e = run_e2e(args, torch, race, _abi)
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    cpu = parity = None
+    if gpu_res is not None:
+        # the reference CPU checker replays the SAME trace (all of it unless
+        # --cpu-blocks bounds it) on every host core: its rate is the CPU
+        # baseline, and each chunk is compared with this run's GPU result
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import c3_parity
         nthreads = host_cores()
-        target = calibrate_cpu(nthreads, args.cpu_seconds)
-        v, kind, sample, thr, _ = cpu_replay(target, nthreads)
-        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": kind, "sample": sample}
+        cb = args.cpu_blocks if args.cpu_blocks else blocks
+        parity = c3_parity.replay_full(gpu_res.triples, gpu_res.line_first, blocks, nthreads, max_blocks=cb)
+        parity["gpu_triples"] = int(gpu_res.n_triples)
+        cpu = {"value": parity["events"] / parity["replay_s"], "unit": UNIT, "cores": nthreads,
+               "cpu_model": cpu_model(), "kind": parity["kind"],
+               "sample": (f"C3 blocks 0..{parity['checked_blocks'] - 1} of {blocks} "
+                          f"({parity['events']} events; "
+                          f"{'reference Machine::recordAccess/clearEpoch' if parity['kind'] == 'reference' else 'oracle/detector.c'}"
+                          f" replay, chunks of 2^16 blocks partitioned over {nthreads} threads; "
+                          f"generation excluded)")}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -292,6 +327,8 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "events": total_events, "blocks": blocks,
                        "reported_triples": total_tri, "parallelism": f"block-shard{ws}",
+                       "parity_checked": bool(parity and parity["checked_blocks"] == parity["of_blocks"]
+                                              and parity["triples_equal"] and parity["line_first_equal"]),
                        "l2": "inputs (16 GiB) >> L2 (126 MB); no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(),
@@ -302,6 +339,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
             "k1": k1,
             "c5": c5,
         }
@@ -362,6 +400,10 @@ def run_c5(args, blocks, dev, ws, rank):
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
+    if args.dump:
+        import numpy as np
+        races, n_r, lf, _ = gr.fetch(out)
+        np.savez(os.path.join(args.dump, f"c5_r{rank}.npz"), races=races, line_first=lf, n=n_r)
     n_races = int(out.n.item())
     status = int(out.status.item())
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -491,8 +533,12 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--blocks", type=int, default=FULL_BLOCKS)
     ap.add_argument("--e2e-blocks", type=int, default=FULL_BLOCKS)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="--impl reference: CPU seconds per step")
+    ap.add_argument("--cpu-blocks", type=int, default=0,
+                    help="blocks the cpu_baseline / parity leg replays (default: all of them)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dump", default="", help="directory: each rank saves its C3/C5 result sets (tests)")
     ap.add_argument("--no-k1", action="store_true")
     ap.add_argument("--k1-racy", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the K1 C4 deadlock-sweep leg")

@@ -172,6 +172,10 @@ int mckg_abi_version(void);
 const char* mckg_last_error(void);
 int mckg_device_count(int* n);
 int mckg_get_launch_stats(mckg_launch_stats* out);
+/* Experiment / test switches of the detector (the MCKG_DEBUG environment
+ * variable read once at load; 32 = the fused K2 kernel alone, which the
+ * tests exercise beside the default two-kernel path). */
+void mckg_set_debug(uint32_t flags);
 
 int mckg_race_out_reset(const mckg_race_out* out, void* stream);
 int mckg_detect_shared(const mckg_trace* trace, const mckg_race_out* out, void* stream);
@@ -325,6 +329,65 @@ int mckg_comm_id(uint8_t out[128]);
  * reported[[obj,byte,line]], stats{...}, engine_error; or frontend_error.
  * *json is malloc'ed: release with mck_free. */
 int mck_run_source(const char* src, const char* filename, const mck_run_opts* opts, char** json);
+
+/* ---- whole-program checking, result records (no JSON) ----
+ * mck_run: compileSource + Machine(prog, opts).run() (program.hpp:59-60,
+ * machine.hpp:359/375; the reference driver's path, driver.cpp:87-161).  The
+ * RunResult stays in an opaque handle; strings and arrays handed out by the
+ * accessors live until mck_result_free.  A frontend failure (LexError /
+ * ParseError / SemanticError, diagnostics.hpp:35-56) is not an ABI error: the
+ * handle reports it in the summary (frontend_stage non-empty, exit_code 2). */
+typedef struct mck_result mck_result;
+
+typedef struct mck_summary {
+  int32_t exit_code;          /* RunResult::exitCode (2 = frontend error)          */
+  int32_t stuck;              /* RunResult::stuck                                   */
+  int32_t has_main_return;    /* RunResult::mainReturn engaged                      */
+  int32_t frontend_line;      /* frontend failure: its line                         */
+  int64_t main_return;
+  uint64_t steps;             /* RunResult::steps                                   */
+  uint64_t n_diags;           /* RunResult::diagnostics, report order               */
+  uint64_t n_stuck;           /* RunResult::stuckReports                            */
+  uint64_t n_reported;        /* RaceState::reported triples, std::set order        */
+  uint64_t n_trace;           /* --trace lines                                      */
+  uint64_t output_bytes;
+  const char* output;         /* RunResult::output (NUL-terminated)                 */
+  const char* engine_error;   /* "" unless the engine abandoned the run             */
+  const char* frontend_stage; /* "" or "lex" / "parse" / "semantic"                 */
+  const char* frontend_message;
+  const char* report_text;    /* formatStuckReports(stuckReports) (machine.hpp:449) */
+} mck_summary;
+
+typedef struct mck_diag_rec {
+  int32_t category;           /* DiagCategory: 0 race, 1 deadlock, 2 memBoundary,
+                                 3 undefinedBehavior, 4 apiError                     */
+  int32_t severity;           /* 0 error, 1 warning                                 */
+  int32_t line;               /* Diagnostic::loc.line                               */
+  int32_t pad;
+  uint64_t sweep;             /* round-robin sweep of the first occurrence          */
+  const char* message;        /* Diagnostic::message                                */
+} mck_diag_rec;
+
+typedef struct mck_stuck_rec {
+  int32_t kind;               /* 0 BarrierDeadlock, 1 HostHang, 2 StreamStall       */
+  uint32_t gid;
+  int32_t bid;
+  uint32_t sid;
+  uint64_t n_waiting, n_missing;
+  const int32_t* waiting;     /* waitingTids, ascending                             */
+  const int32_t* missing;     /* missingTids, ascending                             */
+  const char* reason;
+  const char* item;
+} mck_stuck_rec;
+
+int mck_run(const char* src, const char* filename, const mck_run_opts* opts, mck_result** out);
+int mck_result_summary(const mck_result* r, mck_summary* out);
+int mck_result_diag(const mck_result* r, uint64_t i, mck_diag_rec* out);
+int mck_result_stuck(const mck_result* r, uint64_t i, mck_stuck_rec* out);
+/* triples [first, first + count) of RaceState::reported (machine.hpp:91) */
+int mck_result_reported(const mck_result* r, uint64_t first, uint64_t count, mckg_race_triple* out);
+const char* mck_result_trace(const mck_result* r, uint64_t i);
+void mck_result_free(mck_result* r);
 int mck_disassemble(const char* src, const char* filename, char** text);
 void mck_free(char* p);
 

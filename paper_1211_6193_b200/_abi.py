@@ -34,6 +34,7 @@ EXPORTS = [
     "mckg_last_error",
     "mckg_device_count",
     "mckg_get_launch_stats",
+    "mckg_set_debug",
     "mckg_race_out_reset",
     "mckg_detect_shared",
     "mckg_detect_shared_host",
@@ -47,6 +48,13 @@ EXPORTS = [
     "mck_run_source",
     "mck_disassemble",
     "mck_free",
+    "mck_run",
+    "mck_result_summary",
+    "mck_result_diag",
+    "mck_result_stuck",
+    "mck_result_reported",
+    "mck_result_trace",
+    "mck_result_free",
 ]
 
 
@@ -104,6 +112,8 @@ def load():
     lib.mckg_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
     lib.mckg_get_launch_stats.argtypes = [ctypes.POINTER(LaunchStats)]
     lib.mckg_race_out_reset.argtypes = [ctypes.POINTER(RaceOut), vp]
+    lib.mckg_set_debug.argtypes = [u32]
+    lib.mckg_set_debug.restype = None
     lib.mckg_detect_shared.argtypes = [ctypes.POINTER(Trace), ctypes.POINTER(RaceOut), vp]
     lib.mckg_detect_shared_host.argtypes = [ctypes.POINTER(Trace), vp, u64, ctypes.POINTER(u64),
                                             vp, ctypes.POINTER(u32)]

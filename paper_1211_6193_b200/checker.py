@@ -10,6 +10,8 @@ execution path for device code: a launch without a CUDA device is reported in
 import ctypes
 import json
 
+import numpy as np
+
 from . import _abi
 
 
@@ -71,18 +73,8 @@ def torch_allgather(group=None):
     return gather
 
 
-def run_source(src, filename="test.cu", step_limit=0, race_check=True, device=0,
-               round_robin=True, seed=0, devices=None, rank=0, world=1, comm=None, allgather=None,
-               trace=False):
-    """Machine::run on a source program -> dict (keys: see include/mckg.h).
-
-    devices: list of CUDA ordinals to split every grid over (a repeated
-    ordinal makes virtual devices on one GPU).
-    rank/world: one process per GPU; this rank runs its block range of every
-    grid and the ranks combine memory and reports over NCCL (comm = the id
-    from comm_id() on rank 0) or over `allgather(bytes) -> bytes` (host
-    transport, e.g. torch_allgather())."""
-    lib = _lib()
+def _opts(step_limit=0, race_check=True, device=0, round_robin=True, seed=0, devices=None, rank=0,
+          world=1, comm=None, allgather=None, trace=False):
     devs = list(devices or [])
     arr = (ctypes.c_int32 * 8)(*(devs + [0] * (8 - len(devs))))
     cid = (ctypes.c_uint8 * 128)(*(comm or bytes(128)))
@@ -98,6 +90,22 @@ def run_source(src, filename="test.cu", step_limit=0, race_check=True, device=0,
         cb = ALLGATHER(_cb)
     o = RunOpts(step_limit, seed, 1 if race_check else 0, 1 if round_robin else 0, device, 0, len(devs), arr,
                 rank, world, cid, ctypes.cast(cb, ctypes.c_void_p) if cb else None, None, 1 if trace else 0)
+    o._keep = cb
+    return o
+
+
+def run_source(src, filename="test.cu", **kw):
+    """Machine::run on a source program -> dict (keys: see include/mckg.h).
+
+    Keyword options (RunOptions): step_limit, race_check, device,
+    round_robin, seed, trace; devices: list of CUDA ordinals to split every
+    grid over (a repeated ordinal makes virtual devices on one GPU);
+    rank/world: one process per GPU; this rank runs its block range of every
+    grid and the ranks combine memory and reports over NCCL (comm = the id
+    from comm_id() on rank 0) or over `allgather(bytes) -> bytes` (host
+    transport, e.g. torch_allgather())."""
+    lib = _lib()
+    o = _opts(**kw)
     out = ctypes.c_void_p()
     rc = lib.mck_run_source(src.encode(), filename.encode(), ctypes.byref(o), ctypes.byref(out))
     _abi.check(rc, "mck_run_source")
@@ -113,3 +121,89 @@ def disassemble(src, filename="test.cu"):
     s = ctypes.string_at(out.value).decode()
     lib.mck_free(out)
     return s
+
+
+# ---- result records (mck_run / mck_result_*: no JSON) ----
+TRIPLE_DTYPE = np.dtype([("obj", "<u4"), ("byte", "<u4"), ("line", "<i4")])
+CATEGORIES = ("race", "deadlock", "memBoundary", "undefinedBehavior", "apiError")
+STUCK_KINDS = ("barrier", "host", "stream")
+
+
+class Summary(ctypes.Structure):
+    _fields_ = [("exit_code", ctypes.c_int32), ("stuck", ctypes.c_int32), ("has_main_return", ctypes.c_int32),
+                ("frontend_line", ctypes.c_int32), ("main_return", ctypes.c_int64), ("steps", ctypes.c_uint64),
+                ("n_diags", ctypes.c_uint64), ("n_stuck", ctypes.c_uint64), ("n_reported", ctypes.c_uint64),
+                ("n_trace", ctypes.c_uint64), ("output_bytes", ctypes.c_uint64), ("output", ctypes.c_char_p),
+                ("engine_error", ctypes.c_char_p), ("frontend_stage", ctypes.c_char_p),
+                ("frontend_message", ctypes.c_char_p), ("report_text", ctypes.c_char_p)]
+
+
+class DiagRec(ctypes.Structure):
+    _fields_ = [("category", ctypes.c_int32), ("severity", ctypes.c_int32), ("line", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("sweep", ctypes.c_uint64), ("message", ctypes.c_char_p)]
+
+
+class StuckRec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("gid", ctypes.c_uint32), ("bid", ctypes.c_int32), ("sid", ctypes.c_uint32),
+                ("n_waiting", ctypes.c_uint64), ("n_missing", ctypes.c_uint64),
+                ("waiting", ctypes.POINTER(ctypes.c_int32)), ("missing", ctypes.POINTER(ctypes.c_int32)),
+                ("reason", ctypes.c_char_p), ("item", ctypes.c_char_p)]
+
+
+def _rec_lib():
+    lib = _lib()
+    if not getattr(lib, "_mck_rec_bound", False):
+        vp = ctypes.c_void_p
+        lib.mck_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(RunOpts), ctypes.POINTER(vp)]
+        lib.mck_result_summary.argtypes = [vp, ctypes.POINTER(Summary)]
+        lib.mck_result_diag.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(DiagRec)]
+        lib.mck_result_stuck.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(StuckRec)]
+        lib.mck_result_reported.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, vp]
+        lib.mck_result_trace.argtypes = [vp, ctypes.c_uint64]
+        lib.mck_result_trace.restype = ctypes.c_char_p
+        lib.mck_result_free.argtypes = [vp]
+        lib.mck_result_free.restype = None
+        lib._mck_rec_bound = True
+    return lib
+
+
+def run(src, filename="test.cu", **kw):
+    """Machine::run through the result-record ABI.  Same keys as run_source
+    (exit, output, steps, stuck, main_return, diags, stuck_reports,
+    report_text, engine_error, trace), but `reported` is a numpy array of
+    (obj, byte, line) records in std::set order -- fit for millions of
+    triples."""
+    lib = _rec_lib()
+    o = _opts(**kw)
+    h = ctypes.c_void_p()
+    _abi.check(lib.mck_run(src.encode(), filename.encode(), ctypes.byref(o), ctypes.byref(h)), "mck_run")
+    try:
+        sm = Summary()
+        _abi.check(lib.mck_result_summary(h, ctypes.byref(sm)), "mck_result_summary")
+        if sm.frontend_stage:
+            return {"frontend_error": f"{sm.frontend_stage.decode()}: {sm.frontend_message.decode()}",
+                    "line": sm.frontend_line, "exit": sm.exit_code}
+        diags = []
+        for i in range(sm.n_diags):
+            d = DiagRec()
+            _abi.check(lib.mck_result_diag(h, i, ctypes.byref(d)), "mck_result_diag")
+            diags.append({"cat": CATEGORIES[d.category], "sev": "error" if d.severity == 0 else "warning",
+                          "msg": d.message.decode(), "line": d.line})
+        stuck = []
+        for i in range(sm.n_stuck):
+            r = StuckRec()
+            _abi.check(lib.mck_result_stuck(h, i, ctypes.byref(r)), "mck_result_stuck")
+            stuck.append({"kind": STUCK_KINDS[r.kind], "gid": r.gid, "bid": r.bid,
+                          "waiting": [r.waiting[k] for k in range(r.n_waiting)],
+                          "missing": [r.missing[k] for k in range(r.n_missing)], "reason": r.reason.decode()})
+        rep = np.zeros(sm.n_reported, dtype=TRIPLE_DTYPE)
+        if sm.n_reported:
+            _abi.check(lib.mck_result_reported(h, 0, sm.n_reported, rep.ctypes.data), "mck_result_reported")
+        return {"exit": sm.exit_code, "output": ctypes.string_at(sm.output, sm.output_bytes).decode(),
+                "steps": sm.steps, "stuck": bool(sm.stuck),
+                "main_return": sm.main_return if sm.has_main_return else None,
+                "engine_error": sm.engine_error.decode(), "diags": diags, "stuck_reports": stuck,
+                "report_text": sm.report_text.decode(), "reported": rep,
+                "trace": [lib.mck_result_trace(h, i).decode() for i in range(sm.n_trace)]}
+    finally:
+        lib.mck_result_free(h)

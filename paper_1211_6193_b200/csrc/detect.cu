@@ -34,7 +34,10 @@
 //      global triple array; the first racing timestamp per line is
 //      min-reduced per warp (lane-owned line cache), then globally.
 #include <cub/cub.cuh>
+#include <array>
+#include <atomic>
 #include <map>
+#include <thread>
 #include <mutex>
 #include <type_traits>
 
@@ -955,6 +958,32 @@ __global__ void decode_triples(const unsigned long long* k, mckg_race_triple* t,
                           (int32_t)(v & 0xFFFFu)};
 }
 
+// Experiment / test switches (MCKG_DEBUG at load time, mckg_set_debug later).
+std::atomic<uint32_t>& debug_word() {
+  static std::atomic<uint32_t> w{[] {
+    const char* e = getenv("MCKG_DEBUG");
+    return e ? (uint32_t)atoi(e) : 0u;
+  }()};
+  return w;
+}
+uint32_t debug_flags() { return debug_word().load(std::memory_order_relaxed); }
+
+// The >48 KB dynamic shared-memory opt-in is a per-device function
+// attribute: remembered per (device, kernel), raised on demand.
+cudaError_t ensure_dynamic_smem(void (*k)(Params), size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<int, void (*)(Params)>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, k}];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 }  // namespace
 
 int detect_config(uint32_t cap, uint32_t shmem_bytes, size_t* smem, uint32_t* wpad) {
@@ -968,6 +997,8 @@ int detect_config(uint32_t cap, uint32_t shmem_bytes, size_t* smem, uint32_t* wp
 }  // namespace mckg
 
 using namespace mckg;
+
+extern "C" void mckg_set_debug(uint32_t flags) { debug_word().store(flags); }
 
 extern "C" int mckg_race_out_reset(const mckg_race_out* out, void* stream) {
   if (!out || !out->n_triples || !out->line_first || !out->status) {
@@ -1014,15 +1045,8 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   void (*kt)(Params) = ki == 0 ? race_detect_kernel<4, false> : ki == 1 ? race_detect_kernel<8, false>
                                                                        : race_detect_kernel<16, false>;
   const size_t smem_f = layout(cap, wpad, MCKG_K2_NSTAGE).end, smem_t = layout(cap, wpad, MCKG_K2F_NSTAGE).end;
-  static thread_local size_t configured[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  if (smem_f > configured[0][ki]) {
-    MCKG_CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
-    configured[0][ki] = smem_f;
-  }
-  if (smem_t > configured[1][ki]) {
-    MCKG_CUDA_TRY(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
-    configured[1][ki] = smem_t;
-  }
+  MCKG_CUDA_TRY(ensure_dynamic_smem(kf, smem_f));
+  MCKG_CUDA_TRY(ensure_dynamic_smem(kt, smem_t));
   auto grid_of = [&](void (*k)(Params), size_t sm) -> uint32_t {
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, sm) != cudaSuccess || per_sm < 1)
@@ -1046,10 +1070,7 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.n_tri = out->n_triples;
   P.line_first = out->line_first;
   P.status = out->status;
-  {
-    const char* dbg = getenv("MCKG_DEBUG");
-    P.debug = dbg ? (uint32_t)atoi(dbg) : 0u;
-  }
+  P.debug = debug_flags();
   P.mode = 0;
   P.gate = 0;
   P.cbits = nullptr;
@@ -1070,19 +1091,24 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.wpb = (uint32_t)(ki == 0 ? 4 : ki == 1 ? 8 : 16) * (NT / 32);  // EPT * warps
   // candidate bitmaps: a buffer per stream that only this path writes,
   // cleared once; words carry the call's tag, so stale words never match
+  // (plus the overflow list and its counters), grown on demand
   {
     struct CBuf {
       unsigned long long* p = nullptr;
       size_t words = 0;
       uint32_t tag = 0;
-      int dev = -1;
+      uint32_t* olist = nullptr;  // [0..1] counters, then the overflow list
+      size_t oblocks = 0;
     };
     static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, CBuf> bufs;
+    // key: (device, stream, host thread for the per-thread / legacy default
+    // stream handles, which name a different stream on each thread)
+    static std::map<std::tuple<int, cudaStream_t, std::thread::id>, CBuf> bufs;
     int dev = 0;
     MCKG_CUDA_TRY(cudaGetDevice(&dev));
+    const bool special = s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread;
     std::lock_guard<std::mutex> lock(mu);
-    CBuf& cb = bufs[{dev, s}];
+    CBuf& cb = bufs[{dev, s, special ? std::this_thread::get_id() : std::thread::id()}];
     const size_t need = (size_t)tr->n_blocks * P.wpb;
     if (cb.words < need || cb.tag == 0xFFFFFFFFu) {
       if (cb.p) {
@@ -1096,21 +1122,31 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
       cb.words = words;
       cb.tag = 0;
     }
+    if (cb.oblocks < tr->n_blocks) {
+      if (cb.olist) {
+        MCKG_CUDA_TRY(cudaStreamSynchronize(s));
+        MCKG_CUDA_TRY(cudaFree(cb.olist));
+        cb.olist = nullptr;
+      }
+      MCKG_CUDA_TRY(cudaMalloc(&cb.olist, ((size_t)tr->n_blocks + 2) * sizeof(uint32_t)));
+      cb.oblocks = tr->n_blocks;
+    }
     P.cbits = cb.p;
     P.ctag = ++cb.tag;
+    P.ocount = cb.olist;
+    P.olist = cb.olist + 2;
   }
-  MCKG_CUDA_TRY(cudaMallocAsync(&P.ocount, 2 * sizeof(uint32_t), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&P.olist, (size_t)tr->n_blocks * sizeof(uint32_t), s));
   MCKG_CUDA_TRY(cudaMemsetAsync(P.ocount, 0, 2 * sizeof(uint32_t), s));
   P.mode = 1;
   kt<<<grid_t, NT, smem_t, s>>>(P);
+  // exact_kernel spin-waits on the filter's publications: never launch it
+  // behind a filter that failed to launch
+  MCKG_CUDA_TRY(cudaGetLastError());
   uint32_t launched = 1;
   if (!(P.debug & 1u)) {
-    static int xper = 0;
-    if (!xper) {
-      MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, exact_kernel, XW * 32, 0));
-      if (xper < 1) xper = 1;
-    }
+    int xper = 0;
+    MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, exact_kernel, XW * 32, 0));
+    if (xper < 1) xper = 1;
     uint32_t xgrid = (uint32_t)sm_count() * (uint32_t)xper;
     const uint32_t need = (tr->n_blocks + XW - 1) / XW;
     if (xgrid > need) xgrid = need;
@@ -1133,8 +1169,6 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     launched += 2;
   }
   MCKG_CUDA_TRY(cudaGetLastError());
-  cudaFreeAsync(P.ocount, s);
-  cudaFreeAsync(P.olist, s);
   note_launch(launched, grid_t, NT, (uint32_t)smem_t);
   return MCKG_OK;
 }

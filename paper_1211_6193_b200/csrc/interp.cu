@@ -2006,6 +2006,12 @@ class CudaEngine final : public DeviceEngine {
       out.launches += 2;
       int herr[2];
       CK(cudaMemcpy(herr, R.err.p, sizeof herr, cudaMemcpyDeviceToHost));
+      if (herr[0] == ERR_SWEEPS && g.stepBudget + 2 < (1ull << 26) - 1) {
+        // more sweeps than steps left (each sweep takes >= 1 step): the run
+        // reaches the step limit inside this grid (machine.cpp:1184-1190)
+        out.stepLimitHit = true;
+        continue;
+      }
       if (herr[0]) {
         static const char* why[] = {"", "thread value/scope/frame stack overflow",
                                     "private memory of a thread exceeds the engine limit",
@@ -2094,6 +2100,17 @@ class CudaEngine final : public DeviceEngine {
     out.reported = std::move(tris);
     std::sort(out.stuck.begin(), out.stuck.end(),
               [](const GridResult::Stuck& a, const GridResult::Stuck& b) { return a.bid < b.bid; });
+    if (out.stepLimitHit) {
+      // the run is abandoned inside this grid: its whole budget is spent and
+      // the grid's partial effects are dropped (the host reports the limit)
+      out.deviceSteps = std::max<uint64_t>(out.deviceSteps, g.stepBudget);
+      out.barrierRules = 0;
+      out.diags.clear();
+      out.reported.clear();
+      out.stuck.clear();
+      out.deadlocked = false;
+      out.duration = 0;
+    }
     return true;
   }
 

@@ -3,11 +3,19 @@
 // boundary the Python tests and bench.py call through ctypes.
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <vector>
+
+#include <cuda_runtime_api.h>
 
 #include "mck/checker.hpp"
 #include "mckg.h"
 #include "program.hpp"
+
+namespace mckg {
+void set_error(const char* what, cudaError_t e);  // csrc/abi.cu: mckg_last_error()
+}
 
 namespace {
 
@@ -28,10 +36,7 @@ std::string js(const std::string& s) {
   return o + "\"";
 }
 
-}  // namespace
-
-extern "C" int mck_run_source(const char* src, const char* filename, const mck_run_opts* opts, char** json) {
-  if (!src || !filename || !json) return MCKG_E_ARG;
+mck::RunOptions toOptions(const mck_run_opts* opts) {
   mck::RunOptions ro;
   if (opts) {
     ro.stepLimit = opts->step_limit ? opts->step_limit : ro.stepLimit;
@@ -50,6 +55,14 @@ extern "C" int mck_run_source(const char* src, const char* filename, const mck_r
       ro.allgatherCtx = opts->allgather_ctx;
     }
   }
+  return ro;
+}
+
+}  // namespace
+
+extern "C" int mck_run_source(const char* src, const char* filename, const mck_run_opts* opts, char** json) {
+  if (!src || !filename || !json) return MCKG_E_ARG;
+  const mck::RunOptions ro = toOptions(opts);
   std::string o;
   try {
     auto prog = mck::compileSource(src, filename);
@@ -124,3 +137,107 @@ extern "C" int mckg_comm_id(uint8_t out[128]) {
   std::memcpy(out, id.data(), 128);
   return MCKG_OK;
 }
+
+// ---- result records ----
+struct mck_result {
+  mck::RunResult run;
+  std::string frontendStage, frontendMessage;
+  int frontendLine = 0;
+  std::string reportText;
+  std::vector<std::vector<int32_t>> waiting, missing;
+};
+
+extern "C" int mck_run(const char* src, const char* filename, const mck_run_opts* opts, mck_result** out) {
+  if (!src || !filename || !out) return MCKG_E_ARG;
+  *out = nullptr;
+  auto r = std::make_unique<mck_result>();
+  try {
+    auto prog = mck::compileSource(src, filename);
+    mck::Machine m(prog, toOptions(opts));
+    r->run = m.run();
+  } catch (const mck::FrontendError& e) {
+    r->frontendStage = e.stage;
+    r->frontendMessage = e.message;
+    r->frontendLine = e.loc.line;
+    r->run.exitCode = 2;
+  } catch (const std::exception& e) {
+    mckg::set_error((std::string("mck_run: ") + e.what()).c_str(), cudaSuccess);
+    return MCKG_E_CUDA;
+  }
+  r->reportText = mck::formatStuckReports(r->run.stuckReports);
+  for (const auto& sr : r->run.stuckReports) {
+    r->waiting.emplace_back(sr.waitingTids.begin(), sr.waitingTids.end());
+    r->missing.emplace_back(sr.missingTids.begin(), sr.missingTids.end());
+  }
+  *out = r.release();
+  return MCKG_OK;
+}
+
+extern "C" int mck_result_summary(const mck_result* r, mck_summary* out) {
+  if (!r || !out) return MCKG_E_ARG;
+  const mck::RunResult& x = r->run;
+  *out = mck_summary{};
+  out->exit_code = x.exitCode;
+  out->stuck = x.stuck ? 1 : 0;
+  out->has_main_return = x.mainReturn ? 1 : 0;
+  out->main_return = x.mainReturn ? *x.mainReturn : 0;
+  out->frontend_line = r->frontendLine;
+  out->steps = x.steps;
+  out->n_diags = x.diagnostics.size();
+  out->n_stuck = x.stuckReports.size();
+  out->n_reported = x.reported.size();
+  out->n_trace = x.trace.size();
+  out->output_bytes = x.output.size();
+  out->output = x.output.c_str();
+  out->engine_error = x.engineError.c_str();
+  out->frontend_stage = r->frontendStage.c_str();
+  out->frontend_message = r->frontendMessage.c_str();
+  out->report_text = r->reportText.c_str();
+  return MCKG_OK;
+}
+
+extern "C" int mck_result_diag(const mck_result* r, uint64_t i, mck_diag_rec* out) {
+  if (!r || !out || i >= r->run.diagnostics.size()) return MCKG_E_ARG;
+  const mck::Diagnostic& d = r->run.diagnostics[i];
+  out->category = static_cast<int32_t>(d.category);
+  out->severity = d.severity == mck::Severity::Error ? 0 : 1;
+  out->line = d.loc.line;
+  out->pad = 0;
+  out->sweep = d.sweep;
+  out->message = d.message.c_str();
+  return MCKG_OK;
+}
+
+extern "C" int mck_result_stuck(const mck_result* r, uint64_t i, mck_stuck_rec* out) {
+  if (!r || !out || i >= r->run.stuckReports.size()) return MCKG_E_ARG;
+  const mck::StuckReport& s = r->run.stuckReports[i];
+  out->kind = static_cast<int32_t>(s.kind);
+  out->gid = s.gid;
+  out->bid = s.bid;
+  out->sid = s.sid;
+  out->n_waiting = r->waiting[i].size();
+  out->n_missing = r->missing[i].size();
+  out->waiting = r->waiting[i].data();
+  out->missing = r->missing[i].data();
+  out->reason = s.reason.c_str();
+  out->item = s.item.c_str();
+  return MCKG_OK;
+}
+
+extern "C" int mck_result_reported(const mck_result* r, uint64_t first, uint64_t count, mckg_race_triple* out) {
+  if (!r || (!out && count)) return MCKG_E_ARG;
+  const auto& rep = r->run.reported;
+  if (first > rep.size() || count > rep.size() - first) return MCKG_E_RANGE;
+  for (uint64_t k = 0; k < count; ++k) {
+    const mck::RaceTriple& t = rep[first + k];
+    out[k] = mckg_race_triple{t.object, static_cast<uint32_t>(t.byte), t.line};
+  }
+  return MCKG_OK;
+}
+
+extern "C" const char* mck_result_trace(const mck_result* r, uint64_t i) {
+  if (!r || i >= r->run.trace.size()) return nullptr;
+  return r->run.trace[i].c_str();
+}
+
+extern "C" void mck_result_free(mck_result* r) { delete r; }

@@ -80,6 +80,7 @@ struct GridResult {
   double ms = 0;
   uint32_t launches = 0;
   std::string error;            // engine limitation hit: run abandoned
+  bool stepLimitHit = false;    // the grid ran out of the run's step budget
   // trace mode: per block, completed barrier episodes, and the local arrival
   // sweep + 1 of every thread in its first TRACE_EPISODES episodes (0 = none)
   std::vector<uint32_t> episodes;   // [gridDim]

@@ -1374,6 +1374,12 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
       traceLine(rec.endSweep, 1, (static_cast<uint64_t>(g.gid) << 32) | 0xFFFFFFFFu, 0,
                 "grid gid=" + std::to_string(g.gid) + " completed");
   }
+  // the grid's device steps and barrier rules count toward the step limit
+  // from its dispatch on: the run's total only grows, so a total that reaches
+  // the limit here reaches it in the reference too (machine.cpp:1184)
+  steps_ += rec.res.deviceSteps + rec.res.barrierRules;
+  stats_.deviceSteps += rec.res.deviceSteps;
+  stats_.barrierRules += rec.res.barrierRules;
   ++stats_.grids;
   stats_.gridMs += rec.res.ms;
   stats_.kernelLaunches += rec.res.launches;
@@ -1630,12 +1636,11 @@ mck::RunResult HostMachine::run() {
     if (hitLimit) break;
     ++sweep_;
   }
-  // device steps and barrier rules of every grid
-  for (auto& [gid, g] : grids_) {
-    steps_ += g.res.deviceSteps + g.res.barrierRules;
-    stats_.deviceSteps += g.res.deviceSteps;
-    stats_.barrierRules += g.res.barrierRules;
-  }
+  // Machine::run checks the limit before every transition, including after
+  // the last one (machine.cpp:1183-1191): a run whose total reaches the limit
+  // is abandoned with exactly stepLimit steps
+  if (engineError_.empty() && steps_ >= o_.stepLimit) hitLimit = true;
+  if (hitLimit) steps_ = o_.stepLimit;
   stats_.sweeps = sweep_;
 
   mck::RunResult r;

@@ -1,10 +1,10 @@
-"""K2 (mckg_detect_shared) parity against the CPU oracle: bit-exact reported
+"""K2 (mckg_detect_shared) parity against the reference: bit-exact reported
 triples (RaceState::reported, machine.hpp:91), bit-exact first-detection
 timestamps per line (the Race diagnostic order, machine.cpp:41-46).
 
 Every test runs on both K2 paths: the default two-kernel path (filter ->
 per-block candidate lists -> exact_kernel, with the fused kernel redoing a
-launch whose lists overflow) and the fused kernel alone (MCKG_DEBUG=32)."""
+launch whose lists overflow) and the fused kernel alone (mckg_set_debug(32))."""
 import numpy as np
 import pytest
 
@@ -15,12 +15,12 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True, params=["two_kernel", "fused"])
-def k2_path(request, monkeypatch):
-    if request.param == "fused":
-        monkeypatch.setenv("MCKG_DEBUG", "32")
-    else:
-        monkeypatch.delenv("MCKG_DEBUG", raising=False)
-    return request.param
+def k2_path(request):
+    from paper_1211_6193_b200 import _abi
+    lib = _abi.load()
+    lib.mckg_set_debug(32 if request.param == "fused" else 0)
+    yield request.param
+    lib.mckg_set_debug(0)
 
 
 def _gpu(ev, bs, shmem, capacity=None, obj_base=1, bid_base=0):
@@ -35,10 +35,17 @@ def _gpu(ev, bs, shmem, capacity=None, obj_base=1, bid_base=0):
                               capacity=capacity)
 
 
+def _oracle(trace, nthreads=1, capacity=None):
+    """The reference's own recordAccess/clearEpoch replay (oracle/_ref, built
+    here and shipped to the GPU box); the C restatement only where it is absent."""
+    if ob.ref() is not None:
+        return ob.ref_detect(trace, nthreads=nthreads, capacity=capacity)
+    return ob.port_detect(trace, nthreads=nthreads, capacity=capacity)
+
+
 def _check(ev, bs, shmem, obj_base=1, bid_base=0):
     res = _gpu(ev, bs, shmem, obj_base=obj_base, bid_base=bid_base)
-    rc, tri, n, lf = ob.port_detect(ob.make_trace(ev, bs, shmem, obj_base=obj_base,
-                                                  bid_base=bid_base))
+    rc, tri, n, lf = _oracle(ob.make_trace(ev, bs, shmem, obj_base=obj_base, bid_base=bid_base))
     assert rc == 0
     assert res.status == 0
     assert res.n_triples == n
@@ -114,7 +121,7 @@ def test_empty_and_zero_event_blocks():
 def test_overflow_reports_full_count():
     ev, bs = ob.gen_c3(0, 16)
     res = _gpu(ev, bs, ob.C3_SHMEM, capacity=10)
-    _, _, n, _ = ob.port_detect(ob.make_trace(ev, bs, ob.C3_SHMEM))
+    _, _, n, _ = _oracle(ob.make_trace(ev, bs, ob.C3_SHMEM))
     assert res.status & 1 and res.n_triples == n and len(res.triples) == 10
 
 
@@ -143,9 +150,36 @@ def test_c3_16m_events_matches_oracle():
     ev, bs = race.gen_c3(0, nb)
     res = race.detect_shared(ev, bs, ob.C3_SHMEM)
     hev, hbs = ob.gen_c3(0, nb)
-    rc, tri, n, lf = ob.port_detect(ob.make_trace(hev, hbs, ob.C3_SHMEM), nthreads=8)
+    rc, tri, n, lf = _oracle(ob.make_trace(hev, hbs, ob.C3_SHMEM), nthreads=8)
     assert res.n_triples == n
     assert np.array_equal(res.triples, ob.sorted_triples(tri))
     assert np.array_equal(res.line_first, lf)
     del ev, bs
     torch.cuda.empty_cache()
+
+
+def test_reference_present_on_gpu_box():
+    """oracle/_ref travels with the snapshot: parity here is against the reference."""
+    assert ob.ref() is not None
+
+
+def test_c3_full_size_matches_reference(k2_path):
+    """The headline workload at full size: 2^30 events, 2^20 blocks, every
+    reported triple and every line's first-detection timestamp compared with
+    the reference replay (chunked over all host cores, tests/c3_parity.py)."""
+    if k2_path == "fused":
+        pytest.skip("full size runs once, on the default path")
+    import os
+    import torch
+    import c3_parity
+    from paper_1211_6193_b200 import race
+    nb = 1 << 20
+    ev, bs = race.gen_c3(0, nb)
+    res = race.detect_shared(ev, bs, ob.C3_SHMEM, capacity=nb * 64, max_block_events=1024)
+    del ev, bs
+    torch.cuda.empty_cache()
+    assert res.status == 0
+    got = c3_parity.replay_full(res.triples, res.line_first, nb, len(os.sched_getaffinity(0)))
+    assert got["triples_equal"], got["mismatch"]
+    assert got["line_first_equal"]
+    assert got["reference_triples"] == res.n_triples == 31773232

@@ -52,3 +52,22 @@ def test_launch_without_gpu_fails_loudly():
     src = "__global__ void k(void) { }\nint main(void) { k<<<1, 1>>>(); cudaDeviceSynchronize(); return 0; }\n"
     r = _run(src, "k.cu")
     assert "no CUDA device" in r["engine_error"] or r["engine_error"]
+
+
+@pytest.mark.parametrize("name", sorted(CASES)[::20] + ["fe_" + n for n in sorted(FRONTEND_CASES)[:4]])
+def test_result_record_abi_matches_json_abi(name):
+    """mck_run / mck_result_* (records) return the same RunResult as mck_run_source (JSON)."""
+    from paper_1211_6193_b200 import checker
+    if name.startswith("fe_"):
+        src, fname = FRONTEND_CASES[name[3:]], name[3:] + ".cu"
+    else:
+        fname, src = CASES[name]
+    a = checker.run_source(src, filename=fname, step_limit=HOST_STEP_LIMIT)
+    b = checker.run(src, filename=fname, step_limit=HOST_STEP_LIMIT)
+    if "frontend_error" in a:
+        assert b == {k: a[k] for k in ("frontend_error", "line", "exit")}
+        return
+    b["reported"] = [[int(t["obj"]), int(t["byte"]), int(t["line"])] for t in b["reported"]]
+    for k in ("exit", "output", "steps", "stuck", "main_return", "engine_error", "diags", "stuck_reports",
+              "report_text", "reported", "trace"):
+        assert a[k] == b[k], k

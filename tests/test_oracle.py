@@ -99,3 +99,22 @@ def test_trace_golden_is_the_reference():
     for n in sorted(gold)[:10]:
         f, s = progs[n]
         assert ob.ref_run(s, f, capture=False, trace=True)["trace"] == gold[n]
+
+
+def test_c3_chunked_replay_matches_whole_run():
+    """tests/c3_parity.py (the full-size GPU parity leg) on a CPU-sized trace:
+    the chunked reference replay reproduces a whole-trace detection."""
+    import c3_parity
+    nb = 3000
+    ev, bs = ob.gen_c3(0, nb)
+    rc, tri, n, lf = ob.port_detect(ob.make_trace(ev, bs, ob.C3_SHMEM), nthreads=4)
+    assert rc == 0 and n > 0
+    got = c3_parity.replay_full(ob.sorted_triples(tri), lf, nb, 4, chunk_blocks=1024)
+    assert got["triples_equal"] and got["line_first_equal"], got
+    assert got["reference_triples"] == n
+    bad = ob.sorted_triples(tri).copy()
+    bad["line"][len(bad) // 2] += 1
+    got = c3_parity.replay_full(bad, lf, nb, 4, chunk_blocks=1024)
+    assert not got["triples_equal"]
+    part = c3_parity.replay_full(ob.sorted_triples(tri), lf, nb, 4, chunk_blocks=1024, max_blocks=1500)
+    assert part["triples_equal"] and part["line_first_equal"] is None and part["checked_blocks"] == 1500
