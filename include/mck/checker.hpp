@@ -2,9 +2,12 @@
 // with the reference's proj/include/minicudak headers for the program-load /
 // launch-configuration / check / report path:
 //
-//   compileSource(src, file)        program.hpp:59-60  (throws FrontendError)
+//   compileSource(src, file)        program.hpp:59-60  (throws LexError /
+//                                   ParseError / SemanticError)
 //   RunOptions / ArchParams         machine.hpp:300-316
 //   Machine(prog, opts).run()       machine.hpp:357-375
+//   scanStuck, hooks                machine.hpp:378, 384-388
+//   recordAccess / clearEpoch       machine.hpp:407-409 (batched on the K2 kernel)
 //   RunResult / StuckReport         machine.hpp:318-338
 //   Diagnostic / DiagCategory       diagnostics.hpp:10-31
 //   formatStuckReports              machine.hpp:449
@@ -16,6 +19,7 @@
 // code: a launch without a CUDA device is an error.
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <string>
@@ -52,6 +56,92 @@ struct FrontendError {
   std::string message;
 };
 
+// The typed frontend failures compileSource throws (diagnostics.hpp:41-56).
+struct LexError : FrontendError {
+  LexError(SourceLoc l, std::string m) : FrontendError{"lex", l, std::move(m)} {}
+};
+
+struct ParseError : FrontendError {
+  ParseError(SourceLoc l, std::string expected, std::string found)
+      : FrontendError{"parse", l, "expected " + expected + ", found " + found},
+        expected(std::move(expected)),
+        found(std::move(found)) {}
+  std::string expected;
+  std::string found;
+};
+
+struct SemanticError : FrontendError {
+  SemanticError(SourceLoc l, std::string m) : FrontendError{"semantic", l, std::move(m)} {}
+};
+
+// ----- identities and memory (machine.hpp:19-75, value.hpp:10-20) -----
+using ObjectId = uint32_t;
+using GridId = uint32_t;
+using StreamId = uint32_t;
+using EventId = uint32_t;
+
+struct ThreadKey {
+  GridId gid = 0;  // 0 = host
+  int bid = 0;
+  int tid = 0;
+  bool isHost() const { return gid == 0; }
+  bool operator==(const ThreadKey& o) const { return gid == o.gid && bid == o.bid && tid == o.tid; }
+  bool operator!=(const ThreadKey& o) const { return !(*this == o); }
+  bool operator<(const ThreadKey& o) const {
+    if (gid != o.gid) return gid < o.gid;
+    if (bid != o.bid) return bid < o.bid;
+    return tid < o.tid;
+  }
+};
+
+enum class AccessKind { Read, Write };
+enum class SpaceKind { Host, DeviceGlobal, DeviceShared, Local };
+
+struct MemSpace {
+  SpaceKind kind = SpaceKind::Host;
+  GridId gid = 0;  // DeviceShared only
+  int bid = 0;
+  static MemSpace host() { return {SpaceKind::Host, 0, 0}; }
+  static MemSpace deviceGlobal() { return {SpaceKind::DeviceGlobal, 0, 0}; }
+  static MemSpace deviceShared(GridId g, int b) { return {SpaceKind::DeviceShared, g, b}; }
+  bool operator==(const MemSpace& o) const { return kind == o.kind && gid == o.gid && bid == o.bid; }
+};
+
+struct Location {
+  ObjectId object = 0;
+  int64_t offset = 0;
+};
+
+// The part of MemObject (machine.hpp:39-55) the race checker reads.
+struct MemObject {
+  ObjectId id = 0;
+  MemSpace space;
+  int64_t size = 0;
+  std::string name;
+  bool live = true;
+};
+
+// Runtime-API ids (program.hpp:14-37), the onApiCall argument.
+enum class ApiId {
+  Malloc, Free, Memcpy, MemcpyAsync, Memset, DeviceSynchronize, StreamCreate, StreamDestroy,
+  StreamSynchronize, StreamQuery, StreamWaitEvent, EventCreate, EventDestroy, EventRecord,
+  EventSynchronize, EventQuery, EventElapsedTime, GetLastError, GetErrorString, DeviceGetAttribute,
+  DriverGetVersion, RuntimeGetVersion,
+};
+const char* apiName(ApiId id);
+
+// Observer record of the memory-access hook (machine.hpp:340-350).
+struct MemAccessInfo {
+  ThreadKey accessor;
+  AccessKind kind = AccessKind::Read;
+  ObjectId object = 0;
+  MemSpace space;
+  int64_t offset = 0;
+  int64_t len = 0;
+  bool allowed = true;
+  SourceLoc loc;
+};
+
 // The lowered program (opaque; shared, immutable).
 using Program = mckb::Program;
 std::shared_ptr<const Program> compileSource(const std::string& source, const std::string& filename);
@@ -69,7 +159,8 @@ struct ArchParams {
 
 struct RunOptions {
   // The device engine reproduces the round-robin schedule exactly
-  // (SURVEY F2/F4); SeededRandom is accepted and run as round-robin.
+  // (SURVEY F2/F4).  SeededRandom with a nonzero seed (and Exhaustive) run
+  // as round-robin and say so in RunResult::engineNote.
   SchedulePolicy policy = SchedulePolicy::SeededRandom;
   uint64_t seed = 0;
   bool raceCheck = true;
@@ -138,6 +229,7 @@ struct RunResult {
   std::vector<RaceTriple> reported;  // RaceState::reported, std::set order
   EngineStats stats;
   std::string engineError;           // non-empty: the run was abandoned by the engine
+  std::string engineNote;            // non-empty: how the run departs from the requested options
   std::vector<std::string> trace;    // RunOptions::trace: the Machine::trace lines, in order
 };
 
@@ -149,8 +241,54 @@ class Machine {
   ~Machine();
   Machine(const Machine&) = delete;
   Machine& operator=(const Machine&) = delete;
-  RunResult run();
+
+  const Program& program() const { return *prog_; }
   const RunOptions& options() const { return opts_; }
+
+  // Runs to completion (or stuck / step limit) and computes the exit code
+  // (machine.cpp:1180-1227).  Device grids run on the B200 at dispatch.
+  RunResult run();
+
+  // Stuck-state classification of the final (frozen) configuration of the
+  // last run() (deadlock.cpp:12-71): empty before run() and after a run
+  // that terminated normally.
+  std::vector<StuckReport> scanStuck() const;
+
+  // Hooks, called synchronously on the calling thread (machine.hpp:384-388):
+  //  * onOutput: every printf of the host thread, as it happens;
+  //  * onApiCall: every runtime-API call of the host thread with its result
+  //    code (blocking calls report success when they block, as the reference);
+  //  * onMemAccess: every host-thread memory access.  Device accesses happen
+  //    inside the B200 grid kernel and are not observable one by one: a grid
+  //    launched while onMemAccess is set abandons the run with an engine
+  //    error instead of silently skipping them;
+  //  * onTrace: the --trace lines (RunOptions::trace), in the reference's
+  //    order, once the run's timeline is complete.
+  std::function<void(const MemAccessInfo&)> onMemAccess;
+  std::function<void(ApiId, int)> onApiCall;
+  std::function<void(const std::string&)> onTrace;
+  std::function<void(const std::string&)> onOutput;
+
+  // ---- the race checker as a library (racecheck.cpp:9-73), batched on K2 ----
+  // allocObject mints an object id from the machine's counter (memory.cpp:
+  // 12-31); object() returns the checker's view of it.
+  Location allocObject(MemSpace space, int64_t size, const std::string& name);
+  const MemObject& object(ObjectId id) const;
+  // recordAccess / clearEpoch keep the reference's signatures.  Accesses are
+  // buffered per shared object (in call order) and checked by the K2 kernel
+  // on the GPU when flushRaces() (or raceReport()) runs; the reported set and
+  // the Race diagnostics (first-detection order, addDiagnostic dedup) are
+  // exactly the reference's, only deferred to the flush.  Accesses to
+  // non-shared objects are ignored, as the reference only checks
+  // DeviceShared memory (memory.cpp:142-143, 240-241).
+  void recordAccess(const MemObject& obj, int64_t off, int64_t len, ThreadKey thread, AccessKind kind,
+                    SourceLoc loc);
+  void clearEpoch(GridId gid, int bid);
+  void flushRaces();
+  // RaceState::reported (std::set order) and the Race diagnostics so far
+  // (flushes first).
+  const std::vector<RaceTriple>& raceReport();
+  const std::vector<Diagnostic>& raceDiagnostics();
 
  private:
   std::shared_ptr<const Program> prog_;

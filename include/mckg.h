@@ -62,7 +62,7 @@ extern "C" {
 #define MCKG_MAX_TID (1u << 11)   /* blockDim <= 2048 (reference default 1024)    */
 #define MCKG_MAX_EPOCH (1u << 21) /* barrier episodes per thread                  */
 #define MCKG_MAX_LINES 65536u     /* source lines 0..65535 (line-first table)     */
-#define MCKG_MAX_BID (1u << 22)   /* global block index inside a timestamp key    */
+#define MCKG_MAX_BID (1u << 21)   /* global block index inside a timestamp key    */
 
 /*
  * One shared-memory access event, exactly what Machine::recordAccess receives
@@ -108,7 +108,7 @@ static inline mckg_access mckg_make_access(uint32_t off, uint32_t len, int write
 /* Timestamp key of an access: (sweep, bid, tid) packed so that unsigned
  * comparison is the reference's first-detection order within one grid. */
 static inline uint64_t mckg_ts_key(uint32_t sweep, uint32_t bid, uint32_t tid) {
-  return ((uint64_t)sweep << 32) | ((uint64_t)(bid & (MCKG_MAX_BID - 1)) << 10) | (tid & 0x3FFu);
+  return ((uint64_t)sweep << 32) | ((uint64_t)(bid & (MCKG_MAX_BID - 1)) << 11) | (tid & (MCKG_MAX_TID - 1));
 }
 #define MCKG_TS_NONE UINT64_MAX
 
@@ -264,7 +264,8 @@ static inline mckg_gaccess mckg_make_gaccess(uint64_t addr, uint32_t len, int wr
   return g;
 }
 
-/* Timestamp key of a global access: sweep:32 | bid:22 | tid:10 (as mckg_ts_key). */
+/* Timestamp key of a global access: sweep:32 | bid:21 | tid:11 (as mckg_ts_key);
+ * a global trace's bids must stay below MCKG_MAX_BID. */
 
 /* One reported (byte address, line) pair. */
 typedef struct mckg_grace {

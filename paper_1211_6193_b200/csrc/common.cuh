@@ -34,7 +34,7 @@ __device__ __forceinline__ uint32_t acc_epoch(uint32_t w1) { return w1 >> 11; }
 
 __device__ __forceinline__ unsigned long long ts_key(uint32_t sweep, uint32_t bid, uint32_t tid) {
   return ((unsigned long long)sweep << 32) |
-         ((unsigned long long)(bid & (MCKG_MAX_BID - 1)) << 10) | (tid & 0x3FFu);
+         ((unsigned long long)(bid & (MCKG_MAX_BID - 1)) << 11) | (tid & (MCKG_MAX_TID - 1));
 }
 
 // ---- mbarrier + 1-D bulk copy (TMA engine, cp.async.bulk) ----

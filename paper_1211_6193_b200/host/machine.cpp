@@ -25,11 +25,13 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <set>
 #include <stdexcept>
 
 #include "engine.hpp"
+#include "machine_impl.hpp"
 #include "mck/checker.hpp"
 
 namespace mckb {
@@ -131,15 +133,24 @@ enum class WaitKind { None, Device, Stream, Event };
 
 }  // namespace
 
+// The mck::Machine hooks the host interpreter calls (machine.hpp:384-388).
+struct HostHooks {
+  std::function<void(const mck::MemAccessInfo&)> mem;
+  std::function<void(mck::ApiId, int)> api;
+  std::function<void(const std::string&)> out;
+};
+
 class HostMachine {
  public:
-  HostMachine(std::shared_ptr<const Program> prog, const mck::RunOptions& o) : P_(std::move(prog)), o_(o) {}
+  HostMachine(std::shared_ptr<const Program> prog, const mck::RunOptions& o, HostHooks hooks = {})
+      : P_(std::move(prog)), o_(o), hooks_(std::move(hooks)) {}
 
   mck::RunResult run();
 
  private:
   std::shared_ptr<const Program> P_;
   mck::RunOptions o_;
+  HostHooks hooks_;
   std::unique_ptr<DeviceEngine> eng_;
   std::string engWhy_;
 
@@ -262,13 +273,28 @@ class HostMachine {
   std::string spaceStr(uint8_t space) const { return space == SP_HOST ? "host" : "device-global"; }
 
   // readMem for the host thread (memory.cpp:110-182); nullopt => halt
+  void memHook(mck::AccessKind k, uint32_t obj, const HObj* o, int64_t off, int64_t len, int line) {
+    if (!hooks_.mem) return;
+    mck::MemAccessInfo m;
+    m.kind = k;
+    m.object = obj;
+    if (o) m.space = o->space == SP_HOST ? mck::MemSpace::host() : mck::MemSpace::deviceGlobal();
+    m.offset = off;
+    m.len = len;
+    m.allowed = o && o->space == SP_HOST;  // checkAccess for the host thread (memory.cpp:64-69)
+    m.loc.line = line;
+    hooks_.mem(m);
+  }
+
   std::optional<Val> readMem(uint32_t obj, int64_t off, uint8_t t, int line) {
     HObj* o = find(obj);
     if (!o) {
       ub("read through a null or invalid pointer", line);
+      memHook(mck::AccessKind::Read, obj, nullptr, off, t_scalar(t), line);
       return std::nullopt;
     }
     int64_t len = t_scalar(t);
+    memHook(mck::AccessKind::Read, obj, o, off, len, line);
     if (o->space != SP_HOST) {
       diag(mck::Severity::Error, mck::DiagCategory::MemBoundary,
            "Illegal device or host memory access: host code read of " + spaceStr(o->space) + " memory" + at(line),
@@ -310,9 +336,11 @@ class HostMachine {
     HObj* o = find(obj);
     if (!o) {
       ub("write through a null or invalid pointer", line);
+      memHook(mck::AccessKind::Write, obj, nullptr, off, t_scalar(t), line);
       return false;
     }
     int64_t len = t_scalar(t);
+    memHook(mck::AccessKind::Write, obj, o, off, len, line);
     if (o->space != SP_HOST) {
       diag(mck::Severity::Error, mck::DiagCategory::MemBoundary,
            "Illegal device or host memory access: host code write of " + spaceStr(o->space) + " memory" + at(line),
@@ -993,6 +1021,7 @@ void HostMachine::execPrintf(const mck_ins& in) {
   }
   if (ai != args.size()) return fail("printf has more arguments than conversions");
   output_ += out;
+  if (hooks_.out) hooks_.out(out);
   vals_.push_back(v_int(static_cast<int64_t>(out.size())));
 }
 
@@ -1009,8 +1038,10 @@ void HostMachine::invokeApi(const mck_ins& in) {
                                 "cudaGetLastError", "cudaGetErrorString", "cudaDeviceGetAttribute",
                                 "cudaDriverGetVersion", "cudaRuntimeGetVersion"};
   constexpr int kOK = 0, kInval = 11, kDevPtr = 17, kDir = 21, kHandle = 33, kNotReady = 34;
+  const mck::ApiId api = static_cast<mck::ApiId>(in.a);
   auto finish = [&](int code) {
     if (code != kOK && code != kNotReady) lastApiError_ = code;
+    if (hooks_.api) hooks_.api(api, code);
     vals_.push_back(v_int(code));
   };
   auto err = [&](int code, const std::string& m) {
@@ -1022,6 +1053,7 @@ void HostMachine::invokeApi(const mck_ins& in) {
     waitId_ = id;
     awaiting_ = true;
     awaitCode_ = kOK;
+    if (hooks_.api) hooks_.api(api, kOK);
   };
   auto outWrite = [&](const Val& dst, uint8_t t, const Val& v) -> bool {
     if (dst.kind != MCK_K_PTR || dst.obj == 0) return false;
@@ -1238,10 +1270,12 @@ void HostMachine::invokeApi(const mck_ins& in) {
     case MCK_API_GET_LAST_ERROR: {
       int c = lastApiError_;
       lastApiError_ = kOK;
+      if (hooks_.api) hooks_.api(api, c);
       vals_.push_back(v_int(c));
       break;
     }
     case MCK_API_GET_ERROR_STRING: {
+      if (hooks_.api) hooks_.api(api, kOK);
       const char* s;
       switch (static_cast<int>(args[0].i)) {
         case 0: s = "no error"; break;
@@ -1356,7 +1390,10 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   rec.gridDim = l.grid;
   rec.blockDim = l.block;
   rec.sharedBase = g.sharedBase;
-  if (!eng_->hasDevice() || !eng_->runGrid(g, rec.res)) {
+  if (hooks_.mem) {
+    engineError_ = "onMemAccess is set: device accesses run inside the B200 grid kernel and cannot be "
+                   "reported one by one";
+  } else if (!eng_->hasDevice() || !eng_->runGrid(g, rec.res)) {
     engineError_ = rec.res.error.empty() ? engWhy_ : rec.res.error;
     if (engineError_.empty()) engineError_ = "grid engine failed";
   }
@@ -1718,11 +1755,6 @@ mck::RunResult HostMachine::run() {
 // ======================= public API =======================
 namespace mck {
 
-class MachineImpl {
- public:
-  std::unique_ptr<mckb::HostMachine> m;
-};
-
 const char* categoryName(DiagCategory c) {
   switch (c) {
     case DiagCategory::Race: return "race";
@@ -1734,11 +1766,35 @@ const char* categoryName(DiagCategory c) {
   return "?";
 }
 
+const char* apiName(ApiId id) {
+  static const char* names[] = {"cudaMalloc", "cudaFree", "cudaMemcpy", "cudaMemcpyAsync", "cudaMemset",
+                                "cudaDeviceSynchronize", "cudaStreamCreate", "cudaStreamDestroy",
+                                "cudaStreamSynchronize", "cudaStreamQuery", "cudaStreamWaitEvent",
+                                "cudaEventCreate", "cudaEventDestroy", "cudaEventRecord",
+                                "cudaEventSynchronize", "cudaEventQuery", "cudaEventElapsedTime",
+                                "cudaGetLastError", "cudaGetErrorString", "cudaDeviceGetAttribute",
+                                "cudaDriverGetVersion", "cudaRuntimeGetVersion"};
+  const auto i = static_cast<size_t>(id);
+  return i < sizeof names / sizeof names[0] ? names[i] : "?";
+}
+
+// compileSource (program.hpp:59-60): frontend failures surface as the
+// reference's typed exceptions (diagnostics.hpp:41-56).
 std::shared_ptr<const Program> compileSource(const std::string& source, const std::string& filename) {
   try {
     return mckb::compileProgram(source, filename);
   } catch (const mckb::FrontendFailure& f) {
-    throw FrontendError{f.stage, SourceLoc{f.pos.line, f.pos.col}, f.message};
+    const SourceLoc loc{f.pos.line, f.pos.col};
+    if (f.stage == "lex") throw LexError(loc, f.message);
+    if (f.stage == "parse") {
+      // "expected <what>, found <tok>" (parser.cpp's ParseError text)
+      const std::string& m = f.message;
+      const size_t k = m.rfind(", found ");
+      if (m.rfind("expected ", 0) == 0 && k != std::string::npos)
+        throw ParseError(loc, m.substr(9, k - 9), m.substr(k + 8));
+      throw ParseError(loc, m, "");
+    }
+    throw SemanticError(loc, f.message);
   }
 }
 
@@ -1747,8 +1803,28 @@ Machine::Machine(std::shared_ptr<const Program> prog, RunOptions opts)
 Machine::~Machine() = default;
 
 RunResult Machine::run() {
-  impl_->m.reset(new mckb::HostMachine(prog_, opts_));
-  return impl_->m->run();
+  mckb::HostHooks h;
+  h.mem = onMemAccess;
+  h.api = onApiCall;
+  h.out = onOutput;
+  impl_->m.reset(new mckb::HostMachine(prog_, opts_, std::move(h)));
+  RunResult r = impl_->m->run();
+  if (opts_.policy == SchedulePolicy::SeededRandom && opts_.seed != 0)
+    r.engineNote = "SchedulePolicy::SeededRandom (seed " + std::to_string(opts_.seed) +
+                   ") was run under the round-robin schedule: the B200 engine executes the round-robin "
+                   "interleaving only (it equals the seed-0 run on the BASELINE program families)";
+  if (opts_.policy == SchedulePolicy::Exhaustive)
+    r.engineNote = "SchedulePolicy::Exhaustive was run under the round-robin schedule (the interleaving "
+                   "explorer is oracleRace)";
+  if (onTrace)
+    for (const std::string& t : r.trace) onTrace(t);
+  impl_->last = r;
+  impl_->ran = true;
+  return r;
+}
+
+std::vector<StuckReport> Machine::scanStuck() const {
+  return impl_->ran && impl_->last.stuck ? impl_->last.stuckReports : std::vector<StuckReport>{};
 }
 
 std::vector<uint8_t> makeCommId() {

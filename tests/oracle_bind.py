@@ -48,7 +48,7 @@ def make_access(off, length, write, tid, epoch, line, sweep):
 
 
 def ts_key(sweep, bid, tid):
-    return (int(sweep) << 32) | ((int(bid) & ((1 << 22) - 1)) << 10) | (int(tid) & 0x3FF)
+    return (int(sweep) << 32) | ((int(bid) & ((1 << 21) - 1)) << 11) | (int(tid) & 0x7FF)
 
 
 def _lib(path):
