@@ -929,6 +929,207 @@ __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
   if (lane == 0 && f) atomicOr(P.status, f);
 }
 
+// ---------------- fast_kernel: the default path (one warp per block) ----
+// Every warp streams whole simulated blocks on its own -- no CTA barrier on
+// the per-event path.  A block's 1024 records are read with coalesced
+// 16-byte loads (lane l holds records l, l + 32, ...), validated and packed
+// into one register each, and the word filter of the two-pass design runs in
+// the warp's own shared-memory tag arrays (one per epoch) with __syncwarp
+// between its phases:
+//   P1 tag[w] <- some accessing {tid, write} | P2 tid != tag[w] -> multi
+//   stamp, write -> write stamp | P3 candidate iff both stamps are current.
+// The few candidates (~3 % on C3) go through the exact check: the reference
+// predicate (racecheck.cpp:24-32) on same-word groups found with
+// __match_any_sync, with the block's dedup set and the warp's line-first
+// cache (exact_report).  The fast path takes the shape of trace-mode blocks
+// (C3): exactly FMAX records, aligned 4-byte accesses, at most two epochs,
+// an object of at most FWORDS words.  Any other block -- or one with more
+// than FCMAX candidates -- is appended to the overflow list untouched and
+// redone by the general (fused) kernel, which validates every field.
+constexpr uint32_t FW = 8;         // warps per CTA
+constexpr uint32_t FRPL = 32;      // records per lane
+constexpr uint32_t FMAX = FRPL * 32;
+constexpr uint32_t FWORDS = 1024;  // words per epoch (shared objects <= 4 KiB)
+constexpr uint32_t FCMAX = 128;    // candidates per block
+
+// per-warp dynamic shared memory: tags, dedup set, triple staging, candidates
+constexpr uint32_t FK_TAGS = 0;
+constexpr uint32_t FK_HS = FK_TAGS + 2 * FWORDS * 4;
+constexpr uint32_t FK_TB = FK_HS + XHS * 8;
+constexpr uint32_t FK_CL = FK_TB + XTB * 12;
+constexpr uint32_t FK_WARP_BYTES = (FK_CL + FCMAX * 2 + 127u) & ~127u;
+constexpr uint32_t FK_SMEM = FW * FK_WARP_BYTES;
+
+// Packed record (one register): bits 0..10 tid, 11 write, 14..31 the
+// shared-memory byte address of the word's tag entry {u16 tid | write << 11,
+// u8 multi stamp, u8 write stamp} in its epoch's array, the word index
+// swizzled so that the stride-4-word pattern of per-thread slots (tid * 4 + k)
+// is bank-conflict free.  Bits 0..15 are exactly the u16 P1 stores.
+__device__ __forceinline__ uint32_t fk_addr(uint32_t x) { return x >> 14; }
+
+// Exact check of a block's candidates (the rare path, kept out of line).
+// Aligned 4-byte records overlap iff they name the same word, so X races iff
+// an earlier candidate Y of the same epoch and word, another thread, and X or
+// Y writing exists; all four bytes of X race then.
+__device__ __noinline__ void fk_exact(WarpOut& E, const Params& P, const uint4* src, const uint16_t* cl,
+                                      uint32_t m, uint32_t b, unsigned long long bstamp, unsigned long long* hs,
+                                      mckg_race_triple* tb) {
+  const uint32_t obj = P.obj_base + b, bid = P.bid_base + b;
+  if (m > 32u) {  // crowded block: the general O(m^2) pass
+    exact_warp(E, P, src, cl, m, obj, bid, bstamp, hs, tb);
+    return;
+  }
+  const uint32_t lane = threadIdx.x & 31u;
+  const bool act = lane < m;
+  const uint32_t xi = act ? cl[lane] : 0xFFFFu;
+  const uint4 X = act ? __ldg(src + xi) : make_uint4(0, 0, 0, 0);
+  const uint32_t key = act ? (X.x & 0xFFFFFu) | ((X.y >> 11) << 20) : 0xFFFFFFFFu - lane;
+  uint32_t rest = __match_any_sync(0xFFFFFFFFu, key) & ~(1u << lane);
+  if (!act) rest = 0;
+  bool racing = false;
+  while (__any_sync(0xFFFFFFFFu, rest != 0u)) {
+    const uint32_t y = rest ? (uint32_t)__ffs(rest) - 1u : lane;
+    rest &= rest - 1u;
+    const uint32_t yi = __shfl_sync(0xFFFFFFFFu, xi, y), yx = __shfl_sync(0xFFFFFFFFu, X.x, y),
+                   yy = __shfl_sync(0xFFFFFFFFu, X.y, y);
+    racing |= y != lane && yi < xi && acc_tid(yy) != acc_tid(X.y) && ((X.x | yx) & (1u << 24));
+  }
+  exact_report(E, P, act, X, racing ? 0xFu : 0u, obj, bid, bstamp, hs, tb);
+}
+
+__global__ void __launch_bounds__(FW * 32, 2) fast_kernel(Params P) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  uint8_t* wbase = smem_raw + warp * FK_WARP_BYTES;
+  uint32_t* tags = reinterpret_cast<uint32_t*>(wbase + FK_TAGS);
+  unsigned long long* hs = reinterpret_cast<unsigned long long*>(wbase + FK_HS);
+  mckg_race_triple* tb = reinterpret_cast<mckg_race_triple*>(wbase + FK_TB);
+  uint16_t* cl = reinterpret_cast<uint16_t*>(wbase + FK_CL);
+  for (uint32_t i = lane; i < 2 * FWORDS; i += 32) tags[i] = 0u;
+  for (uint32_t i = lane; i < XHS; i += 32) hs[i] = 0ull;
+  __syncwarp();
+  const uint32_t tagb = smem_u32(tags);
+  WarpOut E{INF, ~0ull, 0u, 0u, 0u};
+  unsigned long long bstamp = 0;
+  uint32_t stamp = 0;
+  const uint32_t nwarps = gridDim.x * FW;
+  const uint32_t shm = P.shmem_bytes;
+  // L2 prefetch of the warp's next block (TMA engine): measured slower
+  // than the plain loads on C3 (4.19 vs 3.99 ms), kept as an experiment
+  const bool prefetch = (P.debug & 8u) != 0u;
+  uint32_t b = blockIdx.x * FW + warp;
+  if (prefetch && lane == 0 && b < P.n_blocks && P.bstart[b + 1] - P.bstart[b] == FMAX)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.ev + P.bstart[b]), "r"(FMAX * 16u) : "memory");
+  for (; b < P.n_blocks; b += nwarps) {
+    const uint64_t s0 = P.bstart[b], s1 = P.bstart[b + 1];
+    // the warp's next block streams into L2 while this one is checked
+    if (prefetch && lane == 0 && b + nwarps < P.n_blocks) {
+      const uint64_t p0 = P.bstart[b + nwarps], p1 = P.bstart[b + nwarps + 1];
+      if (p1 - p0 == FMAX)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.ev + p0), "r"(FMAX * 16u) : "memory");
+    }
+    if (s1 == s0) continue;
+    if (s1 - s0 != FMAX) {
+      if (lane == 0) P.olist[atomicAdd(P.ocount, 1u)] = b;
+      continue;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(P.ev + s0);
+    // ---- load, validate, pack (8 rows in flight ahead of the decode) ----
+    uint32_t pk[FRPL];
+    uint32_t e0 = 0, chk = 0, mo = 0, mz = 0, ms = 0, up = 0;
+    uint4 buf[2][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) buf[0][q] = __ldg(src + q * 32 + lane);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      if (h < 3) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) buf[(h + 1) & 1][q] = __ldg(src + (h + 1) * 256 + q * 32 + lane);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = h * 8 + q;
+        const uint4 r = buf[h & 1][q];
+        const uint32_t ep = acc_epoch(r.y);
+        if (j == 0) e0 = __shfl_sync(0xFFFFFFFFu, ep, 0);
+        const uint32_t slot = ep - e0;
+        const uint32_t off = acc_off(r.x);
+        // aligned 4-byte access (len 4, bits 25..31 clear); the object
+        // bound, the line and the epoch span are checked on per-lane maxima
+        chk |= (r.x & 0xFEF00003u) ^ 0x00400000u;
+        mo = max(mo, off);
+        mz = max(mz, (uint32_t)r.z);
+        ms = max(ms, slot);
+        up |= slot << j;  // bit j: record j * 32 + lane is in the second epoch
+        const uint32_t a = tagb + ((slot << 12) | (off ^ ((off >> 5) & 0x7Cu)));
+        pk[j] = (((r.y & 0x7FFu) | ((r.x >> 13) & 0x800u))) + (a << 14);
+      }
+    }
+    // epochs non-decreasing in record order: every lane's second-epoch rows
+    // form a top segment starting at row f_l with f_l - (T - l)/32 rounding
+    // consistent, i.e. f non-increasing over lanes with f_0 - f_31 <= 1
+    const uint32_t f = up ? (uint32_t)__ffs(up) - 1u : 32u;
+    bool bad = chk != 0u || mo + 4u > shm || mz >= 65536u || ms > 1u || (up != 0u && (up | (up - 1u)) != ~0u);
+    const uint32_t fn = __shfl_down_sync(0xFFFFFFFFu, f, 1);
+    bad |= lane < 31u && fn > f;
+    const uint32_t f0 = __shfl_sync(0xFFFFFFFFu, f, 0), f31 = __shfl_sync(0xFFFFFFFFu, f, 31);
+    bad |= f0 > f31 + 1u;
+    if (__any_sync(0xFFFFFFFFu, bad)) {
+      if (lane == 0) P.olist[atomicAdd(P.ocount, 1u)] = b;
+      continue;
+    }
+    stamp = stamp == 255u ? 1u : stamp + 1u;
+    const uint32_t pat = (stamp | (stamp << 8)) << 16;
+    // P1: the u16 {tid, write} of some accessing record per word
+#pragma unroll
+    for (int j = 0; j < (int)FRPL; ++j)
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(fk_addr(pk[j])), "h"((uint16_t)pk[j]) : "memory");
+    __syncwarp();
+    // P2: words seen by a second thread; written words
+#pragma unroll
+    for (int j = 0; j < (int)FRPL; ++j) {
+      const uint32_t x = pk[j], a = fk_addr(x);
+      uint16_t tg;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(tg) : "r"(a) : "memory");
+      if ((((uint32_t)tg ^ x) & 0x7FFu) != 0u)
+        asm volatile("st.shared.u8 [%0+2], %1;" ::"r"(a), "h"((uint16_t)stamp) : "memory");
+      if (x & 0x800u) asm volatile("st.shared.u8 [%0+3], %1;" ::"r"(a), "h"((uint16_t)stamp) : "memory");
+    }
+    __syncwarp();
+    // P3: candidates -> per-lane row bits
+    uint32_t cm = 0;
+#pragma unroll
+    for (int j = 0; j < (int)FRPL; ++j) {
+      uint32_t v;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(fk_addr(pk[j])) : "memory");
+      cm |= ((v & 0xFFFF0000u) == pat ? 1u : 0u) << j;
+    }
+    // compaction (the list order is free: the exact pass compares indices)
+    const uint32_t c = __popc(cm);
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= (uint32_t)d) incl += t;
+    }
+    const uint32_t m = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (m == 0) continue;
+    if (m > FCMAX) {
+      if (lane == 0) P.olist[atomicAdd(P.ocount, 1u)] = b;
+      continue;
+    }
+    uint32_t pos = incl - c;
+    for (uint32_t g = cm; g; g &= g - 1u) cl[pos++] = (uint16_t)((uint32_t)(__ffs(g) - 1) * 32u + lane);
+    __syncwarp();
+    ++bstamp;
+    fk_exact(E, P, src, cl, m, b, bstamp, hs, tb);
+    __syncwarp();
+  }
+  wo_flush(E, P, tb);
+  if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
+  const uint32_t fl = __reduce_or_sync(0xFFFFFFFFu, E.flags);
+  if (lane == 0 && fl) atomicOr(P.status, fl);
+}
+
 __global__ void reset_kernel(unsigned long long* n_tri, unsigned long long* line_first,
                              uint32_t* status) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -967,6 +1168,35 @@ std::atomic<uint32_t>& debug_word() {
   return w;
 }
 uint32_t debug_flags() { return debug_word().load(std::memory_order_relaxed); }
+
+// The overflow list of the default path (two counters, then up to n_blocks
+// block indices): one buffer per (device, stream, host thread for the
+// special stream handles), grown on demand.
+cudaError_t overflow_list(uint32_t n_blocks, cudaStream_t s, uint32_t** out) {
+  struct Buf {
+    uint32_t* p = nullptr;
+    size_t n = 0;
+  };
+  static std::mutex mu;
+  static std::map<std::tuple<int, cudaStream_t, std::thread::id>, Buf> bufs;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const bool special = s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread;
+  std::lock_guard<std::mutex> lock(mu);
+  Buf& b = bufs[{dev, s, special ? std::this_thread::get_id() : std::thread::id()}];
+  if (b.n < n_blocks || !b.p) {
+    if (b.p) {
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      if ((e = cudaFree(b.p)) != cudaSuccess) return e;
+      b.p = nullptr;
+    }
+    if ((e = cudaMalloc(&b.p, ((size_t)n_blocks + 2) * sizeof(uint32_t))) != cudaSuccess) return e;
+    b.n = n_blocks;
+  }
+  *out = b.p;
+  return cudaSuccess;
+}
 
 // The >48 KB dynamic shared-memory opt-in is a per-device function
 // attribute: remembered per (device, kernel), raised on demand.
@@ -1085,9 +1315,34 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     note_launch(1, grid_f, NT, (uint32_t)smem_f);
     return MCKG_OK;
   }
-  // two-kernel path: filter -> candidate lists -> exact_kernel; the fused
-  // kernel (gated) redoes only the blocks with more than CMAX candidates
   keep_pool_memory();
+  if (!(P.debug & 4u) && tr->shmem_bytes <= FWORDS * 4u) {
+    // default path: fast_kernel (one warp per block); the fused kernel
+    // (gated) redoes the blocks it hands back in the overflow list
+    uint32_t* ol = nullptr;
+    MCKG_CUDA_TRY(overflow_list(tr->n_blocks, s, &ol));
+    P.ocount = ol;
+    P.olist = ol + 2;
+    MCKG_CUDA_TRY(cudaMemsetAsync(P.ocount, 0, 2 * sizeof(uint32_t), s));
+    MCKG_CUDA_TRY(ensure_dynamic_smem(fast_kernel, FK_SMEM));
+    int per = 0;
+    MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fast_kernel, FW * 32, FK_SMEM));
+    if (per < 1) per = 1;
+    uint32_t g = (uint32_t)sm_count() * (uint32_t)per;
+    const uint32_t need = (tr->n_blocks + FW - 1) / FW;
+    if (g > need) g = need;
+    fast_kernel<<<g, FW * 32, FK_SMEM, s>>>(P);
+    MCKG_CUDA_TRY(cudaGetLastError());
+    P.mode = 0;
+    P.gate = 1;
+    kf<<<grid_f, NT, smem_f, s>>>(P);
+    MCKG_CUDA_TRY(cudaGetLastError());
+    note_launch(2, g, FW * 32, FK_SMEM);
+    return MCKG_OK;
+  }
+  // MCKG_DEBUG bit 4: the round-1 two-kernel path (filter -> candidate
+  // bitmaps -> exact_kernel beside it); the fused kernel (gated) redoes the
+  // blocks with more than CMAX candidates
   P.wpb = (uint32_t)(ki == 0 ? 4 : ki == 1 ? 8 : 16) * (NT / 32);  // EPT * warps
   // candidate bitmaps: a buffer per stream that only this path writes,
   // cleared once; words carry the call's tag, so stale words never match
