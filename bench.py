@@ -332,7 +332,7 @@ def run_ours(args):
                        "l2": "inputs (16 GiB) >> L2 (126 MB); no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(),
-                         "kernel": "mckg_detect_shared: race_detect_kernel (filter) + exact_kernel, timed together", "kernel_ms": k_avg,
+                         "kernel": "mckg_detect_shared: fast_kernel (warp per block) + the gated general kernel over its overflow list, timed together", "kernel_ms": k_avg,
                          "peak_source": peak_src,
                          "algorithmic_bytes": "16 B/event + 8 B/block + 12 B/reported triple"},
             "clocks": clocks.summary(),

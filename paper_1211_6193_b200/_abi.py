@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmckg.so")
+# MCKG_LIB: an alternative build of the same library (kernel experiments)
+LIB_PATH = os.environ.get("MCKG_LIB") or os.path.join(_HERE, "libmckg.so")
 
 MCKG_OK = 0
 MCKG_E_ARG = 1

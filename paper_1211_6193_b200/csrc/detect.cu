@@ -940,23 +940,30 @@ __global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
 //   stamp, write -> write stamp | P3 candidate iff both stamps are current.
 // The few candidates (~3 % on C3) go through the exact check: the reference
 // predicate (racecheck.cpp:24-32) on same-word groups found with
-// __match_any_sync, with the block's dedup set and the warp's line-first
-// cache (exact_report).  The fast path takes the shape of trace-mode blocks
+// __match_any_sync, (word, line) dedup by a second match, and the warp's
+// line-first cache.  The fast path takes the shape of trace-mode blocks
 // (C3): exactly FMAX records, aligned 4-byte accesses, at most two epochs,
 // an object of at most FWORDS words.  Any other block -- or one with more
 // than FCMAX candidates -- is appended to the overflow list untouched and
 // redone by the general (fused) kernel, which validates every field.
-constexpr uint32_t FW = 8;         // warps per CTA
+#ifndef MCKG_FK_FW
+#define MCKG_FK_FW 16
+#endif
+#ifndef MCKG_FK_MINB
+#define MCKG_FK_MINB 1
+#endif
+#ifndef MCKG_FK_BR
+#define MCKG_FK_BR 2
+#endif
+constexpr uint32_t FW = MCKG_FK_FW;  // warps per CTA
 constexpr uint32_t FRPL = 32;      // records per lane
 constexpr uint32_t FMAX = FRPL * 32;
 constexpr uint32_t FWORDS = 1024;  // words per epoch (shared objects <= 4 KiB)
-constexpr uint32_t FCMAX = 128;    // candidates per block
+constexpr uint32_t FCMAX = 32;     // candidates per block (one per lane in the exact pass)
 
-// per-warp dynamic shared memory: tags, dedup set, triple staging, candidates
+// per-warp dynamic shared memory: the two epochs' tag arrays, the candidates
 constexpr uint32_t FK_TAGS = 0;
-constexpr uint32_t FK_HS = FK_TAGS + 2 * FWORDS * 4;
-constexpr uint32_t FK_TB = FK_HS + XHS * 8;
-constexpr uint32_t FK_CL = FK_TB + XTB * 12;
+constexpr uint32_t FK_CL = FK_TAGS + 2 * FWORDS * 4;
 constexpr uint32_t FK_WARP_BYTES = (FK_CL + FCMAX * 2 + 127u) & ~127u;
 constexpr uint32_t FK_SMEM = FW * FK_WARP_BYTES;
 
@@ -967,25 +974,21 @@ constexpr uint32_t FK_SMEM = FW * FK_WARP_BYTES;
 // is bank-conflict free.  Bits 0..15 are exactly the u16 P1 stores.
 __device__ __forceinline__ uint32_t fk_addr(uint32_t x) { return x >> 14; }
 
-// Exact check of a block's candidates (the rare path, kept out of line).
+// Exact check and report of a block's m <= 32 candidates, one per lane.
 // Aligned 4-byte records overlap iff they name the same word, so X races iff
 // an earlier candidate Y of the same epoch and word, another thread, and X or
-// Y writing exists; all four bytes of X race then.
-__device__ __noinline__ void fk_exact(WarpOut& E, const Params& P, const uint4* src, const uint16_t* cl,
-                                      uint32_t m, uint32_t b, unsigned long long bstamp, unsigned long long* hs,
-                                      mckg_race_triple* tb) {
-  const uint32_t obj = P.obj_base + b, bid = P.bid_base + b;
-  if (m > 32u) {  // crowded block: the general O(m^2) pass
-    exact_warp(E, P, src, cl, m, obj, bid, bstamp, hs, tb);
-    return;
-  }
+// Y writing exists (racecheck.cpp:24-32); all four bytes of X race then.
+// Reported triples: one (obj, byte, line) set per racing (word, line) of the
+// block (RaceState::reported, machine.hpp:91), appended with one atomic per
+// block; the line's first racing timestamp goes to the warp's line cache.
+__device__ __forceinline__ void fk_exact(WarpOut& E, const Params& P, const uint4* src, const uint16_t* cl,
+                                         uint32_t m, uint32_t b) {
   const uint32_t lane = threadIdx.x & 31u;
   const bool act = lane < m;
   const uint32_t xi = act ? cl[lane] : 0xFFFFu;
   const uint4 X = act ? __ldg(src + xi) : make_uint4(0, 0, 0, 0);
   const uint32_t key = act ? (X.x & 0xFFFFFu) | ((X.y >> 11) << 20) : 0xFFFFFFFFu - lane;
   uint32_t rest = __match_any_sync(0xFFFFFFFFu, key) & ~(1u << lane);
-  if (!act) rest = 0;
   bool racing = false;
   while (__any_sync(0xFFFFFFFFu, rest != 0u)) {
     const uint32_t y = rest ? (uint32_t)__ffs(rest) - 1u : lane;
@@ -994,60 +997,73 @@ __device__ __noinline__ void fk_exact(WarpOut& E, const Params& P, const uint4* 
                    yy = __shfl_sync(0xFFFFFFFFu, X.y, y);
     racing |= y != lane && yi < xi && acc_tid(yy) != acc_tid(X.y) && ((X.x | yx) & (1u << 24));
   }
-  exact_report(E, P, act, X, racing ? 0xFu : 0u, obj, bid, bstamp, hs, tb);
+  const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
+  if (!rm) return;
+  const uint32_t line = X.z;
+  // first racing timestamp per line (min over the block's racing lanes)
+  const unsigned long long ts = ts_key(X.w, P.bid_base + b, acc_tid(X.y));
+  for (uint32_t left = rm; left;) {
+    const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, __ffs(left) - 1);
+    const bool in = racing && line == L;
+    const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, in ? (uint32_t)(ts >> 32) : ~0u);
+    const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, in && (uint32_t)(ts >> 32) == mh ? (uint32_t)ts : ~0u);
+    left &= ~__ballot_sync(0xFFFFFFFFu, in);
+    wo_line1(E, P, L, ((unsigned long long)mh << 32) | ml);
+  }
+  // one reporter per racing (word, line): the lowest racing lane of the group
+  const uint32_t grp = __match_any_sync(0xFFFFFFFFu, racing ? ((X.x & 0xFFFFCu) << 12) ^ line : 0xFFFFFFFFu - lane);
+  const bool rep = racing && (grp & ((1u << lane) - 1u) & rm) == 0u;
+  const uint32_t rb = __ballot_sync(0xFFFFFFFFu, rep);
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(P.n_tri, 4ull * __popc(rb));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  if (rep) {
+    const unsigned long long at = base + 4ull * __popc(rb & ((1u << lane) - 1u));
+    const uint32_t w4 = X.x & 0xFFFFCu;
+    for (uint32_t q = 0; q < 4; ++q) {
+      if (at + q < P.capacity)
+        P.tri[at + q] = mckg_race_triple{P.obj_base + b, w4 + q, (int32_t)line};
+      else
+        E.flags |= ST_OVERFLOW;
+    }
+  }
 }
 
-__global__ void __launch_bounds__(FW * 32, 2) fast_kernel(Params P) {
+__global__ void __launch_bounds__(FW * 32, MCKG_FK_MINB) fast_kernel(Params P) {
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   uint8_t* wbase = smem_raw + warp * FK_WARP_BYTES;
   uint32_t* tags = reinterpret_cast<uint32_t*>(wbase + FK_TAGS);
-  unsigned long long* hs = reinterpret_cast<unsigned long long*>(wbase + FK_HS);
-  mckg_race_triple* tb = reinterpret_cast<mckg_race_triple*>(wbase + FK_TB);
   uint16_t* cl = reinterpret_cast<uint16_t*>(wbase + FK_CL);
   for (uint32_t i = lane; i < 2 * FWORDS; i += 32) tags[i] = 0u;
-  for (uint32_t i = lane; i < XHS; i += 32) hs[i] = 0ull;
   __syncwarp();
   const uint32_t tagb = smem_u32(tags);
   WarpOut E{INF, ~0ull, 0u, 0u, 0u};
-  unsigned long long bstamp = 0;
   uint32_t stamp = 0;
   const uint32_t nwarps = gridDim.x * FW;
   const uint32_t shm = P.shmem_bytes;
-  // L2 prefetch of the warp's next block (TMA engine): measured slower
-  // than the plain loads on C3 (4.19 vs 3.99 ms), kept as an experiment
-  const bool prefetch = (P.debug & 8u) != 0u;
-  uint32_t b = blockIdx.x * FW + warp;
-  if (prefetch && lane == 0 && b < P.n_blocks && P.bstart[b + 1] - P.bstart[b] == FMAX)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.ev + P.bstart[b]), "r"(FMAX * 16u) : "memory");
-  for (; b < P.n_blocks; b += nwarps) {
+  for (uint32_t b = blockIdx.x * FW + warp; b < P.n_blocks; b += nwarps) {
     const uint64_t s0 = P.bstart[b], s1 = P.bstart[b + 1];
-    // the warp's next block streams into L2 while this one is checked
-    if (prefetch && lane == 0 && b + nwarps < P.n_blocks) {
-      const uint64_t p0 = P.bstart[b + nwarps], p1 = P.bstart[b + nwarps + 1];
-      if (p1 - p0 == FMAX)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.ev + p0), "r"(FMAX * 16u) : "memory");
-    }
-    if (s1 == s0) continue;
     if (s1 - s0 != FMAX) {
-      if (lane == 0) P.olist[atomicAdd(P.ocount, 1u)] = b;
+      if (s1 != s0 && lane == 0) P.olist[atomicAdd(P.ocount, 1u)] = b;
       continue;
     }
     const uint4* src = reinterpret_cast<const uint4*>(P.ev + s0);
-    // ---- load, validate, pack (8 rows in flight ahead of the decode) ----
+    // ---- load, validate, pack (4 rows in flight ahead of the decode) ----
     uint32_t pk[FRPL];
     uint32_t e0 = 0, chk = 0, mo = 0, mz = 0, ms = 0, up = 0;
-    uint4 buf[2][8];
+    constexpr int BR = MCKG_FK_BR;  // rows per batch
+    uint4 buf[2][BR];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) buf[0][q] = __ldg(src + q * 32 + lane);
+    for (int q = 0; q < BR; ++q) buf[0][q] = __ldg(src + q * 32 + lane);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      if (h < 3) {
+    for (int h = 0; h < (int)FRPL / BR; ++h) {
+      if (h + 1 < (int)FRPL / BR) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) buf[(h + 1) & 1][q] = __ldg(src + (h + 1) * 256 + q * 32 + lane);
+        for (int q = 0; q < BR; ++q) buf[(h + 1) & 1][q] = __ldg(src + ((h + 1) * BR + q) * 32 + lane);
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int j = h * 8 + q;
+      for (int q = 0; q < BR; ++q) {
+        const int j = h * BR + q;
         const uint4 r = buf[h & 1][q];
         const uint32_t ep = acc_epoch(r.y);
         if (j == 0) e0 = __shfl_sync(0xFFFFFFFFu, ep, 0);
@@ -1065,8 +1081,8 @@ __global__ void __launch_bounds__(FW * 32, 2) fast_kernel(Params P) {
       }
     }
     // epochs non-decreasing in record order: every lane's second-epoch rows
-    // form a top segment starting at row f_l with f_l - (T - l)/32 rounding
-    // consistent, i.e. f non-increasing over lanes with f_0 - f_31 <= 1
+    // form a top segment starting at row f_l, with f non-increasing over the
+    // lanes and f_0 - f_31 <= 1
     const uint32_t f = up ? (uint32_t)__ffs(up) - 1u : 32u;
     bool bad = chk != 0u || mo + 4u > shm || mz >= 65536u || ms > 1u || (up != 0u && (up | (up - 1u)) != ~0u);
     const uint32_t fn = __shfl_down_sync(0xFFFFFFFFu, f, 1);
@@ -1120,11 +1136,9 @@ __global__ void __launch_bounds__(FW * 32, 2) fast_kernel(Params P) {
     uint32_t pos = incl - c;
     for (uint32_t g = cm; g; g &= g - 1u) cl[pos++] = (uint16_t)((uint32_t)(__ffs(g) - 1) * 32u + lane);
     __syncwarp();
-    ++bstamp;
-    fk_exact(E, P, src, cl, m, b, bstamp, hs, tb);
+    fk_exact(E, P, src, cl, m, b);
     __syncwarp();
   }
-  wo_flush(E, P, tb);
   if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
   const uint32_t fl = __reduce_or_sync(0xFFFFFFFFu, E.flags);
   if (lane == 0 && fl) atomicOr(P.status, fl);
