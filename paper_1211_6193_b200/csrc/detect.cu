@@ -8,33 +8,31 @@
 // machine.hpp:91) and the Race diagnostic of a line appears at its first
 // racing access (addDiagnostic dedup, machine.cpp:41-46).
 //
-// Design (one CTA streams many simulated blocks; blocks never
-// interact because each owns its shared object, device.cpp:33-38):
-//   1. stage: each block's 16-byte records are pulled into shared memory by
-//      the TMA engine (cp.async.bulk + mbarrier, 3 stages); every thread keeps
-//      EPT records decoded in registers, so a one-round block releases its
-//      stage to the next TMA load right after the decode.
-//   2. filter, on 4-byte words, NSLOT epochs at once in per-slot arrays (a
-//      "unit" = block x epoch window; one unit per block unless a block spans
-//      more epochs): P1 tag[w] = some accessing tid | barrier | P2 stamp the
-//      words seen by a second tid / written | barrier | P3 an event is a
-//      candidate iff one of its words is both -- fused with P1 of the next
-//      unit.  Two barriers per block.  A byte can race only if its word
-//      passes, so the filter has no false negatives.
-//   3. exact pass over the (rare) candidates -- the reference predicate
-//      verbatim, byte-exact: X races on the bytes it shares with an earlier
-//      candidate Y of the same epoch and another thread where X or Y writes.
-//      Default (two-kernel) path: the filter publishes each block's candidate
-//      list; exact_kernel, launched programmatically beside the filter
-//      (PDL), polls the lists and runs one warp per block (C lanes per
-//      candidate, Y's by shuffle).  A block with more than CMAX candidates is
-//      redone by the fused kernel variant (filter + exact on all threads).
-//   4. report: racing (byte, line) pairs are deduplicated per block through a
-//      (word, line) -> byte-mask table, staged per warp and appended to the
-//      global triple array; the first racing timestamp per line is
-//      min-reduced per warp (lane-owned line cache), then globally.
+// Two kernels, both streaming many simulated blocks (blocks never interact:
+// each owns its shared object, device.cpp:33-38):
+//   * fast_kernel (the default path): one warp per block, for trace-mode
+//     blocks (1024 records, aligned 4-byte accesses, <= 2 epochs, objects of
+//     <= 4 KiB): coalesced 16-byte loads into one packed register per record,
+//     the word filter below in the warp's own shared-memory tag arrays with
+//     __syncwarp between phases, a match_any exact pass over the candidates.
+//     Any other block is handed to
+//   * race_detect_kernel (the general path), one CTA per block at a time:
+//     1. stage: each block's 16-byte records are pulled into shared memory by
+//        the TMA engine (cp.async.bulk + mbarrier, 3 stages);
+//     2. filter, on 4-byte words, NSLOT epochs at once in per-slot arrays (a
+//        "unit" = block x epoch window): P1 tag[w] = some accessing tid |
+//        barrier | P2 stamp the words seen by a second tid / written |
+//        barrier | P3 an event is a candidate iff one of its words is both.
+//        A byte can race only if its word passes, so the filter has no false
+//        negatives;
+//     3. exact pass over the (rare) candidates -- the reference predicate
+//        verbatim, byte-exact: X races on the bytes it shares with an
+//        earlier candidate Y of the same epoch and another thread where X or
+//        Y writes;
+//     4. report: racing (byte, line) pairs are deduplicated per block through
+//        a (word, line) -> byte-mask table, staged and appended to the global
+//        triple array; the first racing timestamp per line is min-reduced.
 #include <cub/cub.cuh>
-#include <array>
 #include <atomic>
 #include <map>
 #include <thread>
@@ -43,19 +41,12 @@
 
 #include "common.cuh"
 
-// TMA stages and CTAs/SM: the fused kernel (report state in static shared
-// memory) 3 / 3; the filter of the two-kernel path 2 / 4
+// TMA stages and CTAs/SM of the general kernel
 #ifndef MCKG_K2_NSTAGE
 #define MCKG_K2_NSTAGE 3
 #endif
 #ifndef MCKG_K2_MINB
 #define MCKG_K2_MINB 3
-#endif
-#ifndef MCKG_K2F_NSTAGE
-#define MCKG_K2F_NSTAGE 3
-#endif
-#ifndef MCKG_K2F_MINB
-#define MCKG_K2F_MINB 4
 #endif
 
 namespace mckg {
@@ -86,22 +77,13 @@ struct Params {
   unsigned long long* n_tri;
   unsigned long long* line_first;
   uint32_t* status;
-  uint32_t debug;  // experiments only (MCKG_DEBUG): 1 skip the exact pass, 2 skip filter + exact
-  // two-kernel mode: the filter writes each block's candidate list (<= CMAX
-  // record indices) for exact_kernel; a block with a longer list is appended
-  // to olist and redone by the fused kernel (filter + exact in one pass)
-  uint32_t mode;       // 0 fused, 1 filter -> candidate lists
-  uint32_t gate;       // fused kernel: 1 = only the blocks of olist
-  // per block, wpb 64-bit words {candidate bits of 32 records, 1}: word
-  // k * 8 + warp covers records k * NT + warp * 32 + lane (0 = not published)
-  unsigned long long* cbits;  // [n_blocks * wpb]; high word = ctag when published
-  uint32_t wpb;
-  uint32_t ctag;              // this call's publication tag (never 0)
-  uint32_t* ocount;    // [0] blocks in olist, [1] exact_kernel's next block
+  uint32_t debug;  // experiments only (MCKG_DEBUG): 1 skip the exact pass, 2 TMA stream only
+  // the general kernel gated on the fast path's overflow list
+  uint32_t gate;       // 1 = only the blocks of olist
+  uint32_t* ocount;    // [0] blocks in olist
   uint32_t* olist;     // [n_blocks]
 };
 
-constexpr uint32_t CMAX = 64;
 
 extern __shared__ __align__(128) uint8_t smem_raw[];
 // fixed-size per-CTA state (static shared memory: compile-time addresses)
@@ -363,21 +345,20 @@ __device__ void flush_triples(const Params& P, int q) {
 //         append the previous block's triples; release its TMA stage
 // P3 reads only ma[], P1 writes only tag[]; the exact pass reads the stage
 // and cl of the previous block, which nothing else touches until (b).
-template <int EPT, bool FUSED>
-__global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2F_MINB) : (EPT <= 8 ? 2 : 1))
+template <int EPT>
+__global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 1))
     race_detect_kernel(Params P) {
-  constexpr int NSTAGE = FUSED ? MCKG_K2_NSTAGE : MCKG_K2F_NSTAGE;
+  constexpr int NSTAGE = MCKG_K2_NSTAGE;
   // the blocks this launch covers: all, or (gated fused pass) the overflow list
-  const uint32_t nblk = FUSED && P.gate ? *(volatile uint32_t*)P.ocount : P.n_blocks;
+  const uint32_t nblk = P.gate ? *(volatile uint32_t*)P.ocount : P.n_blocks;
   if (nblk == 0) return;
-  if constexpr (!FUSED) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  auto blk = [&](uint32_t j) { return FUSED && P.gate ? P.olist[j] : j; };
+  auto blk = [&](uint32_t j) { return P.gate ? P.olist[j] : j; };
   const Lay L = layout(P.cap, P.wpad, NSTAGE);
   const uint32_t t = threadIdx.x, lane = t & 31u;
   uint64_t* mbar = s_mbar;
   uint4* stage = sp<uint4>(L.stage);
   uint16_t* clbuf = sp<uint16_t>(L.cl);  // 2 x cap
-  if constexpr (FUSED) {
+  {
     for (uint32_t i = t; i < HS; i += NT) s_hset[i] = 0ull;
     for (uint32_t i = t; i < LTN; i += NT) {
       s_lt_line[i] = INF;
@@ -417,7 +398,6 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
   const uint32_t slotw = P.wpad;
   uint32_t erel[EPT], wsw[EPT], xa[EPT], meta[EPT];
   uint32_t sphase = 0, stamp = 0;
-  uint32_t cacc = 0;  // candidate bits of the current block (two-kernel path)
   int it = 0;
   uint32_t j = blockIdx.x, b = j < nblk ? blk(j) : 0u;
   uint32_t n = 0, ws = 0, elast = 0;
@@ -500,16 +480,9 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
   while (true) {
     // (a) P1 of this unit and P3 of the previous one are complete
     const bool spans_any = fsync_or(fresh && wmw);
+    (void)spans_any;
     if (fresh) {
-      // two-kernel path: a one-round block without multi-word accesses never
-      // reads its stage again (records live in registers, the exact kernel
-      // reads global memory): stream the next block into it right away
-      held = FUSED || spans_any || elast >= NSLOT;
-      if (!held && t == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t nj = j + (uint32_t)NSTAGE * G;
-        if (nj < nblk) issue(nj, it % NSTAGE);
-      }
+      held = true;  // the exact pass of this block reads its stage
       fresh = false;
     }
     const bool doexact = pend;
@@ -518,9 +491,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
     if (doexact) {
       ++bstamp;
       const uint32_t m = pn > 0 ? s_cnt[pq] : 0u;
-      if constexpr (!FUSED) {
-        (void)m;  // published in P3 of the block's last unit
-      } else if (m > 0 && !(P.debug & 1u)) {
+      if (m > 0 && !(P.debug & 1u)) {
         exact_block(P, stage + (size_t)(pit % NSTAGE) * P.cap, clbuf + (size_t)pq * P.cap, m, pq,
                     P.obj_base + pb, P.bid_base + pb, bstamp);
       }
@@ -548,12 +519,10 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
     fsync();  // (b)
     if (doexact) {
       // the previous block is done: append its triples, free its stage
-      if constexpr (FUSED) {
-        if (t < 32) {
-          flush_triples(P, pq);
-          __syncwarp();
-          if (t == 0) s_cnt[2 + pq] = 0;
-        }
+      if (t < 32) {
+        flush_triples(P, pq);
+        __syncwarp();
+        if (t == 0) s_cnt[2 + pq] = 0;
       }
       if (t == 0) {
         s_cnt[pq] = 0;
@@ -584,9 +553,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
           cmask |= 1u << k;
       }
     }
-    if constexpr (!FUSED) {
-      cacc |= cmask;
-    } else if (__any_sync(0xFFFFFFFFu, cmask)) {
+    if (__any_sync(0xFFFFFFFFu, cmask)) {
 #pragma unroll
       for (int k = 0; k < EPT; ++k) {
         const bool cand = (cmask >> k) & 1u;
@@ -612,22 +579,6 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
       ws = lo < n ? acc_epoch(src[lo].y) - e0 : elast + 1;
       p1(++stamp & 0xFFFFu);
     } else {
-      if constexpr (!FUSED) {
-        // publish this warp's candidate bits of the block (exact_kernel polls)
-        uint32_t mine = 0;
-        if (__any_sync(0xFFFFFFFFu, cacc != 0u)) {
-#pragma unroll
-          for (int k = 0; k < EPT; ++k) {
-            const uint32_t bm = __ballot_sync(0xFFFFFFFFu, (cacc >> k) & 1u);
-            if (lane == (uint32_t)k) mine = bm;
-          }
-        }
-        if (lane < (uint32_t)EPT) {
-          unsigned long long* w = P.cbits + (size_t)b * P.wpb + lane * (NT / 32) + (t >> 5);
-          *(volatile unsigned long long*)w = ((unsigned long long)P.ctag << 32) | mine;
-        }
-        cacc = 0;
-      }
       pend = true;
       pheld = held;
       pit = it;
@@ -648,22 +599,11 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? (FUSED ? MCKG_K2_MINB : MCKG_K2
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if (lane == 0 && flags) atomicOr(&s_flags, flags);
   __syncthreads();
-  if constexpr (FUSED) {
-    if (t < LTN && s_lt_line[t] != INF) atomicMin(P.line_first + s_lt_line[t], s_lt_ts[t]);
-  }
+  if (t < LTN && s_lt_line[t] != INF) atomicMin(P.line_first + s_lt_line[t], s_lt_ts[t]);
   if (t == 0 && s_flags) atomicOr(P.status, s_flags);
 }
 
-// ---------------- exact_kernel: the exact pass of the two-kernel mode ----
-// One warp per simulated block with candidates (grid-stride), lane per X,
-// the Y's by shuffle; the candidate records are read from the trace in
-// global memory (16 B each, ~1.5 % of the records on C3).  Per warp: a
-// lane-owned line-first cache, a (word, line) reported-set table and a
-// triple staging buffer, all contention-free.
-constexpr uint32_t XW = 4;     // warps per CTA (one CTA fits beside 3 filter CTAs per SM)
-constexpr uint32_t XHS = 128;  // reported-set slots per warp
-constexpr uint32_t XTB = 64;   // staged triples per warp
-
+// ---------------- per-warp line-first cache (the fast path's report) ----
 struct WarpOut {
   uint32_t lc_line;          // lane-owned line cache entry
   unsigned long long lc_ts;
@@ -671,47 +611,6 @@ struct WarpOut {
   uint32_t tbn;              // uniform: staged triples
   uint32_t flags;
 };
-
-
-__device__ void wo_flush(WarpOut& E, const Params& P, mckg_race_triple* tb) {
-  const uint32_t lane = threadIdx.x & 31u;
-  __syncwarp();
-  const uint32_t n = E.tbn;
-  if (n == 0) return;
-  unsigned long long base = 0;
-  if (lane == 0) base = atomicAdd(P.n_tri, (unsigned long long)n);
-  base = __shfl_sync(0xFFFFFFFFu, base, 0);
-  for (uint32_t i = lane; i < n; i += 32) {
-    if (base + i < P.capacity)
-      P.tri[base + i] = tb[i];
-    else
-      E.flags |= ST_OVERFLOW;
-  }
-  __syncwarp();
-  E.tbn = 0;
-}
-
-// the (word, line) reported-set table of one warp (see hset_or)
-__device__ uint32_t whset_or(unsigned long long* hs, unsigned long long bstamp, uint32_t word, uint32_t line,
-                             uint32_t mask) {
-  const unsigned long long want = (bstamp << 40) | ((unsigned long long)(word & 0x3FFFFu) << 22) |
-                                  ((unsigned long long)(line & 0xFFFFu) << 6);
-  uint32_t h = (uint32_t)(((want >> 6) * 0x9E3779B97F4A7C15ull) >> 40) & (XHS - 1);
-  for (uint32_t probe = 0; probe < XHS; ++probe) {
-    unsigned long long cur = hs[h];
-    while ((cur >> 40) != bstamp) {
-      const unsigned long long old = atomicCAS(hs + h, cur, want | mask);
-      if (old == cur) return mask;
-      cur = old;
-    }
-    if ((cur & ~0x3Full) == want) {
-      const unsigned long long old = atomicOr(hs + h, (unsigned long long)mask);
-      return mask & ~(uint32_t)old & 0xFu;
-    }
-    h = (h + 1) & (XHS - 1);
-  }
-  return 0x10u | mask;
-}
 
 // one line's first racing timestamp into the lane-owned cache (uniform call)
 __device__ __forceinline__ void wo_line1(WarpOut& E, const Params& P, uint32_t L, unsigned long long T) {
@@ -727,206 +626,6 @@ __device__ __forceinline__ void wo_line1(WarpOut& E, const Params& P, uint32_t L
     }
     E.lc_next = (E.lc_next + 1u) & 31u;
   }
-}
-
-// X (lane-per-X, record R, index xi) races on `bits` (bit j = byte off(X)+j):
-// line-first per distinct line, then the bytes not reported before.
-__device__ void exact_report(WarpOut& E, const Params& P, bool act, const uint4& X, uint32_t bits, uint32_t obj,
-                             uint32_t bid, unsigned long long bstamp, unsigned long long* hs, mckg_race_triple* tb) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const bool racing = act && bits != 0;
-  const uint32_t rm = __ballot_sync(0xFFFFFFFFu, racing);
-  if (!rm) return;
-  const uint32_t line = X.z, xoff = acc_off(X.x), xend = xoff + acc_len(X.x);
-  const unsigned long long ts = ts_key(X.w, bid, acc_tid(X.y));
-  for (uint32_t left = rm; left;) {
-    const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, __ffs(left) - 1);
-    const bool in = racing && line == L;
-    const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, in ? (uint32_t)(ts >> 32) : ~0u);
-    const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, in && (uint32_t)(ts >> 32) == mh ? (uint32_t)ts : ~0u);
-    left &= ~__ballot_sync(0xFFFFFFFFu, in);
-    wo_line1(E, P, L, ((unsigned long long)mh << 32) | ml);
-  }
-  // fresh bytes per word of X (at most 3 words)
-  uint32_t fresh[3] = {0u, 0u, 0u};
-  uint32_t k = 0;
-  if (racing) {
-    const uint64_t ab = (uint64_t)bits << (xoff & 3u);
-    for (uint32_t w = 0; w < 3u && (xoff >> 2) + w <= (xend - 1u) >> 2; ++w) {
-      const uint32_t wm = (uint32_t)(ab >> (4u * w)) & 0xFu;
-      if (!wm) continue;
-      uint32_t f = whset_or(hs, bstamp, (xoff >> 2) + w, line, wm);
-      if (f & 0x10u) {
-        E.flags |= ST_DUP;
-        f &= 0xFu;
-      }
-      fresh[w] = f;
-      k += __popc(f);
-    }
-  }
-  uint32_t incl = k;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-    if (lane >= (uint32_t)d) incl += v;
-  }
-  const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  if (E.tbn + total > XTB) wo_flush(E, P, tb);
-  uint32_t pos = E.tbn + incl - k;
-  for (uint32_t w = 0; w < 3u; ++w)
-    for (uint32_t f = fresh[w]; f; f &= f - 1u, ++pos) {
-      const mckg_race_triple tr{obj, ((xoff >> 2) + w) * 4u + (__ffs(f) - 1u), (int32_t)line};
-      if (pos < XTB) {
-        tb[pos] = tr;
-      } else {  // more than a buffer in one step: straight to global memory
-        const unsigned long long g = atomicAdd(P.n_tri, 1ull);
-        if (g < P.capacity)
-          P.tri[g] = tr;
-        else
-          E.flags |= ST_OVERFLOW;
-      }
-    }
-  __syncwarp();
-  E.tbn = min(E.tbn + total, XTB);
-}
-
-__device__ __forceinline__ uint32_t hit_bits(uint32_t xi, uint32_t Xx, uint32_t Xy, uint32_t yi, uint32_t Yx,
-                                             uint32_t Yy) {
-  const uint32_t xoff = acc_off(Xx), xend = xoff + acc_len(Xx);
-  const uint32_t yoff = acc_off(Yx), yend = yoff + acc_len(Yx);
-  const uint32_t lo = max(xoff, yoff), hi = min(xend, yend);
-  const bool hit = yi < xi && acc_epoch(Yy) == acc_epoch(Xy) && acc_tid(Yy) != acc_tid(Xy) &&
-                   ((Xx | Yx) & (1u << 24)) && lo < hi;
-  return hit ? ((1u << (hi - lo)) - 1u) << (lo - xoff) : 0u;
-}
-
-__device__ void exact_warp(WarpOut& E, const Params& P, const uint4* src, const uint16_t* cl, uint32_t m,
-                           uint32_t obj, uint32_t bid, unsigned long long bstamp, unsigned long long* hs,
-                           mckg_race_triple* tb) {
-  const uint32_t lane = threadIdx.x & 31u;
-  if (m <= 32u) {
-    // candidate j at lane j; C lanes per X, each scanning every C-th Y
-    const bool ya = lane < m;
-    const uint32_t yi_l = ya ? cl[lane] : 0xFFFFu;
-    const uint4 R = ya ? __ldg(src + yi_l) : make_uint4(0, 0, 0, 0);
-    uint32_t C = 32;
-    while (C > 1 && C * m > 32u) C >>= 1;
-    const uint32_t g = lane / C, sub = lane & (C - 1u);
-    const uint32_t xi = __shfl_sync(0xFFFFFFFFu, yi_l, g & 31u);
-    const uint32_t Xx = __shfl_sync(0xFFFFFFFFu, R.x, g & 31u);
-    const uint32_t Xy = __shfl_sync(0xFFFFFFFFu, R.y, g & 31u);
-    uint32_t bits = 0;
-    const uint32_t iters = (m + C - 1u) / C;
-    for (uint32_t it = 0; it < iters; ++it) {
-      const uint32_t j = sub + it * C;
-      const uint32_t yi = __shfl_sync(0xFFFFFFFFu, yi_l, j & 31u);
-      const uint32_t Yx = __shfl_sync(0xFFFFFFFFu, R.x, j & 31u);
-      const uint32_t Yy = __shfl_sync(0xFFFFFFFFu, R.y, j & 31u);
-      if (j < m) bits |= hit_bits(xi, Xx, Xy, yi, Yx, Yy);
-    }
-    for (uint32_t d = 1; d < C; d <<= 1) bits |= __shfl_xor_sync(0xFFFFFFFFu, bits, d);
-    bits = __shfl_sync(0xFFFFFFFFu, bits, (lane * C) & 31u);  // back to lane-per-X
-    exact_report(E, P, ya, R, bits, obj, bid, bstamp, hs, tb);
-    return;
-  }
-  for (uint32_t xb = 0; xb < m; xb += 32u) {
-    const bool act = xb + lane < m;
-    const uint32_t xi = act ? cl[xb + lane] : 0xFFFFu;
-    const uint4 X = act ? __ldg(src + xi) : make_uint4(0, 0, 0, 0);
-    uint32_t bits = 0;
-    for (uint32_t yb = 0; yb < m; yb += 32u) {
-      uint32_t yi_l = xi, y0 = X.x, y1 = X.y;
-      if (yb != xb) {
-        const bool ya = yb + lane < m;
-        yi_l = ya ? cl[yb + lane] : 0xFFFFu;
-        const uint2 Yv = ya ? __ldg(reinterpret_cast<const uint2*>(src + yi_l)) : make_uint2(0, 0);
-        y0 = Yv.x;
-        y1 = Yv.y;
-      }
-      const uint32_t cnt = min(32u, m - yb);
-      for (uint32_t j = 0; j < cnt; ++j)
-        bits |= hit_bits(xi, X.x, X.y, __shfl_sync(0xFFFFFFFFu, yi_l, j), __shfl_sync(0xFFFFFFFFu, y0, j),
-                         __shfl_sync(0xFFFFFFFFu, y1, j));
-    }
-    exact_report(E, P, act, X, act ? bits : 0u, obj, bid, bstamp, hs, tb);
-  }
-}
-
-__global__ void __launch_bounds__(XW * 32) exact_kernel(Params P) {
-  __shared__ unsigned long long hs_all[XW][XHS];
-  __shared__ mckg_race_triple tb_all[XW][XTB];
-  __shared__ uint16_t cl_all[XW][CMAX];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  unsigned long long* hs = hs_all[warp];
-  mckg_race_triple* tb = tb_all[warp];
-  uint16_t* cl = cl_all[warp];
-  for (uint32_t i = lane; i < XHS; i += 32) hs[i] = 0ull;
-  __syncwarp();
-  WarpOut E{INF, ~0ull, 0u, 0u, 0u};
-  unsigned long long bstamp = 0;
-  // blocks are claimed in order from a global counter; this kernel may run
-  // beside the filter (programmatic dependent launch) and waits for each
-  // block's published count
-  constexpr uint32_t CHUNK = 16;  // blocks per claim
-  uint32_t b = 0, bend = 0;
-  while (true) {
-    if (b == bend) {
-      if (lane == 0) b = atomicAdd(P.ocount + 1, CHUNK);
-      b = __shfl_sync(0xFFFFFFFFu, b, 0);
-      bend = min(b + CHUNK, P.n_blocks);
-    }
-    if (b >= P.n_blocks) break;
-    const uint32_t bb = b++;
-    // the block's candidate bits (published by the filter; 0 = not yet)
-    uint32_t mk[4] = {0u, 0u, 0u, 0u};
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint32_t q = (uint32_t)r * 32u + lane;
-      if ((uint32_t)r * 32u >= P.wpb) break;
-      if (q < P.wpb) {
-        const volatile unsigned long long* w = P.cbits + (size_t)bb * P.wpb + q;
-        unsigned long long v = *w;
-        while ((uint32_t)(v >> 32) != P.ctag) {
-          __nanosleep(500);
-          v = *w;
-        }
-        mk[r] = (uint32_t)v;
-        cnt += __popc(mk[r]);
-      }
-    }
-    const uint32_t m = __reduce_add_sync(0xFFFFFFFFu, cnt);
-    if (m == 0) continue;
-    if (m > CMAX) {  // too many candidates: the fused pass redoes this block
-      if (lane == 0) P.olist[atomicAdd(P.ocount, 1u)] = bb;
-      continue;
-    }
-    // candidate list: record (word q) * 32 + bit
-    uint32_t base = 0;
-    const int rounds = (int)((P.wpb + 31u) >> 5);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (r >= rounds) break;
-      const uint32_t c = __popc(mk[r]);
-      uint32_t incl = c;
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-        if (lane >= (uint32_t)d) incl += v;
-      }
-      uint32_t pos = base + incl - c;
-      for (uint32_t f = mk[r]; f; f &= f - 1u) cl[pos++] = (uint16_t)(((uint32_t)r * 32u + lane) * 32u + (__ffs(f) - 1u));
-      base += __shfl_sync(0xFFFFFFFFu, incl, 31);
-    }
-    __syncwarp();
-    ++bstamp;
-    exact_warp(E, P, reinterpret_cast<const uint4*>(P.ev + P.bstart[bb]), cl, m, P.obj_base + bb, P.bid_base + bb,
-               bstamp, hs, tb);
-    __syncwarp();
-  }
-  wo_flush(E, P, tb);
-  if (E.lc_line != INF) atomicMin(P.line_first + E.lc_line, E.lc_ts);
-  const uint32_t f = __reduce_or_sync(0xFFFFFFFFu, E.flags);
-  if (lane == 0 && f) atomicOr(P.status, f);
 }
 
 // ---------------- fast_kernel: the default path (one warp per block) ----
@@ -1283,24 +982,16 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
     set_error("mckg_detect_shared: shared object too large for the shared-memory filter");
     return MCKG_E_RANGE;
   }
+  // the general kernel: records staged per block by TMA, EPT per thread
   const int ki = cap <= 4u * NT ? 0 : cap <= 8u * NT ? 1 : 2;
-  void (*kf)(Params) = ki == 0 ? race_detect_kernel<4, true> : ki == 1 ? race_detect_kernel<8, true>
-                                                                      : race_detect_kernel<16, true>;
-  void (*kt)(Params) = ki == 0 ? race_detect_kernel<4, false> : ki == 1 ? race_detect_kernel<8, false>
-                                                                       : race_detect_kernel<16, false>;
-  const size_t smem_f = layout(cap, wpad, MCKG_K2_NSTAGE).end, smem_t = layout(cap, wpad, MCKG_K2F_NSTAGE).end;
+  void (*kf)(Params) = ki == 0 ? race_detect_kernel<4> : ki == 1 ? race_detect_kernel<8> : race_detect_kernel<16>;
+  const size_t smem_f = layout(cap, wpad, MCKG_K2_NSTAGE).end;
   MCKG_CUDA_TRY(ensure_dynamic_smem(kf, smem_f));
-  MCKG_CUDA_TRY(ensure_dynamic_smem(kt, smem_t));
-  auto grid_of = [&](void (*k)(Params), size_t sm) -> uint32_t {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, sm) != cudaSuccess || per_sm < 1)
-      per_sm = 1;
-    uint32_t g = (uint32_t)sm_count() * (uint32_t)per_sm;
-    return g > tr->n_blocks ? tr->n_blocks : g;
-  };
-  const uint32_t grid_f = grid_of(kf, smem_f), grid_t = grid_of(kt, smem_t);
-  (void)smem;
-  Params P;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, NT, smem_f) != cudaSuccess || per_sm < 1) per_sm = 1;
+  uint32_t grid_f = (uint32_t)sm_count() * (uint32_t)per_sm;
+  if (grid_f > tr->n_blocks) grid_f = tr->n_blocks;
+  Params P{};
   P.ev = tr->events;
   P.bstart = tr->block_start;
   P.n_blocks = tr->n_blocks;
@@ -1315,130 +1006,38 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.line_first = out->line_first;
   P.status = out->status;
   P.debug = debug_flags();
-  P.mode = 0;
   P.gate = 0;
-  P.cbits = nullptr;
-  P.wpb = cap / 32u;
-  P.ctag = 0;
   P.ocount = nullptr;
   P.olist = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
-  if (P.debug & 32u) {  // MCKG_DEBUG=32: the fused kernel alone (tests cover both paths)
+  if ((P.debug & 32u) || tr->shmem_bytes > FWORDS * 4u) {
+    // the general kernel alone (MCKG_DEBUG=32: the tests cover both paths;
+    // shared objects over 4 KiB: no fast path)
     kf<<<grid_f, NT, smem_f, s>>>(P);
     MCKG_CUDA_TRY(cudaGetLastError());
     note_launch(1, grid_f, NT, (uint32_t)smem_f);
     return MCKG_OK;
   }
-  keep_pool_memory();
-  if (!(P.debug & 4u) && tr->shmem_bytes <= FWORDS * 4u) {
-    // default path: fast_kernel (one warp per block); the fused kernel
-    // (gated) redoes the blocks it hands back in the overflow list
-    uint32_t* ol = nullptr;
-    MCKG_CUDA_TRY(overflow_list(tr->n_blocks, s, &ol));
-    P.ocount = ol;
-    P.olist = ol + 2;
-    MCKG_CUDA_TRY(cudaMemsetAsync(P.ocount, 0, 2 * sizeof(uint32_t), s));
-    MCKG_CUDA_TRY(ensure_dynamic_smem(fast_kernel, FK_SMEM));
-    int per = 0;
-    MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fast_kernel, FW * 32, FK_SMEM));
-    if (per < 1) per = 1;
-    uint32_t g = (uint32_t)sm_count() * (uint32_t)per;
-    const uint32_t need = (tr->n_blocks + FW - 1) / FW;
-    if (g > need) g = need;
-    fast_kernel<<<g, FW * 32, FK_SMEM, s>>>(P);
-    MCKG_CUDA_TRY(cudaGetLastError());
-    P.mode = 0;
-    P.gate = 1;
-    kf<<<grid_f, NT, smem_f, s>>>(P);
-    MCKG_CUDA_TRY(cudaGetLastError());
-    note_launch(2, g, FW * 32, FK_SMEM);
-    return MCKG_OK;
-  }
-  // MCKG_DEBUG bit 4: the round-1 two-kernel path (filter -> candidate
-  // bitmaps -> exact_kernel beside it); the fused kernel (gated) redoes the
-  // blocks with more than CMAX candidates
-  P.wpb = (uint32_t)(ki == 0 ? 4 : ki == 1 ? 8 : 16) * (NT / 32);  // EPT * warps
-  // candidate bitmaps: a buffer per stream that only this path writes,
-  // cleared once; words carry the call's tag, so stale words never match
-  // (plus the overflow list and its counters), grown on demand
-  {
-    struct CBuf {
-      unsigned long long* p = nullptr;
-      size_t words = 0;
-      uint32_t tag = 0;
-      uint32_t* olist = nullptr;  // [0..1] counters, then the overflow list
-      size_t oblocks = 0;
-    };
-    static std::mutex mu;
-    // key: (device, stream, host thread for the per-thread / legacy default
-    // stream handles, which name a different stream on each thread)
-    static std::map<std::tuple<int, cudaStream_t, std::thread::id>, CBuf> bufs;
-    int dev = 0;
-    MCKG_CUDA_TRY(cudaGetDevice(&dev));
-    const bool special = s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread;
-    std::lock_guard<std::mutex> lock(mu);
-    CBuf& cb = bufs[{dev, s, special ? std::this_thread::get_id() : std::thread::id()}];
-    const size_t need = (size_t)tr->n_blocks * P.wpb;
-    if (cb.words < need || cb.tag == 0xFFFFFFFFu) {
-      if (cb.p) {
-        MCKG_CUDA_TRY(cudaStreamSynchronize(s));
-        MCKG_CUDA_TRY(cudaFree(cb.p));
-        cb.p = nullptr;
-      }
-      const size_t words = std::max(need, cb.words);
-      MCKG_CUDA_TRY(cudaMalloc(&cb.p, words * sizeof(unsigned long long)));
-      MCKG_CUDA_TRY(cudaMemsetAsync(cb.p, 0, words * sizeof(unsigned long long), s));
-      cb.words = words;
-      cb.tag = 0;
-    }
-    if (cb.oblocks < tr->n_blocks) {
-      if (cb.olist) {
-        MCKG_CUDA_TRY(cudaStreamSynchronize(s));
-        MCKG_CUDA_TRY(cudaFree(cb.olist));
-        cb.olist = nullptr;
-      }
-      MCKG_CUDA_TRY(cudaMalloc(&cb.olist, ((size_t)tr->n_blocks + 2) * sizeof(uint32_t)));
-      cb.oblocks = tr->n_blocks;
-    }
-    P.cbits = cb.p;
-    P.ctag = ++cb.tag;
-    P.ocount = cb.olist;
-    P.olist = cb.olist + 2;
-  }
+  // default path: fast_kernel (one warp per block); the general kernel,
+  // gated on the overflow list, redoes the blocks the fast path hands back
+  uint32_t* ol = nullptr;
+  MCKG_CUDA_TRY(overflow_list(tr->n_blocks, s, &ol));
+  P.ocount = ol;
+  P.olist = ol + 2;
   MCKG_CUDA_TRY(cudaMemsetAsync(P.ocount, 0, 2 * sizeof(uint32_t), s));
-  P.mode = 1;
-  kt<<<grid_t, NT, smem_t, s>>>(P);
-  // exact_kernel spin-waits on the filter's publications: never launch it
-  // behind a filter that failed to launch
+  MCKG_CUDA_TRY(ensure_dynamic_smem(fast_kernel, FK_SMEM));
+  int per = 0;
+  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fast_kernel, FW * 32, FK_SMEM));
+  if (per < 1) per = 1;
+  uint32_t g = (uint32_t)sm_count() * (uint32_t)per;
+  const uint32_t need = (tr->n_blocks + FW - 1) / FW;
+  if (g > need) g = need;
+  fast_kernel<<<g, FW * 32, FK_SMEM, s>>>(P);
   MCKG_CUDA_TRY(cudaGetLastError());
-  uint32_t launched = 1;
-  if (!(P.debug & 1u)) {
-    int xper = 0;
-    MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&xper, exact_kernel, XW * 32, 0));
-    if (xper < 1) xper = 1;
-    uint32_t xgrid = (uint32_t)sm_count() * (uint32_t)xper;
-    const uint32_t need = (tr->n_blocks + XW - 1) / XW;
-    if (xgrid > need) xgrid = need;
-    // programmatic dependent launch: exact_kernel starts once every filter CTA
-    // is resident and consumes the candidate lists as they are published
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(xgrid);
-    cfg.blockDim = dim3(XW * 32);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = (P.debug & 128u) ? 0 : 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    MCKG_CUDA_TRY(cudaLaunchKernelEx(&cfg, exact_kernel, P));
-    P.mode = 0;
-    P.gate = 1;
-    kf<<<grid_f, NT, smem_f, s>>>(P);
-    launched += 2;
-  }
+  P.gate = 1;
+  kf<<<grid_f, NT, smem_f, s>>>(P);
   MCKG_CUDA_TRY(cudaGetLastError());
-  note_launch(launched, grid_t, NT, (uint32_t)smem_t);
+  note_launch(2, g, FW * 32, FK_SMEM);
   return MCKG_OK;
 }
 

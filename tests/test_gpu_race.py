@@ -2,9 +2,9 @@
 triples (RaceState::reported, machine.hpp:91), bit-exact first-detection
 timestamps per line (the Race diagnostic order, machine.cpp:41-46).
 
-Every test runs on both K2 paths: the default two-kernel path (filter ->
-per-block candidate lists -> exact_kernel, with the fused kernel redoing a
-launch whose lists overflow) and the fused kernel alone (mckg_set_debug(32))."""
+Every test runs on both K2 paths: the default path (fast_kernel, one warp per
+trace-mode block, with the general kernel redoing the blocks it hands back)
+and the general kernel alone (mckg_set_debug(32))."""
 import numpy as np
 import pytest
 
@@ -14,11 +14,11 @@ from tracegen_py import random_trace
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["two_kernel", "fused"])
+@pytest.fixture(autouse=True, params=["fast", "general"])
 def k2_path(request):
     from paper_1211_6193_b200 import _abi
     lib = _abi.load()
-    lib.mckg_set_debug(32 if request.param == "fused" else 0)
+    lib.mckg_set_debug(32 if request.param == "general" else 0)
     yield request.param
     lib.mckg_set_debug(0)
 
@@ -167,7 +167,7 @@ def test_c3_full_size_matches_reference(k2_path):
     """The headline workload at full size: 2^30 events, 2^20 blocks, every
     reported triple and every line's first-detection timestamp compared with
     the reference replay (chunked over all host cores, tests/c3_parity.py)."""
-    if k2_path == "fused":
+    if k2_path == "general":
         pytest.skip("full size runs once, on the default path")
     import os
     import torch
@@ -183,3 +183,48 @@ def test_c3_full_size_matches_reference(k2_path):
     assert got["triples_equal"], got["mismatch"]
     assert got["line_first_equal"]
     assert got["reference_triples"] == res.n_triples == 31773232
+
+
+def _mixed_blocks(seed, nb=80):
+    """Full 1024-record C3 blocks, every fifth one left as is and the others
+    mutated so that the fast path must hand them to the general kernel: a hot
+    word (> 32 candidates), a third epoch, a 1-byte access, a 2-byte access."""
+    ev, bs = ob.gen_c3(seed * 1000, nb)
+    ev = ev.copy()
+    rng = np.random.default_rng(seed)
+    for b in range(nb):
+        blk = ev[b * 1024:(b + 1) * 1024]
+        kind = b % 5
+        if kind == 1:  # 64 threads of epoch 0 write slot 0
+            for i in rng.choice(512, 64, replace=False):
+                blk["w0"][i] = (blk["w0"][i] & ~0xFFFFF) | 0 | (1 << 24)
+        elif kind == 2:  # the last 100 records move to a third epoch
+            e = (blk["w1"][-1] >> 11) + 1
+            blk["w1"][-100:] = (blk["w1"][-100:] & 0x7FF) | (e << 11)
+        elif kind == 3:  # one aligned 1-byte access
+            i = int(rng.integers(1024))
+            blk["w0"][i] = (blk["w0"][i] & ~(0xF << 20)) | (1 << 20)
+        elif kind == 4:  # one 2-byte access in the upper half of a word
+            i = int(rng.integers(1024))
+            blk["w0"][i] = ((blk["w0"][i] & ~(0xF << 20)) | (2 << 20)) + 2
+        ev[b * 1024:(b + 1) * 1024] = blk
+    return ev, bs
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fast_path_hands_back_other_blocks(seed):
+    """Blocks outside the fast path's shape are redone by the general kernel
+    and the whole result still equals the reference's."""
+    ev, bs = _mixed_blocks(seed)
+    res, n = _check(ev, bs, ob.C3_SHMEM, obj_base=5, bid_base=seed * 1000)
+    assert n > 0
+
+
+def test_unsorted_epochs_are_flagged():
+    ev, bs = ob.gen_c3(0, 8)
+    ev = ev.copy()
+    blk = ev[3 * 1024:4 * 1024]
+    blk["w1"][[10, 900]] = blk["w1"][[900, 10]]  # an epoch-1 record before an epoch-0 one
+    ev[3 * 1024:4 * 1024] = blk
+    res = _gpu(ev, bs, ob.C3_SHMEM)
+    assert res.status & 4
