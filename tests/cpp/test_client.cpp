@@ -7,6 +7,7 @@
 // the cases that launch grids need a CUDA device and are skipped without one
 // (argv[1] == "--no-gpu").
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -66,48 +67,37 @@ struct Case {
   std::function<void()> body;
 };
 
-const char* kFig1 =
-    "#include <stdio.h>\n"
-    "#include <cuda.h>\n"
-    "#define N 18\n"
-    "#define NBLOCKS 2\n"
-    "#define NTHREADS (N/NBLOCKS)\n"
-    "__global__ void sum(int* in, int* out) {\n"
-    "  extern __shared__ int shared[];\n"
-    "  int i, tid = threadIdx.x, bid = blockIdx.x, bdim = blockDim.x;\n"
-    "  shared[tid] = in[bid * bdim + tid];\n"
-    "  __syncthreads();\n"
-    "  if (tid < bdim/2) {\n"
-    "    shared[tid] += shared[bdim/2 + tid];\n"
-    "  }\n"
-    "  __syncthreads();\n"
-    "  if (tid == 0) {\n"
-    "    for (i=1; i != (bdim/2)+(bdim%2); ++i) {\n"
-    "      shared[0] += shared[i];\n"
-    "    }\n"
-    "    out[bid] = shared[0];\n"
-    "  }\n"
-    "}\n"
-    "int main(void) {\n"
-    "  int i, *dev_in, *dev_out, host[N];\n"
-    "  printf(\"INPUT: \");\n"
-    "  for(i = 0; i != N; ++i) {\n"
-    "    host[i] = (21*i + 29) % 100;\n"
-    "    printf(\" %d \", host[i]);\n"
-    "  }\n"
-    "  printf(\"\\n\");\n"
-    "  cudaMalloc(&dev_in, N * sizeof(int));\n"
-    "  cudaMalloc(&dev_out, NBLOCKS * sizeof(int));\n"
-    "  cudaMemcpy(dev_in, host, N * sizeof(int), cudaMemcpyHostToDevice);\n"
-    "  sum<<<NBLOCKS, NTHREADS, NTHREADS * sizeof(int)>>>(dev_in, dev_out);\n"
-    "  sum<<<1, NBLOCKS, NBLOCKS * sizeof(int)>>>(dev_out, dev_out);\n"
-    "  cudaMemcpy(host, dev_out, sizeof(int), cudaMemcpyDeviceToHost);\n"
-    "  cudaDeviceSynchronize();\n"
-    "  printf(\"OUTPUT: %d\\n\", *host);\n"
-    "  cudaFree(dev_in);\n"
-    "  cudaFree(dev_out);\n"
-    "  return 0;\n"
-    "}\n";
+// The reference corpus file (tests/golden/sum.cu = proj/tests/corpus/sum.cu),
+// read from $MCK_CORPUS_DIR as the reference tests' corpusPath() does.
+std::string slurp(const std::string& path) {
+  std::string s;
+  if (FILE* f = std::fopen(path.c_str(), "rb")) {
+    char buf[4096];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) s.append(buf, n);
+    std::fclose(f);
+  }
+  return s;
+}
+
+std::string corpusPath(const std::string& name) {
+  const char* d = std::getenv("MCK_CORPUS_DIR");
+  return std::string(d ? d : ".") + "/" + name;
+}
+
+// line k (1-based) of src replaced by `text`
+std::string withLine(const std::string& src, int k, const std::string& text) {
+  std::string out;
+  size_t pos = 0;
+  for (int line = 1; pos <= src.size(); ++line) {
+    size_t e = src.find('\n', pos);
+    if (e == std::string::npos) e = src.size();
+    out += (line == k ? text : src.substr(pos, e - pos));
+    if (e < src.size()) out += '\n';
+    pos = e + 1;
+  }
+  return out;
+}
 
 std::vector<Case> cases() {
   std::vector<Case> c;
@@ -204,15 +194,26 @@ std::vector<Case> cases() {
                  CHECK(hasCategory(r, DiagCategory::ApiError));
                }});
   c.push_back({"the figure program computes its sum and the mutants are diagnosed", true, [] {
-                 auto r = runSource(kFig1, {}, "sum.cu");
+                 const std::string fig1 = slurp(corpusPath("sum.cu"));
+                 CHECK(!fig1.empty());
+                 auto r = runSource(fig1, {}, "sum.cu");
                  CHECK(r.exitCode == 0);
                  CHECK(r.output.find("OUTPUT: 767\n") != std::string::npos);
-                 CHECK(r.steps == 3114);
-                 std::string race = kFig1;
-                 race.replace(race.find("  __syncthreads();\n  if (tid == 0)"), 19, "\n");
-                 auto rr = runSource(race, {}, "sum.cu");
+                 CHECK(r.steps == 3114);  // the reference's count
+                 auto rr = runSource(withLine(fig1, 14, ""), {}, "sum.cu");  // the race mutant
                  CHECK(rr.exitCode == 1);
-                 CHECK(hasCategory(rr, DiagCategory::Race));
+                 CHECK(rr.steps == 2994);
+                 CHECK(!rr.diagnostics.empty() &&
+                       rr.diagnostics[0].message == "Possible race on shared device memory detected at sum.cu:17.");
+                 auto rd = runSource(withLine(fig1, 12, "    shared[tid] += shared[bdim/2 + tid]; __syncthreads();"),
+                                     {}, "sum.cu");  // the deadlock mutant
+                 CHECK(rd.exitCode == 3);
+                 CHECK(rd.steps == 2408);
+                 CHECK(rd.stuckReports.size() == 3);
+                 CHECK(formatStuckReports(rd.stuckReports) ==
+                       "barrier-deadlock gid=1 bid=0 waiting=[0,1,2,3] finished-or-absent=[4,5,6,7,8]\n"
+                       "barrier-deadlock gid=1 bid=1 waiting=[0,1,2,3] finished-or-absent=[4,5,6,7,8]\n"
+                       "host-hang: host thread is blocked waiting for stream 0 to drain\n");
                }});
   // ---- test_frontend.cpp ----
   c.push_back({"frontend failures are the reference's typed exceptions", false, [] {
@@ -265,7 +266,7 @@ std::vector<Case> cases() {
   c.push_back({"onTrace receives the --trace lines in order", true, [] {
                  RunOptions o;
                  o.trace = true;
-                 Machine m(compile(kFig1, "sum.cu"), o);
+                 Machine m(compile(slurp(corpusPath("sum.cu")), "sum.cu"), o);
                  std::vector<std::string> lines;
                  m.onTrace = [&](const std::string& s) { lines.push_back(s); };
                  auto r = m.run();

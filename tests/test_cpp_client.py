@@ -20,7 +20,8 @@ def _build(tmp_path):
 
 
 def _run(exe, *args):
-    out = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, MCK_CORPUS_DIR=os.path.join(ROOT, "tests", "golden"))
+    out = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0, out.stdout + out.stderr
     return out.stdout
 
