@@ -414,8 +414,19 @@ def run_c5(args, blocks, dev, ws, rank):
     ms = float(t[0])
     events = int(tot[0])
     sent = ev.shape[0] * 16 * (ws - 1) / max(1, ws)  # bytes leaving this rank (uniform partition)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        peak = json.load(open(peaks_path))["hbm_gbs"]
+    except (OSError, ValueError, KeyError):
+        peak = 6650.0
+    per_rank = ev.shape[0] * 16  # algorithmic: one 16-byte read per record on its rank
+    achieved = per_rank / (ms / 1e3) / 1e9
     return {"workload": f"C5: {events} global 4-byte accesses, {blocks} blocks, 1% cross-block, "
                         f"address-range all-to-all over {ws} GPU(s)",
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "kernel": "mckg_detect_global (sample, bucket count, scan, "
+                         "bucket scatter, bucket_detect)" + (" + K3 partition + NCCL all-to-all" if ws > 1 else ""),
+                         "algorithmic_bytes": "16 B/event read (+ (P-1)/P x 16 B/event over NVLink at P ranks)"},
             "events_per_s": events / (ms / 1e3), "ms_per_step": ms, "races_reported": int(tot[1]),
             "status": status, "nvlink_bytes_per_rank": sent,
             "nvlink_GBps_per_rank": sent / (ms / 1e3) / 1e9 if ws > 1 else None,

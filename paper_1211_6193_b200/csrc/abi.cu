@@ -3,6 +3,8 @@
 // the device in chunks on two CUDA streams so that the PCIe copies of chunk
 // c+1 overlap the detection of chunk c.
 #include <array>
+#include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <cstdio>
@@ -36,6 +38,16 @@ void note_launch(uint32_t kernels, uint32_t grid, uint32_t block, uint32_t smem)
 
 void add_launches(uint32_t kernels) { g_stats.kernels = kernels; }
 
+// Experiment / test switches (MCKG_DEBUG at load time, mckg_set_debug later).
+static std::atomic<uint32_t>& debug_word() {
+  static std::atomic<uint32_t> w{[] {
+    const char* e = getenv("MCKG_DEBUG");
+    return e ? (uint32_t)atoi(e) : 0u;
+  }()};
+  return w;
+}
+uint32_t debug_flags() { return debug_word().load(std::memory_order_relaxed); }
+
 int sm_count() {
   static thread_local int dev = -1, sms = 0;
   int d = 0;
@@ -63,6 +75,8 @@ void keep_pool_memory() {
 }
 
 }  // namespace mckg
+
+extern "C" void mckg_set_debug(uint32_t flags) { mckg::debug_word().store(flags); }
 
 using namespace mckg;
 

@@ -11,6 +11,9 @@ namespace mckg {
 void set_error(const char* what, cudaError_t e = cudaSuccess);
 void note_launch(uint32_t kernels, uint32_t grid, uint32_t block, uint32_t smem);
 void add_launches(uint32_t kernels);
+// MCKG_DEBUG / mckg_set_debug switches (experiments, and the tests that
+// exercise the general paths)
+uint32_t debug_flags();
 int sm_count();
 // Keeps freed stream-ordered allocations in the device's default memory pool
 // (release threshold = max): the detectors allocate multi-GB scratch per call.

@@ -872,15 +872,7 @@ __global__ void decode_triples(const unsigned long long* k, mckg_race_triple* t,
                           (int32_t)(v & 0xFFFFu)};
 }
 
-// Experiment / test switches (MCKG_DEBUG at load time, mckg_set_debug later).
-std::atomic<uint32_t>& debug_word() {
-  static std::atomic<uint32_t> w{[] {
-    const char* e = getenv("MCKG_DEBUG");
-    return e ? (uint32_t)atoi(e) : 0u;
-  }()};
-  return w;
-}
-uint32_t debug_flags() { return debug_word().load(std::memory_order_relaxed); }
+
 
 // The overflow list of the default path (two counters, then up to n_blocks
 // block indices): one buffer per (device, stream, host thread for the
@@ -940,8 +932,6 @@ int detect_config(uint32_t cap, uint32_t shmem_bytes, size_t* smem, uint32_t* wp
 }  // namespace mckg
 
 using namespace mckg;
-
-extern "C" void mckg_set_debug(uint32_t flags) { debug_word().store(flags); }
 
 extern "C" int mckg_race_out_reset(const mckg_race_out* out, void* stream) {
   if (!out || !out->n_triples || !out->line_first || !out->status) {

@@ -14,7 +14,7 @@
 //      BLOCK where X or Y writes (racecheck.cpp:24-32 with thread -> block).
 //      Racing (byte, line) keys are appended, then sorted + uniqued; the first
 //      racing timestamp per line is min-reduced per CTA, then globally.
-#include <cub/cub.cuh>
+#include <vector>
 
 #include "common.cuh"
 
@@ -131,120 +131,751 @@ __global__ void owner_scatter_kernel(const mckg_gaccess* ev, uint64_t n, uint32_
   }
 }
 
-// ---- K6: detection ----
-__device__ __forceinline__ uint32_t words_of(uint64_t a) {
-  const uint64_t addr = ga_addr(a);
-  const uint32_t len = ga_len(a);
-  if (len == 0) return 0;
-  return (uint32_t)(((addr + len - 1) >> 2) - (addr >> 2) + 1);
+// ---- K6: detection (bucket partition + per-bucket filter and exact pass) ----
+//
+// Semantics (oracle/global_detector.c): records in timestamp order (sweep,
+// bid, tid); X races on byte b iff X writes and an earlier access to b came
+// from another block, or X reads and an earlier write to b came from another
+// block (racecheck.cpp:24-32 with "thread" replaced by "block").  Per byte
+// this needs only four minima over the timestamp keys, which embed the
+// block: f1 = the earliest access, f2 = the earliest access from a block
+// other than f1's, and w1 / w2 likewise over the writes.  X (block B, key t)
+// then has an earlier access from another block iff (blk(f1) != B) or
+// (f2 < t), and an earlier write from another block iff (blk(w1) != B and
+// w1 < t) or (blk(w1) == B and w2 < t) -- no sort, no order of arrival.
+//
+// Dataflow, all hand-written:
+//   1. the address span is estimated from a strided sample; buckets are
+//      2^shift-byte address ranges sized for ~256 records;
+//   2. bucket_count: a record counts in every bucket its bytes touch
+//      (warp-aggregated atomics);
+//   3. an exclusive scan of the counts (scan_* kernels);
+//   4. bucket_scatter: re-read, write each record into its bucket(s);
+//   5. bucket_detect, one CTA per bucket, tables in shared memory:
+//      P1/P2/P3 the word filter of K2 (some accessing block per word, then
+//      "a second block" and "a write" stamps) -> candidates; E1-E3 the four
+//      per-byte minima over the candidates' bytes (any Y that X can race
+//      with is a candidate too) -> racing (byte, line) pairs, deduplicated
+//      per bucket (a byte lives in one bucket); first racing key per line.
+//      A bucket beyond the shared-memory tables is redone by the same code
+//      with tables in global memory sized for it (bucket_detect_big).
+constexpr uint32_t BT = 256;      // threads per detect CTA
+constexpr uint32_t BCAP = 1024;   // records of a shared-memory bucket
+constexpr uint32_t BWS = 2048;    // word-table slots (shared)
+constexpr uint32_t BCC = 128;     // candidates (shared)
+constexpr uint32_t BBS = 512;     // candidate-byte slots (shared)
+constexpr uint32_t BDS = 512;     // reported (byte, line) slots (shared)
+constexpr uint32_t BLT = 32;      // line-first cache entries
+constexpr unsigned long long KEMPTY = 0ull;
+constexpr unsigned long long TSMAX = ~0ull;
+
+__device__ __forceinline__ uint32_t ts_bid(unsigned long long ts) {
+  return (uint32_t)(ts >> 11) & (MCKG_MAX_BID - 1);
+}
+__device__ __forceinline__ unsigned long long ga_ts(const mckg_gaccess& r) {
+  return ts_key(r.sweep, r.b & 0xFFFFFFu, ga_tid(r.a));
+}
+__device__ __forceinline__ uint32_t hash64(unsigned long long k, uint32_t mask) {
+  return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> 40) & mask;
 }
 
-__global__ void word_count_kernel(const mckg_gaccess* ev, uint64_t n, uint32_t* nw) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    nw[i] = words_of(ev[i].a);
-}
+// The tables of one bucket (shared memory or global memory).
+struct BTab {
+  unsigned long long* wkey;  // stamp << 41 | word address + 1
+  uint32_t* wtag;            // some accessing block
+  uint32_t* wflag;           // {second-block stamp u16, write stamp u16}
+  uint32_t wmask;
+  uint32_t* cand;            // candidate record indices
+  uint32_t ccap;
+  unsigned long long* bkey;  // stamp << 41 | byte address + 1
+  unsigned long long* bmin;  // [4 * slots]: f1, f2, w1, w2
+  uint32_t bmask;
+  unsigned long long* dkey;  // reported (byte, line): stamp << 56 | (byte & 2^40-1) << 16 | line
+  uint32_t dmask;
+};
 
-__global__ void word_emit_kernel(const mckg_gaccess* ev, uint64_t n, const uint32_t* off, uint64_t addr_lo,
-                                 unsigned long long* keys, uint32_t* vals) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t a = ev[i].a;
-    const uint32_t k = words_of(a);
-    const uint64_t w0 = (ga_addr(a) - addr_lo) >> 2;
-    for (uint32_t q = 0; q < k; ++q) {
-      keys[off[i] + q] = w0 + q;
-      vals[off[i] + q] = (uint32_t)i;
+// open-addressing insert / find; keys carry the bucket stamp, so keys of
+// other stamps read as empty.  Returns the slot, or ~0u when full.
+__device__ __forceinline__ uint32_t tab_insert(unsigned long long* keys, uint32_t mask, unsigned long long key,
+                                               uint32_t stamp_shift, bool* claimed) {
+  const unsigned long long st = key >> stamp_shift;
+  uint32_t h = hash64(key, mask);
+  *claimed = false;
+  for (uint32_t p = 0; p <= mask; ++p) {
+    unsigned long long cur = keys[h];
+    while ((cur >> stamp_shift) != st) {  // stale or empty: claim it
+      const unsigned long long old = atomicCAS(keys + h, cur, key);
+      if (old == cur) {
+        *claimed = true;
+        return h;
+      }
+      cur = old;
     }
+    if (cur == key) return h;
+    h = (h + 1) & mask;
   }
+  return ~0u;
 }
 
-constexpr uint32_t LT = 64;
+__device__ __forceinline__ uint32_t tab_find(const unsigned long long* keys, uint32_t mask, unsigned long long key) {
+  uint32_t h = hash64(key, mask);
+  for (uint32_t p = 0; p <= mask; ++p) {
+    const unsigned long long cur = keys[h];
+    if (cur == key) return h;
+    h = (h + 1) & mask;
+  }
+  return ~0u;
+}
 
-__global__ void scan_runs_kernel(const mckg_gaccess* ev, const unsigned long long* keys, const uint32_t* vals,
-                                 uint64_t m, uint64_t addr_lo, unsigned long long* out, unsigned long long cap,
-                                 unsigned long long* n_out, unsigned long long* line_first, uint32_t* status) {
-  __shared__ uint32_t s_line[LT];
-  __shared__ unsigned long long s_ts[LT];
-  for (uint32_t i = threadIdx.x; i < LT; i += blockDim.x) {
-    s_line[i] = 0xFFFFFFFFu;
-    s_ts[i] = ~0ull;
+struct BOut {
+  mckg_grace* races;
+  unsigned long long cap;
+  unsigned long long* n;
+  unsigned long long* line_first;
+  uint32_t* status;
+};
+
+// One bucket [blo, bhi) of m records at R, by the CTA.  Returns false (all
+// threads) when the tables overflow: the caller redoes the bucket with
+// bigger ones.  stamp: 1..2^23, unique per bucket processed by this CTA.
+__device__ bool detect_bucket(const mckg_gaccess* R, uint32_t m, uint64_t blo, uint64_t bhi, const BTab& T,
+                              uint32_t stamp, const BOut& O, uint32_t* s_line, unsigned long long* s_lts,
+                              uint32_t* s_cnt, uint32_t* s_flag) {
+  const uint32_t t = threadIdx.x;
+  const unsigned long long sk = (unsigned long long)stamp << 41;
+  const uint32_t st16 = stamp & 0xFFFFu ? stamp & 0xFFFFu : 1u;
+  if (t == 0) {
+    s_cnt[0] = 0;
+    *s_flag = 0;
   }
   __syncthreads();
-  for (uint64_t e0 = blockIdx.x * (uint64_t)blockDim.x; e0 < m; e0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = e0 + threadIdx.x;
-    if (e < m) {
-      const unsigned long long w = keys[e];
-      // a word touched by one access only cannot race: skip without loading
-      const bool single = (e == 0 || keys[e - 1] != w) && (e + 1 >= m || keys[e + 1] != w);
-      if (single) continue;
-      const mckg_gaccess X = ev[vals[e]];
-      const uint32_t xbid = X.b & 0xFFFFFFu, xtid = ga_tid(X.a);
-      const unsigned long long xts = ts_key(X.sweep, xbid, xtid);
-      const bool xw = ga_write(X.a);
-      const uint64_t wb = addr_lo + (w << 2);  // byte address of the word
-      const uint64_t xa = ga_addr(X.a);
-      // X's bytes inside this word, as a 4-bit mask
-      const uint64_t lo = xa > wb ? xa : wb, hi = (xa + ga_len(X.a)) < wb + 4 ? (xa + ga_len(X.a)) : wb + 4;
-      const uint32_t xm = ((1u << (uint32_t)(hi - lo)) - 1u) << (uint32_t)(lo - wb);
-      uint32_t raced = 0;
-      // the run of this word: walk both directions
-      for (int dir = -1; dir <= 1; dir += 2) {
-        for (uint64_t f = e + dir; f < m && (raced & xm) != xm; f += dir) {
-          if (keys[f] != w) break;
-          const mckg_gaccess Y = ev[vals[f]];
-          const uint32_t ybid = Y.b & 0xFFFFFFu;
-          if (ybid == xbid || !(xw || ga_write(Y.a))) continue;
-          if (ts_key(Y.sweep, ybid, ga_tid(Y.a)) >= xts) continue;
-          const uint64_t ya = ga_addr(Y.a);
-          const uint64_t ylo = ya > wb ? ya : wb, yhi = (ya + ga_len(Y.a)) < wb + 4 ? (ya + ga_len(Y.a)) : wb + 4;
-          if (ylo >= yhi) continue;
-          raced |= (((1u << (uint32_t)(yhi - ylo)) - 1u) << (uint32_t)(ylo - wb)) & xm;
-        }
+  // P1: claim a slot per touched word, store some accessing block
+  for (uint32_t i = t; i < m; i += blockDim.x) {
+    const mckg_gaccess r = R[i];
+    const uint64_t a = ga_addr(r.a);
+    const uint32_t len = ga_len(r.a);
+    const uint64_t b0 = a > blo ? a : blo, b1 = (a + len) < bhi ? (a + len) : bhi;
+    for (uint64_t w = b0 >> 2; (w << 2) < b1; ++w) {
+      bool cl;
+      const uint32_t h = tab_insert(T.wkey, T.wmask, sk | (w + 1), 41, &cl);
+      if (h == ~0u) {
+        *s_flag = 1;
+        break;
       }
-      if (raced) {
-        const int32_t line = ga_line(X.a, X.b);
-        for (uint32_t q = 0; q < 4; ++q) {
-          if (!((raced >> q) & 1u)) continue;
-          const unsigned long long i = atomicAdd(n_out, 1ull);
-          if (i < cap)
-            out[i] = ((unsigned long long)((wb + q) & 0xFFFFFFFFFFull) << 16) | ((uint32_t)line & 0xFFFFu);
-          else
-            atomicOr(status, (uint32_t)MCKG_ST_OVERFLOW);
-        }
-        if ((uint32_t)line < MCKG_MAX_LINES) {
-          uint32_t h = (uint32_t)line & (LT - 1);
-          bool done = false;
-          for (uint32_t p = 0; p < LT && !done; ++p) {
-            uint32_t v = s_line[h];
-            if (v == 0xFFFFFFFFu) {
-              const uint32_t old = atomicCAS(s_line + h, 0xFFFFFFFFu, (uint32_t)line);
-              v = old == 0xFFFFFFFFu ? (uint32_t)line : old;
-            }
-            if (v == (uint32_t)line) {
-              atomicMin(s_ts + h, xts);
-              done = true;
-            }
-            h = (h + 1) & (LT - 1);
+      if (cl) T.wflag[h] = 0u;
+      T.wtag[h] = r.b & 0xFFFFFFu;
+    }
+  }
+  __syncthreads();
+  if (*s_flag) return false;
+  // P2: words touched by a second block; written words
+  for (uint32_t i = t; i < m; i += blockDim.x) {
+    const mckg_gaccess r = R[i];
+    const uint64_t a = ga_addr(r.a);
+    const uint32_t len = ga_len(r.a), bid = r.b & 0xFFFFFFu;
+    const bool wr = ga_write(r.a);
+    const uint64_t b0 = a > blo ? a : blo, b1 = (a + len) < bhi ? (a + len) : bhi;
+    for (uint64_t w = b0 >> 2; (w << 2) < b1; ++w) {
+      const uint32_t h = tab_find(T.wkey, T.wmask, sk | (w + 1));
+      uint16_t* f = reinterpret_cast<uint16_t*>(T.wflag + h);
+      if (T.wtag[h] != bid) f[0] = (uint16_t)st16;
+      if (wr) f[1] = (uint16_t)st16;
+    }
+  }
+  __syncthreads();
+  // P3: candidates = records with a word touched by two blocks and written
+  for (uint32_t i = t; i < m; i += blockDim.x) {
+    const mckg_gaccess r = R[i];
+    const uint64_t a = ga_addr(r.a);
+    const uint32_t len = ga_len(r.a);
+    const uint64_t b0 = a > blo ? a : blo, b1 = (a + len) < bhi ? (a + len) : bhi;
+    bool c = false;
+    for (uint64_t w = b0 >> 2; (w << 2) < b1; ++w)
+      c |= T.wflag[tab_find(T.wkey, T.wmask, sk | (w + 1))] == (st16 | (st16 << 16));
+    if (c) {
+      const uint32_t k = atomicAdd(s_cnt, 1u);
+      if (k < T.ccap) T.cand[k] = i; else *s_flag = 1;
+    }
+  }
+  __syncthreads();
+  if (*s_flag) return false;
+  const uint32_t nc = s_cnt[0];
+  if (nc == 0) return true;
+  // E1: claim the candidates' bytes, initialise their minima
+  for (uint32_t q = t; q < nc * 8u; q += blockDim.x) {
+    const mckg_gaccess r = R[T.cand[q >> 3]];
+    const uint64_t a = ga_addr(r.a) + (q & 7u);
+    if ((q & 7u) >= ga_len(r.a) || a < blo || a >= bhi) continue;
+    bool cl;
+    const uint32_t h = tab_insert(T.bkey, T.bmask, sk | (a + 1), 41, &cl);
+    if (h == ~0u) {
+      *s_flag = 1;
+      continue;
+    }
+    if (cl) {
+      T.bmin[4 * h] = TSMAX;
+      T.bmin[4 * h + 1] = TSMAX;
+      T.bmin[4 * h + 2] = TSMAX;
+      T.bmin[4 * h + 3] = TSMAX;
+    }
+  }
+  __syncthreads();
+  if (*s_flag) return false;
+  // E2: f1 / w1, then E3: f2 / w2 (another block than f1's / w1's)
+  for (int pass = 0; pass < 2; ++pass) {
+    for (uint32_t q = t; q < nc * 8u; q += blockDim.x) {
+      const mckg_gaccess r = R[T.cand[q >> 3]];
+      const uint64_t a = ga_addr(r.a) + (q & 7u);
+      if ((q & 7u) >= ga_len(r.a) || a < blo || a >= bhi) continue;
+      const uint32_t h = tab_find(T.bkey, T.bmask, sk | (a + 1));
+      const unsigned long long ts = ga_ts(r);
+      const bool wr = ga_write(r.a);
+      unsigned long long* mn = T.bmin + 4 * h;
+      if (pass == 0) {
+        atomicMin(mn, ts);
+        if (wr) atomicMin(mn + 2, ts);
+      } else {
+        const uint32_t bid = r.b & 0xFFFFFFu;
+        if (ts_bid(mn[0]) != bid) atomicMin(mn + 1, ts);
+        if (wr && ts_bid(mn[2]) != bid) atomicMin(mn + 3, ts);
+      }
+    }
+    __syncthreads();
+  }
+  // E4: racing bytes -> (byte, line) once per bucket; first key per line
+  for (uint32_t q = t; q < nc * 8u; q += blockDim.x) {
+    const mckg_gaccess r = R[T.cand[q >> 3]];
+    const uint64_t a = ga_addr(r.a) + (q & 7u);
+    if ((q & 7u) >= ga_len(r.a) || a < blo || a >= bhi) continue;
+    const unsigned long long* mn = T.bmin + 4 * tab_find(T.bkey, T.bmask, sk | (a + 1));
+    const unsigned long long ts = ga_ts(r);
+    const uint32_t bid = r.b & 0xFFFFFFu;
+    bool race;
+    if (ga_write(r.a))
+      race = ts_bid(mn[0]) != bid || mn[1] < ts;
+    else
+      race = (mn[2] != TSMAX && ts_bid(mn[2]) != bid && mn[2] < ts) || (ts_bid(mn[2]) == bid && mn[3] < ts);
+    if (!race) continue;
+    const int32_t line = ga_line(r.a, r.b);
+    const unsigned long long dk =
+        ((unsigned long long)(stamp & 0xFFu) << 56) | ((a & 0xFFFFFFFFFFull) << 16) | ((uint32_t)line & 0xFFFFu);
+    bool fresh;
+    // dedup keys: stamp in the top 8 bits (bucket-local tables; 0 = empty)
+    const uint32_t h = tab_insert(T.dkey, T.dmask, dk, 56, &fresh);
+    if (h == ~0u) {
+      atomicOr(O.status, (uint32_t)MCKG_ST_DUP);
+      fresh = true;
+    }
+    if (fresh) {
+      const unsigned long long k = atomicAdd(O.n, 1ull);
+      if (k < O.cap)
+        O.races[k] = mckg_grace{a, line, 0};
+      else
+        atomicOr(O.status, (uint32_t)MCKG_ST_OVERFLOW);
+    }
+    // first racing key of the line: a CTA cache, global atomicMin otherwise
+    const uint32_t l = (uint32_t)line;
+    uint32_t hh = l & (BLT - 1);
+    bool done = false;
+    for (uint32_t p = 0; p < BLT && !done; ++p) {
+      uint32_t v = s_line[hh];
+      if (v == 0xFFFFFFFFu) {
+        const uint32_t old = atomicCAS(s_line + hh, 0xFFFFFFFFu, l);
+        v = old == 0xFFFFFFFFu ? l : old;
+      }
+      if (v == l) {
+        atomicMin(s_lts + hh, ts);
+        done = true;
+      }
+      hh = (hh + 1) & (BLT - 1);
+    }
+    if (!done) atomicMin(O.line_first + l, ts);
+  }
+  __syncthreads();
+  return true;
+}
+
+// bucket b's byte range under the sampled span (edge buckets are open)
+__device__ __forceinline__ void bucket_range(uint32_t b, uint32_t nb, uint32_t shift, uint64_t base, uint64_t* lo,
+                                             uint64_t* hi) {
+  *lo = b == 0 ? 0ull : base + ((uint64_t)b << shift);
+  *hi = b + 1 >= nb ? ~0ull : base + ((uint64_t)(b + 1) << shift);
+}
+
+__device__ __forceinline__ uint32_t bucket_of(uint64_t a, uint32_t nb, uint32_t shift, uint64_t base) {
+  if (a < base) return 0;
+  const uint64_t q = (a - base) >> shift;
+  return q >= nb ? nb - 1 : (uint32_t)q;
+}
+
+// min / max address over one record per stride-sized window, at a hashed
+// position inside the window (a fixed position can alias the input's period)
+__global__ void span_sample_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t stride, unsigned long long* mm) {
+  unsigned long long lo = ~0ull, hi = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w * stride < n;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t i = w * stride + sm64(w) % stride;
+    if (i >= n) i = n - 1;
+    const uint64_t a = ga_addr(ev[i].a);
+    lo = a < lo ? a : lo;
+    hi = a > hi ? a : hi;
+  }
+  atomicMin(mm, lo);
+  atomicMax(mm + 1, hi);
+}
+
+__global__ void bucket_count_kernel(const mckg_gaccess* ev, uint64_t n, uint32_t nb, uint32_t shift, uint64_t base,
+                                    uint32_t* cnt, uint32_t* status) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < n; i0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
+    if (i < n) {
+      const mckg_gaccess r = ev[i];
+      const uint32_t len = ga_len(r.a);
+      if ((r.b & 0xFFFFFFu) >= MCKG_MAX_BID || len - 1u >= MCKG_MAX_LEN) {
+        atomicOr(status, (uint32_t)MCKG_ST_RANGE);
+      } else {
+        const uint64_t a = ga_addr(r.a);
+        b0 = bucket_of(a, nb, shift, base);
+        const uint32_t bl = bucket_of(a + len - 1u, nb, shift, base);
+        if (bl != b0) b1 = bl;
+      }
+    }
+    uint32_t g = __match_any_sync(0xFFFFFFFFu, b0);
+    if (b0 != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(g) - 1)) atomicAdd(cnt + b0, (uint32_t)__popc(g));
+    if (__any_sync(0xFFFFFFFFu, b1 != 0xFFFFFFFFu) && b1 != 0xFFFFFFFFu) atomicAdd(cnt + b1, 1u);
+  }
+}
+
+__global__ void bucket_scatter_kernel(const mckg_gaccess* ev, uint64_t n, uint32_t nb, uint32_t shift,
+                                      uint64_t base, const uint64_t* off, uint32_t* cur, mckg_gaccess* out) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < n; i0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    uint32_t b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
+    mckg_gaccess r{};
+    if (i < n) {
+      r = ev[i];
+      const uint32_t len = ga_len(r.a);
+      if ((r.b & 0xFFFFFFu) < MCKG_MAX_BID && len - 1u < MCKG_MAX_LEN) {
+        const uint64_t a = ga_addr(r.a);
+        b0 = bucket_of(a, nb, shift, base);
+        const uint32_t bl = bucket_of(a + len - 1u, nb, shift, base);
+        if (bl != b0) b1 = bl;
+      }
+    }
+    const uint32_t g = __match_any_sync(0xFFFFFFFFu, b0);
+    const int leader = __ffs(g) - 1;
+    uint32_t p = 0;
+    if (b0 != 0xFFFFFFFFu && lane == (uint32_t)leader) p = atomicAdd(cur + b0, (uint32_t)__popc(g));
+    p = __shfl_sync(0xFFFFFFFFu, p, leader) + __popc(g & ((1u << lane) - 1u));
+    if (b0 != 0xFFFFFFFFu) out[off[b0] + p] = r;
+    if (b1 != 0xFFFFFFFFu) out[off[b1] + atomicAdd(cur + b1, 1u)] = r;
+  }
+}
+
+// ---- exclusive scan of the bucket counts (three kernels) ----
+constexpr uint32_t SCT = 1024;  // elements per scan tile
+
+__global__ void scan_tiles_kernel(const uint32_t* in, uint32_t n, uint64_t* tile_sum) {
+  __shared__ uint64_t ws[32];
+  const uint32_t i = blockIdx.x * SCT + threadIdx.x;
+  uint64_t v = i < n ? in[i] : 0u;
+  for (int d = 16; d; d >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, d);
+  if ((threadIdx.x & 31u) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint64_t s = ws[threadIdx.x];
+    for (int d = 16; d; d >>= 1) s += __shfl_down_sync(0xFFFFFFFFu, s, d);
+    if (threadIdx.x == 0) tile_sum[blockIdx.x] = s;
+  }
+}
+
+// exclusive scan of <= SCT * SCT tile sums by one CTA, in place
+__global__ void scan_sums_kernel(uint64_t* sums, uint32_t n) {
+  __shared__ uint64_t ws[32];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  for (uint32_t c0 = 0; c0 < n; c0 += SCT) {
+    __syncthreads();
+    const uint32_t i = c0 + threadIdx.x;
+    const uint64_t v = i < n ? sums[i] : 0u;
+    uint64_t x = v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+      if ((threadIdx.x & 31u) >= (uint32_t)d) x += y;
+    }
+    if ((threadIdx.x & 31u) == 31u) ws[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint64_t w = ws[threadIdx.x];
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, w, d);
+        if (threadIdx.x >= (uint32_t)d) w += y;
+      }
+      ws[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const uint64_t excl = carry + (threadIdx.x >= 32 ? ws[(threadIdx.x >> 5) - 1] : 0u) + x - v;
+    if (i < n) sums[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == SCT - 1) carry = excl + v;
+  }
+}
+
+__global__ void scan_apply_kernel(const uint32_t* in, uint32_t n, const uint64_t* tile_off, uint64_t* out) {
+  __shared__ uint64_t ws[32];
+  const uint32_t i = blockIdx.x * SCT + threadIdx.x;
+  const uint64_t v = i < n ? in[i] : 0u;
+  uint64_t x = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+    if ((threadIdx.x & 31u) >= (uint32_t)d) x += y;
+  }
+  if ((threadIdx.x & 31u) == 31u) ws[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint64_t w = ws[threadIdx.x];
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, w, d);
+      if (threadIdx.x >= (uint32_t)d) w += y;
+    }
+    ws[threadIdx.x] = w;
+  }
+  __syncthreads();
+  const uint64_t excl = tile_off[blockIdx.x] + (threadIdx.x >= 32 ? ws[(threadIdx.x >> 5) - 1] : 0u) + x - v;
+  if (i < n) out[i] = excl;
+  if (i == n - 1) out[n] = excl + v;
+}
+
+// ---- the dense-span fast path: one warp per 4 KiB bucket ----
+// Buckets of FB_WORDS words, direct-indexed tag arrays per warp (no hashing),
+// races staged per warp and appended FB_STAGE at a time,
+// the K2 word filter with __syncwarp between its phases, and the exact pass
+// on <= 32 candidates (one per lane, same-word groups by __match_any_sync).
+// A bucket with more than FB_MAX records, a record crossing a word, or more
+// than 32 candidates is handed to the general kernel (bucket_detect_kernel).
+constexpr uint32_t FB_SHIFT = 11;             // 2 KiB buckets
+constexpr uint32_t FB_WORDS = 1u << (FB_SHIFT - 2);
+constexpr uint32_t FB_ROWS = 16;               // records per lane
+constexpr uint32_t FB_MAX = FB_ROWS * 32;
+constexpr uint32_t FB_WARPS = 16;
+constexpr int FB_BR = 2;                       // rows per load batch
+constexpr uint32_t FB_STAGE = 64;              // staged races per warp
+constexpr uint32_t FB_WARP_BYTES = FB_WORDS * 8 + 32 * 4 + FB_STAGE * 16;
+constexpr uint32_t FB_SMEM = FB_WARPS * FB_WARP_BYTES;
+
+struct LineCache {  // lane-owned first-racing-key cache of one warp
+  uint32_t line;
+  unsigned long long ts;
+  uint32_t next;
+};
+
+__device__ __forceinline__ void lc_note(LineCache& C, unsigned long long* line_first, uint32_t L,
+                                        unsigned long long T) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t own = __ballot_sync(0xFFFFFFFFu, C.line == L);
+  if (own) {
+    if (lane == (uint32_t)(__ffs(own) - 1) && T < C.ts) C.ts = T;
+  } else {
+    if (lane == C.next) {
+      if (C.line != 0xFFFFFFFFu) atomicMin(line_first + C.line, C.ts);
+      C.line = L;
+      C.ts = T;
+    }
+    C.next = (C.next + 1u) & 31u;
+  }
+}
+
+// appends a warp's staged races (one atomic per flush)
+__device__ __forceinline__ void fb_flush(const BOut& O, const mckg_grace* stg, uint32_t n, uint32_t& flags) {
+  const uint32_t lane = threadIdx.x & 31u;
+  __syncwarp();
+  if (n == 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(O.n, (unsigned long long)n);
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  for (uint32_t i = lane; i < n; i += 32) {
+    if (base + i < O.cap)
+      O.races[base + i] = stg[i];
+    else
+      flags |= MCKG_ST_OVERFLOW;
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mckg_gaccess* recs, const uint64_t* off,
+                                                                       uint32_t nb, uint64_t base, BOut O,
+                                                                       uint32_t* big, uint32_t* nbig) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  uint32_t* tag = reinterpret_cast<uint32_t*>(sm + warp * FB_WARP_BYTES);
+  uint32_t* flg = tag + FB_WORDS;
+  uint32_t* cl = flg + FB_WORDS;
+  mckg_grace* stg = reinterpret_cast<mckg_grace*>(cl + 32);  // staged races
+  uint32_t nstg = 0;                                          // warp-uniform
+  for (uint32_t i = lane; i < FB_WORDS; i += 32) flg[i] = 0u;
+  __syncwarp();
+  LineCache C{0xFFFFFFFFu, ~0ull, 0u};
+  uint32_t stamp = 0;
+  uint32_t flags = 0;
+  const uint32_t nwarps = gridDim.x * FB_WARPS;
+  for (uint32_t b = blockIdx.x * FB_WARPS + warp; b < nb; b += nwarps) {
+    const uint64_t o0 = off[b], o1 = off[b + 1];
+    if (o1 - o0 < 2) continue;  // a lone record cannot race
+    if (o1 - o0 > FB_MAX) {
+      if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
+      continue;
+    }
+    const uint32_t m = (uint32_t)(o1 - o0);
+    const mckg_gaccess* R = recs + o0;
+    uint64_t blo, bhi;
+    bucket_range(b, nb, FB_SHIFT, base, &blo, &bhi);
+    // load + pack: word (10 bits) | write << 10 | bid << 11 (rows of 32
+    // records, FB_BR rows in flight ahead of the decode)
+    uint32_t pk[FB_ROWS];
+    bool bad = false;
+    const uint4* R4 = reinterpret_cast<const uint4*>(R);
+    uint4 buf[2][FB_BR];
+#pragma unroll
+    for (int q = 0; q < FB_BR; ++q) {
+      const uint32_t i = (uint32_t)q * 32u + lane;
+      buf[0][q] = i < m ? __ldg(R4 + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int h = 0; h < (int)(FB_ROWS / FB_BR); ++h) {
+      if ((uint32_t)h * FB_BR * 32u < m) {  // warp-uniform
+        if (h + 1 < (int)(FB_ROWS / FB_BR)) {
+#pragma unroll
+          for (int q = 0; q < FB_BR; ++q) {
+            const uint32_t i = (uint32_t)((h + 1) * FB_BR + q) * 32u + lane;
+            buf[(h + 1) & 1][q] = i < m ? __ldg(R4 + i) : make_uint4(0, 0, 0, 0);
           }
-          if (!done) atomicMin(line_first + line, xts);
-        } else {
-          atomicOr(status, (uint32_t)MCKG_ST_RANGE);
         }
+#pragma unroll
+        for (int q = 0; q < FB_BR; ++q) {
+          const int j = h * FB_BR + q;
+          const uint32_t i = (uint32_t)j * 32u + lane;
+          const uint4 r = buf[h & 1][q];
+          const unsigned long long a64 = ((unsigned long long)r.y << 32) | r.x;
+          const uint64_t a = ga_addr(a64);
+          const bool in = i < m;
+          bad |= in && ((a & 3u) + ga_len(a64) > 4u || a < blo || a >= bhi);
+          pk[j] = in ? (uint32_t)((a - blo) >> 2) | (ga_write(a64) << 10) | ((r.w & 0x1FFFFFu) << 11) : 0xFFFFFFFFu;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < FB_BR; ++q) pk[h * FB_BR + q] = 0xFFFFFFFFu;
       }
+    }
+    if (__any_sync(0xFFFFFFFFu, bad)) {
+      if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
+      continue;
+    }
+    stamp = stamp == 0xFFFFu ? 1u : stamp + 1u;
+    const uint32_t pat = stamp | (stamp << 16);
+    // P1 / P2 / P3 (__syncwarp between them)
+#pragma unroll
+    for (int j = 0; j < (int)FB_ROWS; ++j)
+      if (pk[j] != 0xFFFFFFFFu) tag[pk[j] & (FB_WORDS - 1)] = pk[j] >> 11;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < (int)FB_ROWS; ++j) {
+      const uint32_t x = pk[j];
+      if (x == 0xFFFFFFFFu) continue;
+      uint16_t* f = reinterpret_cast<uint16_t*>(flg + (x & (FB_WORDS - 1)));
+      if (tag[x & (FB_WORDS - 1)] != (x >> 11)) f[0] = (uint16_t)stamp;
+      if (x & 0x400u) f[1] = (uint16_t)stamp;
+    }
+    __syncwarp();
+    uint32_t cm = 0;
+#pragma unroll
+    for (int j = 0; j < (int)FB_ROWS; ++j)
+      if (pk[j] != 0xFFFFFFFFu && flg[pk[j] & (FB_WORDS - 1)] == pat) cm |= 1u << j;
+    const uint32_t c = __popc(cm);
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= (uint32_t)d) incl += t;
+    }
+    const uint32_t nc = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (nc == 0) continue;
+    if (nc > 32u) {
+      if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
+      continue;
+    }
+    uint32_t pos = incl - c;
+    for (uint32_t g = cm; g; g &= g - 1u) cl[pos++] = (uint32_t)(__ffs(g) - 1) * 32u + lane;
+    __syncwarp();
+    // exact pass: lane per candidate X; same-word group by match_any
+    const bool act = lane < nc;
+    mckg_gaccess X{};
+    if (act) X = R[cl[lane]];
+    const uint64_t xa = ga_addr(X.a);
+    const uint32_t xw = act ? (uint32_t)((xa - blo) >> 2) : 0xFFFF0000u + lane;
+    const uint32_t xmask = act ? ((1u << ga_len(X.a)) - 1u) << (xa & 3u) : 0u;
+    const unsigned long long xts = ga_ts(X);
+    const uint32_t xbid = X.b & 0xFFFFFFu, xwr = ga_write(X.a);
+    uint32_t rest = __match_any_sync(0xFFFFFFFFu, xw) & ~(1u << lane);
+    uint32_t race = 0;
+    while (__any_sync(0xFFFFFFFFu, rest != 0u)) {
+      const uint32_t y = rest ? (uint32_t)__ffs(rest) - 1u : lane;
+      rest &= rest - 1u;
+      const uint32_t ymask = __shfl_sync(0xFFFFFFFFu, xmask, y), ybid = __shfl_sync(0xFFFFFFFFu, xbid, y),
+                     ywr = __shfl_sync(0xFFFFFFFFu, xwr, y);
+      const unsigned long long yts = ((unsigned long long)__shfl_sync(0xFFFFFFFFu, (uint32_t)(xts >> 32), y) << 32) |
+                                     __shfl_sync(0xFFFFFFFFu, (uint32_t)xts, y);
+      if (y != lane && yts < xts && ybid != xbid && (xwr | ywr)) race |= xmask & ymask;
+    }
+    const uint32_t rm = __ballot_sync(0xFFFFFFFFu, race != 0u);
+    if (!rm) continue;
+    const uint32_t line = (uint32_t)ga_line(X.a, X.b);
+    // first racing key per line
+    for (uint32_t left = rm; left;) {
+      const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, __ffs(left) - 1);
+      const bool in = race && line == L;
+      const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, in ? (uint32_t)(xts >> 32) : ~0u);
+      const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, in && (uint32_t)(xts >> 32) == mh ? (uint32_t)xts : ~0u);
+      left &= ~__ballot_sync(0xFFFFFFFFu, in);
+      lc_note(C, O.line_first, L, ((unsigned long long)mh << 32) | ml);
+    }
+    // one report per racing (byte, line): the group of a (word, line) ORs
+    // its members' byte masks, its lowest racing lane reports
+    const uint32_t gkey = race ? ((uint32_t)((xa - blo) >> 2) << 16) | (line & 0xFFFFu) : 0xFFFFFFFFu - lane;
+    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, gkey);
+    const uint32_t mine = __reduce_or_sync(grp, race);
+    const bool rep = race && (grp & rm & ((1u << lane) - 1u)) == 0u;
+    const uint32_t cnt = rep ? __popc(mine) : 0u;
+    uint32_t ci = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ci, d);
+      if (lane >= (uint32_t)d) ci += t;
+    }
+    const uint32_t tot = __shfl_sync(0xFFFFFFFFu, ci, 31);
+    if (nstg + tot > FB_STAGE) {
+      fb_flush(O, stg, nstg, flags);
+      nstg = 0;
+    }
+    if (tot > FB_STAGE) {  // more than a buffer from one bucket: straight out
+      unsigned long long base_o = 0;
+      if (lane == 0) base_o = atomicAdd(O.n, (unsigned long long)tot);
+      base_o = __shfl_sync(0xFFFFFFFFu, base_o, 0) + ci - cnt;
+      if (rep)
+        for (uint32_t q = mine; q; q &= q - 1u, ++base_o) {
+          if (base_o < O.cap)
+            O.races[base_o] = mckg_grace{(xa & ~3ull) + (uint32_t)(__ffs(q) - 1), (int32_t)line, 0};
+          else
+            flags |= MCKG_ST_OVERFLOW;
+        }
+      continue;
+    }
+    if (rep) {
+      uint32_t p = nstg + ci - cnt;
+      for (uint32_t q = mine; q; q &= q - 1u, ++p)
+        stg[p] = mckg_grace{(xa & ~3ull) + (uint32_t)(__ffs(q) - 1), (int32_t)line, 0};
+    }
+    nstg += tot;
+    __syncwarp();
+  }
+  fb_flush(O, stg, nstg, flags);
+  if (C.line != 0xFFFFFFFFu) atomicMin(O.line_first + C.line, C.ts);
+  flags = __reduce_or_sync(0xFFFFFFFFu, flags);
+  if (lane == 0 && flags) atomicOr(O.status, flags);
+}
+
+// shared-memory layout of bucket_detect (bytes)
+constexpr uint32_t BD_WKEY = 0;
+constexpr uint32_t BD_WTAG = BD_WKEY + BWS * 8;
+constexpr uint32_t BD_WFLAG = BD_WTAG + BWS * 4;
+constexpr uint32_t BD_BKEY = BD_WFLAG + BWS * 4;
+constexpr uint32_t BD_BMIN = BD_BKEY + BBS * 8;
+constexpr uint32_t BD_DKEY = BD_BMIN + BBS * 32;
+constexpr uint32_t BD_CAND = BD_DKEY + BDS * 8;
+constexpr uint32_t BD_SMEM = BD_CAND + BCC * 4;
+
+// One CTA per bucket (grid-stride); buckets over BCAP records or whose tables
+// overflow go to the big list.
+__global__ void __launch_bounds__(BT) bucket_detect_kernel(const mckg_gaccess* recs, const uint64_t* off, uint32_t nb,
+                                                           uint32_t shift, uint64_t base, const uint32_t* list,
+                                                           const uint32_t* nlist, BOut O, uint32_t* big,
+                                                           uint32_t* nbig) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint32_t s_line[BLT];
+  __shared__ unsigned long long s_lts[BLT];
+  __shared__ uint32_t s_cnt[1], s_flag[1];
+  BTab T;
+  T.wkey = reinterpret_cast<unsigned long long*>(sm + BD_WKEY);
+  T.wtag = reinterpret_cast<uint32_t*>(sm + BD_WTAG);
+  T.wflag = reinterpret_cast<uint32_t*>(sm + BD_WFLAG);
+  T.wmask = BWS - 1;
+  T.bkey = reinterpret_cast<unsigned long long*>(sm + BD_BKEY);
+  T.bmin = reinterpret_cast<unsigned long long*>(sm + BD_BMIN);
+  T.bmask = BBS - 1;
+  T.dkey = reinterpret_cast<unsigned long long*>(sm + BD_DKEY);
+  T.dmask = BDS - 1;
+  T.cand = reinterpret_cast<uint32_t*>(sm + BD_CAND);
+  T.ccap = BCC;
+  for (uint32_t i = threadIdx.x; i < BWS; i += BT) T.wkey[i] = KEMPTY;
+  for (uint32_t i = threadIdx.x; i < BBS; i += BT) T.bkey[i] = KEMPTY;
+  for (uint32_t i = threadIdx.x; i < BDS; i += BT) T.dkey[i] = KEMPTY;
+  for (uint32_t i = threadIdx.x; i < BLT; i += BT) {
+    s_line[i] = 0xFFFFFFFFu;
+    s_lts[i] = ~0ull;
+  }
+  __syncthreads();
+  uint32_t stamp = 0;
+  const uint32_t nwork = list ? *nlist : nb;
+  for (uint32_t jb = blockIdx.x; jb < nwork; jb += gridDim.x) {
+    const uint32_t b = list ? list[jb] : jb;
+    const uint64_t o0 = off[b], m = off[b + 1] - o0;
+    if (m < 2) continue;  // a lone record cannot race
+    if (m > BCAP) {
+      if (threadIdx.x == 0) big[atomicAdd(nbig, 1u)] = b;
+      continue;
+    }
+    // stamps 1..255 (the dedup keys keep 8 bits): re-clear the tables on wrap
+    if (++stamp == 256u) {
+      stamp = 1;
+      for (uint32_t i = threadIdx.x; i < BWS; i += BT) T.wkey[i] = KEMPTY;
+      for (uint32_t i = threadIdx.x; i < BBS; i += BT) T.bkey[i] = KEMPTY;
+      for (uint32_t i = threadIdx.x; i < BDS; i += BT) T.dkey[i] = KEMPTY;
+      __syncthreads();
+    }
+    uint64_t blo, bhi;
+    bucket_range(b, nb, shift, base, &blo, &bhi);
+    if (!detect_bucket(recs + o0, (uint32_t)m, blo, bhi, T, stamp, O, s_line, s_lts, s_cnt, s_flag)) {
+      if (threadIdx.x == 0) big[atomicAdd(nbig, 1u)] = b;
+      __syncthreads();
     }
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < LT; i += blockDim.x)
-    if (s_line[i] != 0xFFFFFFFFu) atomicMin(line_first + s_line[i], s_ts[i]);
+  for (uint32_t i = threadIdx.x; i < BLT; i += BT)
+    if (s_line[i] != 0xFFFFFFFFu) atomicMin(O.line_first + s_line[i], s_lts[i]);
 }
 
-__global__ void decode_races_kernel(const unsigned long long* k, const unsigned long long* n_dev,
-                                    mckg_grace* out, uint64_t cap) {
-  const uint64_t n = *n_dev;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n && i < cap;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long v = k[i];
-    out[i] = mckg_grace{v >> 16, (int32_t)(v & 0xFFFFu), 0};
+// One big bucket with tables in global memory (zeroed by the caller, stamp 1).
+__global__ void __launch_bounds__(BT) bucket_detect_big_kernel(const mckg_gaccess* recs, const uint64_t* off,
+                                                               uint32_t b, uint32_t nb, uint32_t shift, uint64_t base,
+                                                               BTab T, BOut O) {
+  __shared__ uint32_t s_line[BLT];
+  __shared__ unsigned long long s_lts[BLT];
+  __shared__ uint32_t s_cnt[1], s_flag[1];
+  for (uint32_t i = threadIdx.x; i < BLT; i += BT) {
+    s_line[i] = 0xFFFFFFFFu;
+    s_lts[i] = ~0ull;
   }
+  __syncthreads();
+  const uint64_t o0 = off[b], m = off[b + 1] - o0;
+  uint64_t blo, bhi;
+  bucket_range(b, nb, shift, base, &blo, &bhi);
+  if (!detect_bucket(recs + o0, (uint32_t)m, blo, bhi, T, 1u, O, s_line, s_lts, s_cnt, s_flag) && threadIdx.x == 0)
+    atomicOr(O.status, (uint32_t)MCKG_ST_RANGE);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < BLT; i += BT)
+    if (s_line[i] != 0xFFFFFFFFu) atomicMin(O.line_first + s_line[i], s_lts[i]);
 }
 
 uint32_t grid_for(uint64_t n, uint32_t per_sm = 8) {
@@ -308,76 +939,138 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
     set_error("mckg_detect_global: more than 2^32 records on one rank");
     return MCKG_E_RANGE;
   }
+  (void)addr_lo;  // buckets follow the sampled span of the records themselves
   cudaStream_t s = (cudaStream_t)stream;
   keep_pool_memory();
   MCKG_CUDA_TRY(cudaMemsetAsync(n_races, 0, sizeof(unsigned long long), s));
   if (n == 0) return MCKG_OK;
-  uint32_t *nw = nullptr, *off = nullptr, *vals = nullptr, *vals2 = nullptr;
-  unsigned long long *keys = nullptr, *keys2 = nullptr, *tmp_keys = nullptr, *uniq = nullptr;
-  void* tmp = nullptr;
-  size_t tmp_bytes = 0, t2 = 0;
-  uint32_t m32 = 0;
-  const uint32_t g = grid_for(n);
-  MCKG_CUDA_TRY(cudaMallocAsync(&nw, n * sizeof(uint32_t), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&off, (n + 1) * sizeof(uint32_t), s));
-  word_count_kernel<<<g, 256, 0, s>>>(events, n, nw);
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, nw, off, (int64_t)n + 0, s);
-  MCKG_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
-  MCKG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, nw, off, (int64_t)n, s));
-  cudaFreeAsync(tmp, s);
-  // total word entries m = off[n-1] + nw[n-1]
-  uint32_t last[2];
-  MCKG_CUDA_TRY(cudaMemcpyAsync(&last[0], off + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  MCKG_CUDA_TRY(cudaMemcpyAsync(&last[1], nw + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  uint32_t launches = 0;
+  // 1. span from a strided sample -> bucket shift (~256 records per bucket)
+  unsigned long long* mm = nullptr;
+  MCKG_CUDA_TRY(cudaMallocAsync(&mm, 2 * sizeof(unsigned long long), s));
+  const unsigned long long init[2] = {~0ull, 0ull};
+  MCKG_CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s));
+  const uint64_t stride = n > (1u << 16) ? n >> 16 : 1;
+  span_sample_kernel<<<grid_for(n / stride), 256, 0, s>>>(events, n, stride, mm);
+  ++launches;
+  unsigned long long hm[2];
+  MCKG_CUDA_TRY(cudaMemcpyAsync(hm, mm, sizeof hm, cudaMemcpyDeviceToHost, s));
   MCKG_CUDA_TRY(cudaStreamSynchronize(s));
-  m32 = last[0] + last[1];
-  const uint64_t m = m32;
-  MCKG_CUDA_TRY(cudaMallocAsync(&keys, m * sizeof(unsigned long long), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&keys2, m * sizeof(unsigned long long), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&vals, m * sizeof(uint32_t), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&vals2, m * sizeof(uint32_t), s));
-  word_emit_kernel<<<g, 256, 0, s>>>(events, n, off, addr_lo, keys, vals);
-  // word index < 2^38 (40-bit byte addresses)
-  tmp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int64_t)m, 0, 38, s);
-  MCKG_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
-  MCKG_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int64_t)m, 0, 38, s));
-  cudaFreeAsync(tmp, s);
-  // racing (byte, line) keys: at most 4 per word entry; capacity m/8 + 1M
-  const unsigned long long cap = m / 8 + (1ull << 20);
-  MCKG_CUDA_TRY(cudaMallocAsync(&tmp_keys, cap * sizeof(unsigned long long), s));
-  unsigned long long* n_raw = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&n_raw, sizeof(unsigned long long), s));
-  MCKG_CUDA_TRY(cudaMemsetAsync(n_raw, 0, sizeof(unsigned long long), s));
-  scan_runs_kernel<<<grid_for(m), 256, 0, s>>>(events, keys2, vals2, m, addr_lo, tmp_keys, cap, n_raw, line_first,
-                                               status);
-  MCKG_CUDA_TRY(cudaGetLastError());
-  unsigned long long nr = 0;
-  MCKG_CUDA_TRY(cudaMemcpyAsync(&nr, n_raw, sizeof nr, cudaMemcpyDeviceToHost, s));
-  MCKG_CUDA_TRY(cudaStreamSynchronize(s));
-  if (nr > cap) nr = cap;
-  if (nr) {
-    MCKG_CUDA_TRY(cudaMallocAsync(&uniq, nr * sizeof(unsigned long long), s));
-    tmp_bytes = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, tmp_keys, uniq, (int64_t)nr, 0, 56, s);
-    cub::DeviceSelect::Unique(nullptr, t2, uniq, tmp_keys, n_races, (int64_t)nr, s);
-    tmp_bytes = tmp_bytes > t2 ? tmp_bytes : t2;
-    MCKG_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
-    MCKG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, tmp_keys, uniq, (int64_t)nr, 0, 56, s));
-    MCKG_CUDA_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, uniq, tmp_keys, n_races, (int64_t)nr, s));
-    cudaFreeAsync(tmp, s);
-    if (capacity) decode_races_kernel<<<grid_for(nr), 256, 0, s>>>(tmp_keys, n_races, races, capacity);
-    MCKG_CUDA_TRY(cudaGetLastError());
-    cudaFreeAsync(uniq, s);
+  cudaFreeAsync(mm, s);
+  // the sample can miss the extremes: the edge buckets are open, and a
+  // margin keeps the top records out of one crowded last bucket
+  const uint64_t base = hm[0] & ~0xFFFull;
+  const uint64_t span = (hm[1] + 16 - base) + ((hm[1] - base) >> 6) + 65536;
+  // dense spans: 4 KiB buckets for the warp-per-bucket kernel; sparse ones:
+  // buckets sized for ~256 records, hashed tables only
+  const bool dense = (span >> FB_SHIFT) + 1 <= 2 * n + 1024 && !(debug_flags() & 128u);
+  uint32_t shift = FB_SHIFT;
+  if (!dense) {
+    const uint64_t want_nb = (n + 255) / 256;
+    shift = 4;
+    while (shift < 40 && (span >> shift) > want_nb) ++shift;
   }
-  cudaFreeAsync(n_raw, s);
-  cudaFreeAsync(tmp_keys, s);
-  cudaFreeAsync(nw, s);
+  const uint32_t nb = (uint32_t)((span >> shift) + 1);
+  // 2-4. count, scan, scatter
+  uint32_t *cnt = nullptr, *cur = nullptr, *big = nullptr;
+  uint64_t *off = nullptr, *tsum = nullptr;
+  mckg_gaccess* recs = nullptr;
+  const uint32_t ntiles = (nb + SCT - 1) / SCT;
+  MCKG_CUDA_TRY(cudaMallocAsync(&cnt, (size_t)nb * 4, s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&cur, (size_t)nb * 4, s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&off, ((size_t)nb + 1) * 8, s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&tsum, (size_t)ntiles * 8, s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&big, ((size_t)nb + 1) * 4, s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)nb * 4, s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(cur, 0, (size_t)nb * 4, s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(big, 0, 4, s));
+  const uint32_t g = grid_for(n, 16);
+  bucket_count_kernel<<<g, 256, 0, s>>>(events, n, nb, shift, base, cnt, status);
+  scan_tiles_kernel<<<ntiles, SCT, 0, s>>>(cnt, nb, tsum);
+  scan_sums_kernel<<<1, SCT, 0, s>>>(tsum, ntiles);
+  scan_apply_kernel<<<ntiles, SCT, 0, s>>>(cnt, nb, tsum, off);
+  MCKG_CUDA_TRY(cudaGetLastError());
+  // a record counts once per bucket it touches (at most two): 2n slots
+  // bound the layout without waiting for the count
+  MCKG_CUDA_TRY(cudaMallocAsync(&recs, 2 * n * sizeof(mckg_gaccess), s));
+  bucket_scatter_kernel<<<g, 256, 0, s>>>(events, n, nb, shift, base, off, cur, recs);
+  launches += 5;
+  // 5. detection
+  BOut O{races, capacity, n_races, line_first, status};
+  MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BD_SMEM));
+  int per = 0;
+  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_detect_kernel, BT, BD_SMEM));
+  const uint32_t gd = (uint32_t)sm_count() * (uint32_t)(per > 0 ? per : 1);
+  if (dense) {
+    // warp per bucket; the buckets it hands back go to the general kernel
+    uint32_t* mid = nullptr;
+    MCKG_CUDA_TRY(cudaMallocAsync(&mid, ((size_t)nb + 1) * 4, s));
+    MCKG_CUDA_TRY(cudaMemsetAsync(mid, 0, 4, s));
+    MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM));
+    int pf = 0;
+    MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, bucket_fast_kernel, FB_WARPS * 32, FB_SMEM));
+    const uint32_t gf = (uint32_t)sm_count() * (uint32_t)(pf > 0 ? pf : 1);
+    bucket_fast_kernel<<<gf, FB_WARPS * 32, FB_SMEM, s>>>(recs, off, nb, base, O, mid + 1, mid);
+    bucket_detect_kernel<<<gd, BT, BD_SMEM, s>>>(recs, off, nb, shift, base, mid + 1, mid, O, big + 1, big);
+    MCKG_CUDA_TRY(cudaGetLastError());
+    cudaFreeAsync(mid, s);
+    launches += 2;
+  } else {
+    bucket_detect_kernel<<<gd < nb ? gd : nb, BT, BD_SMEM, s>>>(recs, off, nb, shift, base, nullptr, nullptr, O,
+                                                                 big + 1, big);
+    MCKG_CUDA_TRY(cudaGetLastError());
+    ++launches;
+  }
+  uint32_t nbig = 0;
+  MCKG_CUDA_TRY(cudaMemcpyAsync(&nbig, big, 4, cudaMemcpyDeviceToHost, s));
+  MCKG_CUDA_TRY(cudaStreamSynchronize(s));
+  if (nbig) {
+    // the rare path: one bucket at a time, tables in global memory
+    std::vector<uint32_t> bl(nbig);
+    MCKG_CUDA_TRY(cudaMemcpy(bl.data(), big + 1, nbig * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t b : bl) {
+      uint64_t ob[2];
+      MCKG_CUDA_TRY(cudaMemcpy(ob, off + b, sizeof ob, cudaMemcpyDeviceToHost));
+      const uint64_t m = ob[1] - ob[0];
+      if (m > (1ull << 26)) {
+        set_error("mckg_detect_global: more than 2^26 records in one address bucket");
+        return MCKG_E_RANGE;
+      }
+      auto pow2 = [](uint64_t x) {
+        uint64_t p = 64;
+        while (p < x) p <<= 1;
+        return p;
+      };
+      const uint64_t ws = pow2(6 * m), bs = pow2(16 * m), ds = pow2(16 * m);
+      uint8_t* scratch = nullptr;
+      const size_t cand_bytes = (m * 4 + 15) & ~(size_t)15;  // keeps the 8-byte tables aligned
+      const size_t bytes = ws * 16 + cand_bytes + bs * 40 + ds * 8;
+      MCKG_CUDA_TRY(cudaMallocAsync(&scratch, bytes, s));
+      MCKG_CUDA_TRY(cudaMemsetAsync(scratch, 0, bytes, s));
+      BTab T;
+      T.wkey = reinterpret_cast<unsigned long long*>(scratch);
+      T.wtag = reinterpret_cast<uint32_t*>(scratch + ws * 8);
+      T.wflag = reinterpret_cast<uint32_t*>(scratch + ws * 12);
+      T.wmask = (uint32_t)(ws - 1);
+      T.cand = reinterpret_cast<uint32_t*>(scratch + ws * 16);
+      T.ccap = (uint32_t)m;
+      T.bkey = reinterpret_cast<unsigned long long*>(scratch + ws * 16 + cand_bytes);
+      T.bmin = reinterpret_cast<unsigned long long*>(scratch + ws * 16 + cand_bytes + bs * 8);
+      T.bmask = (uint32_t)(bs - 1);
+      T.dkey = reinterpret_cast<unsigned long long*>(scratch + ws * 16 + cand_bytes + bs * 40);
+      T.dmask = (uint32_t)(ds - 1);
+      bucket_detect_big_kernel<<<1, BT, 0, s>>>(recs, off, b, nb, shift, base, T, O);
+      MCKG_CUDA_TRY(cudaGetLastError());
+      cudaFreeAsync(scratch, s);
+      ++launches;
+    }
+  }
+  cudaFreeAsync(recs, s);
+  cudaFreeAsync(cnt, s);
+  cudaFreeAsync(cur, s);
   cudaFreeAsync(off, s);
-  cudaFreeAsync(keys, s);
-  cudaFreeAsync(keys2, s);
-  cudaFreeAsync(vals, s);
-  cudaFreeAsync(vals2, s);
-  add_launches(8);
+  cudaFreeAsync(tsum, s);
+  cudaFreeAsync(big, s);
+  add_launches(launches);
   return MCKG_OK;
 }

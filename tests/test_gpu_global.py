@@ -10,6 +10,18 @@ import oracle_bind as ob
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["dense", "sparse"])
+def k6_mode(request):
+    """Both K6 bucket modes: dense spans (warp per 4 KiB bucket, direct
+    tables, the general kernel for what it hands back) and the sparse mode
+    (hashed tables only), forced by mckg_set_debug(128)."""
+    from paper_1211_6193_b200 import _abi
+    lib = _abi.load()
+    lib.mckg_set_debug(128 if request.param == "sparse" else 0)
+    yield request.param
+    lib.mckg_set_debug(0)
+
+
 def _dev(ev):
     import torch
     return torch.from_numpy(np.ascontiguousarray(ev).view(np.int32).reshape(-1, 4).copy()).cuda()
@@ -61,6 +73,28 @@ def _random(seed, n=20000, nblocks=12, span=4096):
 @pytest.mark.parametrize("seed", range(6))
 def test_random_global_traces(seed):
     _check(_random(seed))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_wide_sparse_traces(seed):
+    """Records spread over a 2^36-byte window with clusters: empty buckets,
+    crowded buckets, accesses crossing words and buckets."""
+    rng = np.random.default_rng(100 + seed)
+    rows = []
+    centers = rng.integers(0, 1 << 36, size=8)
+    for i in range(30000):
+        c = int(centers[rng.integers(0, 8)])
+        addr = c + int(rng.integers(0, 1 << int(rng.integers(4, 14))))
+        rows.append(ob.make_gaccess(addr, int(rng.choice([1, 2, 4, 8])), rng.random() < 0.5,
+                                    int(rng.integers(0, 32)), int(rng.integers(0, 6)), int(rng.integers(1, 60)),
+                                    int(rng.integers(0, 3000))))
+    _check(np.array(rows, dtype=ob.GACCESS_DTYPE))
+
+
+def test_hot_word_many_blocks():
+    """Thousands of blocks on one word: the global-memory tables path."""
+    rows = [ob.make_gaccess(4096, 4, (i % 3) == 0, i % 64, i % 5000, 7 + (i % 3), i) for i in range(20000)]
+    _check(np.array(rows, dtype=ob.GACCESS_DTYPE))
 
 
 def test_two_owner_emulation_on_one_gpu():
