@@ -563,7 +563,7 @@ constexpr uint32_t FB_MAX = FB_ROWS * 32;
 constexpr uint32_t FB_WARPS = 16;
 constexpr int FB_BR = 2;                       // rows per load batch
 constexpr uint32_t FB_STAGE = 64;              // staged races per warp
-constexpr uint32_t FB_WARP_BYTES = FB_WORDS * 8 + 32 * 4 + FB_STAGE * 16;
+constexpr uint32_t FB_WARP_BYTES = FB_WORDS * 8 + 32 * 8 + FB_STAGE * 16;
 constexpr uint32_t FB_SMEM = FB_WARPS * FB_WARP_BYTES;
 
 struct LineCache {  // lane-owned first-racing-key cache of one warp
@@ -605,6 +605,87 @@ __device__ __forceinline__ void fb_flush(const BOut& O, const mckg_grace* stg, u
   __syncwarp();
 }
 
+// Exact pass over a warp's batch of n <= 32 candidates (global record
+// offsets in cl, from one or more buckets): lane per candidate X; X races on
+// the bytes it shares with an earlier (timestamp) candidate Y of another
+// block where X or Y writes; same-word groups by __match_any_sync (buckets
+// are disjoint, so a word's candidates all sit in one bucket).  Racing
+// (byte, line) pairs are reported once (the group of a (word, line) ORs its
+// byte masks), staged per warp; the first racing key per line goes to the
+// warp's line cache.
+__device__ __noinline__ void fb_exact(const BOut& O, const mckg_gaccess* recs, const uint64_t* cl, uint32_t nc,
+                                      LineCache& C, mckg_grace* stg, uint32_t& nstg, uint32_t& flags) {
+  const uint32_t lane = threadIdx.x & 31u;
+  __syncwarp();
+  if (nc == 0) return;
+  const bool act = lane < nc;
+  mckg_gaccess X{};
+  if (act) X = recs[cl[lane]];
+  const uint64_t xa = ga_addr(X.a);
+  const unsigned long long xw = act ? (unsigned long long)(xa >> 2) : ~0ull - lane;
+  const uint32_t xmask = act ? ((1u << ga_len(X.a)) - 1u) << (xa & 3u) : 0u;
+  const unsigned long long xts = ga_ts(X);
+  const uint32_t xbid = X.b & 0xFFFFFFu, xwr = ga_write(X.a);
+  uint32_t rest = __match_any_sync(0xFFFFFFFFu, xw) & ~(1u << lane);
+  uint32_t race = 0;
+  while (__any_sync(0xFFFFFFFFu, rest != 0u)) {
+    const uint32_t y = rest ? (uint32_t)__ffs(rest) - 1u : lane;
+    rest &= rest - 1u;
+    const uint32_t ymask = __shfl_sync(0xFFFFFFFFu, xmask, y), ybid = __shfl_sync(0xFFFFFFFFu, xbid, y),
+                   ywr = __shfl_sync(0xFFFFFFFFu, xwr, y);
+    const unsigned long long yts = __shfl_sync(0xFFFFFFFFu, xts, y);
+    if (y != lane && yts < xts && ybid != xbid && (xwr | ywr)) race |= xmask & ymask;
+  }
+  const uint32_t rm = __ballot_sync(0xFFFFFFFFu, race != 0u);
+  if (!rm) return;
+  const uint32_t line = (uint32_t)ga_line(X.a, X.b);
+  // first racing key per line
+  for (uint32_t left = rm; left;) {
+    const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, __ffs(left) - 1);
+    const bool in = race && line == L;
+    const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, in ? (uint32_t)(xts >> 32) : ~0u);
+    const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, in && (uint32_t)(xts >> 32) == mh ? (uint32_t)xts : ~0u);
+    left &= ~__ballot_sync(0xFFFFFFFFu, in);
+    lc_note(C, O.line_first, L, ((unsigned long long)mh << 32) | ml);
+  }
+  const unsigned long long gkey = race ? ((unsigned long long)(xa >> 2) << 16) | (line & 0xFFFFu) : ~0ull - lane;
+  const uint32_t grp = __match_any_sync(0xFFFFFFFFu, gkey);
+  const uint32_t mine = __reduce_or_sync(grp, race);
+  const bool rep = race && (grp & rm & ((1u << lane) - 1u)) == 0u;
+  const uint32_t cnt = rep ? __popc(mine) : 0u;
+  uint32_t ci = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ci, d);
+    if (lane >= (uint32_t)d) ci += t;
+  }
+  const uint32_t tot = __shfl_sync(0xFFFFFFFFu, ci, 31);
+  if (nstg + tot > FB_STAGE) {
+    fb_flush(O, stg, nstg, flags);
+    nstg = 0;
+  }
+  if (tot > FB_STAGE) {  // more than a buffer at once: straight out
+    unsigned long long base_o = 0;
+    if (lane == 0) base_o = atomicAdd(O.n, (unsigned long long)tot);
+    base_o = __shfl_sync(0xFFFFFFFFu, base_o, 0) + ci - cnt;
+    if (rep)
+      for (uint32_t q = mine; q; q &= q - 1u, ++base_o) {
+        if (base_o < O.cap)
+          O.races[base_o] = mckg_grace{(xa & ~3ull) + (uint32_t)(__ffs(q) - 1), (int32_t)line, 0};
+        else
+          flags |= MCKG_ST_OVERFLOW;
+      }
+    return;
+  }
+  if (rep) {
+    uint32_t p = nstg + ci - cnt;
+    for (uint32_t q = mine; q; q &= q - 1u, ++p)
+      stg[p] = mckg_grace{(xa & ~3ull) + (uint32_t)(__ffs(q) - 1), (int32_t)line, 0};
+  }
+  nstg += tot;
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mckg_gaccess* recs, const uint64_t* off,
                                                                        uint32_t nb, uint64_t base, BOut O,
                                                                        uint32_t* big, uint32_t* nbig) {
@@ -612,8 +693,9 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   uint32_t* tag = reinterpret_cast<uint32_t*>(sm + warp * FB_WARP_BYTES);
   uint32_t* flg = tag + FB_WORDS;
-  uint32_t* cl = flg + FB_WORDS;
-  mckg_grace* stg = reinterpret_cast<mckg_grace*>(cl + 32);  // staged races
+  uint64_t* cl = reinterpret_cast<uint64_t*>(flg + FB_WORDS);  // the candidate batch
+  mckg_grace* stg = reinterpret_cast<mckg_grace*>(cl + 32);     // staged races
+  uint32_t nbatch = 0;                                          // warp-uniform
   uint32_t nstg = 0;                                          // warp-uniform
   for (uint32_t i = lane; i < FB_WORDS; i += 32) flg[i] = 0u;
   __syncwarp();
@@ -706,80 +788,17 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
       if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
       continue;
     }
-    uint32_t pos = incl - c;
-    for (uint32_t g = cm; g; g &= g - 1u) cl[pos++] = (uint32_t)(__ffs(g) - 1) * 32u + lane;
-    __syncwarp();
-    // exact pass: lane per candidate X; same-word group by match_any
-    const bool act = lane < nc;
-    mckg_gaccess X{};
-    if (act) X = R[cl[lane]];
-    const uint64_t xa = ga_addr(X.a);
-    const uint32_t xw = act ? (uint32_t)((xa - blo) >> 2) : 0xFFFF0000u + lane;
-    const uint32_t xmask = act ? ((1u << ga_len(X.a)) - 1u) << (xa & 3u) : 0u;
-    const unsigned long long xts = ga_ts(X);
-    const uint32_t xbid = X.b & 0xFFFFFFu, xwr = ga_write(X.a);
-    uint32_t rest = __match_any_sync(0xFFFFFFFFu, xw) & ~(1u << lane);
-    uint32_t race = 0;
-    while (__any_sync(0xFFFFFFFFu, rest != 0u)) {
-      const uint32_t y = rest ? (uint32_t)__ffs(rest) - 1u : lane;
-      rest &= rest - 1u;
-      const uint32_t ymask = __shfl_sync(0xFFFFFFFFu, xmask, y), ybid = __shfl_sync(0xFFFFFFFFu, xbid, y),
-                     ywr = __shfl_sync(0xFFFFFFFFu, xwr, y);
-      const unsigned long long yts = ((unsigned long long)__shfl_sync(0xFFFFFFFFu, (uint32_t)(xts >> 32), y) << 32) |
-                                     __shfl_sync(0xFFFFFFFFu, (uint32_t)xts, y);
-      if (y != lane && yts < xts && ybid != xbid && (xwr | ywr)) race |= xmask & ymask;
+    // the bucket's candidates join the warp's batch (exact pass per 32)
+    if (nbatch + nc > 32u) {
+      fb_exact(O, recs, cl, nbatch, C, stg, nstg, flags);
+      nbatch = 0;
     }
-    const uint32_t rm = __ballot_sync(0xFFFFFFFFu, race != 0u);
-    if (!rm) continue;
-    const uint32_t line = (uint32_t)ga_line(X.a, X.b);
-    // first racing key per line
-    for (uint32_t left = rm; left;) {
-      const uint32_t L = __shfl_sync(0xFFFFFFFFu, line, __ffs(left) - 1);
-      const bool in = race && line == L;
-      const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, in ? (uint32_t)(xts >> 32) : ~0u);
-      const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, in && (uint32_t)(xts >> 32) == mh ? (uint32_t)xts : ~0u);
-      left &= ~__ballot_sync(0xFFFFFFFFu, in);
-      lc_note(C, O.line_first, L, ((unsigned long long)mh << 32) | ml);
-    }
-    // one report per racing (byte, line): the group of a (word, line) ORs
-    // its members' byte masks, its lowest racing lane reports
-    const uint32_t gkey = race ? ((uint32_t)((xa - blo) >> 2) << 16) | (line & 0xFFFFu) : 0xFFFFFFFFu - lane;
-    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, gkey);
-    const uint32_t mine = __reduce_or_sync(grp, race);
-    const bool rep = race && (grp & rm & ((1u << lane) - 1u)) == 0u;
-    const uint32_t cnt = rep ? __popc(mine) : 0u;
-    uint32_t ci = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ci, d);
-      if (lane >= (uint32_t)d) ci += t;
-    }
-    const uint32_t tot = __shfl_sync(0xFFFFFFFFu, ci, 31);
-    if (nstg + tot > FB_STAGE) {
-      fb_flush(O, stg, nstg, flags);
-      nstg = 0;
-    }
-    if (tot > FB_STAGE) {  // more than a buffer from one bucket: straight out
-      unsigned long long base_o = 0;
-      if (lane == 0) base_o = atomicAdd(O.n, (unsigned long long)tot);
-      base_o = __shfl_sync(0xFFFFFFFFu, base_o, 0) + ci - cnt;
-      if (rep)
-        for (uint32_t q = mine; q; q &= q - 1u, ++base_o) {
-          if (base_o < O.cap)
-            O.races[base_o] = mckg_grace{(xa & ~3ull) + (uint32_t)(__ffs(q) - 1), (int32_t)line, 0};
-          else
-            flags |= MCKG_ST_OVERFLOW;
-        }
-      continue;
-    }
-    if (rep) {
-      uint32_t p = nstg + ci - cnt;
-      for (uint32_t q = mine; q; q &= q - 1u, ++p)
-        stg[p] = mckg_grace{(xa & ~3ull) + (uint32_t)(__ffs(q) - 1), (int32_t)line, 0};
-    }
-    nstg += tot;
+    uint32_t pos = nbatch + incl - c;
+    for (uint32_t g = cm; g; g &= g - 1u) cl[pos++] = o0 + (uint64_t)((__ffs(g) - 1) * 32u + lane);
+    nbatch += nc;
     __syncwarp();
   }
+  fb_exact(O, recs, cl, nbatch, C, stg, nstg, flags);
   fb_flush(O, stg, nstg, flags);
   if (C.line != 0xFFFFFFFFu) atomicMin(O.line_first + C.line, C.ts);
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
