@@ -688,7 +688,8 @@ __device__ __noinline__ void fb_exact(const BOut& O, const mckg_gaccess* recs, c
 
 __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mckg_gaccess* recs, const uint64_t* off,
                                                                        uint32_t nb, uint64_t base, BOut O,
-                                                                       uint32_t* big, uint32_t* nbig) {
+                                                                       uint32_t* big, uint32_t* nbig,
+                                                                       uint32_t* next) {
   extern __shared__ __align__(16) uint8_t sm[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   uint32_t* tag = reinterpret_cast<uint32_t*>(sm + warp * FB_WARP_BYTES);
@@ -702,18 +703,29 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
   LineCache C{0xFFFFFFFFu, ~0ull, 0u};
   uint32_t stamp = 0;
   uint32_t flags = 0;
-  const uint32_t nwarps = gridDim.x * FB_WARPS;
-  for (uint32_t b = blockIdx.x * FB_WARPS + warp; b < nb; b += nwarps) {
-    const uint64_t o0 = off[b], o1 = off[b + 1];
+  // buckets are claimed in chunks from a counter: a fixed stride can alias
+  // the data's period (e.g. every other 32 KiB empty) and idle half the warps
+  constexpr uint32_t CH = 8;
+  uint32_t b = 0, bend = 0;
+  while (true) {
+    if (b == bend) {
+      uint32_t c0 = 0;
+      if (lane == 0) c0 = atomicAdd(next, CH);
+      b = __shfl_sync(0xFFFFFFFFu, c0, 0);
+      bend = min(b + CH, nb);
+    }
+    if (b >= nb) break;
+    const uint32_t bb = b++;
+    const uint64_t o0 = off[bb], o1 = off[bb + 1];
     if (o1 - o0 < 2) continue;  // a lone record cannot race
     if (o1 - o0 > FB_MAX) {
-      if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
+      if (lane == 0) big[atomicAdd(nbig, 1u)] = bb;
       continue;
     }
     const uint32_t m = (uint32_t)(o1 - o0);
     const mckg_gaccess* R = recs + o0;
     uint64_t blo, bhi;
-    bucket_range(b, nb, FB_SHIFT, base, &blo, &bhi);
+    bucket_range(bb, nb, FB_SHIFT, base, &blo, &bhi);
     // load + pack: word (10 bits) | write << 10 | bid << 11 (rows of 32
     // records, FB_BR rows in flight ahead of the decode)
     uint32_t pk[FB_ROWS];
@@ -752,7 +764,7 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
       }
     }
     if (__any_sync(0xFFFFFFFFu, bad)) {
-      if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
+      if (lane == 0) big[atomicAdd(nbig, 1u)] = bb;
       continue;
     }
     stamp = stamp == 0xFFFFu ? 1u : stamp + 1u;
@@ -785,7 +797,7 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
     const uint32_t nc = __shfl_sync(0xFFFFFFFFu, incl, 31);
     if (nc == 0) continue;
     if (nc > 32u) {
-      if (lane == 0) big[atomicAdd(nbig, 1u)] = b;
+      if (lane == 0) big[atomicAdd(nbig, 1u)] = bb;
       continue;
     }
     // the bucket's candidates join the warp's batch (exact pass per 32)
@@ -1017,20 +1029,22 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
   // 5. detection
   BOut O{races, capacity, n_races, line_first, status};
   MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BD_SMEM));
+  MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_detect_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per = 0;
   MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bucket_detect_kernel, BT, BD_SMEM));
   const uint32_t gd = (uint32_t)sm_count() * (uint32_t)(per > 0 ? per : 1);
   if (dense) {
     // warp per bucket; the buckets it hands back go to the general kernel
     uint32_t* mid = nullptr;
-    MCKG_CUDA_TRY(cudaMallocAsync(&mid, ((size_t)nb + 1) * 4, s));
-    MCKG_CUDA_TRY(cudaMemsetAsync(mid, 0, 4, s));
+    MCKG_CUDA_TRY(cudaMallocAsync(&mid, ((size_t)nb + 2) * 4, s));
+    MCKG_CUDA_TRY(cudaMemsetAsync(mid, 0, 8, s));  // [0] handed-back buckets, [1] claim counter
     MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM));
+    MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_fast_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     int pf = 0;
     MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf, bucket_fast_kernel, FB_WARPS * 32, FB_SMEM));
     const uint32_t gf = (uint32_t)sm_count() * (uint32_t)(pf > 0 ? pf : 1);
-    bucket_fast_kernel<<<gf, FB_WARPS * 32, FB_SMEM, s>>>(recs, off, nb, base, O, mid + 1, mid);
-    bucket_detect_kernel<<<gd, BT, BD_SMEM, s>>>(recs, off, nb, shift, base, mid + 1, mid, O, big + 1, big);
+    bucket_fast_kernel<<<gf, FB_WARPS * 32, FB_SMEM, s>>>(recs, off, nb, base, O, mid + 2, mid, mid + 1);
+    bucket_detect_kernel<<<gd, BT, BD_SMEM, s>>>(recs, off, nb, shift, base, mid + 2, mid, O, big + 1, big);
     MCKG_CUDA_TRY(cudaGetLastError());
     cudaFreeAsync(mid, s);
     launches += 2;
