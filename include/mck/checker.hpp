@@ -175,7 +175,11 @@ struct RunOptions {
   // host transport instead of NCCL (gather n bytes per rank, rank order; 0 = ok)
   int (*allgather)(void* ctx, const void* send, uint64_t n, void* recv) = nullptr;
   void* allgatherCtx = nullptr;
-  bool globalRaceCheck = false;  // SURVEY Appendix E (off: reference-identical output)
+  // SURVEY Appendix E (builder-defined; off: reference-identical output):
+  // cross-block races on global memory within one grid, reported as
+  // "Possible race on global device memory detected at <file>:<line>."
+  // (one device, one rank)
+  bool globalRaceCheck = false;
 };
 
 struct StuckReport {

@@ -192,6 +192,8 @@ enum {
   MCK_D_NEG_NONARITH,      /* negation of a non-arithmetic value                               */
   MCK_D_BITNOT_NONINT,     /* bitwise complement of a non-integer value                        */
   MCK_D_FIXED_UB,          /* OP_UB: p0 = MCK_UB_* code, name                                  */
+  MCK_D_GRACE,             /* RunOptions::globalRaceCheck (builder-defined):
+                              Possible race on global device memory detected at F:L.           */
   MCK_D_COUNT
 };
 

@@ -320,6 +320,7 @@ typedef struct mck_run_opts {
   int (*allgather)(void* ctx, const void* send, uint64_t n, void* recv);
   void* allgather_ctx;
   int32_t trace;              /* RunOptions::trace: JSON "trace" = the --trace lines  */
+  int32_t global_race_check;  /* RunOptions::globalRaceCheck       */
 } mck_run_opts;
 
 /* A fresh NCCL communicator id for mck_run_opts.comm_id. */

@@ -31,6 +31,7 @@ class RunOpts(ctypes.Structure):
         ("allgather", ctypes.c_void_p),
         ("allgather_ctx", ctypes.c_void_p),
         ("trace", ctypes.c_int32),
+        ("global_race_check", ctypes.c_int32),
     ]
 
 
@@ -74,7 +75,7 @@ def torch_allgather(group=None):
 
 
 def _opts(step_limit=0, race_check=True, device=0, round_robin=True, seed=0, devices=None, rank=0,
-          world=1, comm=None, allgather=None, trace=False):
+          world=1, comm=None, allgather=None, trace=False, global_race_check=False):
     devs = list(devices or [])
     arr = (ctypes.c_int32 * 8)(*(devs + [0] * (8 - len(devs))))
     cid = (ctypes.c_uint8 * 128)(*(comm or bytes(128)))
@@ -89,7 +90,8 @@ def _opts(step_limit=0, race_check=True, device=0, round_robin=True, seed=0, dev
                 return 1
         cb = ALLGATHER(_cb)
     o = RunOpts(step_limit, seed, 1 if race_check else 0, 1 if round_robin else 0, device, 0, len(devs), arr,
-                rank, world, cid, ctypes.cast(cb, ctypes.c_void_p) if cb else None, None, 1 if trace else 0)
+                rank, world, cid, ctypes.cast(cb, ctypes.c_void_p) if cb else None, None, 1 if trace else 0,
+                1 if global_race_check else 0)
     o._keep = cb
     return o
 

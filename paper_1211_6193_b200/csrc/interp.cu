@@ -41,6 +41,7 @@
 #include <vector>
 
 #include "../host/engine.hpp"
+#include "mckg.h"
 #include "core.cuh"
 
 namespace mckb {
@@ -64,7 +65,7 @@ constexpr int LINES = 65536;
 constexpr int RACE_SET = 1024;  // per-block (byte, line) dedup entries
 
 enum : int { ERR_NONE = 0, ERR_STACK, ERR_PRIV, ERR_SHARED_PTR_ESCAPE, ERR_DIAG_FULL, ERR_TRIPLES_FULL,
-             ERR_LINE, ERR_SWEEPS, ERR_OPCODE };
+             ERR_LINE, ERR_SWEEPS, ERR_OPCODE, ERR_GLOG_FULL };
 
 struct PObj {
   uint16_t off, size, gen;
@@ -136,6 +137,10 @@ struct KP {
   uint32_t* tarr;             // trace mode: [block][episode < TEP][tid] arrival sweep + 1
   int markDirty;              // record global writes in META_DIRTY (replicated memory)
   uint32_t maxSweeps;         // < 2^26; each sweep takes >= 1 step (step limit)
+  // RunOptions::globalRaceCheck: every global access appended here (K6 input)
+  mckg_gaccess* glog;
+  unsigned long long* nglog;
+  unsigned long long glogCap;
   // outputs
   unsigned long long* lineFirst;
   int32_t* triples;           // (obj, byte, line) records of 3 x int32
@@ -198,7 +203,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   return x;
 }
 
-__device__ __forceinline__ unsigned long long tskey(uint32_t sweep, uint32_t bid, uint32_t tid, uint32_t sub) {
+__host__ __device__ __forceinline__ unsigned long long tskey(uint32_t sweep, uint32_t bid, uint32_t tid, uint32_t sub) {
   return ((unsigned long long)sweep << 38) | ((unsigned long long)(bid & 0x3FFFFFFu) << 12) |
          ((unsigned long long)(tid & 1023u) << 2) | (sub & 3u);
 }
@@ -757,6 +762,22 @@ __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq
   } else {
     b = P.gbytes + rq.base + rq.off;
     m = P.gmeta + rq.base + rq.off;
+    if (P.glog) {  // the global-race log: one 16-byte record per access
+      const unsigned long long i = atomicAdd(P.nglog, 1ull);
+      if (i < P.glogCap) {
+        mckg_gaccess g;
+        const uint64_t addr = rq.base + (uint64_t)rq.off;
+        const uint32_t ln = (uint32_t)rq.line;
+        g.a = (addr & 0xFFFFFFFFFFull) | ((unsigned long long)(len & 0xF) << 40) |
+              ((unsigned long long)(rq.kind == 2 ? 1u : 0u) << 44) | ((unsigned long long)(c.tid & 0x7FFu) << 45) |
+              ((unsigned long long)(ln & 0xFFu) << 56);
+        g.sweep = c.sweep;
+        g.b = (c.bid & 0xFFFFFFu) | (((ln >> 8) & 0xFFu) << 24);
+        P.glog[i] = g;
+      } else {
+        set_error(P, ERR_GLOG_FULL, 0);
+      }
+    }
   }
   if (rq.kind == 2) {
     if (rq.space == R_OK_SHARED)
@@ -1703,6 +1724,9 @@ struct Replica {
   DBuf<k1::BlockOut> blocks;
   DBuf<uint32_t> tarr;
   DBuf<int> err;
+  DBuf<mckg_gaccess> glog;          // RunOptions::globalRaceCheck
+  DBuf<unsigned long long> gcnt;    // [0] log length, [1] K6 races, [2..] K6 line table
+  DBuf<uint32_t> gstat;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   uint32_t b0 = 0, nb = 0;
 };
@@ -1883,6 +1907,10 @@ class CudaEngine final : public DeviceEngine {
     }
     void (*kern)(KP) = K == 1 ? grid_kernel<1> : K == 2 ? grid_kernel<2> : K == 4 ? grid_kernel<4> : grid_kernel<8>;
     const size_t total = (size_t)g.gridDim;
+    if (g.globalRaceCheck && (exch_ || reps_.size() > 1 || total >= MCKG_MAX_BID)) {
+      out.error = "globalRaceCheck runs a grid of < 2^21 blocks on one device and one rank";
+      return false;
+    }
     if (g.trace && (exch_ || total * (size_t)TEP * (size_t)g.blockDim > (1ull << 26))) {
       out.error = exch_ ? "--trace is single-rank" : "--trace supports grids up to 2^20 threads";
       return false;
@@ -1930,6 +1958,15 @@ class CudaEngine final : public DeviceEngine {
           (g.trace && !R.tarr.ensure(nb * TEP * (size_t)g.blockDim, err)) ||
           !R.err.ensure(2, err))
         return false;
+      // the global-race log: up to 64 accesses per simulated thread, within
+      // [2^20, 2^27] records; a fuller log is an engine error, never a miss
+      const size_t glogCap = g.globalRaceCheck
+                                 ? std::min<size_t>(1ull << 27, std::max<size_t>(1ull << 20, 64 * nb * (size_t)g.blockDim))
+                                 : 0;
+      if (g.globalRaceCheck && (!R.glog.ensure(glogCap, err) || !R.gcnt.ensure(2 + LINES, err) ||
+                                !R.gstat.ensure(1, err)))
+        return false;
+      if (g.globalRaceCheck) CK(cudaMemsetAsync(R.gcnt.p, 0, sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.line.p, 0xFF, LINES * sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.ntri.p, 0, sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.diag.p, 0, diagN * sizeof(DevDiagRec), R.stream));
@@ -1967,6 +2004,9 @@ class CudaEngine final : public DeviceEngine {
       kp.tarr = g.trace ? R.tarr.p : nullptr;
       kp.markDirty = (D > 1 || exch_) ? 1 : 0;
       kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
+      kp.glog = g.globalRaceCheck ? R.glog.p : nullptr;
+      kp.nglog = g.globalRaceCheck ? R.gcnt.p : nullptr;
+      kp.glogCap = glogCap;
       kp.lineFirst = R.line.p;
       kp.triples = R.tri.p;
       kp.tripleCap = triCaps[ri];
@@ -2018,8 +2058,9 @@ class CudaEngine final : public DeviceEngine {
                                     "a pointer to a thread-private object was stored to shared or global memory",
                                     "too many distinct diagnostics", "too many reported race triples",
                                     "source line outside 0..65535",
-                                    "sweep budget exhausted (step limit or 2^26 sweeps)", "bad opcode"};
-        out.error = std::string("B200 engine limitation: ") + why[herr[0] < 9 ? herr[0] : 0] + " (info " +
+                                    "sweep budget exhausted (step limit or 2^26 sweeps)", "bad opcode",
+                                    "global-race access log full"};
+        out.error = std::string("B200 engine limitation: ") + why[herr[0] < 10 ? herr[0] : 0] + " (info " +
                     std::to_string(herr[1]) + ")";
         return false;
       }
@@ -2076,6 +2117,35 @@ class CudaEngine final : public DeviceEngine {
       std::vector<unsigned long long> lf(LINES);
       CK(cudaMemcpy(lf.data(), R.line.p, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
       for (int l = 0; l < LINES; ++l) lfAll[(size_t)l] = std::min(lfAll[(size_t)l], lf[(size_t)l]);
+      if (g.globalRaceCheck) {
+        // cross-block global races of this grid: K6 over the access log
+        // (a builder-defined extension, off by default)
+        unsigned long long nlog = 0;
+        CK(cudaMemcpy(&nlog, R.gcnt.p, sizeof nlog, cudaMemcpyDeviceToHost));
+        unsigned long long* glf = R.gcnt.p + 2;
+        CK(cudaMemsetAsync(glf, 0xFF, LINES * sizeof(unsigned long long), R.stream));
+        CK(cudaMemsetAsync(R.gstat.p, 0, sizeof(uint32_t), R.stream));
+        if (mckg_detect_global(R.glog.p, nlog, 0, nullptr, 0, R.gcnt.p + 1, glf, R.gstat.p, R.stream) != MCKG_OK) {
+          out.error = std::string("global-race detection failed: ") + mckg_last_error();
+          return false;
+        }
+        std::vector<unsigned long long> gl(LINES);
+        CK(cudaMemcpyAsync(gl.data(), glf, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost, R.stream));
+        CK(cudaStreamSynchronize(R.stream));
+        out.launches += 6;
+        for (int l = 0; l < LINES; ++l)
+          if (gl[(size_t)l] != ~0ull) {
+            // K6 key sweep:32 | bid:21 | tid:11 -> the device-diagnostic key
+            const unsigned long long k = gl[(size_t)l];
+            DevDiag d;
+            d.key = tskey((uint32_t)(k >> 32), (uint32_t)(k >> 11) & (MCKG_MAX_BID - 1), (uint32_t)k & 0x7FFu, 0);
+            d.code = MCK_D_GRACE;
+            d.line = l;
+            d.p[0] = d.p[1] = d.p[2] = d.p[3] = 0;
+            d.name = -1;
+            out.diags.push_back(d);
+          }
+      }
       unsigned long long ntri = 0;
       CK(cudaMemcpy(&ntri, R.ntri.p, sizeof ntri, cudaMemcpyDeviceToHost));
       if (ntri) {

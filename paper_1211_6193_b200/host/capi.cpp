@@ -47,6 +47,7 @@ mck::RunOptions toOptions(const mck_run_opts* opts) {
     if (opts->max_threads_per_block > 0) ro.arch.maxThreadsPerBlock = opts->max_threads_per_block;
     for (int i = 0; i < opts->n_devices && i < 8; ++i) ro.devices.push_back(opts->devices[i]);
     ro.trace = opts->trace != 0;
+    ro.globalRaceCheck = opts->global_race_check != 0;
     if (opts->world > 1) {
       ro.rank = opts->rank;
       ro.world = opts->world;

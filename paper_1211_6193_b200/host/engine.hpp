@@ -51,6 +51,7 @@ struct GridSpec {
   // shared arrays of earlier grids (for memBoundary messages): (first id, count, gid)
   std::vector<std::array<uint32_t, 3>> sharedRanges;
   bool trace = false;               // record barrier arrivals (GridResult::arrivals)
+  bool globalRaceCheck = false;     // log global accesses, run K6 on them after the grid
 };
 
 struct DevDiag {

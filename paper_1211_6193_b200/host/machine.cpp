@@ -414,6 +414,10 @@ class HostMachine {
         cat = mck::DiagCategory::Race;
         sev = mck::Severity::Warning;
         return "Possible race on shared device memory detected at " + P_->filename + ":" + std::to_string(r.line) + ".";
+      case MCK_D_GRACE:  // RunOptions::globalRaceCheck (builder-defined, off by default)
+        cat = mck::DiagCategory::Race;
+        sev = mck::Severity::Warning;
+        return "Possible race on global device memory detected at " + P_->filename + ":" + std::to_string(r.line) + ".";
       case MCK_D_MEMBOUNDARY: {
         cat = mck::DiagCategory::MemBoundary;
         std::string sp = r.p[1] == 0 ? "host" : r.p[1] == 1 ? "device-global"
@@ -1374,6 +1378,7 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   g.globalIds = globalIds_;
   g.sharedRanges = sharedRanges_;
   g.trace = o_.trace;
+  g.globalRaceCheck = o_.globalRaceCheck;
   const int nparams = P_->fns[static_cast<size_t>(l.kernel)].n_params;
   // spawnGrid allocates gridDim shared objects, then nparams objects per thread
   const uint64_t reserve = static_cast<uint64_t>(l.grid) + static_cast<uint64_t>(l.grid) * l.block * nparams;

@@ -1,0 +1,53 @@
+"""RunOptions::globalRaceCheck end to end: K1 logs every global access of a
+grid, K6 finds the cross-block races, the host reports them as
+"Possible race on global device memory detected at <file>:<line>." in
+first-detection order (builder-defined).  With the option
+off the run is the reference's own (goldens in tests/golden/global_check.json)."""
+import json
+import os
+
+import pytest
+
+from global_check_programs import PROGRAMS
+from program_corpus import project
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "global_check.json")))
+
+
+@pytest.mark.parametrize("name", sorted(PROGRAMS))
+def test_option_off_is_the_reference(name):
+    from paper_1211_6193_b200 import checker
+    r = checker.run_source(PROGRAMS[name][0], filename="g.cu")
+    assert r["engine_error"] == ""
+    got = project(r)
+    for k, v in GOLD[name].items():
+        assert got[k] == v, k
+
+
+@pytest.mark.parametrize("name", sorted(PROGRAMS))
+def test_global_races_reported(name):
+    from paper_1211_6193_b200 import checker
+    src, lines = PROGRAMS[name]
+    r = checker.run_source(src, filename="g.cu", global_race_check=True)
+    assert r["engine_error"] == ""
+    grace = [d for d in r["diags"] if "global device memory" in d["msg"]]
+    assert [d["line"] for d in grace] == lines
+    assert all(d["msg"] == f"Possible race on global device memory detected at g.cu:{d['line']}." and
+               d["cat"] == "race" and d["sev"] == "warning" for d in grace)
+    # everything else is unchanged; any diagnostic makes the exit code 1
+    base = GOLD[name]
+    assert r["output"] == base["output"] and r["steps"] == base["steps"]
+    assert [d for d in r["diags"] if "global device memory" not in d["msg"]] == base["diags"]
+    assert r["exit"] == (1 if lines and base["exit"] == 0 else base["exit"])
+
+
+def test_full_size_c2_has_no_global_race():
+    """The Fig. 1 reduction at 2^20 ints: blocks read disjoint inputs and
+    write disjoint partial sums."""
+    import gen_programs as gp
+    from paper_1211_6193_b200 import checker
+    r = checker.run_source(gp.scaled(1 << 20, 256), "c2.cu", step_limit=8_000_000_000, global_race_check=True)
+    assert r["engine_error"] == ""
+    assert r["exit"] == 0 and r["diags"] == []
