@@ -216,16 +216,27 @@ def run_ours(args):
                          max_block_events=EVENTS_PER_BLOCK)
     out = race.RaceOut(capacity=nb * EVENTS_PER_BLOCK // 8, device=dev)
     stream = torch.cuda.current_stream()
+    # real multi-GPU: the library's own NCCL communicator does the exchange
+    # (mckg_detect_shared_mgpu); the shared-GPU gloo dry run reduces in Python
+    comm = None
+    if ws > 1 and not shared:
+        from paper_1211_6193_b200 import checker
+        obj = [checker.comm_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = race.Comm(obj[0], rank, ws, local)
     torch.cuda.synchronize()
 
     def step(ev0=None, ev1=None):
         out.reset(stream)
         if ev0 is not None:
             ev0.record(stream)
-        race.detect_shared_async(tr, out, stream, reset=False)
+        if comm is not None:
+            race.detect_shared_mgpu(comm, tr, out, stream, reset=False)
+        else:
+            race.detect_shared_async(tr, out, stream, reset=False)
         if ev1 is not None:
             ev1.record(stream)
-        if ws > 1:
+        if ws > 1 and comm is None:
             lf = out.line_first
             lf.bitwise_xor_(-(1 << 63))  # unsigned order -> signed order
             _all_reduce(lf, dist.ReduceOp.MIN)
@@ -298,7 +309,7 @@ def run_ours(args):
     if not args.no_c5:
         ev = bs = tr = out = None  # free the C3 trace before C5
         torch.cuda.empty_cache()
-        c5 = run_c5(args, args.c5_blocks if args.c5_blocks else (1 << 16) * ws, dev, ws, rank)
+        c5 = run_c5(args, args.c5_blocks if args.c5_blocks else (1 << 16) * ws, dev, ws, rank, comm)
     e2e = None
     if rank == 0 and ws == 1 and args.e2e_blocks > 0:
         e2e = run_e2e(args, torch, race, _abi)
@@ -344,6 +355,8 @@ def run_ours(args):
             "c5": c5,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if ws > 1:
         dist.destroy_process_group()
 
@@ -359,7 +372,7 @@ def _all_reduce(t, op):
         dist.all_reduce(t, op=op)
 
 
-def run_c5(args, blocks, dev, ws, rank):
+def run_c5(args, blocks, dev, ws, rank, comm=None):
     """C5 (configs[4]): cross-block global races over `blocks` simulated blocks
     sharded over the ranks: K3 partition -> NCCL all-to-all -> K6 detect ->
     MIN-all-reduce of the line table.  Device-timed (CUDA events), max over
@@ -374,6 +387,10 @@ def run_c5(args, blocks, dev, ws, rank):
     stream = torch.cuda.current_stream()
 
     def step():
+        if comm is not None:  # the exchange inside the library (mckg_detect_global_mgpu)
+            out = gr.GlobalOut(max(1, 2 * ev.shape[0] // 8), device=dev)
+            gr.detect_mgpu(comm, ev, space, out.reset(), stream)
+            return out, -1
         if ws > 1:
             grouped, counts = gr.partition(ev, ws, space, stream)
             mine = gr.exchange(grouped, counts)
@@ -407,7 +424,7 @@ def run_c5(args, blocks, dev, ws, rank):
     n_races = int(out.n.item())
     status = int(out.status.item())
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    tot = torch.tensor([ev.shape[0], n_races, recv], dtype=torch.int64, device=dev)
+    tot = torch.tensor([ev.shape[0], n_races, max(recv, 0)], dtype=torch.int64, device=dev)
     if ws > 1:
         _all_reduce(t, dist.ReduceOp.MAX)
         _all_reduce(tot, dist.ReduceOp.SUM)

@@ -298,6 +298,29 @@ int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64_t addr_lo,
                        uint64_t capacity, unsigned long long* n_races, unsigned long long* line_first,
                        uint32_t* status, void* stream);
 
+/* ---- multi-GPU (one process per GPU) ----
+ * An NCCL communicator owned by the library: `id` from mckg_comm_id() on
+ * rank 0, broadcast by the launcher; `device` the CUDA ordinal of this rank. */
+typedef struct mckg_comm mckg_comm;
+int mckg_comm_init(const uint8_t id[128], int rank, int world, int device, mckg_comm** out);
+void mckg_comm_destroy(mckg_comm* comm);
+
+/* C3 sharded by blocks: mckg_detect_shared on this rank's shard, then an
+ * all-reduce(MIN) of out->line_first, so every rank holds the Race diagnostic
+ * order of the whole grid.  Triples stay with the rank that found them (the
+ * shards own disjoint shared objects). */
+int mckg_detect_shared_mgpu(mckg_comm* comm, const mckg_trace* shard, const mckg_race_out* out, void* stream);
+
+/* C5: the global-race exchange in the library -- partition this rank's
+ * records by owner (rank r owns addresses [r*A/P, (r+1)*A/P), A = addr_space),
+ * count all-gather, grouped ncclSend/ncclRecv of the records, then
+ * mckg_detect_global on the owned range and an all-reduce(MIN) of line_first
+ * (reset by the caller beforehand).  races / n_races: this rank's (byte,
+ * line) pairs, disjoint across ranks. */
+int mckg_detect_global_mgpu(mckg_comm* comm, const mckg_gaccess* events, uint64_t n, uint64_t addr_space,
+                            mckg_grace* races, uint64_t capacity, unsigned long long* n_races,
+                            unsigned long long* line_first, uint32_t* status, void* stream);
+
 #define MCKG_C5_EVENTS_PER_BLOCK 4096u
 #define MCKG_C5_RANGE 65536u
 #define MCKG_C5_SEED 0x12116193ull

@@ -46,6 +46,10 @@ EXPORTS = [
     "mckg_partition_global",
     "mckg_detect_global",
     "mckg_comm_id",
+    "mckg_comm_init",
+    "mckg_comm_destroy",
+    "mckg_detect_shared_mgpu",
+    "mckg_detect_global_mgpu",
     "mck_run_source",
     "mck_disassemble",
     "mck_free",
@@ -124,6 +128,11 @@ def load():
     lib.mckg_gen_c5.argtypes = [vp, u32, u32, u32, u64, vp]
     lib.mckg_partition_global.argtypes = [vp, u64, u32, u64, vp, vp, vp]
     lib.mckg_detect_global.argtypes = [vp, u64, u64, vp, u64, vp, vp, vp, vp]
+    lib.mckg_comm_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.mckg_comm_destroy.argtypes = [vp]
+    lib.mckg_comm_destroy.restype = None
+    lib.mckg_detect_shared_mgpu.argtypes = [vp, ctypes.POINTER(Trace), ctypes.POINTER(RaceOut), vp]
+    lib.mckg_detect_global_mgpu.argtypes = [vp, vp, u64, u64, vp, u64, vp, vp, vp, vp]
     _lib = lib
     return lib
 

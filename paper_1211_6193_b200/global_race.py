@@ -105,6 +105,15 @@ def detect(ev, addr_lo, out, stream=None):
     return out
 
 
+def detect_mgpu(comm, ev, addr_space, out, stream=None):
+    """mckg_detect_global_mgpu: owner partition, all-to-all over NCCL, K6 on
+    the owned range and the line-table MIN, all inside the library."""
+    _abi.check(_abi.load().mckg_detect_global_mgpu(comm.handle, _p(ev), ev.shape[0], addr_space, _p(out.races),
+                                                   out.capacity, _p(out.n), _p(out.line_first), _p(out.status),
+                                                   _s(stream)), "mckg_detect_global_mgpu")
+    return out
+
+
 def min_allreduce_u64(t, group=None):
     """MIN all-reduce of uint64 values stored in an int64 tensor."""
     import torch.distributed as dist

@@ -188,3 +188,41 @@ def gen_c3(blk0, n_blocks, seed=_abi.C3_SEED, device="cuda", stream=None):
     _abi.check(_abi.load().mckg_gen_c3(_ptr(ev), _ptr(bs), blk0, n_blocks, seed,
                                        _stream_handle(stream)), "mckg_gen_c3")
     return ev, bs
+
+
+class Comm:
+    """The library-owned NCCL communicator of the multi-GPU entry points
+    (mckg_comm_init): one process per GPU; `comm_id` is checker.comm_id() of
+    rank 0, broadcast by the launcher."""
+
+    def __init__(self, comm_id, rank, world, device):
+        lib = _abi.load()
+        buf = (ctypes.c_uint8 * 128)(*comm_id)
+        self._h = ctypes.c_void_p()
+        _abi.check(lib.mckg_comm_init(buf, rank, world, device, ctypes.byref(self._h)), "mckg_comm_init")
+        self.rank, self.world, self.device = rank, world, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            _abi.load().mckg_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+
+def detect_shared_mgpu(comm, trace, out, stream=None, reset=True):
+    """mckg_detect_shared_mgpu: this rank's shard + the line-table MIN over ranks."""
+    lib = _abi.load()
+    if reset:
+        out.reset(stream)
+    _abi.check(lib.mckg_detect_shared_mgpu(comm.handle, ctypes.byref(trace), ctypes.byref(out._c),
+                                           _stream_handle(stream)), "mckg_detect_shared_mgpu")
+    return out
