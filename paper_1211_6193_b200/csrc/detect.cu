@@ -33,7 +33,9 @@
 //        a (word, line) -> byte-mask table, staged and appended to the global
 //        triple array; the first racing timestamp per line is min-reduced.
 #include <cub/cub.cuh>
+#include <algorithm>
 #include <atomic>
+#include <vector>
 #include <map>
 #include <thread>
 #include <mutex>
@@ -80,6 +82,7 @@ struct Params {
   uint32_t debug;  // experiments only (MCKG_DEBUG): 1 skip the exact pass, 2 TMA stream only
   // the general kernel gated on the fast path's overflow list
   uint32_t gate;       // 1 = only the blocks of olist
+  uint32_t skip_big;   // blocks over `cap` records are left to the oversize route (no ST_RANGE)
   uint32_t* ocount;    // [0] blocks in olist
   uint32_t* olist;     // [n_blocks]
 };
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(NT, EPT <= 4 ? MCKG_K2_MINB : (EPT <= 8 ? 2 : 
   auto issue = [&](uint32_t j, int st) {  // j: position in the launch's block sequence
     const uint32_t b = blk(j);
     const uint64_t s0 = P.bstart[b], n = P.bstart[b + 1] - s0;
-    if (n > P.cap) flags |= ST_RANGE;
+    if (n > P.cap && !P.skip_big) flags |= ST_RANGE;
     const bool go = n > 0 && n <= P.cap;
     s_n[st] = go ? (uint32_t)n : 0u;
     if (!go) return;
@@ -919,6 +922,100 @@ cudaError_t ensure_dynamic_smem(void (*k)(Params), size_t bytes) {
   return e;
 }
 
+// ---- the oversize route: blocks beyond the kernels' staging (more than
+// 4096 records) or shared objects beyond the on-chip filter ----
+// One block at a time through K6 (mckg_detect_global) with the K2 semantics
+// mapped onto it: address = (epoch - first epoch) << 20 | byte offset, so
+// records of different epochs never meet; the "block" of a K6 record is the
+// thread (races are between threads here); its sweep is the record's index
+// in the block, so K6's "earlier" is the replay order of recordAccess
+// (racecheck.cpp:24-32).  Racing (address, line) pairs become the block's
+// (obj, byte, line) triples; K6's first racing key per line names the
+// record, whose real (sweep, bid, tid) key is MIN-ed into line_first.
+__global__ void oversize_map_kernel(const mckg_access* ev, uint64_t n, uint32_t shmem, mckg_gaccess* out,
+                                    uint32_t* status) {
+  const uint32_t e0 = n ? acc_epoch(ev[0].w1) : 0u;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const mckg_access r = ev[i];
+    const uint32_t off = acc_off(r.w0), len = acc_len(r.w0), tid = acc_tid(r.w1), ep = acc_epoch(r.w1);
+    const uint32_t prev = i ? acc_epoch(ev[i - 1].w1) : ep;
+    bool ok = len - 1u < MCKG_MAX_LEN && off + len <= shmem && (uint32_t)r.line < MCKG_MAX_LINES;
+    if (ep < prev) atomicOr(status, ST_ORDER);
+    const uint32_t rel = ep - e0;
+    if (ep < e0 || rel >= (1u << 20)) ok = false;
+    if (!ok) atomicOr(status, ST_RANGE);
+    // one (byte, line) racing in two epochs is two K6 addresses: the triples
+    // may repeat, and the caller's sort restores the set (MCKG_ST_DUP)
+    if (__any_sync(__activemask(), rel > 0) && (threadIdx.x & 31u) == (uint32_t)(__ffs(__activemask()) - 1))
+      atomicOr(status, ST_DUP);
+    const uint32_t ln = (uint32_t)r.line;
+    mckg_gaccess g;
+    g.a = ((((unsigned long long)rel << 20) | off) & 0xFFFFFFFFFFull) | ((unsigned long long)(ok ? len : 0u) << 40) |
+          ((unsigned long long)acc_write(r.w0) << 44) | ((unsigned long long)tid << 45) |
+          ((unsigned long long)(ln & 0xFFu) << 56);
+    g.sweep = (uint32_t)i;
+    g.b = tid | (((ln >> 8) & 0xFFu) << 24);
+    out[i] = g;
+  }
+}
+
+__global__ void oversize_report_kernel(const mckg_grace* races, const unsigned long long* n_races, uint64_t cap_races,
+                                       uint32_t obj, mckg_race_triple* tri, unsigned long long capacity,
+                                       unsigned long long* n_tri, uint32_t* status) {
+  const uint64_t n = *n_races < cap_races ? *n_races : cap_races;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = atomicAdd(n_tri, 1ull);
+    if (k < capacity)
+      tri[k] = mckg_race_triple{obj, (uint32_t)(races[i].addr & 0xFFFFFu), races[i].line};
+    else
+      atomicOr(status, ST_OVERFLOW);
+  }
+}
+
+__global__ void oversize_lines_kernel(const unsigned long long* lf6, const mckg_access* ev, uint32_t bid,
+                                      unsigned long long* line_first) {
+  const uint32_t l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= MCKG_MAX_LINES || lf6[l] == ~0ull) return;
+  const mckg_access r = ev[lf6[l] >> 32];  // the first racing record of the line
+  atomicMin(line_first + l, ts_key(r.sweep, bid, acc_tid(r.w1)));
+}
+
+int detect_oversize(const mckg_trace* tr, const mckg_race_out* out, cudaStream_t s, const std::vector<uint32_t>& blocks,
+                    const std::vector<uint64_t>& hbs) {
+  uint64_t maxn = 0;
+  for (uint32_t b : blocks) maxn = std::max<uint64_t>(maxn, hbs[b + 1] - hbs[b]);
+  if (maxn == 0) return MCKG_OK;
+  mckg_gaccess* g = nullptr;
+  mckg_grace* races = nullptr;
+  unsigned long long* cnt = nullptr;  // [0] races, [1..] K6 line table
+  uint32_t* st6 = nullptr;
+  const uint64_t rcap = maxn * 8 + 64;
+  MCKG_CUDA_TRY(cudaMallocAsync(&g, maxn * sizeof(mckg_gaccess), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&races, rcap * sizeof(mckg_grace), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&cnt, (1 + MCKG_MAX_LINES) * sizeof(unsigned long long), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&st6, sizeof(uint32_t), s));
+  for (uint32_t b : blocks) {
+    const uint64_t n = hbs[b + 1] - hbs[b];
+    if (n == 0) continue;
+    const mckg_access* ev = tr->events + hbs[b];
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count() * 8);
+    oversize_map_kernel<<<grid, 256, 0, s>>>(ev, n, tr->shmem_bytes, g, out->status);
+    MCKG_CUDA_TRY(cudaMemsetAsync(cnt + 1, 0xFF, MCKG_MAX_LINES * sizeof(unsigned long long), s));
+    MCKG_CUDA_TRY(cudaMemsetAsync(st6, 0, sizeof(uint32_t), s));
+    int rc = mckg_detect_global(g, n, 0, races, rcap, cnt, cnt + 1, st6, s);
+    if (rc != MCKG_OK) return rc;
+    oversize_report_kernel<<<grid, 256, 0, s>>>(races, cnt, rcap, tr->obj_base + b, out->triples, out->capacity,
+                                                out->n_triples, out->status);
+    oversize_lines_kernel<<<MCKG_MAX_LINES / 256, 256, 0, s>>>(cnt + 1, ev, tr->bid_base + b, out->line_first);
+    MCKG_CUDA_TRY(cudaGetLastError());
+  }
+  cudaFreeAsync(g, s);
+  cudaFreeAsync(races, s);
+  cudaFreeAsync(cnt, s);
+  cudaFreeAsync(st6, s);
+  return MCKG_OK;
+}
+
 }  // namespace
 
 int detect_config(uint32_t cap, uint32_t shmem_bytes, size_t* smem, uint32_t* wpad) {
@@ -962,15 +1059,26 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   }
   uint32_t cap = tr->max_block_events ? tr->max_block_events : 1024u;
   cap = (cap + 31u) & ~31u;
-  if (cap > (uint32_t)EPT_MAX * NT) {
-    set_error("mckg_detect_shared: a block holds more than 4096 events (staging limit)");
-    return MCKG_E_RANGE;
-  }
+  cudaStream_t s = (cudaStream_t)stream;
   size_t smem;
   uint32_t wpad;
-  if (detect_config(cap, tr->shmem_bytes, &smem, &wpad) != MCKG_OK) {
-    set_error("mckg_detect_shared: shared object too large for the shared-memory filter");
-    return MCKG_E_RANGE;
+  const bool big_blocks = cap > (uint32_t)EPT_MAX * NT;
+  const bool big_object = detect_config(std::min<uint32_t>(cap, EPT_MAX * NT), tr->shmem_bytes, &smem, &wpad) != MCKG_OK;
+  if (big_blocks || big_object) {
+    // blocks past the on-chip staging / filter take the oversize route
+    std::vector<uint64_t> hbs((size_t)tr->n_blocks + 1);
+    MCKG_CUDA_TRY(cudaMemcpyAsync(hbs.data(), tr->block_start, hbs.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    MCKG_CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<uint32_t> big;
+    for (uint32_t b = 0; b < tr->n_blocks; ++b)
+      if (big_object || hbs[b + 1] - hbs[b] > (uint64_t)EPT_MAX * NT) big.push_back(b);
+    keep_pool_memory();
+    const int rc = detect_oversize(tr, out, s, big, hbs);
+    if (rc != MCKG_OK || big_object) {
+      add_launches((uint32_t)big.size() * 9u);
+      return rc;
+    }
+    cap = EPT_MAX * NT;  // the rest: the kernels below, oversize blocks skipped
   }
   // the general kernel: records staged per block by TMA, EPT per thread
   const int ki = cap <= 4u * NT ? 0 : cap <= 8u * NT ? 1 : 2;
@@ -997,9 +1105,9 @@ extern "C" int mckg_detect_shared(const mckg_trace* tr, const mckg_race_out* out
   P.status = out->status;
   P.debug = debug_flags();
   P.gate = 0;
+  P.skip_big = big_blocks ? 1u : 0u;
   P.ocount = nullptr;
   P.olist = nullptr;
-  cudaStream_t s = (cudaStream_t)stream;
   if ((P.debug & 32u) || tr->shmem_bytes > FWORDS * 4u) {
     // the general kernel alone (MCKG_DEBUG=32: the tests cover both paths;
     // shared objects over 4 KiB: no fast path)

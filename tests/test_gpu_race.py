@@ -228,3 +228,26 @@ def test_unsorted_epochs_are_flagged():
     ev[3 * 1024:4 * 1024] = blk
     res = _gpu(ev, bs, ob.C3_SHMEM)
     assert res.status & 4
+
+
+def test_oversize_blocks_8192_events():
+    """Blocks beyond the kernels' 4096-record staging (the reference bounds
+    neither): 8192-event blocks beside ordinary ones, through the oversize
+    route, against the reference."""
+    ev1, bs1 = random_trace(11, n_blocks=3, threads=512, shmem=2048, epochs=3, per_epoch=2800,
+                            kinds=("int", "char", "long"), hot=0.3)
+    ev2, bs2 = random_trace(12, n_blocks=4, threads=64, shmem=2048, epochs=2, per_epoch=100)
+    ev = np.concatenate([ev1, ev2])
+    bs = np.concatenate([bs1, bs2[1:] + bs1[-1]]).astype(np.uint64)
+    assert np.diff(bs.astype(np.int64)).max() > 4096
+    res, n = _check(ev, bs, 2048)
+    assert n > 0
+
+
+def test_oversize_shared_object():
+    """A 256 KiB shared object: past the on-chip filter, every block takes
+    the oversize route."""
+    ev, bs = random_trace(13, n_blocks=5, threads=96, shmem=262144, epochs=2, per_epoch=400,
+                          kinds=("int", "long"), hot=0.6)
+    res, n = _check(ev, bs, 262144)
+    assert n > 0
