@@ -50,13 +50,18 @@ namespace k1 {
 using namespace mck_core;
 
 // ---- per-thread capacity (local memory) ----
-constexpr int VS = 48;       // value stack entries
-constexpr int SCOPES = 32;
-constexpr int OWNED = 48;
-constexpr int FRAMES = 16;
-constexpr int BINDS = 96;
-constexpr int POBJ = 48;
-constexpr int PB = 768;      // private bytes (locals and params of all frames)
+// (sized for recursion ~64 deep; local memory is reserved for the resident
+// threads only, and only the used top of each array is touched)
+#ifndef MCKG_K1_DEEP
+#define MCKG_K1_DEEP 1
+#endif
+constexpr int VS = MCKG_K1_DEEP ? 160 : 48;       // value stack entries
+constexpr int SCOPES = MCKG_K1_DEEP ? 160 : 32;
+constexpr int OWNED = MCKG_K1_DEEP ? 160 : 48;
+constexpr int FRAMES = MCKG_K1_DEEP ? 80 : 16;
+constexpr int BINDS = MCKG_K1_DEEP ? 320 : 96;
+constexpr int POBJ = MCKG_K1_DEEP ? 160 : 48;
+constexpr int PB = MCKG_K1_DEEP ? 2560 : 768;     // private bytes (locals and params of all frames)
 constexpr int TEP = TRACE_EPISODES;
 
 constexpr uint32_t PRIV = 0x80000000u;

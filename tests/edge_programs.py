@@ -62,8 +62,42 @@ int main(void) {
 """
 
 
-def _two_grid_total():
-    return None  # filled from the golden run (limit cases T-1, T, T+1)
+RECURSION = r"""__device__ int depth(int n) {
+  int local = n * 3;
+  if (n == 0) { return 0; }
+  return depth(n - 1) + (local %% 7);
+}
+__global__ void k(int* g, int n) {
+  g[blockIdx.x * blockDim.x + threadIdx.x] = depth(n + threadIdx.x %% 3);
+}
+int main(void) {
+  int* g;
+  int h[8];
+  cudaMalloc(&g, 8 * sizeof(int));
+  k<<<2, 4>>>(g, %(n)d);
+  cudaMemcpy(h, g, 8 * sizeof(int), cudaMemcpyDeviceToHost);
+  printf("%%d %%d %%d\n", h[0], h[5], h[7]);
+  return 0;
+}
+"""
+
+WIDE_RACE = r"""__global__ void k(int* g) {
+  extern __shared__ int s[];
+  int i;
+  for (i = 0; i != 4; ++i) {
+    s[(threadIdx.x * 4 + i) %% %(words)d] = threadIdx.x;
+  }
+  s[(threadIdx.x * 7) %% %(words)d] += 1;
+  g[threadIdx.x] = s[threadIdx.x];
+}
+int main(void) {
+  int* g;
+  cudaMalloc(&g, %(threads)d * sizeof(int));
+  k<<<%(blocks)d, %(threads)d, %(words)d * sizeof(int)>>>(g);
+  cudaDeviceSynchronize();
+  return 0;
+}
+"""
 
 
 def edge_cases():
@@ -80,4 +114,9 @@ def edge_cases():
     }
     for d in (-1, 0, 1):
         out[f"limit_two_grids_total{d:+d}"] = ("tg.cu", ("T", d), TWO_GRIDS)
+    # capacity cases the reference has no bound for
+    out["recursion_depth_64"] = ("rec.cu", 50_000_000, RECURSION % dict(n=62))
+    out["recursion_depth_20"] = ("rec.cu", 50_000_000, RECURSION % dict(n=20))
+    out["wide_race_1024x16k"] = ("wide.cu", 200_000_000, WIDE_RACE % dict(words=4096, threads=1024, blocks=1))
+    out["wide_race_2x512x8k"] = ("wide2.cu", 200_000_000, WIDE_RACE % dict(words=2048, threads=512, blocks=2))
     return out
