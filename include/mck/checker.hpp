@@ -8,6 +8,7 @@
 //   Machine(prog, opts).run()       machine.hpp:357-375
 //   scanStuck, hooks                machine.hpp:378, 384-388
 //   recordAccess / clearEpoch       machine.hpp:407-409 (batched on the K2 kernel)
+//   oracleRace                      oracle.hpp:34 (explored on the GPU)
 //   RunResult / StuckReport         machine.hpp:318-338
 //   Diagnostic / DiagCategory       diagnostics.hpp:10-31
 //   formatStuckReports              machine.hpp:449
@@ -299,6 +300,30 @@ class Machine {
   RunOptions opts_;
   std::unique_ptr<MachineImpl> impl_;
 };
+
+// ---- the exhaustive-interleaving oracle (oracle.hpp:10-34) ----
+// Explores every interleaving of the shared-memory accesses of a small
+// program's grid on the GPU (one explorer thread per schedule prefix, replay
+// DFS); invisible steps run eagerly in the canonical order.  The ground truth
+// looks for a conflicting pair on one byte with no barrier of its block in
+// between; detectorRace is the shadow detector's verdict on any schedule.
+// B200 bounds: grids of <= 8 threads, one kernel launch per program.
+struct OracleOptions {
+  uint64_t maxInterleavings = 1'000'000;
+  int maxThreads = 3;
+  int maxAccessesPerThread = 8;
+  ArchParams arch;
+};
+
+struct OracleResult {
+  bool oracleRace = false;    // ground truth from exhaustive trace analysis
+  bool detectorRace = false;  // any explored schedule where the shadow detector reports
+  uint64_t interleavings = 0;
+  bool aborted = false;       // a limit was exceeded
+  std::string error;
+};
+
+OracleResult oracleRace(std::shared_ptr<const Program> prog, OracleOptions opts = {});
 
 // A fresh 128-byte communicator id for RunOptions::commId (rank 0 makes it,
 // the launcher broadcasts it).  Empty on failure.

@@ -413,6 +413,18 @@ int mck_result_stuck(const mck_result* r, uint64_t i, mck_stuck_rec* out);
 int mck_result_reported(const mck_result* r, uint64_t first, uint64_t count, mckg_race_triple* out);
 const char* mck_result_trace(const mck_result* r, uint64_t i);
 void mck_result_free(mck_result* r);
+/* oracleRace (oracle.hpp:34): every interleaving of the shared accesses of a
+ * small program's grid, explored on the GPU. */
+typedef struct mck_oracle_result {
+  int32_t oracle_race;     /* ground truth: a conflicting pair with no barrier between */
+  int32_t detector_race;   /* the shadow detector reported on some schedule            */
+  int32_t aborted;         /* a bound was hit (error says which)                         */
+  int32_t frontend_error;  /* the program did not compile (error holds the message)      */
+  uint64_t interleavings;
+  char error[256];
+} mck_oracle_result;
+int mck_oracle(const char* src, const char* filename, uint64_t max_interleavings, int32_t max_threads,
+               int32_t max_accesses_per_thread, mck_oracle_result* out);
 int mck_disassemble(const char* src, const char* filename, char** text);
 void mck_free(char* p);
 

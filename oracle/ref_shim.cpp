@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "minicudak/machine.hpp"
+#include "minicudak/oracle.hpp"
 #include "minicudak/program.hpp"
 
 extern "C" {
@@ -283,6 +284,32 @@ int mckref_run(const char* src, const char* filename, int policy, uint64_t seed,
           << e.sweep << "," << e.step << "]";
     }
     o << "]}";
+    *json = strdup(o.str().c_str());
+    return 0;
+}
+
+// oracleRace (oracle.cpp:140-152): the reference's exhaustive interleaving
+// explorer on a source program; JSON {oracle_race, detector_race,
+// interleavings, aborted, error} or {frontend_error}.
+int mckref_oracle(const char* src, const char* filename, uint64_t max_interleavings, int max_threads,
+                  int max_accesses, char** json) {
+    std::ostringstream o;
+    try {
+        auto prog = compileSource(src, filename);
+        OracleOptions opts;
+        opts.maxInterleavings = max_interleavings;
+        opts.maxThreads = max_threads;
+        opts.maxAccessesPerThread = max_accesses;
+        OracleResult r = oracleRace(prog, opts);
+        o << "{\"oracle_race\":" << (r.oracleRace ? "true" : "false")
+          << ",\"detector_race\":" << (r.detectorRace ? "true" : "false")
+          << ",\"interleavings\":" << r.interleavings << ",\"aborted\":" << (r.aborted ? "true" : "false")
+          << ",\"error\":" << jsonStr(r.error) << "}";
+    } catch (const FrontendError& e) {
+        o << "{\"frontend_error\":" << jsonStr(e.stage + ": " + e.message) << "}";
+    } catch (const std::exception& e) {
+        o << "{\"internal_error\":" << jsonStr(e.what()) << "}";
+    }
     *json = strdup(o.str().c_str());
     return 0;
 }

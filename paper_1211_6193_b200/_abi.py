@@ -54,6 +54,7 @@ EXPORTS = [
     "mck_disassemble",
     "mck_free",
     "mck_run",
+    "mck_oracle",
     "mck_result_summary",
     "mck_result_diag",
     "mck_result_stuck",

@@ -209,3 +209,23 @@ def run(src, filename="test.cu", **kw):
                 "trace": [lib.mck_result_trace(h, i).decode() for i in range(sm.n_trace)]}
     finally:
         lib.mck_result_free(h)
+
+
+class OracleResult(ctypes.Structure):
+    _fields_ = [("oracle_race", ctypes.c_int32), ("detector_race", ctypes.c_int32), ("aborted", ctypes.c_int32),
+                ("frontend_error", ctypes.c_int32), ("interleavings", ctypes.c_uint64), ("error", ctypes.c_char * 256)]
+
+
+def oracle_race(src, filename="test.cu", max_interleavings=1_000_000, max_threads=3, max_accesses_per_thread=8):
+    """oracleRace (oracle.hpp:34) through mck_oracle: every interleaving of the
+    grid's shared accesses, explored on the GPU."""
+    lib = _lib()
+    lib.mck_oracle.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32,
+                               ctypes.POINTER(OracleResult)]
+    r = OracleResult()
+    _abi.check(lib.mck_oracle(src.encode(), filename.encode(), max_interleavings, max_threads,
+                              max_accesses_per_thread, ctypes.byref(r)), "mck_oracle")
+    if r.frontend_error:
+        return {"frontend_error": r.error.decode()}
+    return {"oracle_race": bool(r.oracle_race), "detector_race": bool(r.detector_race),
+            "interleavings": int(r.interleavings), "aborted": bool(r.aborted), "error": r.error.decode()}

@@ -1603,6 +1603,325 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
   }
 }
 
+// ======================= GPU exhaustive-interleaving oracle =======================
+// oracleRace (oracle.cpp:73-154) on the B200: every interleaving of the
+// grid's VISIBLE steps -- device steps whose next Item is a load or store
+// (LoadRV, LoadKeepLV, StoreAssign, StoreCompound, StoreIncDec) with a
+// DeviceShared lvalue on the operand stack, array decays included
+// (oracle.cpp:12-36) -- while every invisible step runs eagerly in the
+// canonical order (the lowest (gid, bid, tid) first, barrier rules after
+// device steps, oracle.cpp:81-103).  A path is a sequence of choices (the
+// index of the chosen visible transition among the enabled ones, in key
+// order); one GPU thread explores the subtree below one prefix, depth-first,
+// re-simulating the grid from its spawn state for every leaf (replay DFS).
+// At a leaf: the ground truth (a conflicting pair on one shared byte with no
+// barrier of its block between them, traceHasRace oracle.cpp:47-71) and the
+// shadow detector's verdict along the path (racecheck.cpp:24-32).
+constexpr int OMAX = 8;      // simulated threads of an explored grid
+constexpr int ODEPTH = 128;  // visible steps on one path
+constexpr int OTRACE = 192;  // trace entries of one path (accesses + epoch marks)
+
+struct OQ {
+  const uint8_t* prefixes;   // [nprefix][ODEPTH] choices
+  const uint8_t* plens;      // [nprefix] prefix lengths
+  uint32_t nprefix;
+  int expand;                // 1: only expand each prefix by one choice point
+  uint8_t* outPrefixes;      // expand: children prefixes
+  uint8_t* outLens;
+  uint32_t* nOut;
+  uint32_t outCap;
+  uint8_t* arenas;           // [GPU thread][2 * arenaSize]: bytes then meta
+  const uint8_t* arenaInit;  // the spawn-time global image (bytes then meta)
+  uint64_t arenaSize;
+  unsigned long long* leaves;
+  uint32_t* flags;           // [0] ground-truth race, [1] detector race, [2] error (1 accesses, 2 depth, 3 trace, 4 leaves)
+  uint32_t maxAccesses;      // per thread along one path
+  unsigned long long maxLeaves;
+  uint32_t S;                // shared bytes per block, rounded to 16
+  uint32_t slice;            // shared memory per GPU thread (bytes)
+};
+
+struct OEv {  // one trace entry
+  uint16_t thread;  // simulated thread index; 0xFFFF = epoch mark of block `obj`
+  uint8_t len, write;
+  uint32_t obj;
+  int64_t off;
+};
+
+__device__ __forceinline__ bool o_visible(const TS& t, const KP& P) {
+  const mck_ins* code = P.code;
+  int pc = t.pc;
+  mck_ins in = ldg_ins(code + pc);
+  while (in.op == OP_JMP) in = ldg_ins(code + in.a);
+  int depth;
+  switch (in.op) {
+    case OP_LOADRV:
+    case OP_LOADKEEP: depth = 0; break;
+    case OP_STORE:
+    case OP_STORE_INC: depth = 1; break;
+    case OP_STORE_OP: depth = 2; break;
+    default: return false;
+  }
+  if (t.nv <= depth) return false;
+  const Val& lv = t.vals[t.nv - 1 - depth];
+  if (lv.kind != MCK_K_LV) return false;
+  const uint32_t obj = lv.obj;
+  if (obj >= P.sharedBase && (int64_t)(obj - P.sharedBase) < P.gridDim) return true;
+  for (int i = 0; i < P.nranges; ++i)
+    if (obj >= P.shRanges[3 * i] && obj - P.shRanges[3 * i] < P.shRanges[3 * i + 1]) return true;
+  return false;
+}
+
+__global__ void __launch_bounds__(64, 1) oracle_kernel(KP P0, OQ Q) {
+  extern __shared__ __align__(16) uint8_t osm[];
+  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gt >= Q.nprefix) return;
+  const uint32_t nt = (uint32_t)(P0.gridDim * P0.blockDim);
+  const uint32_t nb = (uint32_t)P0.gridDim;
+  // this GPU thread's shared-memory slice: per block bytes, meta, shadow (S each x 1, 1, 4)
+  uint8_t* mysm = osm + (size_t)threadIdx.x * Q.slice;
+  BlockShared& bs = *reinterpret_cast<BlockShared*>(mysm + nb * 6 * Q.S);
+  KP P = P0;
+  P.raceCheck = 0;  // the oracle runs the shadow itself
+  P.tarr = nullptr;
+  P.glog = nullptr;
+  P.markDirty = 0;
+  uint8_t* arena = Q.arenas + (size_t)gt * 2 * Q.arenaSize;
+  P.gbytes = arena;
+  P.gmeta = arena + Q.arenaSize;
+  TS t[OMAX];
+  Thread th[OMAX];
+  uint8_t choice[ODEPTH], nopt[ODEPTH];
+  const uint8_t* pre = Q.prefixes + (size_t)gt * ODEPTH;
+  const uint32_t plen = Q.plens[gt];
+  for (uint32_t d = 0; d < plen; ++d) choice[d] = pre[d];
+  uint32_t depth = plen;  // levels of choice[] fixed so far (the prefix, then this subtree's path)
+  OEv tr[OTRACE];
+  unsigned long long leaves = 0;
+  bool gtRace = false, detRace = false;
+  uint32_t err = 0;
+  while (true) {
+    // ---- replay from the spawn state, following choice[0 .. ) ----
+    for (uint64_t i = 0; i < 2 * Q.arenaSize; ++i) arena[i] = Q.arenaInit[i];
+    for (uint32_t i = 0; i < nb * 6 * Q.S; ++i) mysm[i] = 0;
+    uint32_t* shb = reinterpret_cast<uint32_t*>(mysm);  // shadow of block b at + (6b + 2) S
+    for (uint32_t b = 0; b < nb; ++b) {
+      uint32_t* sh = reinterpret_cast<uint32_t*>(mysm + (size_t)(6 * b + 2) * Q.S);
+      for (uint32_t i = 0; i < Q.S; ++i) sh[i] = shadow_empty(0);
+    }
+    (void)shb;
+    uint32_t epoch[OMAX];
+    uint32_t acc[OMAX];
+    for (uint32_t i = 0; i < nt; ++i) {
+      const uint32_t bid = i / (uint32_t)P.blockDim;
+      TS& tk = t[i];
+      Thread& hk = th[i];
+      hk.state = S_READY;
+      hk.readyAt = 0;
+      hk.E = 0;
+      hk.syncKind = 0;
+      hk.operand = 0;
+      tk.pc = 0;
+      tk.nv = tk.nscope = tk.nowned = tk.nframe = tk.npobj = tk.ptop = 0;
+      tk.steps = tk.allocs = 0;
+      for (int j = 0; j < POBJ; ++j) tk.pobj[j].gen = 0;
+      for (int j = 0; j < BINDS; ++j) tk.binds[j] = 0;
+      const mck_fn& kf = P.fns[P.kernel];
+      tk.frames[0].retPc = -1;
+      tk.frames[0].bindBase = 0;
+      tk.frames[0].fn = P.kernel;
+      tk.frames[0].scopeDepth = 0;
+      tk.frames[0].valueDepth = 0;
+      tk.nframe = 1;
+      tk.scopeMark[0] = 0;
+      tk.nscope = 1;
+      tk.bb = 0;
+      tk.fn = P.kernel;
+      for (int a = 0; a < P.nargs; ++a) {
+        const mck_local& pl = P.locals[kf.local_base + a];
+        uint32_t id;
+        if (!priv_alloc(tk, P, pl.size, pl.name, id)) {
+          hk.state = S_FIN;
+          break;
+        }
+        priv_poke(tk, tk.pobj[id & 0xFFFFF], 0, pl.type, P.args[a]);
+        tk.binds[a] = id;
+      }
+      if (kf.dyn_shared_slot >= 0) tk.binds[kf.dyn_shared_slot] = P.sharedBase + bid;
+      tk.pc = kf.entry;
+      epoch[i] = 0;
+      acc[i] = 0;
+    }
+    uint32_t d = 0, ntr = 0;
+    bool detHere = false;
+    bool aborted = false;
+    // one step of simulated thread i (the memory request served at once)
+    auto do_step = [&](uint32_t i) {
+      const uint32_t bid = i / (uint32_t)P.blockDim, tid = i % (uint32_t)P.blockDim;
+      Ctx c;
+      c.bid = bid;
+      c.tid = tid;
+      c.sub = 0;
+      c.sweep = 0;
+      Req rq;
+      Pend pd;
+      rq.kind = 0;
+      if (step(t[i], P, c, th[i], rq, pd, bs, (uint32_t)P.blockDim) && th[i].state != S_FIN) {
+        SmemLay L;
+        L.bytes = (uint32_t)(mysm - osm) + (6 * bid) * Q.S;
+        L.meta = L.bytes + Q.S;
+        L.shadow = L.bytes + 2 * Q.S;
+        L.htKey = L.htVal = L.raceSet = L.end = 0;
+        if (rq.space == R_OK_SHARED) {
+          const int len = (int)t_scalar(rq.ty);
+          // recordAccess (racecheck.cpp:9-52): the shadow detector's verdict
+          if (shadow_access(reinterpret_cast<uint32_t*>(osm + L.shadow), rq.off, len, tid, rq.kind == 2,
+                            epoch[i] & 0xFFu))
+            detHere = true;
+          if (ntr < OTRACE)
+            tr[ntr++] = OEv{(uint16_t)i, (uint8_t)len, (uint8_t)(rq.kind == 2), rq.obj, rq.off};
+          else
+            aborted = true, err = err ? err : 3u;
+        }
+        unsigned long long se = 0;
+        do_request(P, c, th[i], rq, L, 0, 0, se);
+        finish_request(t[i], P, th[i], rq, pd);
+      }
+      // barrier: a block whose threads all wait is released (the up /
+      // turnaround / down / release rules are invisible, device.cpp:143-200);
+      // the turnaround clears the block's race epoch (an epoch mark)
+      if (th[i].state == S_WAIT) {
+        const uint32_t b0 = bid * (uint32_t)P.blockDim, b1 = b0 + (uint32_t)P.blockDim;
+        bool all = true;
+        int nz = 0, allc = 0;
+        for (uint32_t j = b0; j < b1; ++j) {
+          if (th[j].state != S_WAIT) all = false;
+          if (th[j].operand != 0) ++nz;
+          if (th[j].operand != 0 || th[j].syncKind == MCK_SYNC_PLAIN) ++allc;
+        }
+        if (all) {
+          for (uint32_t j = b0; j < b1; ++j) {
+            Val res;
+            switch (th[j].syncKind) {
+              case MCK_SYNC_AND: res = v_int(allc == (int)P.blockDim ? 1 : 0); break;
+              case MCK_SYNC_OR: res = v_int(nz > 0 ? 1 : 0); break;
+              case MCK_SYNC_COUNT: res = v_int(nz); break;
+              default: res = v_void(); break;
+            }
+            push(t[j], P, res);
+            th[j].state = S_READY;
+            th[j].operand = 0;
+            ++th[j].E;
+            ++epoch[j];
+          }
+          if (ntr < OTRACE)
+            tr[ntr++] = OEv{0xFFFFu, 0, 0, P.sharedBase + bid, 0};
+          else
+            aborted = true, err = err ? err : 3u;
+        }
+      }
+    };
+    bool leaf = false;
+    bool branched = false;  // expand mode: the choice point past the prefix was reached
+    while (!aborted) {
+      // closure: the first READY thread (key order) with an invisible next step
+      bool moved = true;
+      while (moved && !aborted) {
+        moved = false;
+        for (uint32_t i = 0; i < nt; ++i)
+          if (th[i].state == S_READY && !o_visible(t[i], P)) {
+            do_step(i);
+            moved = true;
+            break;
+          }
+      }
+      if (aborted) break;
+      // the choice point: visible transitions in key order
+      uint32_t opts[OMAX], no = 0;
+      for (uint32_t i = 0; i < nt; ++i)
+        if (th[i].state == S_READY) opts[no++] = i;
+      if (no == 0) {
+        leaf = true;
+        break;
+      }
+      if (d >= ODEPTH) {
+        aborted = true;
+        err = err ? err : 2u;
+        break;
+      }
+      if (Q.expand && d == plen) {
+        // one level down: the children of this prefix
+        for (uint32_t k = 0; k < no; ++k) {
+          const uint32_t o = atomicAdd(Q.nOut, 1u);
+          if (o < Q.outCap) {
+            for (uint32_t j = 0; j < plen; ++j) Q.outPrefixes[(size_t)o * ODEPTH + j] = choice[j];
+            Q.outPrefixes[(size_t)o * ODEPTH + plen] = (uint8_t)k;
+            Q.outLens[o] = (uint8_t)(plen + 1);
+          }
+        }
+        branched = true;
+        break;
+      }
+      if (d >= depth) {  // a new level on this path: take the first option
+        choice[d] = 0;
+        nopt[d] = (uint8_t)no;
+        depth = d + 1;
+      }
+      const uint32_t i = opts[choice[d] < no ? choice[d] : no - 1];
+      if (++acc[i] > Q.maxAccesses) {
+        aborted = true;
+        err = err ? err : 1u;
+        break;
+      }
+      ++d;
+      do_step(i);
+    }
+    if (aborted) break;
+    if (leaf) {
+      // the leaf budget: flushed in batches, checked against maxInterleavings
+      if (++leaves == 1024) {
+        const unsigned long long tot = atomicAdd(Q.leaves, leaves) + leaves;
+        leaves = 0;
+        if (tot > Q.maxLeaves) {
+          err = err ? err : 4u;
+          break;
+        }
+      }
+      detRace |= detHere;
+      // ground truth (traceHasRace, oracle.cpp:47-71)
+      for (uint32_t a = 0; a < ntr && !gtRace; ++a) {
+        if (tr[a].thread == 0xFFFFu) continue;
+        for (uint32_t b = a + 1; b < ntr; ++b) {
+          if (tr[b].thread == 0xFFFFu || tr[a].obj != tr[b].obj || tr[a].thread == tr[b].thread) continue;
+          if (!tr[a].write && !tr[b].write) continue;
+          if (!(tr[a].off < tr[b].off + tr[b].len && tr[b].off < tr[a].off + tr[a].len)) continue;
+          bool sep = false;
+          for (uint32_t k = a + 1; k < b; ++k)
+            if (tr[k].thread == 0xFFFFu && tr[k].obj == tr[a].obj) {
+              sep = true;
+              break;
+            }
+          if (!sep) {
+            gtRace = true;
+            break;
+          }
+        }
+      }
+    }
+    if (Q.expand || branched) break;
+    // next path below the prefix: the deepest level with an untried option
+    int lv = (int)depth - 1;
+    while (lv >= (int)plen && choice[lv] + 1u >= nopt[lv]) --lv;
+    if (lv < (int)plen) break;
+    ++choice[lv];
+    depth = (uint32_t)lv + 1;
+  }
+  if (leaves) atomicAdd(Q.leaves, leaves);
+  if (gtRace) atomicOr(Q.flags + 0, 1u);
+  if (detRace) atomicOr(Q.flags + 1, 1u);
+  if (err) atomicCAS(Q.flags + 2, 0u, err);
+}
+
 }  // namespace k1
 
 // ======================= host side of the engine =======================
@@ -1845,6 +2164,163 @@ class CudaEngine final : public DeviceEngine {
     bool ok = run(g, out, err);
     if (!ok && out.error.empty()) out.error = err;
     return ok;
+  }
+
+  // The exhaustive-interleaving oracle over one grid (k1::oracle_kernel):
+  // the frontier of schedule prefixes is expanded level by level until it
+  // fills the GPU, then every prefix's subtree is explored by one thread.
+  bool exploreGrid(const GridSpec& g, const OracleSpec& o, OracleOut& res) override {
+    using namespace k1;
+    std::string err;
+    auto fail = [&](const std::string& m) {
+      res.error = m.empty() ? err : m;
+      return false;
+    };
+    const Program& P = *g.prog;
+    const uint64_t nt = (uint64_t)g.gridDim * (uint64_t)g.blockDim;
+    if (nt > (uint64_t)OMAX) return fail("the GPU oracle explores grids of at most 8 threads");
+    if (reps_.size() != 1 || exch_) return fail("the GPU oracle runs on one device and one rank");
+    Replica& R = reps_[0];
+    CK(cudaSetDevice(R.dev));
+    CK(cudaStreamSynchronize(nullptr));
+    if (R.prog != &P) {
+      if (!upload(R.code, P.code, err) || !upload(R.fns, P.fns, err) || !upload(R.locals, P.locals, err))
+        return fail("");
+      R.prog = &P;
+    }
+    std::vector<uint32_t> ids;
+    for (const auto& ob : g.objects) ids.push_back(ob.id);
+    std::vector<uint32_t> rng;
+    for (const auto& r : g.sharedRanges) rng.insert(rng.end(), r.begin(), r.end());
+    if (!upload(R.ids, ids, err) || !upload(R.objs, g.objects, err) || !upload(R.glob, g.globalIds, err) ||
+        !upload(R.args, g.args, err) || !upload(R.ranges, rng, err) || !R.diag.ensure(1024, err))
+      return fail("");
+    CK(cudaMemset(R.diag.p, 0, 1024 * sizeof(DevDiagRec)));
+    const mck_fn& kf = P.fns[(size_t)g.kernel];
+    KP kp{};
+    kp.code = R.code.p;
+    kp.fns = R.fns.p;
+    kp.locals = R.locals.p;
+    kp.kernel = g.kernel;
+    kp.nargs = (int)g.args.size();
+    kp.args = R.args.p;
+    kp.gid = g.gid;
+    kp.sharedBase = g.sharedBase;
+    kp.nextId = g.nextId;
+    kp.gridDim = g.gridDim;
+    kp.blockDim = g.blockDim;
+    kp.shmem = g.shmemBytes;
+    kp.sharedName = kf.dyn_shared_slot >= 0 ? P.locals[(size_t)(kf.local_base + kf.dyn_shared_slot)].name
+                                            : P.sharedDefaultName;
+    kp.warpSize = g.warpSize;
+    kp.objIds = R.ids.p;
+    kp.objs = R.objs.p;
+    kp.nobjs = (int)g.objects.size();
+    kp.globalIds = R.glob.p;
+    kp.shRanges = R.ranges.p;
+    kp.nranges = (int)g.sharedRanges.size();
+    kp.maxSweeps = ~0u;
+    kp.diags = R.diag.p;
+    kp.diagMask = 1023;
+    kp.error = nullptr;
+    // per explorer: the spawn-time global image (bytes then meta)
+    const uint64_t asz = std::max<uint64_t>(16, top_);
+    DBuf<uint8_t> init;
+    if (!init.ensure(2 * asz, err)) return fail("");
+    if (top_) {
+      CK(cudaMemcpy(init.p, R.bytes, top_, cudaMemcpyDeviceToDevice));
+      CK(cudaMemcpy(init.p + asz, R.meta, top_, cudaMemcpyDeviceToDevice));
+    }
+    DBuf<int> errbuf;
+    if (!errbuf.ensure(2, err)) return fail("");
+    CK(cudaMemset(errbuf.p, 0, 2 * sizeof(int)));
+    kp.error = errbuf.p;
+    kp.errorInfo = errbuf.p + 1;
+    OQ q{};
+    q.S = (uint32_t)((g.shmemBytes + 15) & ~15ll);
+    q.slice = (uint32_t)(((size_t)g.gridDim * 6 * q.S + sizeof(BlockShared) + 15) & ~(size_t)15);
+    q.arenaSize = asz;
+    q.arenaInit = init.p;
+    q.maxAccesses = (uint32_t)std::min<int64_t>(o.maxAccessesPerThread, ODEPTH);
+    q.maxLeaves = o.maxInterleavings;
+    const uint32_t TPB = 64;
+    const size_t smem = (size_t)TPB * q.slice;
+    if (smem > 200 * 1024) return fail("the GPU oracle's per-explorer shared arrays exceed shared memory");
+    CK(cudaFuncSetAttribute(oracle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DBuf<unsigned long long> leaves;
+    DBuf<uint32_t> flags, nout;
+    if (!leaves.ensure(1, err) || !flags.ensure(3, err) || !nout.ensure(1, err)) return fail("");
+    CK(cudaMemset(leaves.p, 0, sizeof(unsigned long long)));
+    CK(cudaMemset(flags.p, 0, 3 * sizeof(uint32_t)));
+    // frontier: start from the empty prefix
+    const uint32_t kFrontier = 8192;
+    DBuf<uint8_t> pa, pb, la, lb, arenas;
+    if (!pa.ensure((size_t)kFrontier * 64 * ODEPTH, err) || !pb.ensure((size_t)kFrontier * 64 * ODEPTH, err) ||
+        !la.ensure((size_t)kFrontier * 64, err) || !lb.ensure((size_t)kFrontier * 64, err))
+      return fail("");
+    CK(cudaMemset(pa.p, 0, ODEPTH));
+    CK(cudaMemset(la.p, 0, 1));
+    uint8_t *curP = pa.p, *nxtP = pb.p, *curL = la.p, *nxtL = lb.p;
+    uint32_t n = 1;
+    auto launch = [&](const uint8_t* pre, const uint8_t* lens, uint32_t cnt, int expand, uint8_t* op, uint8_t* ol,
+                      uint32_t cap) -> bool {
+      if (!arenas.ensure((size_t)cnt * 2 * asz, err)) return false;
+      q.prefixes = pre;
+      q.plens = lens;
+      q.nprefix = cnt;
+      q.expand = expand;
+      q.outPrefixes = op;
+      q.outLens = ol;
+      q.nOut = nout.p;
+      q.outCap = cap;
+      q.arenas = arenas.p;
+      q.leaves = leaves.p;
+      q.flags = flags.p;
+      CK(cudaMemset(nout.p, 0, sizeof(uint32_t)));
+      oracle_kernel<<<(cnt + TPB - 1) / TPB, TPB, smem>>>(kp, q);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      return true;
+    };
+    for (int level = 0; level < ODEPTH && n > 0 && n < kFrontier; ++level) {
+      if (!launch(curP, curL, n, 1, nxtP, nxtL, kFrontier * 64)) return fail("");
+      uint32_t m = 0;
+      CK(cudaMemcpy(&m, nout.p, sizeof m, cudaMemcpyDeviceToHost));
+      uint32_t fl[3];
+      CK(cudaMemcpy(fl, flags.p, sizeof fl, cudaMemcpyDeviceToHost));
+      if (fl[2] || m > kFrontier * 64) {
+        if (m > kFrontier * 64) return fail("oracle frontier overflow");
+        n = 0;
+        break;
+      }
+      std::swap(curP, nxtP);
+      std::swap(curL, nxtL);
+      n = m;
+    }
+    if (n > 0 && !launch(curP, curL, n, 0, nullptr, nullptr, 0)) return fail("");
+    unsigned long long lv = 0;
+    uint32_t fl[3];
+    int kerr[2];
+    CK(cudaMemcpy(&lv, leaves.p, sizeof lv, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(fl, flags.p, sizeof fl, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(kerr, errbuf.p, sizeof kerr, cudaMemcpyDeviceToHost));
+    if (kerr[0]) return fail("B200 engine limitation inside the oracle (code " + std::to_string(kerr[0]) + ")");
+    res.interleavings = lv;
+    res.oracleRace = fl[0] != 0;
+    res.detectorRace = fl[1] != 0;
+    switch (fl[2]) {
+      case 0: break;
+      case 1: res.aborted = true; res.error = "a thread performs more shared accesses than the oracle size bound"; break;
+      case 2: res.aborted = true; res.error = "a path exceeds the GPU oracle's depth bound"; break;
+      case 3: res.aborted = true; res.error = "a path exceeds the GPU oracle's trace bound"; break;
+      default: res.aborted = true; res.error = "interleaving budget exceeded"; break;
+    }
+    if (lv > o.maxInterleavings) {
+      res.aborted = true;
+      res.error = "interleaving budget exceeded";
+      res.interleavings = o.maxInterleavings + 1;  // the count at which the reference stops
+    }
+    return true;
   }
 
  private:

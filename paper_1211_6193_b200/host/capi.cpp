@@ -1,6 +1,7 @@
 // capi.cpp -- C ABI over the mck:: C++ API (declared in include/mckg.h):
 // run a CUDA-C program end to end and return the RunResult as JSON, the
 // boundary the Python tests and bench.py call through ctypes.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -242,3 +243,28 @@ extern "C" const char* mck_result_trace(const mck_result* r, uint64_t i) {
 }
 
 extern "C" void mck_result_free(mck_result* r) { delete r; }
+
+extern "C" int mck_oracle(const char* src, const char* filename, uint64_t max_interleavings, int32_t max_threads,
+                          int32_t max_accesses_per_thread, mck_oracle_result* out) {
+  if (!src || !filename || !out) return MCKG_E_ARG;
+  *out = mck_oracle_result{};
+  std::string err;
+  try {
+    auto prog = mck::compileSource(src, filename);
+    mck::OracleOptions o;
+    o.maxInterleavings = max_interleavings;
+    o.maxThreads = max_threads;
+    o.maxAccessesPerThread = max_accesses_per_thread;
+    const mck::OracleResult r = mck::oracleRace(prog, o);
+    out->oracle_race = r.oracleRace;
+    out->detector_race = r.detectorRace;
+    out->aborted = r.aborted;
+    out->interleavings = r.interleavings;
+    err = r.error;
+  } catch (const mck::FrontendError& e) {
+    out->frontend_error = 1;
+    err = e.stage + ": " + e.message;
+  }
+  std::snprintf(out->error, sizeof out->error, "%s", err.c_str());
+  return MCKG_OK;
+}

@@ -88,6 +88,17 @@ struct GridResult {
   std::vector<uint32_t> arrivals;   // [gridDim][TRACE_EPISODES][blockDim]
 };
 
+// The exhaustive-interleaving oracle over one grid (oracle.hpp:10-34).
+struct OracleSpec {
+  uint64_t maxInterleavings = 1'000'000;
+  int maxAccessesPerThread = 8;
+};
+struct OracleOut {
+  bool oracleRace = false, detectorRace = false, aborted = false;
+  uint64_t interleavings = 0;
+  std::string error;
+};
+
 class DeviceEngine {
  public:
   virtual ~DeviceEngine() = default;
@@ -98,6 +109,13 @@ class DeviceEngine {
   virtual void copy(uint64_t dst, uint64_t src, int64_t n) = 0;
   virtual void fill(uint64_t base, uint8_t v, uint8_t meta, int64_t n) = 0;
   virtual bool runGrid(const GridSpec& spec, GridResult& out) = 0;
+  // explores every interleaving of the grid's visible steps; false: error set
+  virtual bool exploreGrid(const GridSpec& spec, const OracleSpec& o, OracleOut& out) {
+    (void)spec;
+    (void)o;
+    out.error = "no CUDA device: the oracle explores on the GPU";
+    return false;
+  }
 };
 
 // Rank sharding (one process per GPU): rank r runs blocks

@@ -147,7 +147,22 @@ class HostMachine {
 
   mck::RunResult run();
 
+  // oracle mode (oracleRace): the first grid is explored exhaustively on the
+  // GPU before it runs as usual
+  void setOracle(const OracleSpec& spec, int maxThreads) {
+    oracle_ = spec;
+    oracleOn_ = true;
+    oracleMaxThreads_ = maxThreads;
+  }
+  const OracleOut& oracleOut() const { return oracleOut_; }
+  int oracleGrids() const { return oracleGrids_; }
+
  private:
+  bool oracleOn_ = false;
+  OracleSpec oracle_;
+  int oracleMaxThreads_ = 3;
+  OracleOut oracleOut_;
+  int oracleGrids_ = 0;
   std::shared_ptr<const Program> P_;
   mck::RunOptions o_;
   HostHooks hooks_;
@@ -1395,6 +1410,19 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   rec.gridDim = l.grid;
   rec.blockDim = l.block;
   rec.sharedBase = g.sharedBase;
+  if (oracleOn_ && !oracleOut_.aborted) {
+    // oracle.cpp:81-99: the size bounds, then every interleaving of the grid
+    if (oracleGrids_++ > 0) {
+      oracleOut_.aborted = true;
+      oracleOut_.error = "the GPU oracle explores programs with one kernel launch";
+    } else if (l.grid * l.block > oracleMaxThreads_) {
+      oracleOut_.aborted = true;
+      oracleOut_.error = "kernel spawns more threads than the oracle size bound";
+    } else if (!eng_->hasDevice() || !eng_->exploreGrid(g, oracle_, oracleOut_)) {
+      oracleOut_.aborted = true;
+      if (oracleOut_.error.empty()) oracleOut_.error = engWhy_.empty() ? "oracle exploration failed" : engWhy_;
+    }
+  }
   if (hooks_.mem) {
     engineError_ = "onMemAccess is set: device accesses run inside the B200 grid kernel and cannot be "
                    "reported one by one";
@@ -1826,6 +1854,31 @@ RunResult Machine::run() {
   impl_->last = r;
   impl_->ran = true;
   return r;
+}
+
+OracleResult oracleRace(std::shared_ptr<const Program> prog, OracleOptions opts) {
+  RunOptions ro;
+  ro.policy = SchedulePolicy::RoundRobin;
+  ro.raceCheck = true;
+  ro.arch = opts.arch;
+  mckb::HostMachine hm(std::move(prog), ro);
+  mckb::OracleSpec spec;
+  spec.maxInterleavings = opts.maxInterleavings;
+  spec.maxAccessesPerThread = opts.maxAccessesPerThread;
+  hm.setOracle(spec, opts.maxThreads);
+  const RunResult r = hm.run();
+  OracleResult out;
+  const mckb::OracleOut& o = hm.oracleOut();
+  out.oracleRace = o.oracleRace;
+  out.detectorRace = o.detectorRace;
+  out.aborted = o.aborted;
+  out.error = o.error;
+  out.interleavings = hm.oracleGrids() ? o.interleavings : 1;  // no grid: one (host-only) schedule
+  if (!r.engineError.empty() && !out.aborted) {
+    out.aborted = true;
+    out.error = r.engineError;
+  }
+  return out;
 }
 
 std::vector<StuckReport> Machine::scanStuck() const {

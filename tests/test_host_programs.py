@@ -71,3 +71,11 @@ def test_result_record_abi_matches_json_abi(name):
     for k in ("exit", "output", "steps", "stuck", "main_return", "engine_error", "diags", "stuck_reports",
               "report_text", "reported", "trace"):
         assert a[k] == b[k], k
+
+
+def test_oracle_without_a_kernel_runs_on_the_host():
+    """oracleRace of a host-only program: one schedule, nothing to explore."""
+    from paper_1211_6193_b200 import checker
+    r = checker.oracle_race("int main(void) { int x = 3; return x - 3; }\n")
+    assert r == {"oracle_race": False, "detector_race": False, "interleavings": 1, "aborted": False, "error": ""}
+    assert "frontend_error" in checker.oracle_race("int main(void) { return 0 }\n")
