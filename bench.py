@@ -180,12 +180,11 @@ def run_reference(args):
     }), flush=True)
 
 
-def load_traffic():
+def load_traffic(key="detect_call"):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-            return d.get("detect_call", d.get("race_detect_kernel"))
+            return json.load(f).get(key)
     except (OSError, ValueError):
         return None
 
@@ -441,7 +440,8 @@ def run_c5(args, blocks, dev, ws, rank, comm=None):
     return {"workload": f"C5: {events} global 4-byte accesses, {blocks} blocks, 1% cross-block, "
                         f"address-range all-to-all over {ws} GPU(s)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "kernel": "mckg_detect_global (sample, bucket count, scan, "
+                         "frac": achieved / peak, "traffic": load_traffic("c5_call") if ws == 1 else None,
+                         "kernel": "mckg_detect_global (sample, bucket count, scan, "
                          "bucket scatter, bucket_detect)" + (" + K3 partition + NCCL all-to-all" if ws > 1 else ""),
                          "algorithmic_bytes": "16 B/event read (+ (P-1)/P x 16 B/event over NVLink at P ranks)"},
             "events_per_s": events / (ms / 1e3), "ms_per_step": ms, "races_reported": int(tot[1]),

@@ -197,16 +197,16 @@ def _mixed_blocks(seed, nb=80):
         kind = b % 5
         if kind == 1:  # 64 threads of epoch 0 write slot 0
             for i in rng.choice(512, 64, replace=False):
-                blk["w0"][i] = (blk["w0"][i] & ~0xFFFFF) | 0 | (1 << 24)
+                blk["w0"][i] = (int(blk["w0"][i]) & 0xFFF00000) | (1 << 24)
         elif kind == 2:  # the last 100 records move to a third epoch
             e = (blk["w1"][-1] >> 11) + 1
-            blk["w1"][-100:] = (blk["w1"][-100:] & 0x7FF) | (e << 11)
+            blk["w1"][-100:] = (blk["w1"][-100:] & np.uint32(0x7FF)) | np.uint32(int(e) << 11)
         elif kind == 3:  # one aligned 1-byte access
             i = int(rng.integers(1024))
-            blk["w0"][i] = (blk["w0"][i] & ~(0xF << 20)) | (1 << 20)
+            blk["w0"][i] = (int(blk["w0"][i]) & 0xFF0FFFFF) | (1 << 20)
         elif kind == 4:  # one 2-byte access in the upper half of a word
             i = int(rng.integers(1024))
-            blk["w0"][i] = ((blk["w0"][i] & ~(0xF << 20)) | (2 << 20)) + 2
+            blk["w0"][i] = ((int(blk["w0"][i]) & 0xFF0FFFFF) | (2 << 20)) + 2
         ev[b * 1024:(b + 1) * 1024] = blk
     return ev, bs
 
