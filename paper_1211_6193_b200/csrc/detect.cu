@@ -32,7 +32,6 @@
 //     4. report: racing (byte, line) pairs are deduplicated per block through
 //        a (word, line) -> byte-mask table, staged and appended to the global
 //        triple array; the first racing timestamp per line is min-reduced.
-#include <cub/cub.cuh>
 #include <algorithm>
 #include <atomic>
 #include <vector>
@@ -42,6 +41,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 // TMA stages and CTAs/SM of the general kernel
 #ifndef MCKG_K2_NSTAGE
@@ -1148,30 +1148,24 @@ extern "C" int mckg_sort_triples(mckg_race_triple* triples, uint64_t n, uint32_t
     return MCKG_OK;
   }
   if (!triples) return MCKG_E_ARG;
+  // (obj - obj_base):22 | byte:20 | line:16 keys, radix-sorted (sort.cu),
+  // optionally reduced to the distinct ones, decoded back in place
   unsigned long long *k0 = nullptr, *k1 = nullptr;
-  void* tmp = nullptr;
-  size_t tmp_bytes = 0, tmp2 = 0;
   MCKG_CUDA_TRY(cudaMallocAsync(&k0, n * sizeof(unsigned long long), s));
   MCKG_CUDA_TRY(cudaMallocAsync(&k1, n * sizeof(unsigned long long), s));
   uint32_t nb = (uint32_t)((n + 255) / 256);
+  uint32_t launches = 1;
   encode_triples<<<nb, 256, 0, s>>>(triples, k0, n, obj_base);
-  cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, k0, k1, (int64_t)n, 0, 58, s);
+  MCKG_CUDA_TRY(radix_sort_u64(k0, k1, n, 58, s, &launches));
   if (n_unique) {
-    cub::DeviceSelect::Unique(nullptr, tmp2, k1, k0, n_unique, (int64_t)n, s);
-    tmp_bytes = std::max(tmp_bytes, tmp2);
-  }
-  MCKG_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
-  MCKG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, k0, k1, (int64_t)n, 0, 58, s));
-  if (n_unique) {
-    MCKG_CUDA_TRY(cub::DeviceSelect::Unique(tmp, tmp_bytes, k1, k0, n_unique, (int64_t)n, s));
-    decode_triples<<<nb, 256, 0, s>>>(k0, triples, n_unique, n, obj_base);
+    MCKG_CUDA_TRY(unique_sorted_u64(k0, n, k1, n_unique, s, &launches));
+    decode_triples<<<nb, 256, 0, s>>>(k1, triples, n_unique, n, obj_base);
   } else {
-    decode_triples<<<nb, 256, 0, s>>>(k1, triples, nullptr, n, obj_base);
+    decode_triples<<<nb, 256, 0, s>>>(k0, triples, nullptr, n, obj_base);
   }
   MCKG_CUDA_TRY(cudaGetLastError());
-  cudaFreeAsync(tmp, s);
   cudaFreeAsync(k0, s);
   cudaFreeAsync(k1, s);
-  add_launches(n_unique ? 4 : 3);
+  add_launches(launches + 1);
   return MCKG_OK;
 }

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 namespace mckg {
 namespace {
@@ -475,81 +476,7 @@ __global__ void bucket_scatter_kernel(const mckg_gaccess* ev, uint64_t n, uint32
   }
 }
 
-// ---- exclusive scan of the bucket counts (three kernels) ----
-constexpr uint32_t SCT = 1024;  // elements per scan tile
-
-__global__ void scan_tiles_kernel(const uint32_t* in, uint32_t n, uint64_t* tile_sum) {
-  __shared__ uint64_t ws[32];
-  const uint32_t i = blockIdx.x * SCT + threadIdx.x;
-  uint64_t v = i < n ? in[i] : 0u;
-  for (int d = 16; d; d >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, d);
-  if ((threadIdx.x & 31u) == 0) ws[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint64_t s = ws[threadIdx.x];
-    for (int d = 16; d; d >>= 1) s += __shfl_down_sync(0xFFFFFFFFu, s, d);
-    if (threadIdx.x == 0) tile_sum[blockIdx.x] = s;
-  }
-}
-
-// exclusive scan of <= SCT * SCT tile sums by one CTA, in place
-__global__ void scan_sums_kernel(uint64_t* sums, uint32_t n) {
-  __shared__ uint64_t ws[32];
-  __shared__ uint64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  for (uint32_t c0 = 0; c0 < n; c0 += SCT) {
-    __syncthreads();
-    const uint32_t i = c0 + threadIdx.x;
-    const uint64_t v = i < n ? sums[i] : 0u;
-    uint64_t x = v;
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
-      if ((threadIdx.x & 31u) >= (uint32_t)d) x += y;
-    }
-    if ((threadIdx.x & 31u) == 31u) ws[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      uint64_t w = ws[threadIdx.x];
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, w, d);
-        if (threadIdx.x >= (uint32_t)d) w += y;
-      }
-      ws[threadIdx.x] = w;
-    }
-    __syncthreads();
-    const uint64_t excl = carry + (threadIdx.x >= 32 ? ws[(threadIdx.x >> 5) - 1] : 0u) + x - v;
-    if (i < n) sums[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == SCT - 1) carry = excl + v;
-  }
-}
-
-__global__ void scan_apply_kernel(const uint32_t* in, uint32_t n, const uint64_t* tile_off, uint64_t* out) {
-  __shared__ uint64_t ws[32];
-  const uint32_t i = blockIdx.x * SCT + threadIdx.x;
-  const uint64_t v = i < n ? in[i] : 0u;
-  uint64_t x = v;
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
-    if ((threadIdx.x & 31u) >= (uint32_t)d) x += y;
-  }
-  if ((threadIdx.x & 31u) == 31u) ws[threadIdx.x >> 5] = x;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    uint64_t w = ws[threadIdx.x];
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xFFFFFFFFu, w, d);
-      if (threadIdx.x >= (uint32_t)d) w += y;
-    }
-    ws[threadIdx.x] = w;
-  }
-  __syncthreads();
-  const uint64_t excl = tile_off[blockIdx.x] + (threadIdx.x >= 32 ? ws[(threadIdx.x >> 5) - 1] : 0u) + x - v;
-  if (i < n) out[i] = excl;
-  if (i == n - 1) out[n] = excl + v;
-}
-
-// ---- the dense-span fast path: one warp per 4 KiB bucket ----
+// ---- the dense-span fast path: one warp per 2 KiB bucket ----
 // Buckets of FB_WORDS words, direct-indexed tag arrays per warp (no hashing),
 // races staged per warp and appended FB_STAGE at a time,
 // the K2 word filter with __syncwarp between its phases, and the exact pass
@@ -1004,28 +931,24 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
   const uint32_t nb = (uint32_t)((span >> shift) + 1);
   // 2-4. count, scan, scatter
   uint32_t *cnt = nullptr, *cur = nullptr, *big = nullptr;
-  uint64_t *off = nullptr, *tsum = nullptr;
+  uint64_t* off = nullptr;
   mckg_gaccess* recs = nullptr;
-  const uint32_t ntiles = (nb + SCT - 1) / SCT;
   MCKG_CUDA_TRY(cudaMallocAsync(&cnt, (size_t)nb * 4, s));
   MCKG_CUDA_TRY(cudaMallocAsync(&cur, (size_t)nb * 4, s));
   MCKG_CUDA_TRY(cudaMallocAsync(&off, ((size_t)nb + 1) * 8, s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&tsum, (size_t)ntiles * 8, s));
   MCKG_CUDA_TRY(cudaMallocAsync(&big, ((size_t)nb + 1) * 4, s));
   MCKG_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)nb * 4, s));
   MCKG_CUDA_TRY(cudaMemsetAsync(cur, 0, (size_t)nb * 4, s));
   MCKG_CUDA_TRY(cudaMemsetAsync(big, 0, 4, s));
   const uint32_t g = grid_for(n, 16);
   bucket_count_kernel<<<g, 256, 0, s>>>(events, n, nb, shift, base, cnt, status);
-  scan_tiles_kernel<<<ntiles, SCT, 0, s>>>(cnt, nb, tsum);
-  scan_sums_kernel<<<1, SCT, 0, s>>>(tsum, ntiles);
-  scan_apply_kernel<<<ntiles, SCT, 0, s>>>(cnt, nb, tsum, off);
+  MCKG_CUDA_TRY(exclusive_scan_u32(cnt, nb, off, s, &launches));
   MCKG_CUDA_TRY(cudaGetLastError());
   // a record counts once per bucket it touches (at most two): 2n slots
   // bound the layout without waiting for the count
   MCKG_CUDA_TRY(cudaMallocAsync(&recs, 2 * n * sizeof(mckg_gaccess), s));
   bucket_scatter_kernel<<<g, 256, 0, s>>>(events, n, nb, shift, base, off, cur, recs);
-  launches += 5;
+  launches += 2;
   // 5. detection
   BOut O{races, capacity, n_races, line_first, status};
   MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BD_SMEM));
@@ -1102,7 +1025,6 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
   cudaFreeAsync(cnt, s);
   cudaFreeAsync(cur, s);
   cudaFreeAsync(off, s);
-  cudaFreeAsync(tsum, s);
   cudaFreeAsync(big, s);
   add_launches(launches);
   return MCKG_OK;

@@ -10,9 +10,9 @@
 // 32 tids builds the waiting mask (the report's waitingTids; its complement
 // is missingTids), and __syncthreads_or flags the block.  Deadlocked bids are
 // stream-compacted in ascending order (the std::map walk of deadlock.cpp:15).
-#include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 namespace mckg {
 namespace {
@@ -71,15 +71,10 @@ extern "C" int mckg_scan_stuck(const uint32_t* arrivals, uint32_t n_blocks, uint
   uint32_t grid = n_blocks < (uint32_t)sm_count() * 8u ? n_blocks : (uint32_t)sm_count() * 8u;
   stuck_kernel<<<grid, NT, 0, s>>>(arrivals, n_blocks, block_dim, words, waiting_mask, flags);
   MCKG_CUDA_TRY(cudaGetLastError());
-  cub::CountingInputIterator<uint32_t> ids(bid_base);
-  size_t tmp_bytes = 0;
-  cub::DeviceSelect::Flagged(nullptr, tmp_bytes, ids, flags, dl_bids, n_dl, (int64_t)n_blocks, s);
-  void* tmp = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
-  MCKG_CUDA_TRY(cub::DeviceSelect::Flagged(tmp, tmp_bytes, ids, flags, dl_bids, n_dl,
-                                           (int64_t)n_blocks, s));
-  cudaFreeAsync(tmp, s);
+  // the deadlocked bids in ascending order (hand-written compaction, sort.cu)
+  uint32_t launches = 1;
+  MCKG_CUDA_TRY(select_flagged_index(flags, n_blocks, bid_base, dl_bids, n_dl, s, &launches));
   cudaFreeAsync(flags, s);
-  note_launch(2, grid, NT, 0);
+  note_launch(launches, grid, NT, 0);
   return MCKG_OK;
 }

@@ -251,3 +251,28 @@ def test_oversize_shared_object():
                           kinds=("int", "long"), hot=0.6)
     res, n = _check(ev, bs, 262144)
     assert n > 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 4095, 4097, 3_000_000])
+def test_sort_triples_hand_written_radix(n):
+    """mckg_sort_triples (the hand-written radix sort + unique of sort.cu):
+    std::set order and the distinct set, against numpy."""
+    import ctypes
+    import torch
+    from paper_1211_6193_b200 import _abi, race
+    rng = np.random.default_rng(n)
+    tri = np.zeros(n, dtype=ob.TRIPLE_DTYPE)
+    tri["obj"] = 7 + rng.integers(0, 1 << 12, n)
+    tri["byte"] = rng.integers(0, 1 << 20, n)
+    tri["line"] = rng.integers(0, 1 << 16, n)
+    tri[n // 2:] = tri[: n - n // 2]  # duplicates
+    dev = torch.from_numpy(tri.view(np.int32).reshape(-1, 3).copy()).cuda()
+    nu = torch.zeros(1, dtype=torch.int64, device="cuda")
+    lib = _abi.load()
+    _abi.check(lib.mckg_sort_triples(ctypes.c_void_p(dev.data_ptr()), n, 7, ctypes.c_void_p(nu.data_ptr()),
+                                     race._stream_handle(None)), "mckg_sort_triples")
+    torch.cuda.synchronize()
+    want = np.unique(tri[np.lexsort((tri["line"], tri["byte"], tri["obj"]))])
+    k = int(nu.item())
+    got = dev[:k].cpu().numpy().view(ob.TRIPLE_DTYPE).reshape(-1)
+    assert k == len(want) and np.array_equal(got, want)
