@@ -142,6 +142,13 @@ struct KP {
   uint32_t* tarr;             // trace mode: [block][episode < TEP][tid] arrival sweep + 1
   int markDirty;              // record global writes in META_DIRTY (replicated memory)
   uint32_t maxSweeps;         // < 2^26; each sweep takes >= 1 step (step limit)
+  // serial tails (K = 1): a block whose last unfinished thread runs alone is
+  // suspended into a slot and finished by tail_kernel, 32 tails per warp
+  struct TailState* tails;    // [tailCap]
+  uint8_t* tailSmem;          // [tailCap][tailStride]: bytes, meta, shadow, race set
+  uint32_t* tailCount;        // slots taken
+  uint32_t* tailBlk;          // [tailCap] the block (launch index) of each slot
+  uint32_t tailCap, tailStride;
   // RunOptions::globalRaceCheck: every global access appended here (K6 input)
   mckg_gaccess* glog;
   unsigned long long* nglog;
@@ -192,6 +199,7 @@ struct BlockShared {
   uint32_t lastSweep;
   uint32_t nextRun[2][32];  // per warp: first sweep a thread of it can step (~0u: none), by sweep parity
   uint32_t soloSweep;  // sweep reached by a solo warp
+  int tailSlot;        // >= 0: the block was suspended into this tail slot
 };
 
 __device__ __forceinline__ void set_error(const KP& P, int code, int info) {
@@ -598,6 +606,28 @@ struct Thread {
   uint32_t E;  // completed episodes (the race epoch)
 };
 
+// A suspended block's last thread and the block's counters (tail_kernel).
+struct TailState {
+  TS t;
+  Thread th;
+  BlockShared bs;  // step()'s barrier counters
+  uint32_t sweep, E, lastStep, tid;
+};
+
+// The layout of a suspended block's shared state in global memory.
+__host__ __device__ inline SmemLay tailLayout(int64_t shmem, int raceCheck) {
+  SmemLay L;
+  const uint32_t S = (uint32_t)((shmem + 15) & ~15ll);
+  L.bytes = 0;
+  L.meta = S;
+  L.shadow = 2 * S;
+  L.raceSet = (raceCheck ? 6 * S : 2 * S);
+  L.htKey = L.htVal = 0;
+  L.end = L.raceSet + (raceCheck ? 8 * RACE_SET : 0);
+  L.end = (L.end + 15) & ~15u;
+  return L;
+}
+
 __device__ __forceinline__ const mck_local& local_of(const KP& P, int fn, int slot) {
   return P.locals[P.fns[fn].local_base + slot];
 }
@@ -752,17 +782,19 @@ __device__ int mem_write(TS& t, const KP& P, Ctx& c, Thread& th, uint32_t obj, i
 }
 
 // Performs a pending shared/global request (memory phase).
+// sb: the base of the block's shared state laid out by L (the CTA's shared
+// memory, or a suspended block's copy in global memory)
 __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq, const SmemLay& L, uint32_t stamp,
-                           uint32_t bstamp, unsigned long long& sharedEvents) {
+                                        uint32_t bstamp, unsigned long long& sharedEvents, uint8_t* sb) {
   int len = (int)t_scalar(rq.ty);
   uint8_t *b, *m;
   if (rq.space == R_OK_SHARED) {
-    b = smem + L.bytes + rq.off;
-    m = smem + L.meta + rq.off;
+    b = sb + L.bytes + rq.off;
+    m = sb + L.meta + rq.off;
     if (P.raceCheck) {
       ++sharedEvents;
-      uint32_t raced = shadow_access((uint32_t*)(smem + L.shadow), rq.off, len, c.tid, rq.kind == 2, stamp);
-      report_race(P, c, (unsigned long long*)(smem + L.raceSet), rq.obj, rq.off, raced, rq.line, bstamp);
+      uint32_t raced = shadow_access((uint32_t*)(sb + L.shadow), rq.off, len, c.tid, rq.kind == 2, stamp);
+      report_race(P, c, (unsigned long long*)(sb + L.raceSet), rq.obj, rq.off, raced, rq.line, bstamp);
     }
   } else {
     b = P.gbytes + rq.base + rq.off;
@@ -786,7 +818,7 @@ __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq
   }
   if (rq.kind == 2) {
     if (rq.space == R_OK_SHARED)
-      store_raw(smem + L.bytes, smem + L.meta, rq.size, rq.off, len, rq.raw, rq.ptr);
+      store_raw(sb + L.bytes, sb + L.meta, rq.size, rq.off, len, rq.raw, rq.ptr);
     else {
       store_raw(P.gbytes + rq.base, P.gmeta + rq.base, rq.size, rq.off, len, rq.raw, rq.ptr);
       if (P.markDirty)
@@ -1158,6 +1190,39 @@ __device__ __forceinline__ int ht_insert(unsigned long long* keys, uint32_t* val
 }
 
 
+// Copies a block's shared state into its tail slot (threads g < nthr of the
+// calling group take part) and the block's last READY thread's state.
+__device__ void suspend_block(const KP& P, BlockShared& bs, const SmemLay& L, const TS& t, const Thread& th,
+                              uint32_t g, uint32_t nthr, uint32_t n, uint32_t sweep, uint32_t E, uint32_t lastStep,
+                              uint32_t lb) {
+  const int sl = *(volatile int*)&bs.tailSlot;
+  TailState& TSs = P.tails[sl];
+  uint8_t* dst = P.tailSmem + (size_t)sl * P.tailStride;
+  const SmemLay TL = tailLayout(P.shmem, P.raceCheck);
+  const uint32_t me = g % nthr;
+  for (uint32_t i = me; i < (uint32_t)P.shmem; i += nthr) {
+    dst[TL.bytes + i] = smem[L.bytes + i];
+    dst[TL.meta + i] = smem[L.meta + i];
+  }
+  if (P.raceCheck) {
+    const uint32_t* sh = (const uint32_t*)(smem + L.shadow);
+    uint32_t* dsh = (uint32_t*)(dst + TL.shadow);
+    for (uint32_t i = me; i < (uint32_t)P.shmem; i += nthr) dsh[i] = sh[i];
+    const unsigned long long* rs = (const unsigned long long*)(smem + L.raceSet);
+    unsigned long long* drs = (unsigned long long*)(dst + TL.raceSet);
+    for (uint32_t i = me; i < RACE_SET; i += nthr) drs[i] = rs[i];
+  }
+  if (g < n && th.state == S_READY) {
+    TSs.t = t;
+    TSs.th = th;
+    TSs.sweep = sweep;
+    TSs.E = E;
+    TSs.lastStep = lastStep;
+    TSs.tid = g;
+    P.tailBlk[sl] = lb;
+  }
+}
+
 // ================= the kernel =================
 // K simulated threads per GPU thread: simulated tid = k * CT + threadIdx.x
 // (CT = blockDim.x, a multiple of 32).  Smaller CTAs let more simulated
@@ -1207,6 +1272,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
     bs.lastSweep = 0;
     for (int w = 0; w < 32; ++w) bs.nextRun[0][w] = bs.nextRun[1][w] = 0u;
     bs.soloSweep = 0;
+    bs.tailSlot = -1;
   }
   __syncthreads();
 
@@ -1277,6 +1343,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
   uint32_t lastStep = 0;
   const uint32_t Lt = n - 1;
   bool justSolo = true;  // the next-run table is valid only after a full sweep
+  bool noTail = false;   // a tail slot was refused: no further suspension attempts
   bool released = false;  // an episode completed at the loop top (closed-form release)
   uint32_t relT = 0;
   uint32_t soloH = ~0u;   // solo: the first sweep another warp can step
@@ -1349,6 +1416,24 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
         deadlocked = true;
         break;
       }
+      // ---- the serial tail: one unfinished thread left and it is READY
+      // (K = 1).  The block is suspended into a tail slot -- its shared
+      // state, the thread's interpreter state and the block's counters --
+      // and the CTA is freed; tail_kernel finishes it, one lane per block ----
+      if (K == 1 && P.tailCap && !noTail && nfin == (int)SLOTS - 1) {
+        if (g == 0) {
+          const uint32_t sl = atomicAdd(P.tailCount, 1u);
+          bs.tailSlot = sl < P.tailCap ? (int)sl : -2;
+        }
+        __syncthreads();
+        if (bs.tailSlot >= 0) {
+          suspend_block(P, bs, L, t[0], th[0], g, CT, n, sweep, E, lastStep, lb);
+          break;
+        }
+        __syncthreads();
+        if (g == 0) bs.tailSlot = -1;
+        noTail = true;  // the slots are taken: this block finishes here
+      }
       // ---- solo mode: when a single warp holds every READY thread, no other
       // thread can move until that warp arrives at a barrier or finishes, so
       // it runs sweeps alone with warp-level synchronisation while the other
@@ -1380,6 +1465,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
           const uint32_t s0 = sweep;
           bar_named(1, CT);  // until the solo warp is done
           soloCycles += clock64() - c0;
+          if (*(volatile int*)&bs.tailSlot >= 0) break;  // the block was suspended
           sweep = bs.soloSweep;
           soloSweeps += sweep - s0;
           justSolo = true;
@@ -1401,6 +1487,28 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       bar_named(1, CT);
       justSolo = true;
       continue;
+    }
+    if (solo && K == 1 && P.tailCap && !noTail && *(volatile int*)&bs.fin == (int)SLOTS - 1) {
+      // the solo warp's last thread is the block's last: suspend it (the
+      // other warps are parked and join the exit below)
+      int sl = 0;
+      if (lane == 0) {
+        const uint32_t x = atomicAdd(P.tailCount, 1u);
+        sl = x < P.tailCap ? (int)x : -2;
+      }
+      sl = __shfl_sync(0xFFFFFFFFu, sl, 0);
+      if (sl >= 0) {
+        if (lane == 0) bs.tailSlot = sl;
+        __syncwarp();
+        suspend_block(P, bs, L, t[0], th[0], g, 32u, n, sweep, E, lastStep, lb);
+        soloCycles += clock64() - soloC0;
+        soloSweeps += sweep - soloS0;
+        if (lane == 0) bs.soloSweep = sweep;
+        __threadfence_block();
+        bar_named(1, CT);  // release the parked warps
+        break;
+      }
+      noTail = true;
     }
     ++sweep;
     if (sweep >= P.maxSweeps) {
@@ -1487,7 +1595,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
         if (!((pendMask >> k) & 1u)) continue;
         c.tid = (uint32_t)k * CT + g;
         c.sub = 1;
-        do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents);
+        do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents, smem);
         finish_request(t[k], P, th[k], rq[k], pd[k]);
         if (th[k].state == S_FIN) atomicAdd(&bs.fin, 1);
       }
@@ -1501,7 +1609,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
               if (lane == l && ((pendMask >> k) & 1u)) {
                 c.tid = (uint32_t)k * CT + g;
                 c.sub = 1;
-                do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents);
+                do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents, smem);
                 finish_request(t[k], P, th[k], rq[k], pd[k]);
                 if (th[k].state == S_FIN) atomicAdd(&bs.fin, 1);
               }
@@ -1553,6 +1661,35 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
     __syncthreads();
   }
 
+  if (bs.tailSlot >= 0) {
+    // suspended: the counters of every thread but the tail's go to the
+    // block's partial outputs; tail_kernel adds the rest
+    unsigned long long mySteps = 0, myAllocs = 0;
+    if (!(g < n && th[0].state == S_READY)) {
+      mySteps = t[0].steps;
+      myAllocs = t[0].allocs;
+    }
+    atomicAdd(&bs.steps, mySteps);
+    atomicAdd(&bs.allocs, myAllocs);
+    atomicAdd(&bs.sharedEvents, sharedEvents);
+    atomicMax(&bs.lastSweep, lastStep);
+    __syncthreads();
+    if (g == 0) {
+      BlockOut& o = P.blocks[lb];
+      o.sweeps = bs.soloSweep > sweep ? bs.soloSweep : sweep;
+      o.soloSweeps = soloSweeps;
+      o.cycles = (unsigned long long)(clock64() - kStart);
+      o.soloCycles = (unsigned long long)soloCycles;
+      o.steps = bs.steps;
+      o.rules = rules;
+      o.allocs = bs.allocs;
+      o.sharedEvents = bs.sharedEvents;
+      o.lastSweep = bs.lastSweep;
+      o.deadlocked = 0;
+      o.episodes = E;
+    }
+    return;
+  }
   // ---- block outputs ----
   const uint32_t words = (n + 31) / 32;
   unsigned long long steps = 0, allocs = 0;
@@ -1600,6 +1737,99 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
     o.lastSweep = bs.lastSweep;
     o.deadlocked = deadlocked ? 1 : 0;
     o.episodes = E;
+  }
+}
+
+// ---- tail_kernel: suspended serial tails, one lane per block ----
+// The lane continues its block's last thread exactly where grid_kernel left
+// it: one step per sweep from max(sweep + 1, readyAt), memory requests served
+// at once against the block's shared state in global memory (a lone thread
+// has no conflicts), the same shadow and dedup set.  A barrier completes at
+// once for a one-thread block (Turnaround and FinalRelease in the arrival
+// sweep, Appendix A); with finished peers it never does: a deadlock whose
+// up-sweep stops at the first finished thread.  The tails of C2's blocks run
+// the same code, so a warp executes 32 of them in lockstep.
+__global__ void __launch_bounds__(128) tail_kernel(KP P) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t cnt = min(*P.tailCount, P.tailCap);
+  if (i >= cnt) return;
+  TailState& S = P.tails[i];
+  const uint32_t lb = P.tailBlk[i];
+  const uint32_t bid = lb + P.bidBase;
+  const uint32_t n = (uint32_t)P.blockDim;
+  uint8_t* sb = P.tailSmem + (size_t)i * P.tailStride;
+  const SmemLay TL = tailLayout(P.shmem, P.raceCheck);
+  TS& t = S.t;
+  Thread th = S.th;
+  uint32_t sweep = S.sweep, lastStep = S.lastStep, E = S.E;
+  const uint32_t tid = S.tid, sweep0 = S.sweep;
+  unsigned long long sharedEvents = 0, rules = 0;
+  const long long c0 = clock64();
+  bool deadlocked = false;
+  Ctx c;
+  c.bid = bid;
+  c.tid = tid;
+  while (true) {
+    if (th.state == S_WAIT) {
+      if (n != 1) {
+        deadlocked = true;  // every peer has finished: the episode never completes
+        break;
+      }
+      // a one-thread block: the episode completes in the arrival sweep
+      Val res;
+      switch (th.syncKind) {
+        case MCK_SYNC_AND: res = v_int(th.operand != 0 ? 1 : 0); break;
+        case MCK_SYNC_OR: res = v_int(th.operand != 0 ? 1 : 0); break;
+        case MCK_SYNC_COUNT: res = v_int(th.operand != 0 ? 1 : 0); break;
+        default: res = v_void(); break;
+      }
+      push(t, P, res);
+      th.state = S_READY;
+      th.readyAt = sweep + 1;
+      th.operand = 0;
+      ++th.E;
+      ++E;
+      rules += 2;
+      if (P.raceCheck && (E & 0xFF) == 0) {  // stamp wrap: clear the shadow
+        uint32_t* sh = (uint32_t*)(sb + TL.shadow);
+        for (uint32_t b = 0; b < (uint32_t)P.shmem; ++b) sh[b] = shadow_empty(0);
+      }
+    }
+    if (th.state != S_READY) break;
+    sweep = max(sweep + 1, th.readyAt);
+    if (sweep >= P.maxSweeps) {
+      set_error(P, ERR_SWEEPS, 0);
+      break;
+    }
+    c.sweep = sweep;
+    c.sub = 0;
+    lastStep = sweep;
+    Req rq;
+    Pend pd;
+    rq.kind = 0;
+    if (step(t, P, c, th, rq, pd, S.bs, n) && th.state != S_FIN) {
+      c.sub = 1;
+      do_request(P, c, th, rq, TL, E & 0xFF, bid, sharedEvents, sb);
+      finish_request(t, P, th, rq, pd);
+    }
+  }
+  BlockOut& o = P.blocks[lb];
+  o.steps += t.steps;
+  o.allocs += t.allocs;
+  o.sharedEvents += sharedEvents;
+  o.lastSweep = max(o.lastSweep, lastStep);
+  o.sweeps = sweep;
+  o.soloSweeps += sweep - sweep0;
+  o.cycles += (unsigned long long)(clock64() - c0);
+  o.rules += rules;
+  o.episodes = E;
+  if (deadlocked) {
+    const uint32_t words = (n + 31) / 32;
+    o.deadlocked = 1;
+    P.waitMask[(size_t)lb * words + tid / 32] = 1u << (tid % 32);
+    // up-sweep rules of the stuck episode: first non-waiting tid - 1
+    const uint32_t firstNot = tid == 0 ? 1u : 0u;
+    if (firstNot >= 1) o.rules += firstNot - 1;
   }
 }
 
@@ -1784,7 +2014,7 @@ __global__ void __launch_bounds__(64, 1) oracle_kernel(KP P0, OQ Q) {
             aborted = true, err = err ? err : 3u;
         }
         unsigned long long se = 0;
-        do_request(P, c, th[i], rq, L, 0, 0, se);
+        do_request(P, c, th[i], rq, L, 0, 0, se, osm);
         finish_request(t[i], P, th[i], rq, pd);
       }
       // barrier: a block whose threads all wait is released (the up /
@@ -2048,6 +2278,10 @@ struct Replica {
   DBuf<k1::BlockOut> blocks;
   DBuf<uint32_t> tarr;
   DBuf<int> err;
+  DBuf<k1::TailState> tails;        // suspended serial tails (K = 1)
+  DBuf<uint8_t> tailSmem;
+  DBuf<uint32_t> tailCnt, tailBlk;
+  uint32_t tailCap = 0;             // tail slots of the current grid (0: none)
   DBuf<mckg_gaccess> glog;          // RunOptions::globalRaceCheck
   DBuf<unsigned long long> gcnt;    // [0] log length, [1] K6 races, [2..] K6 line table
   DBuf<uint32_t> gstat;
@@ -2078,6 +2312,20 @@ class CudaEngine final : public DeviceEngine {
       CK(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
       CK(cudaEventCreate(&r.e0));
       CK(cudaEventCreate(&r.e1));
+      // reserve the interpreter's local memory now (per-thread frames of
+      // tens of KB x every resident thread): a lazy reservation at the first
+      // grid launch would land inside the grid's timed region
+      static bool reserved[64] = {};
+      if (r.dev >= 0 && r.dev < 64 && !reserved[r.dev]) {
+        cudaFuncAttributes fa;
+        size_t frame = 0;
+        if (cudaFuncGetAttributes(&fa, k1::grid_kernel<1>) == cudaSuccess) frame = std::max(frame, fa.localSizeBytes);
+        if (cudaFuncGetAttributes(&fa, k1::grid_kernel<4>) == cudaSuccess) frame = std::max(frame, fa.localSizeBytes);
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitStackSize);
+        if (frame > cur) CK(cudaDeviceSetLimit(cudaLimitStackSize, frame));
+        reserved[r.dev] = true;
+      }
     }
     // peer access between distinct physical devices (NVLink / NVSwitch)
     for (size_t i = 0; i < devs_.size(); ++i)
@@ -2485,6 +2733,24 @@ class CudaEngine final : public DeviceEngine {
       kp.tarr = g.trace ? R.tarr.p : nullptr;
       kp.markDirty = (D > 1 || exch_) ? 1 : 0;
       kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
+      // serial-tail slots (K = 1; MCKG_K1_TAILS=0 turns the offload off)
+      static const bool tailsOn = [] {
+        const char* e = getenv("MCKG_K1_TAILS");
+        return !(e && e[0] == '0');
+      }();
+      const uint32_t tailCap = (K == 1 && tailsOn) ? (uint32_t)std::min<size_t>(nb, 1u << 16) : 0u;
+      const SmemLay TL = tailLayout(g.shmemBytes, g.raceCheck ? 1 : 0);
+      if (tailCap && (!R.tails.ensure(tailCap, err) || !R.tailSmem.ensure((size_t)tailCap * TL.end, err) ||
+                      !R.tailCnt.ensure(1, err) || !R.tailBlk.ensure(tailCap, err)))
+        return false;
+      if (tailCap) CK(cudaMemsetAsync(R.tailCnt.p, 0, sizeof(uint32_t), R.stream));
+      kp.tails = tailCap ? R.tails.p : nullptr;
+      kp.tailSmem = tailCap ? R.tailSmem.p : nullptr;
+      kp.tailCount = tailCap ? R.tailCnt.p : nullptr;
+      kp.tailBlk = tailCap ? R.tailBlk.p : nullptr;
+      kp.tailCap = tailCap;
+      kp.tailStride = TL.end;
+      R.tailCap = tailCap;
       kp.glog = g.globalRaceCheck ? R.glog.p : nullptr;
       kp.nglog = g.globalRaceCheck ? R.gcnt.p : nullptr;
       kp.glogCap = glogCap;
@@ -2509,6 +2775,7 @@ class CudaEngine final : public DeviceEngine {
       }
       cudaEventRecord(R.e0, R.stream);
       kern<<<(unsigned)nb, threads, L.end, R.stream>>>(kp);
+      if (tailCap) tail_kernel<<<(tailCap + 127) / 128, 128, 0, R.stream>>>(kp);
       cudaEventRecord(R.e1, R.stream);
       CK(cudaGetLastError());
     }
@@ -2524,7 +2791,7 @@ class CudaEngine final : public DeviceEngine {
       float ms = 0;
       cudaEventElapsedTime(&ms, R.e0, R.e1);
       out.ms = std::max<double>(out.ms, ms);
-      out.launches += 2;
+      out.launches += R.tailCap ? 3 : 2;
       int herr[2];
       CK(cudaMemcpy(herr, R.err.p, sizeof herr, cudaMemcpyDeviceToHost));
       if (herr[0] == ERR_SWEEPS && g.stepBudget + 2 < (1ull << 26) - 1) {
