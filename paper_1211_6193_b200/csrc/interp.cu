@@ -1749,7 +1749,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
 // sweep, Appendix A); with finished peers it never does: a deadlock whose
 // up-sweep stops at the first finished thread.  The tails of C2's blocks run
 // the same code, so a warp executes 32 of them in lockstep.
-__global__ void __launch_bounds__(128) tail_kernel(KP P) {
+__global__ void __launch_bounds__(32) tail_kernel(KP P) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t cnt = min(*P.tailCount, P.tailCap);
   if (i >= cnt) return;
@@ -1759,7 +1759,7 @@ __global__ void __launch_bounds__(128) tail_kernel(KP P) {
   const uint32_t n = (uint32_t)P.blockDim;
   uint8_t* sb = P.tailSmem + (size_t)i * P.tailStride;
   const SmemLay TL = tailLayout(P.shmem, P.raceCheck);
-  TS& t = S.t;
+  TS t = S.t;  // into local memory (L1-cached), the tail's working copy
   Thread th = S.th;
   uint32_t sweep = S.sweep, lastStep = S.lastStep, E = S.E;
   const uint32_t tid = S.tid, sweep0 = S.sweep;
@@ -2775,7 +2775,7 @@ class CudaEngine final : public DeviceEngine {
       }
       cudaEventRecord(R.e0, R.stream);
       kern<<<(unsigned)nb, threads, L.end, R.stream>>>(kp);
-      if (tailCap) tail_kernel<<<(tailCap + 127) / 128, 128, 0, R.stream>>>(kp);
+      if (tailCap) tail_kernel<<<(tailCap + 31) / 32, 32, 0, R.stream>>>(kp);
       cudaEventRecord(R.e1, R.stream);
       CK(cudaGetLastError());
     }
