@@ -301,9 +301,11 @@ extern "C" int mckg_detect_shared_host(const mckg_trace* tr, mckg_race_triple* t
       fail("cudaMemcpy(results)", e);
       break;
     }
-    if ((*status_host & MCKG_ST_DUP) && n > 0) {
-      // the per-block dedup set overflowed: restore the exact set on device
-      if ((rc = mckg_sort_triples(out.triples, std::min<uint64_t>(n, capacity), tr->obj_base,
+    if ((*status_host & MCKG_ST_DUP) && n > 0 && n <= capacity) {
+      // the per-block dedup set overflowed: restore the exact set on device.
+      // (Past capacity the prefix's unique count would understate the total,
+      // so the overflow count and the DUP flag are returned as they are.)
+      if ((rc = mckg_sort_triples(out.triples, n, tr->obj_base,
                                   out.n_triples, st[0])))
         break;
       launches += 4;

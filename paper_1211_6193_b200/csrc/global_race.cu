@@ -421,8 +421,16 @@ __global__ void span_sample_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t 
     lo = a < lo ? a : lo;
     hi = a > hi ? a : hi;
   }
-  atomicMin(mm, lo);
-  atomicMax(mm + 1, hi);
+  // one atomic pair per warp (a single address hit by every thread serialises)
+  for (int d = 16; d; d >>= 1) {
+    const unsigned long long l = __shfl_xor_sync(0xFFFFFFFFu, lo, d), h = __shfl_xor_sync(0xFFFFFFFFu, hi, d);
+    lo = l < lo ? l : lo;
+    hi = h > hi ? h : hi;
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
 }
 
 __global__ void bucket_count_kernel(const mckg_gaccess* ev, uint64_t n, uint32_t nb, uint32_t shift, uint64_t base,
@@ -632,19 +640,74 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
   uint32_t flags = 0;
   // buckets are claimed in chunks from a counter: a fixed stride can alias
   // the data's period (e.g. every other 32 KiB empty) and idle half the warps
-  constexpr uint32_t CH = 8;
+  // (a chunk is 32 buckets: lane l holds bucket l's record range, so empty
+  // and single-record buckets cost no memory round trip)
+  constexpr uint32_t CH = 32;
   uint32_t b = 0, bend = 0;
+  uint64_t lo0 = 0, lo1 = 0;  // lane l: off[b0 + l], off[b0 + l + 1]
+  uint32_t b0 = 0;
   while (true) {
     if (b == bend) {
       uint32_t c0 = 0;
       if (lane == 0) c0 = atomicAdd(next, CH);
-      b = __shfl_sync(0xFFFFFFFFu, c0, 0);
+      b = b0 = __shfl_sync(0xFFFFFFFFu, c0, 0);
       bend = min(b + CH, nb);
+      if (b >= nb) break;
+      const uint32_t mine = b0 + lane;
+      lo0 = mine < nb ? off[mine] : 0;
+      lo1 = mine < nb ? off[mine + 1] : 0;
     }
-    if (b >= nb) break;
-    const uint32_t bb = b++;
-    const uint64_t o0 = off[bb], o1 = off[bb + 1];
-    if (o1 - o0 < 2) continue;  // a lone record cannot race
+    // the next bucket of the chunk with >= 2 records
+    const uint32_t busy = __ballot_sync(0xFFFFFFFFu, b0 + lane >= b && b0 + lane < bend && lo1 - lo0 >= 2);
+    if (!busy) {
+      b = bend;
+      continue;
+    }
+    const uint32_t bl = (uint32_t)__ffs(busy) - 1u;
+    const uint32_t bb = b0 + bl;
+    b = bb + 1;
+    const uint64_t o0 = __shfl_sync(0xFFFFFFFFu, lo0, bl), o1 = __shfl_sync(0xFFFFFFFFu, lo1, bl);
+    if (o1 - o0 <= 32u) {
+      // small buckets skip the filter: a run of whole buckets (contiguous
+      // records, disjoint words) of <= 32 records joins the exact batch --
+      // the filter only prunes, fb_exact decides every pair itself
+      if (nbatch + (uint32_t)(o1 - o0) > 32u) {
+        fb_exact(O, recs, cl, nbatch, C, stg, nstg, flags);
+        nbatch = 0;
+      }
+      const uint32_t room = 32u - nbatch;
+      const uint32_t fits = __ballot_sync(0xFFFFFFFFu, lane >= bl && b0 + lane < bend && lo1 - o0 <= room);
+      const uint32_t r = __popc(fits);  // buckets bl .. bl + r - 1 (lo1 is monotonic)
+      const uint64_t e = __shfl_sync(0xFFFFFFFFu, lo1, bl + r - 1u);
+      const uint32_t len = (uint32_t)(e - o0);
+      bool badr = false;
+      if (lane < len) {
+        const uint64_t a64 = recs[o0 + lane].a;
+        badr = (ga_addr(a64) & 3u) + ga_len(a64) > 4u;  // a word-contained record lies in its bucket
+      }
+      const uint32_t badm = __ballot_sync(0xFFFFFFFFu, badr);
+      if (badm) {
+        // hand the buckets holding crossing records to the general kernel;
+        // the rest of the run is retried from the next bucket on
+        const uint32_t p = (uint32_t)__ffs(badm) - 1u;  // first crossing record
+        const uint32_t hb = __ffs(__ballot_sync(0xFFFFFFFFu, lane >= bl && lane < bl + r &&
+                                                             lo0 - o0 <= p && p < lo1 - o0)) - 1u;
+        if (lane == 0) big[atomicAdd(nbig, 1u)] = b0 + hb;
+        b = b0 + hb + 1;
+        if (hb > bl) {  // the buckets before it are clean
+          const uint32_t clen = (uint32_t)(__shfl_sync(0xFFFFFFFFu, lo0, hb) - o0);
+          if (lane < clen) cl[nbatch + lane] = o0 + lane;
+          nbatch += clen;
+        }
+        __syncwarp();
+        continue;
+      }
+      if (lane < len) cl[nbatch + lane] = o0 + lane;
+      nbatch += len;
+      b = b0 + bl + r;
+      __syncwarp();
+      continue;
+    }
     if (o1 - o0 > FB_MAX) {
       if (lane == 0) big[atomicAdd(nbig, 1u)] = bb;
       continue;
@@ -653,6 +716,7 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
     const mckg_gaccess* R = recs + o0;
     uint64_t blo, bhi;
     bucket_range(bb, nb, FB_SHIFT, base, &blo, &bhi);
+
     // load + pack: word (10 bits) | write << 10 | bid << 11 (rows of 32
     // records, FB_BR rows in flight ahead of the decode)
     uint32_t pk[FB_ROWS];
@@ -683,7 +747,11 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
           const uint64_t a = ga_addr(a64);
           const bool in = i < m;
           bad |= in && ((a & 3u) + ga_len(a64) > 4u || a < blo || a >= bhi);
-          pk[j] = in ? (uint32_t)((a - blo) >> 2) | (ga_write(a64) << 10) | ((r.w & 0x1FFFFFu) << 11) : 0xFFFFFFFFu;
+          // the word index is swizzled (w ^ (w >> 5)): a row of records of
+          // consecutive threads at a 32-word stride (one thread's 128 B run
+          // per 4-byte slot) would otherwise land on one bank
+          const uint32_t w = (uint32_t)((a - blo) >> 2);
+          pk[j] = in ? (w ^ ((w >> 5) & 31u)) | (ga_write(a64) << 10) | ((r.w & 0x1FFFFFu) << 11) : 0xFFFFFFFFu;
         }
       } else {
 #pragma unroll
@@ -742,6 +810,347 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
   if (C.line != 0xFFFFFFFFu) atomicMin(O.line_first + C.line, C.ts);
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
   if (lane == 0 && flags) atomicOr(O.status, flags);
+}
+
+// ---- the in-place tile path (block-clustered inputs: a K1 log, C5) ----
+// Records come grouped by simulated block and a block's accesses mostly fall
+// in its own address range.  Instead of partitioning every record into
+// address buckets (count: read; scatter: read + write; detect: read), tiles of
+// TT consecutive records are checked where they lie:
+//   pass 0 (tile_claim): a tile's window is TW consecutive 2 KiB buckets from
+//     an anchor chosen on a sample of its records (the anchor covering most
+//     samples); it claims the window buckets it occupies (claim[b] += 1).
+//     Every other record of the tile (outside the window, crossing a word,
+//     out of range) is FOREIGN: appended to the side list, its words marked
+//     in a bitmap over the span;
+//   pass 1 (tile_detect): a record in its tile's window is OWN when its bucket
+//     was claimed by that tile alone and its word is unmarked.  No record of
+//     another tile touches an own record's word, so a tile whose own records
+//     all come from one block has no race among them (races are
+//     cross-block); otherwise they run the word filter of bucket_fast over
+//     the window's TW x 512 words.  The rest (contested buckets, marked
+//     words) are MIXED and join the side list;
+//   the side list (foreign + mixed, every record on their words) then runs
+//     through the bucket pipeline.
+// Each word is decided by exactly one of the two, so the race sets are
+// disjoint and their union is the bucket pipeline's on the whole input.
+// The window choice only moves records between the two routes.
+constexpr uint32_t TT = 4096;                // records per tile
+constexpr uint32_t TB = 512;                 // threads per tile CTA
+constexpr uint32_t TR = TT / TB;             // records per thread
+constexpr uint32_t TW = 16;                  // window buckets per tile
+constexpr uint32_t TWW = TW * FB_WORDS;      // window words
+constexpr uint32_t TS = 16;                  // anchor samples per tile
+constexpr uint32_t TBW = FB_WORDS / 32;      // bitmap words per bucket
+// pass-1 word table: bid (21 bits) | MULTI | WRITE (flags set by atomicOr)
+constexpr uint32_t TAG_MULTI = 1u << 30, TAG_WRITE = 1u << 31;
+// dynamic shared memory: the tile stage (TT records, filled by the bulk-copy
+// engine one tile ahead) + pass 1's word table
+constexpr uint32_t TC_SMEM = TT * 16;
+constexpr uint32_t TD_SMEM = TT * 16 + TWW * 4;
+
+// the bucket of an in-span, word-contained record, else ~0u
+__device__ __forceinline__ uint32_t tile_bucket(uint64_t a64, uint32_t bid, uint64_t base, uint32_t nbk) {
+  const uint64_t a = ga_addr(a64);
+  const uint32_t len = ga_len(a64);
+  if (len == 0 || (a & 3u) + len > 4u || a < base || bid >= MCKG_MAX_BID) return ~0u;
+  const uint64_t q = (a - base) >> FB_SHIFT;
+  return q < nbk ? (uint32_t)q : ~0u;
+}
+
+// one tile into the stage (thread 0; the stage's readers are past a barrier)
+__device__ __forceinline__ void tile_fetch(const mckg_gaccess* ev, uint64_t n, uint64_t t, void* stage,
+                                           uint64_t* bar) {
+  const uint64_t r0 = t * TT;
+  const uint32_t bytes = (uint32_t)((n - r0 < TT ? n - r0 : TT) * sizeof(mckg_gaccess));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(stage, ev + r0, bytes, bar);
+}
+
+__device__ __forceinline__ unsigned long long rec_a(const uint4& r) {
+  return ((unsigned long long)r.y << 32) | r.x;
+}
+
+// This thread's slot among a tile's flagged records (bits of `fm`): a warp
+// scan plus one shared-memory atomic per warp on the tile's counter.
+__device__ __forceinline__ uint32_t side_slot(uint32_t fm, uint32_t* cnt) {
+  const uint32_t lane = threadIdx.x & 31u;
+  if (!__any_sync(0xFFFFFFFFu, fm != 0u)) return 0;
+  const uint32_t c = __popc(fm);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= (uint32_t)d) incl += x;
+  }
+  uint32_t wb = 0;
+  if (lane == 31) wb = atomicAdd(cnt, incl);
+  return __shfl_sync(0xFFFFFFFFu, wb, 31) + incl - c;
+}
+
+// The deferred write of this thread's flagged records of the tile at r0
+// (re-read from ev: rare, L2-resident) to side[base + slot ...].
+__device__ __forceinline__ void side_write(uint32_t fm, uint32_t slot, unsigned long long base,
+                                           const mckg_gaccess* ev, uint64_t r0, mckg_gaccess* side) {
+  unsigned long long p = base + slot;
+  for (uint32_t q = fm; q; q &= q - 1u) side[p++] = ev[r0 + (uint64_t)((__ffs(q) - 1) * TB + threadIdx.x)];
+}
+
+// Pass 0, persistent: a CTA walks tiles blockIdx.x, + gridDim.x, ...; the
+// next tile streams into the stage while this one is classified.  Two
+// barriers per tile: the side-list base of a tile is taken after its second
+// barrier and its records are written after the next tile's first.  Output
+// per tile: win[t] = anchor | occupied-bucket mask << 32 (~0: no window).
+__global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t ntiles,
+                                                           uint64_t base, uint32_t nbk, uint32_t* claim,
+                                                           uint32_t* bits, unsigned long long* win,
+                                                           mckg_gaccess* side, unsigned long long* nside) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint4* stage = reinterpret_cast<const uint4*>(sm);
+  __shared__ uint32_t s_anchor, s_occ[2], s_cnt[2];
+  __shared__ unsigned long long s_base[2];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nwords = nbk * FB_WORDS;  // nbk <= 2^22
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    s_occ[0] = s_occ[1] = 0;
+    s_cnt[0] = s_cnt[1] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < ntiles) tile_fetch(ev, n, blockIdx.x, sm, &bar);
+  uint32_t pfm = 0, pslot = 0;  // the previous tile's foreign records (deferred)
+  uint64_t pr0 = 0;
+  uint32_t it = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const uint32_t cb = it & 1u;
+    const uint64_t r0 = t * TT;
+    const uint32_t m = (uint32_t)(n - r0 < TT ? n - r0 : TT);
+    mbar_wait(&bar, cb);
+    if (threadIdx.x < 32) {
+      // the anchor: of TS sampled buckets, the one whose TW-bucket window
+      // covers most samples (ties: the lowest)
+      const uint32_t si = lane * (TT / TS);
+      uint32_t sb = ~0u;
+      if (lane < TS && si < m) {
+        const uint4 r = stage[si];
+        sb = tile_bucket(rec_a(r), r.w & 0xFFFFFFu, base, nbk);
+      }
+      uint32_t cover = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < TS; ++j) {
+        const uint32_t u = __shfl_sync(0xFFFFFFFFu, sb, j);
+        cover += (u != ~0u && u - sb < TW);
+      }
+      const uint32_t key = sb == ~0u ? 0u : (cover << 23) | ((1u << 23) - 1u - sb);
+      const uint32_t best = __reduce_max_sync(0xFFFFFFFFu, key);
+      if (lane == 0) s_anchor = best ? (1u << 23) - 1u - (best & ((1u << 23) - 1u)) : ~0u;
+    }
+    __syncthreads();  // #1: s_anchor; the previous tile's side base
+    if (pfm) side_write(pfm, pslot, s_base[cb ^ 1u], ev, pr0, side);
+    const uint32_t anchor = s_anchor;
+    uint32_t fm = 0, occ = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < TR; ++k) {
+      const uint32_t i = k * TB + threadIdx.x;
+      if (i >= m) continue;
+      const uint4 r = stage[i];
+      const unsigned long long a64 = rec_a(r);
+      const uint32_t b = tile_bucket(a64, r.w & 0xFFFFFFu, base, nbk);
+      const uint32_t j = b - anchor;
+      if (b != ~0u && anchor != ~0u && j < TW) {
+        occ |= 1u << j;
+        continue;
+      }
+      fm |= 1u << k;
+      // foreign: mark the words it touches (clipped to the span)
+      const uint64_t a = ga_addr(a64);
+      const uint32_t len = ga_len(a64) ? ga_len(a64) : 1u;
+      if (a + len > base && a < base + ((uint64_t)nwords << 2)) {
+        const uint32_t w0 = a < base ? 0u : (uint32_t)((a - base) >> 2);
+        const uint64_t wl = (a + len - 1 - base) >> 2;
+        const uint32_t w1 = wl < nwords ? (uint32_t)wl : nwords - 1u;
+        for (uint32_t w = w0; w <= w1; ++w) atomicOr(bits + (w >> 5), 1u << (w & 31u));
+      }
+    }
+    occ = __reduce_or_sync(0xFFFFFFFFu, occ);
+    if (lane == 0 && occ) atomicOr(&s_occ[cb], occ);
+    const uint32_t slot = side_slot(fm, &s_cnt[cb]);
+    __syncthreads();  // #2: the stage is free; s_occ / s_cnt of this tile final
+    if (threadIdx.x == 0) {
+      if (t + gridDim.x < ntiles) tile_fetch(ev, n, t + gridDim.x, sm, &bar);
+      s_base[cb] = s_cnt[cb] ? atomicAdd(nside, (unsigned long long)s_cnt[cb]) : 0ull;
+      s_cnt[cb ^ 1u] = 0;  // the next tile's (last read before #2)
+      s_occ[cb ^ 1u] = 0;
+    }
+    const uint32_t so = s_occ[cb];
+    if (threadIdx.x == 32) win[t] = (anchor == ~0u || !so) ? ~0ull : ((unsigned long long)so << 32) | anchor;
+    if (threadIdx.x < TW && ((so >> threadIdx.x) & 1u)) atomicAdd(claim + anchor + threadIdx.x, 1u);
+    pfm = fm;
+    pslot = slot;
+    pr0 = r0;
+  }
+  __syncthreads();
+  if (pfm) side_write(pfm, pslot, s_base[(it - 1u) & 1u], ev, pr0, side);
+}
+
+// Pass 1, persistent like pass 0; the window metadata of a CTA's next tile
+// (claims, word marks) is fetched while this one is checked.
+__global__ void __launch_bounds__(TB, 2) tile_detect_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t ntiles,
+                                                            uint64_t base, uint32_t nbk, const uint32_t* claim,
+                                                            const uint32_t* bits, const unsigned long long* win,
+                                                            mckg_gaccess* side, unsigned long long* nside, BOut O) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const uint4* stage = reinterpret_cast<const uint4*>(sm);
+  uint32_t* tag = reinterpret_cast<uint32_t*>(sm + TT * 16);
+  __shared__ uint32_t s_anc[2], s_ok[2], s_bmin[2], s_bmax[2], s_cnt[2], s_nc, s_cnt2;
+  __shared__ unsigned long long s_base[2], s_base2;
+  __shared__ uint32_t sbits[2][TW * TBW];
+  __shared__ uint64_t cl[32];
+  __shared__ mckg_grace stg[FB_STAGE];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t lane = threadIdx.x & 31u;
+  // the window metadata of tile t into buffer q (s_ok[q] is 0 on entry)
+  auto meta = [&](uint32_t q, uint64_t t) {
+    const unsigned long long wv = win[t];
+    const uint32_t anchor = (uint32_t)wv, occ = (uint32_t)(wv >> 32);
+    if (threadIdx.x == 0) s_anc[q] = anchor;
+    if (anchor == ~0u) return;
+    if (threadIdx.x < TW && ((occ >> threadIdx.x) & 1u) && claim[anchor + threadIdx.x] == 1u)
+      atomicOr(&s_ok[q], 1u << threadIdx.x);
+    if (threadIdx.x < TW * TBW && ((occ >> (threadIdx.x / TBW)) & 1u))
+      sbits[q][threadIdx.x] = bits[(uint64_t)anchor * TBW + threadIdx.x];
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    for (int q = 0; q < 2; ++q) {
+      s_ok[q] = 0;
+      s_cnt[q] = 0;
+      s_bmin[q] = ~0u;
+      s_bmax[q] = 0;
+    }
+    s_cnt2 = 0;
+  }
+  __syncthreads();
+  if (blockIdx.x < ntiles) {
+    if (threadIdx.x == 0) tile_fetch(ev, n, blockIdx.x, sm, &bar);
+    meta(0, blockIdx.x);
+  }
+  LineCache C{0xFFFFFFFFu, ~0ull, 0u};  // warp 0's
+  uint32_t nstg = 0, flags = 0;          // warp 0's
+  uint32_t pmm = 0, pslot = 0;           // the previous tile's mixed records (deferred)
+  uint64_t pr0 = 0;
+  uint32_t it = 0;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const uint32_t cb = it & 1u;
+    const uint64_t r0 = t * TT;
+    const uint32_t m = (uint32_t)(n - r0 < TT ? n - r0 : TT);
+    mbar_wait(&bar, cb);
+    __syncthreads();  // #1: this tile's metadata; the previous tile's side base
+    if (pmm) side_write(pmm, pslot, s_base[cb ^ 1u], ev, pr0, side);
+    if (threadIdx.x == 0) {  // the next tile's counters (last read before #1)
+      s_ok[cb ^ 1u] = 0;
+      s_cnt[cb ^ 1u] = 0;
+      s_bmin[cb ^ 1u] = ~0u;
+      s_bmax[cb ^ 1u] = 0;
+      s_nc = 0;
+    }
+    const uint32_t anchor = s_anc[cb], ok = s_ok[cb];
+    uint32_t wp[TR], bp[TR];  // own: window word | write << 13, bid; else bp = ~0u
+    uint32_t bmin = ~0u, bmax = 0, mm = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < TR; ++k) {
+      const uint32_t i = k * TB + threadIdx.x;
+      bp[k] = ~0u;
+      wp[k] = 0;
+      if (i >= m || anchor == ~0u) continue;
+      const uint4 r = stage[i];
+      const unsigned long long a64 = rec_a(r);
+      const uint32_t bid = r.w & 0xFFFFFFu;
+      const uint32_t j = tile_bucket(a64, bid, base, nbk) - anchor;  // ~0u - anchor >= TW
+      if (j >= TW) continue;  // foreign: sent in pass 0
+      const uint32_t w = (uint32_t)((ga_addr(a64) - base) >> 2) & (FB_WORDS - 1u);
+      if (((ok >> j) & 1u) && !((sbits[cb][j * TBW + (w >> 5)] >> (w & 31u)) & 1u)) {
+        wp[k] = (j * FB_WORDS + (w ^ ((w >> 5) & 31u))) | (ga_write(a64) << 13);  // swizzled as in bucket_fast
+        bp[k] = bid;
+        bmin = min(bmin, bid);
+        bmax = max(bmax, bid);
+      } else {
+        mm |= 1u << k;  // mixed
+      }
+    }
+    bmin = __reduce_min_sync(0xFFFFFFFFu, bmin);
+    bmax = __reduce_max_sync(0xFFFFFFFFu, bmax);
+    if (lane == 0 && bmin != ~0u) {
+      atomicMin(&s_bmin[cb], bmin);
+      atomicMax(&s_bmax[cb], bmax);
+    }
+    const uint32_t slot = side_slot(mm, &s_cnt[cb]);
+    __syncthreads();  // #2: the stage is free; this tile's counters final
+    if (threadIdx.x == 0) {
+      if (t + gridDim.x < ntiles) tile_fetch(ev, n, t + gridDim.x, sm, &bar);
+      s_base[cb] = s_cnt[cb] ? atomicAdd(nside, (unsigned long long)s_cnt[cb]) : 0ull;
+    }
+    if (t + gridDim.x < ntiles) meta(cb ^ 1u, t + gridDim.x);
+    pmm = mm;
+    pslot = slot;
+    pr0 = r0;
+    if (s_bmin[cb] == ~0u || s_bmin[cb] == s_bmax[cb]) continue;  // no own records, or all of one block
+    // the word filter: P1 last bid per word, P2 multi-block / write flags
+    // (atomicOr: the bid bits stay readable), P3 candidates
+#pragma unroll
+    for (uint32_t k = 0; k < TR; ++k)
+      if (bp[k] != ~0u) tag[wp[k] & (TWW - 1)] = bp[k];
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < TR; ++k) {
+      if (bp[k] == ~0u) continue;
+      const uint32_t x = wp[k] & (TWW - 1);
+      const uint32_t f = ((tag[x] & (MCKG_MAX_BID - 1)) != bp[k] ? TAG_MULTI : 0u) | ((wp[k] & TWW) ? TAG_WRITE : 0u);
+      if (f) atomicOr(tag + x, f);
+    }
+    __syncthreads();
+    uint32_t cm = 0;
+#pragma unroll
+    for (uint32_t k = 0; k < TR; ++k)
+      if (bp[k] != ~0u && (tag[wp[k] & (TWW - 1)] & (TAG_MULTI | TAG_WRITE)) == (TAG_MULTI | TAG_WRITE))
+        cm |= 1u << k;
+    const uint32_t c = __popc(cm);
+    uint32_t pos = c ? atomicAdd(&s_nc, c) : 0u;
+    for (uint32_t q = cm; q; q &= q - 1u, ++pos)
+      if (pos < 32) cl[pos] = r0 + (uint64_t)((__ffs(q) - 1) * TB + threadIdx.x);
+    __syncthreads();
+    const uint32_t nc = s_nc;
+    if (nc > 32) {
+      // too many candidates for one exact batch: the tile's own records join
+      // the side list (all of them: every record on their words is here)
+      uint32_t om = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < TR; ++k) om |= (bp[k] != ~0u ? 1u : 0u) << k;
+      const uint32_t os = side_slot(om, &s_cnt2);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_base2 = atomicAdd(nside, (unsigned long long)s_cnt2);
+        s_cnt2 = 0;
+      }
+      __syncthreads();
+      if (om) side_write(om, os, s_base2, ev, r0, side);
+    } else if (nc && threadIdx.x < 32) {
+      fb_exact(O, ev, cl, nc, C, stg, nstg, flags);
+    }
+    __syncthreads();  // cl / tag / s_nc / s_base2 reused by the next tile
+  }
+  __syncthreads();
+  if (pmm) side_write(pmm, pslot, s_base[(it - 1u) & 1u], ev, pr0, side);
+  if (threadIdx.x < 32) {
+    fb_flush(O, stg, nstg, flags);
+    if (C.line != 0xFFFFFFFFu) atomicMin(O.line_first + C.line, C.ts);
+    flags = __reduce_or_sync(0xFFFFFFFFu, flags);
+    if (threadIdx.x == 0 && flags) atomicOr(O.status, flags);
+  }
 }
 
 // shared-memory layout of bucket_detect (bytes)
@@ -886,24 +1295,12 @@ extern "C" int mckg_partition_global(const mckg_gaccess* events, uint64_t n, uin
   return MCKG_OK;
 }
 
-extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64_t addr_lo, mckg_grace* races,
-                                  uint64_t capacity, unsigned long long* n_races, unsigned long long* line_first,
-                                  uint32_t* status, void* stream) {
-  if ((!events && n) || !n_races || !line_first || !status || (!races && capacity)) {
-    set_error("mckg_detect_global: null argument");
-    return MCKG_E_ARG;
-  }
-  if (n >= (1ull << 32)) {
-    set_error("mckg_detect_global: more than 2^32 records on one rank");
-    return MCKG_E_RANGE;
-  }
-  (void)addr_lo;  // buckets follow the sampled span of the records themselves
-  cudaStream_t s = (cudaStream_t)stream;
-  keep_pool_memory();
-  MCKG_CUDA_TRY(cudaMemsetAsync(n_races, 0, sizeof(unsigned long long), s));
-  if (n == 0) return MCKG_OK;
-  uint32_t launches = 0;
-  // 1. span from a strided sample -> bucket shift (~256 records per bucket)
+namespace mckg {
+namespace {
+
+// the sampled address span of n records: {min, max} over a strided sample
+int sample_span(const mckg_gaccess* events, uint64_t n, unsigned long long hm[2], cudaStream_t s,
+                uint32_t& launches) {
   unsigned long long* mm = nullptr;
   MCKG_CUDA_TRY(cudaMallocAsync(&mm, 2 * sizeof(unsigned long long), s));
   const unsigned long long init[2] = {~0ull, 0ull};
@@ -911,10 +1308,17 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
   const uint64_t stride = n > (1u << 16) ? n >> 16 : 1;
   span_sample_kernel<<<grid_for(n / stride), 256, 0, s>>>(events, n, stride, mm);
   ++launches;
-  unsigned long long hm[2];
-  MCKG_CUDA_TRY(cudaMemcpyAsync(hm, mm, sizeof hm, cudaMemcpyDeviceToHost, s));
+  MCKG_CUDA_TRY(cudaMemcpyAsync(hm, mm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   MCKG_CUDA_TRY(cudaStreamSynchronize(s));
   cudaFreeAsync(mm, s);
+  return MCKG_OK;
+}
+
+// The bucket pipeline on n >= 1 records: span, count, scan, scatter, detect.
+int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStream_t s, uint32_t& launches) {
+  unsigned long long hm[2];
+  if (int rc = sample_span(events, n, hm, s, launches)) return rc;
+  uint32_t* status = O.status;
   // the sample can miss the extremes: the edge buckets are open, and a
   // margin keeps the top records out of one crowded last bucket
   const uint64_t base = hm[0] & ~0xFFFull;
@@ -950,7 +1354,6 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
   bucket_scatter_kernel<<<g, 256, 0, s>>>(events, n, nb, shift, base, off, cur, recs);
   launches += 2;
   // 5. detection
-  BOut O{races, capacity, n_races, line_first, status};
   MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BD_SMEM));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_detect_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per = 0;
@@ -1026,6 +1429,89 @@ extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64
   cudaFreeAsync(cur, s);
   cudaFreeAsync(off, s);
   cudaFreeAsync(big, s);
-  add_launches(launches);
   return MCKG_OK;
+}
+
+// The tile path (see tile_claim_kernel): returns false (nothing launched
+// that reports) when the span is too wide for its bitmap.
+int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStream_t s, uint32_t& launches,
+                 bool& used) {
+  used = false;
+  unsigned long long hm[2];
+  if (int rc = sample_span(events, n, hm, s, launches)) return rc;
+  // window buckets live in the sampled span (records outside it are foreign)
+  const uint64_t base = hm[0] & ~(uint64_t)((1u << FB_SHIFT) - 1);
+  const uint64_t nbk64 = ((hm[1] - base) >> FB_SHIFT) + 1;
+  if (nbk64 > (1ull << 22)) return MCKG_OK;  // > 8 GiB: the bitmap would not pay (anchors keep 23 bits)
+  if (reinterpret_cast<uintptr_t>(events) & 15u) return MCKG_OK;  // the bulk copies need 16-byte alignment
+  used = true;
+  const uint32_t nbk = (uint32_t)nbk64;
+  const uint64_t ntiles = (n + TT - 1) / TT;
+  uint32_t *claim = nullptr, *bits = nullptr;
+  unsigned long long* win = nullptr;
+  mckg_gaccess* side = nullptr;
+  unsigned long long* nside = nullptr;
+  MCKG_CUDA_TRY(cudaMallocAsync(&claim, (size_t)nbk * 4, s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&bits, (size_t)nbk * (FB_WORDS / 8), s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&win, (size_t)ntiles * 8, s));
+  MCKG_CUDA_TRY(cudaMallocAsync(&side, (size_t)n * sizeof(mckg_gaccess), s));  // each record joins at most once
+  MCKG_CUDA_TRY(cudaMallocAsync(&nside, 8, s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(claim, 0, (size_t)nbk * 4, s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(bits, 0, (size_t)nbk * (FB_WORDS / 8), s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(nside, 0, 8, s));
+  MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+  MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TD_SMEM));
+  MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_detect_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int pc = 0, pd = 0;
+  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pc, tile_claim_kernel, TB, TC_SMEM));
+  MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pd, tile_detect_kernel, TB, TD_SMEM));
+  const uint64_t gc = std::min<uint64_t>(ntiles, (uint64_t)sm_count() * (uint64_t)(pc > 0 ? pc : 1));
+  const uint64_t gdt = std::min<uint64_t>(ntiles, (uint64_t)sm_count() * (uint64_t)(pd > 0 ? pd : 1));
+  tile_claim_kernel<<<(unsigned)gc, TB, TC_SMEM, s>>>(events, n, ntiles, base, nbk, claim, bits, win, side, nside);
+  tile_detect_kernel<<<(unsigned)gdt, TB, TD_SMEM, s>>>(events, n, ntiles, base, nbk, claim, bits, win, side, nside,
+                                                        O);
+  MCKG_CUDA_TRY(cudaGetLastError());
+  launches += 2;
+  unsigned long long ns = 0;
+  MCKG_CUDA_TRY(cudaMemcpyAsync(&ns, nside, 8, cudaMemcpyDeviceToHost, s));
+  MCKG_CUDA_TRY(cudaStreamSynchronize(s));
+  int rc = ns ? detect_buckets(side, ns, O, s, launches) : MCKG_OK;
+  cudaFreeAsync(claim, s);
+  cudaFreeAsync(bits, s);
+  cudaFreeAsync(win, s);
+  cudaFreeAsync(side, s);
+  cudaFreeAsync(nside, s);
+  return rc;
+}
+
+}  // namespace
+}  // namespace mckg
+
+extern "C" int mckg_detect_global(const mckg_gaccess* events, uint64_t n, uint64_t addr_lo, mckg_grace* races,
+                                  uint64_t capacity, unsigned long long* n_races, unsigned long long* line_first,
+                                  uint32_t* status, void* stream) {
+  if ((!events && n) || !n_races || !line_first || !status || (!races && capacity)) {
+    set_error("mckg_detect_global: null argument");
+    return MCKG_E_ARG;
+  }
+  if (n >= (1ull << 32)) {
+    set_error("mckg_detect_global: more than 2^32 records on one rank");
+    return MCKG_E_RANGE;
+  }
+  (void)addr_lo;  // buckets follow the sampled span of the records themselves
+  cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_memory();
+  MCKG_CUDA_TRY(cudaMemsetAsync(n_races, 0, sizeof(unsigned long long), s));
+  if (n == 0) return MCKG_OK;
+  uint32_t launches = 0;
+  const BOut O{races, capacity, n_races, line_first, status};
+  // the tile path for large inputs (debug 512: always, 256: never)
+  const uint32_t dbg = debug_flags();
+  bool used = false;
+  int rc = MCKG_OK;
+  if (!(dbg & 256u) && (n >= (1ull << 20) || (dbg & 512u))) rc = detect_tiles(events, n, O, s, launches, used);
+  if (rc == MCKG_OK && !used) rc = detect_buckets(events, n, O, s, launches);
+  add_launches(launches);
+  return rc;
 }

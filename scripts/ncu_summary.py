@@ -5,7 +5,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+flt = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []  # one kernel of a multi-kernel report
+raw = subprocess.run(["ncu", "-i", rep, *flt, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
 h, v = r[0], r[2] if len(r) > 2 else r[1]
 want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
@@ -18,7 +19,7 @@ for k, x in zip(h, v):
     if k in want or (k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("per_issue_active.ratio")
                      and float(x or 0) > 0.2):
         print(f"{k:80s} {x}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+src = subprocess.run(["ncu", "-i", rep, *flt, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 fname, out = None, []
 for row in csv.reader(src.splitlines()):

@@ -10,14 +10,20 @@ import oracle_bind as ob
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["dense", "sparse"])
+MODES = {"dense": 256, "sparse": 128 | 256, "tile": 512}
+
+
+@pytest.fixture(autouse=True, params=list(MODES))
 def k6_mode(request):
-    """Both K6 bucket modes: dense spans (warp per 4 KiB bucket, direct
-    tables, the general kernel for what it hands back) and the sparse mode
-    (hashed tables only), forced by mckg_set_debug(128)."""
+    """Every K6 route: the bucket pipeline in dense spans (warp per 2 KiB
+    bucket, direct tables, the general kernel for what it hands back) and in
+    sparse mode (hashed tables only, mckg_set_debug(128)), and the in-place
+    tile path (pass 0 claim / foreign, pass 1 own words, the side list through
+    the bucket pipeline), forced at any size by mckg_set_debug(512) and taken
+    by default from 2^20 records."""
     from paper_1211_6193_b200 import _abi
     lib = _abi.load()
-    lib.mckg_set_debug(128 if request.param == "sparse" else 0)
+    lib.mckg_set_debug(MODES[request.param])
     yield request.param
     lib.mckg_set_debug(0)
 
@@ -125,3 +131,54 @@ def test_two_owner_emulation_on_one_gpu():
     rc, want, wn, wlf = ob.port_detect_global(ev)
     assert sorted(allr) == sorted(zip(want["addr"].tolist(), want["line"].tolist()))
     assert np.array_equal(np.minimum(lfs[0], lfs[1]), wlf)
+
+
+def _tiled(nt, seed, shared_words, bids_per_tile=2, foreign=0.01, unaligned=0.0, overlap=False):
+    """Block-clustered records, one TT-record tile per 32 KiB range: tile t
+    writes/reads its range from `bids_per_tile` blocks; `shared_words` words
+    per tile are touched by two of them (candidates inside a tile), a
+    `foreign` fraction lands in the next range, `unaligned` cross words, and
+    with `overlap` neighbouring tiles share half their range (contested
+    buckets)."""
+    rng = np.random.default_rng(seed)
+    n = nt * 4096
+    t = np.repeat(np.arange(nt, dtype=np.uint64), 4096)
+    j = np.tile(np.arange(4096, dtype=np.uint64), nt)
+    stride = 16384 if overlap else 32768
+    addr = t * stride + (j * 8) % 32768
+    bid = (t * bids_per_tile + (j % bids_per_tile)).astype(np.uint64)
+    if shared_words:  # record k takes the word of record k ^ 1 (another block)
+        k = rng.integers(0, 4096, size=(nt, shared_words)).astype(np.uint64)
+        rows = (np.arange(nt, dtype=np.uint64)[:, None] * 4096 + k).reshape(-1)
+        addr[rows] = addr[rows ^ np.uint64(1)]
+    f = rng.random(n) < foreign
+    addr[f] = ((t[f] + 1) % nt) * stride + (j[f] * 8) % 32768
+    u = rng.random(n) < unaligned
+    addr[u] += 2
+    write = rng.random(n) < 0.5
+    ln = np.full(n, 4, dtype=np.uint64)
+    line = (100 + (j % 7)).astype(np.uint64)
+    tid = j % 256
+    a = (addr & 0xFFFFFFFFFF) | (ln << 40) | (write.astype(np.uint64) << 44) | (tid << 45) | ((line & 0xFF) << 56)
+    ev = np.zeros(n, dtype=ob.GACCESS_DTYPE)
+    ev["a"] = a
+    ev["sweep"] = (j // 256).astype(np.uint32)
+    ev["b"] = (bid & 0xFFFFFF).astype(np.uint32) | ((line >> 8).astype(np.uint32) << 24)
+    return ev
+
+
+@pytest.mark.parametrize("case", [
+    dict(shared_words=0, bids_per_tile=1),                       # C5-like: own words race-free
+    dict(shared_words=4, bids_per_tile=2, foreign=0.0),          # <= 32 candidates per tile
+    dict(shared_words=200, bids_per_tile=2, foreign=0.0),        # > 32: the tile joins the side list
+    dict(shared_words=8, bids_per_tile=3, foreign=0.02, unaligned=0.01),
+    dict(shared_words=4, bids_per_tile=2, overlap=True),         # contested buckets
+])
+def test_block_clustered_traces(case):
+    n = _check(_tiled(24, 7, **case))
+    assert n >= 0
+
+
+def test_c5_two_million_records():
+    """2^21 C5 records: the size at which the tile path is the default."""
+    assert _check(ob.gen_c5(0, 512, 512)) > 0
