@@ -403,7 +403,7 @@ def run_c5(args, blocks, dev, ws, rank, comm=None):
             out.line_first.bitwise_xor_(-(1 << 63))
         return out, mine.shape[0]
 
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(3, args.warmup)):  # the first calls size the stream-ordered pool
         step()
     torch.cuda.synchronize()
     if ws > 1:
@@ -441,8 +441,9 @@ def run_c5(args, blocks, dev, ws, rank, comm=None):
                         f"address-range all-to-all over {ws} GPU(s)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic("c5_call") if ws == 1 else None,
-                         "kernel": "mckg_detect_global (sample, bucket count, scan, "
-                         "bucket scatter, bucket_detect)" + (" + K3 partition + NCCL all-to-all" if ws > 1 else ""),
+                         "kernel": "mckg_detect_global: tile path (span sample, tile_claim, tile_detect, "
+                         "tile_multi; side list through the bucket pipeline)"
+                         + (" + K3 partition + NCCL all-to-all" if ws > 1 else ""),
                          "algorithmic_bytes": "16 B/event read (+ (P-1)/P x 16 B/event over NVLink at P ranks)"},
             "events_per_s": events / (ms / 1e3), "ms_per_step": ms, "races_reported": int(tot[1]),
             "status": status, "nvlink_bytes_per_rank": sent,

@@ -845,9 +845,10 @@ constexpr uint32_t TBW = FB_WORDS / 32;      // bitmap words per bucket
 // pass-1 word table: bid (21 bits) | MULTI | WRITE (flags set by atomicOr)
 constexpr uint32_t TAG_MULTI = 1u << 30, TAG_WRITE = 1u << 31;
 // dynamic shared memory: the tile stage (TT records, filled by the bulk-copy
-// engine one tile ahead) + pass 1's word table
+// engine one tile ahead); tile_multi's word table
 constexpr uint32_t TC_SMEM = TT * 16;
-constexpr uint32_t TD_SMEM = TT * 16 + TWW * 4;
+constexpr uint32_t TD_SMEM = TT * 16;
+constexpr uint32_t TM_SMEM = TWW * 4;
 
 // the bucket of an in-span, word-contained record, else ~0u
 __device__ __forceinline__ uint32_t tile_bucket(uint64_t a64, uint32_t bid, uint64_t base, uint32_t nbk) {
@@ -870,6 +871,21 @@ __device__ __forceinline__ void tile_fetch(const mckg_gaccess* ev, uint64_t n, u
 
 __device__ __forceinline__ unsigned long long rec_a(const uint4& r) {
   return ((unsigned long long)r.y << 32) | r.x;
+}
+
+// The window slot of record r for a tile whose window starts at byte wbase
+// and has jmax = min(TW, nbk - anchor) buckets, else ~0u -- exactly
+// tile_bucket(r) - anchor < TW, in fewer instructions (the hot test of both
+// passes).  *rel: the byte offset in the window.
+__device__ __forceinline__ uint32_t win_slot(const uint4& r, uint64_t wbase, uint32_t jmax, uint32_t* rel) {
+  const unsigned long long a = ((unsigned long long)(r.y & 0xFFu) << 32) | r.x;
+  const uint32_t len = (r.y >> 8) & 0xFu;
+  const uint64_t d = a - wbase;  // wraps high below the window
+  const uint32_t dl = (uint32_t)d, j = dl >> FB_SHIFT;
+  *rel = dl;
+  const bool in = d < ((uint64_t)TW << FB_SHIFT) && j < jmax && len != 0u && (dl & 3u) + len <= 4u &&
+                  (r.w & 0xFFFFFFu) < MCKG_MAX_BID;
+  return in ? j : ~0u;
 }
 
 // This thread's slot among a tile's flagged records (bits of `fm`): a warp
@@ -951,19 +967,21 @@ __global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* e
     __syncthreads();  // #1: s_anchor; the previous tile's side base
     if (pfm) side_write(pfm, pslot, s_base[cb ^ 1u], ev, pr0, side);
     const uint32_t anchor = s_anchor;
+    const uint64_t wbase = base + ((uint64_t)anchor << FB_SHIFT);
+    const uint32_t jmax = anchor == ~0u ? 0u : min(TW, nbk - anchor);
     uint32_t fm = 0, occ = 0;
 #pragma unroll
     for (uint32_t k = 0; k < TR; ++k) {
       const uint32_t i = k * TB + threadIdx.x;
       if (i >= m) continue;
       const uint4 r = stage[i];
-      const unsigned long long a64 = rec_a(r);
-      const uint32_t b = tile_bucket(a64, r.w & 0xFFFFFFu, base, nbk);
-      const uint32_t j = b - anchor;
-      if (b != ~0u && anchor != ~0u && j < TW) {
+      uint32_t rel;
+      const uint32_t j = win_slot(r, wbase, jmax, &rel);
+      if (j != ~0u) {
         occ |= 1u << j;
         continue;
       }
+      const unsigned long long a64 = rec_a(r);
       fm |= 1u << k;
       // foreign: mark the words it touches (clipped to the span)
       const uint64_t a = ga_addr(a64);
@@ -997,19 +1015,20 @@ __global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* e
 }
 
 // Pass 1, persistent like pass 0; the window metadata of a CTA's next tile
-// (claims, word marks) is fetched while this one is checked.
-__global__ void __launch_bounds__(TB, 2) tile_detect_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t ntiles,
+// (claims, word marks) is fetched while this one is checked.  A tile whose
+// own records come from two or more blocks is listed for tile_multi_kernel
+// (the word filter needs a 32 KiB table that would cost this kernel a CTA
+// per SM).
+__global__ void __launch_bounds__(TB, 3) tile_detect_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t ntiles,
                                                             uint64_t base, uint32_t nbk, const uint32_t* claim,
                                                             const uint32_t* bits, const unsigned long long* win,
-                                                            mckg_gaccess* side, unsigned long long* nside, BOut O) {
+                                                            mckg_gaccess* side, unsigned long long* nside,
+                                                            uint32_t* multi, uint32_t* nmulti) {
   extern __shared__ __align__(16) uint8_t sm[];
   const uint4* stage = reinterpret_cast<const uint4*>(sm);
-  uint32_t* tag = reinterpret_cast<uint32_t*>(sm + TT * 16);
-  __shared__ uint32_t s_anc[2], s_ok[2], s_bmin[2], s_bmax[2], s_cnt[2], s_nc, s_cnt2;
-  __shared__ unsigned long long s_base[2], s_base2;
+  __shared__ uint32_t s_anc[2], s_ok[2], s_bmin[2], s_bmax[2], s_cnt[2];
+  __shared__ unsigned long long s_base[2];
   __shared__ uint32_t sbits[2][TW * TBW];
-  __shared__ uint64_t cl[32];
-  __shared__ mckg_grace stg[FB_STAGE];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t lane = threadIdx.x & 31u;
   // the window metadata of tile t into buffer q (s_ok[q] is 0 on entry)
@@ -1032,15 +1051,12 @@ __global__ void __launch_bounds__(TB, 2) tile_detect_kernel(const mckg_gaccess* 
       s_bmin[q] = ~0u;
       s_bmax[q] = 0;
     }
-    s_cnt2 = 0;
   }
   __syncthreads();
   if (blockIdx.x < ntiles) {
     if (threadIdx.x == 0) tile_fetch(ev, n, blockIdx.x, sm, &bar);
     meta(0, blockIdx.x);
   }
-  LineCache C{0xFFFFFFFFu, ~0ull, 0u};  // warp 0's
-  uint32_t nstg = 0, flags = 0;          // warp 0's
   uint32_t pmm = 0, pslot = 0;           // the previous tile's mixed records (deferred)
   uint64_t pr0 = 0;
   uint32_t it = 0;
@@ -1056,26 +1072,22 @@ __global__ void __launch_bounds__(TB, 2) tile_detect_kernel(const mckg_gaccess* 
       s_cnt[cb ^ 1u] = 0;
       s_bmin[cb ^ 1u] = ~0u;
       s_bmax[cb ^ 1u] = 0;
-      s_nc = 0;
     }
     const uint32_t anchor = s_anc[cb], ok = s_ok[cb];
-    uint32_t wp[TR], bp[TR];  // own: window word | write << 13, bid; else bp = ~0u
+    const uint64_t wbase = base + ((uint64_t)anchor << FB_SHIFT);
+    const uint32_t jmax = anchor == ~0u ? 0u : min(TW, nbk - anchor);
     uint32_t bmin = ~0u, bmax = 0, mm = 0;
 #pragma unroll
     for (uint32_t k = 0; k < TR; ++k) {
       const uint32_t i = k * TB + threadIdx.x;
-      bp[k] = ~0u;
-      wp[k] = 0;
-      if (i >= m || anchor == ~0u) continue;
+      if (i >= m) continue;
       const uint4 r = stage[i];
-      const unsigned long long a64 = rec_a(r);
+      uint32_t rel;
+      const uint32_t j = win_slot(r, wbase, jmax, &rel);
+      if (j == ~0u) continue;  // foreign: sent in pass 0
+      const uint32_t w = (rel >> 2) & (FB_WORDS - 1u);
       const uint32_t bid = r.w & 0xFFFFFFu;
-      const uint32_t j = tile_bucket(a64, bid, base, nbk) - anchor;  // ~0u - anchor >= TW
-      if (j >= TW) continue;  // foreign: sent in pass 0
-      const uint32_t w = (uint32_t)((ga_addr(a64) - base) >> 2) & (FB_WORDS - 1u);
       if (((ok >> j) & 1u) && !((sbits[cb][j * TBW + (w >> 5)] >> (w & 31u)) & 1u)) {
-        wp[k] = (j * FB_WORDS + (w ^ ((w >> 5) & 31u))) | (ga_write(a64) << 13);  // swizzled as in bucket_fast
-        bp[k] = bid;
         bmin = min(bmin, bid);
         bmax = max(bmax, bid);
       } else {
@@ -1098,9 +1110,69 @@ __global__ void __launch_bounds__(TB, 2) tile_detect_kernel(const mckg_gaccess* 
     pmm = mm;
     pslot = slot;
     pr0 = r0;
-    if (s_bmin[cb] == ~0u || s_bmin[cb] == s_bmax[cb]) continue;  // no own records, or all of one block
-    // the word filter: P1 last bid per word, P2 multi-block / write flags
-    // (atomicOr: the bid bits stay readable), P3 candidates
+    if (threadIdx.x == 0 && s_bmin[cb] != ~0u && s_bmin[cb] != s_bmax[cb]) multi[atomicAdd(nmulti, 1u)] = (uint32_t)t;
+  }
+  __syncthreads();
+  if (pmm) side_write(pmm, pslot, s_base[(it - 1u) & 1u], ev, pr0, side);
+}
+
+// The listed tiles of pass 1 (own records from two or more blocks): the own
+// records again (same classification), then the word filter of bucket_fast
+// over the window -- P1 last bid per word, P2 multi-block / write flags
+// (atomicOr keeps the bid bits readable), P3 candidates -- and the exact pass
+// (<= 32 candidates) or, past that, the tile's own records to the side list.
+__global__ void __launch_bounds__(TB) tile_multi_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t base,
+                                                        uint32_t nbk, const uint32_t* claim, const uint32_t* bits,
+                                                        const unsigned long long* win, const uint32_t* multi,
+                                                        const uint32_t* nmulti, mckg_gaccess* side,
+                                                        unsigned long long* nside, BOut O) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint32_t* tag = reinterpret_cast<uint32_t*>(sm);
+  __shared__ uint32_t s_ok, s_nc, s_cnt;
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t sbits[TW * TBW];
+  __shared__ uint64_t cl[32];
+  __shared__ mckg_grace stg[FB_STAGE];
+  LineCache C{0xFFFFFFFFu, ~0ull, 0u};  // warp 0's
+  uint32_t nstg = 0, flags = 0;          // warp 0's
+  const uint32_t nl = *nmulti;
+  for (uint32_t li = blockIdx.x; li < nl; li += gridDim.x) {
+    const uint64_t t = multi[li];
+    const uint64_t r0 = t * TT;
+    const uint32_t m = (uint32_t)(n - r0 < TT ? n - r0 : TT);
+    const unsigned long long wv = win[t];
+    const uint32_t anchor = (uint32_t)wv, occ = (uint32_t)(wv >> 32);
+    if (threadIdx.x == 0) {
+      s_ok = 0;
+      s_nc = 0;
+      s_cnt = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x < TW && ((occ >> threadIdx.x) & 1u) && claim[anchor + threadIdx.x] == 1u)
+      atomicOr(&s_ok, 1u << threadIdx.x);
+    if (threadIdx.x < TW * TBW && ((occ >> (threadIdx.x / TBW)) & 1u))
+      sbits[threadIdx.x] = bits[(uint64_t)anchor * TBW + threadIdx.x];
+    __syncthreads();
+    const uint32_t ok = s_ok;
+    const uint64_t wbase = base + ((uint64_t)anchor << FB_SHIFT);
+    const uint32_t jmax = min(TW, nbk - anchor);
+    uint32_t wp[TR], bp[TR];  // own: window word | write << 13, bid; else bp = ~0u
+#pragma unroll
+    for (uint32_t k = 0; k < TR; ++k) {
+      const uint32_t i = k * TB + threadIdx.x;
+      bp[k] = ~0u;
+      wp[k] = 0;
+      if (i >= m) continue;
+      const uint4 r = reinterpret_cast<const uint4*>(ev + r0)[i];
+      uint32_t rel;
+      const uint32_t j = win_slot(r, wbase, jmax, &rel);
+      if (j == ~0u) continue;
+      const uint32_t w = (rel >> 2) & (FB_WORDS - 1u);
+      if (((ok >> j) & 1u) && !((sbits[j * TBW + (w >> 5)] >> (w & 31u)) & 1u)) {
+        wp[k] = (j * FB_WORDS + (w ^ ((w >> 5) & 31u))) | (((r.y >> 12) & 1u) << 13);
+        bp[k] = r.w & 0xFFFFFFu;
+      }
+    }
 #pragma unroll
     for (uint32_t k = 0; k < TR; ++k)
       if (bp[k] != ~0u) tag[wp[k] & (TWW - 1)] = bp[k];
@@ -1130,21 +1202,16 @@ __global__ void __launch_bounds__(TB, 2) tile_detect_kernel(const mckg_gaccess* 
       uint32_t om = 0;
 #pragma unroll
       for (uint32_t k = 0; k < TR; ++k) om |= (bp[k] != ~0u ? 1u : 0u) << k;
-      const uint32_t os = side_slot(om, &s_cnt2);
+      const uint32_t os = side_slot(om, &s_cnt);
       __syncthreads();
-      if (threadIdx.x == 0) {
-        s_base2 = atomicAdd(nside, (unsigned long long)s_cnt2);
-        s_cnt2 = 0;
-      }
+      if (threadIdx.x == 0) s_base = atomicAdd(nside, (unsigned long long)s_cnt);
       __syncthreads();
-      if (om) side_write(om, os, s_base2, ev, r0, side);
+      if (om) side_write(om, os, s_base, ev, r0, side);
     } else if (nc && threadIdx.x < 32) {
       fb_exact(O, ev, cl, nc, C, stg, nstg, flags);
     }
-    __syncthreads();  // cl / tag / s_nc / s_base2 reused by the next tile
+    __syncthreads();  // tables reused by the next tile
   }
-  __syncthreads();
-  if (pmm) side_write(pmm, pslot, s_base[(it - 1u) & 1u], ev, pr0, side);
   if (threadIdx.x < 32) {
     fb_flush(O, stg, nstg, flags);
     if (C.line != 0xFFFFFFFFu) atomicMin(O.line_first + C.line, C.ts);
@@ -1315,9 +1382,15 @@ int sample_span(const mckg_gaccess* events, uint64_t n, unsigned long long hm[2]
 }
 
 // The bucket pipeline on n >= 1 records: span, count, scan, scatter, detect.
-int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStream_t s, uint32_t& launches) {
+int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStream_t s, uint32_t& launches,
+                   const unsigned long long* span_in = nullptr) {
   unsigned long long hm[2];
-  if (int rc = sample_span(events, n, hm, s, launches)) return rc;
+  if (span_in) {  // a span known to the caller (buckets are open at both ends)
+    hm[0] = span_in[0];
+    hm[1] = span_in[1];
+  } else if (int rc = sample_span(events, n, hm, s, launches)) {
+    return rc;
+  }
   uint32_t* status = O.status;
   // the sample can miss the extremes: the edge buckets are open, and a
   // margin keeps the top records out of one crowded last bucket
@@ -1459,6 +1532,9 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   MCKG_CUDA_TRY(cudaMemsetAsync(claim, 0, (size_t)nbk * 4, s));
   MCKG_CUDA_TRY(cudaMemsetAsync(bits, 0, (size_t)nbk * (FB_WORDS / 8), s));
   MCKG_CUDA_TRY(cudaMemsetAsync(nside, 0, 8, s));
+  uint32_t* multi = nullptr;  // [ntiles] tiles for tile_multi, then their count
+  MCKG_CUDA_TRY(cudaMallocAsync(&multi, ((size_t)ntiles + 1) * 4, s));
+  MCKG_CUDA_TRY(cudaMemsetAsync(multi + ntiles, 0, 4, s));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TD_SMEM));
@@ -1470,18 +1546,22 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   const uint64_t gdt = std::min<uint64_t>(ntiles, (uint64_t)sm_count() * (uint64_t)(pd > 0 ? pd : 1));
   tile_claim_kernel<<<(unsigned)gc, TB, TC_SMEM, s>>>(events, n, ntiles, base, nbk, claim, bits, win, side, nside);
   tile_detect_kernel<<<(unsigned)gdt, TB, TD_SMEM, s>>>(events, n, ntiles, base, nbk, claim, bits, win, side, nside,
-                                                        O);
+                                                        multi, multi + ntiles);
+  MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM));
+  tile_multi_kernel<<<(unsigned)gdt, TB, TM_SMEM, s>>>(events, n, base, nbk, claim, bits, win, multi, multi + ntiles,
+                                                       side, nside, O);
   MCKG_CUDA_TRY(cudaGetLastError());
-  launches += 2;
+  launches += 3;
   unsigned long long ns = 0;
   MCKG_CUDA_TRY(cudaMemcpyAsync(&ns, nside, 8, cudaMemcpyDeviceToHost, s));
   MCKG_CUDA_TRY(cudaStreamSynchronize(s));
-  int rc = ns ? detect_buckets(side, ns, O, s, launches) : MCKG_OK;
+  int rc = ns ? detect_buckets(side, ns, O, s, launches, hm) : MCKG_OK;
   cudaFreeAsync(claim, s);
   cudaFreeAsync(bits, s);
   cudaFreeAsync(win, s);
   cudaFreeAsync(side, s);
   cudaFreeAsync(nside, s);
+  cudaFreeAsync(multi, s);
   return rc;
 }
 
