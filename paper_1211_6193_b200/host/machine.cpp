@@ -303,6 +303,20 @@ class HostMachine {
 
   std::optional<Val> readMem(uint32_t obj, int64_t off, uint8_t t, int line) {
     HObj* o = find(obj);
+    if (__builtin_expect(o && !hooks_.mem && o->space == SP_HOST && o->live && MCK_T_PTR(t) == 0, 1)) {
+      // the common case: a defined scalar inside a live host object
+      const int64_t len = t_scalar(t);
+      if (off >= 0 && off + len <= o->size) {
+        const uint8_t* m = o->meta.data() + off;
+        bool def = true;
+        uint64_t raw = 0;
+        for (int64_t i = 0; i < len; ++i) {
+          def &= (m[i] & META_DEF) != 0;
+          raw |= static_cast<uint64_t>(o->bytes[static_cast<size_t>(off + i)]) << (8 * i);
+        }
+        if (def) return decode_scalar(raw, t);
+      }
+    }
     if (!o) {
       ub("read through a null or invalid pointer", line);
       memHook(mck::AccessKind::Read, obj, nullptr, off, t_scalar(t), line);
@@ -377,6 +391,9 @@ class HostMachine {
   }
 
   void reportDiags(const Diags& d, int line) {
+    if (__builtin_expect(d.n != 0, 0)) reportDiagsSlow(d, line);
+  }
+  __attribute__((noinline)) void reportDiagsSlow(const Diags& d, int line) {
     for (int i = 0; i < d.n; ++i) ub(ubText(d.code[i]), line);
   }
 
@@ -1661,15 +1678,21 @@ mck::RunResult HostMachine::run() {
       for (const auto& g : grids_)
         if (!g.second.completed && g.second.endSweep != NEVER) nextEnd = std::min(nextEnd, g.second.endSweep);
     if (hostRun && !anyDispatch && nextEnd == NEVER && !awaiting_) {
-      // fast path: only the host thread can move (one step per sweep)
-      if (steps_ >= o_.stepLimit) {
-        hitLimit = true;
-        break;
-      }
-      hostStep();
-      ++steps_;
-      ++stats_.hostSteps;
-      ++sweep_;
+      // fast path: only the host thread can move (one step per sweep); it
+      // keeps stepping until a step changes what can move (a stream item,
+      // an await, a halt) or the limit is reached
+      const uint64_t lim = o_.stepLimit;
+      do {
+        if (steps_ >= lim) {
+          hitLimit = true;
+          break;
+        }
+        hostStep();
+        ++steps_;
+        ++stats_.hostSteps;
+        ++sweep_;
+      } while (!queued_ && !awaiting_ && !hostDone_ && !hostHalted_ && !runningGrids_ && engineError_.empty());
+      if (hitLimit) break;
       continue;
     }
     if (!hostRun && !anyDispatch) {
