@@ -18,7 +18,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fas
   -o gpurun_out/prof_detect python bench.py --steps 3 --warmup 3 --no-cpu --no-k1 --no-c5 --e2e-blocks 0 \
   > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 python scripts/ncu_summary.py gpurun_out/prof_detect.ncu-rep 25 > gpurun_out/k2_ncu_summary.txt 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"bucket|span|scan" --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"bucket|span|scan|tile" --csv \
   --log-file gpurun_out/c5_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-k1 --e2e-blocks 0 --blocks 1024 \
   > gpurun_out/ncu_c5.log 2>&1; echo "ncu c5 rc=$?"
 fi
