@@ -879,8 +879,10 @@ __device__ __forceinline__ mck_ins ldg_ins(const mck_ins* p) {
   return in;
 }
 
+// (barrier.sync, not bar.sync: the parked warps and the solo warp meet at
+// different instructions, and a warp need not be converged at its own)
 __device__ __forceinline__ void bar_named(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // One small step of thread `t`.  Returns 1 when a shared/global request is
@@ -1541,6 +1543,8 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       }
     }
     bool conflict = false;
+    uint32_t ins[3 * K];  // hash slots this thread inserted this sweep (it alone clears them)
+    uint32_t nins = 0;
     if (solo) {
       // warp-local memory phase: the other warps are parked
       uint32_t nreq = 0;
@@ -1566,6 +1570,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
             const unsigned long long old = atomicCAS(hk + h, 0ull, key);
             if (old == 0ull || old == key) {
               slot = (int)h;
+              if (old == 0ull) ins[nins++] = h;
               break;
             }
             h = (h + 1) & hmask;
@@ -1621,6 +1626,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       }
     }
     if (solo) {
+      __syncwarp();  // this sweep's shared writes before the next sweep's reads (lanes are not lockstep)
       bool arrivedNow = false;
 #pragma unroll 1
       for (int k = 0; k < K; ++k) arrivedNow |= ((runMask >> k) & 1u) && th[k].state == S_WAIT;
@@ -1635,28 +1641,12 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       }
       continue;
     }
-    // clear the hash slots of this sweep (every inserter clears its keys)
+    // clear the hash slots of this sweep: each by the thread that inserted
+    // its key (no probing, so no thread reads a slot another one clears)
 #pragma unroll 1
-    for (int k = 0; k < K; ++k) {
-      if (!((pendMask >> k) & 1u)) continue;
-      const Req& r = rq[k];
-      const int len = (int)t_scalar(r.ty);
-      const unsigned long long addr =
-          r.space == R_OK_SHARED ? (unsigned long long)r.off : (1ull << 40) | (r.base + (unsigned long long)r.off);
-      for (unsigned long long w = addr >> 2; w <= (addr + len - 1) >> 2; ++w) {
-        const unsigned long long key = w + 1;
-        uint32_t h = (uint32_t)mix64(key) & hmask;
-        for (uint32_t probe = 0; probe <= hmask; ++probe) {
-          const unsigned long long cur = hk[h];
-          if (cur == key) {
-            hk[h] = 0ull;
-            hv[h] = 0u;
-            break;
-          }
-          if (cur == 0ull) break;
-          h = (h + 1) & hmask;
-        }
-      }
+    for (uint32_t i = 0; i < nins; ++i) {
+      hk[ins[i]] = 0ull;
+      hv[ins[i]] = 0u;
     }
     __syncthreads();
   }
@@ -1934,12 +1924,10 @@ __global__ void __launch_bounds__(64, 1) oracle_kernel(KP P0, OQ Q) {
     // ---- replay from the spawn state, following choice[0 .. ) ----
     for (uint64_t i = 0; i < 2 * Q.arenaSize; ++i) arena[i] = Q.arenaInit[i];
     for (uint32_t i = 0; i < nb * 6 * Q.S; ++i) mysm[i] = 0;
-    uint32_t* shb = reinterpret_cast<uint32_t*>(mysm);  // shadow of block b at + (6b + 2) S
     for (uint32_t b = 0; b < nb; ++b) {
       uint32_t* sh = reinterpret_cast<uint32_t*>(mysm + (size_t)(6 * b + 2) * Q.S);
       for (uint32_t i = 0; i < Q.S; ++i) sh[i] = shadow_empty(0);
     }
-    (void)shb;
     uint32_t epoch[OMAX];
     uint32_t acc[OMAX];
     for (uint32_t i = 0; i < nt; ++i) {
