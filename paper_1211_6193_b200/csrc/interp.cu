@@ -142,7 +142,7 @@ struct KP {
   uint32_t* tarr;             // trace mode: [block][episode < TEP][tid] arrival sweep + 1
   int markDirty;              // record global writes in META_DIRTY (replicated memory)
   uint32_t maxSweeps;         // < 2^26; each sweep takes >= 1 step (step limit)
-  // serial tails (K = 1): a block whose last unfinished thread runs alone is
+  // serial tails: a block whose last unfinished thread runs alone is
   // suspended into a slot and finished by tail_kernel, 32 tails per warp
   struct TailState* tails;    // [tailCap]
   uint8_t* tailSmem;          // [tailCap][tailStride]: bytes, meta, shadow, race set
@@ -1194,9 +1194,25 @@ __device__ __forceinline__ int ht_insert(unsigned long long* keys, uint32_t* val
 
 // Copies a block's shared state into its tail slot (threads g < nthr of the
 // calling group take part) and the block's last READY thread's state.
+// the sub-thread of GPU thread g that is READY (0 when none: suspend_block
+// then stores nothing for it)
+// A lone thread is suspended once it has run TAIL_MIN sweeps alone: short
+// tails (C4's last arrivals) are cheaper finished in place than copied out.
+constexpr uint32_t TAIL_MIN = 64;
+
+template <int K>
+__device__ __forceinline__ int ready_sub(const Thread* th, uint32_t g, uint32_t CT, uint32_t n) {
+  int kk = 0;
+#pragma unroll 1
+  for (int k = 0; k < K; ++k)
+    if ((uint32_t)k * CT + g < n && th[k].state == S_READY) kk = k;
+  return kk;
+}
+
+// (t/th: this GPU thread's READY sub-thread, simulated tid `tid`, if any)
 __device__ void suspend_block(const KP& P, BlockShared& bs, const SmemLay& L, const TS& t, const Thread& th,
-                              uint32_t g, uint32_t nthr, uint32_t n, uint32_t sweep, uint32_t E, uint32_t lastStep,
-                              uint32_t lb) {
+                              uint32_t g, uint32_t tid, uint32_t nthr, uint32_t n, uint32_t sweep, uint32_t E,
+                              uint32_t lastStep, uint32_t lb) {
   const int sl = *(volatile int*)&bs.tailSlot;
   TailState& TSs = P.tails[sl];
   uint8_t* dst = P.tailSmem + (size_t)sl * P.tailStride;
@@ -1214,13 +1230,13 @@ __device__ void suspend_block(const KP& P, BlockShared& bs, const SmemLay& L, co
     unsigned long long* drs = (unsigned long long*)(dst + TL.raceSet);
     for (uint32_t i = me; i < RACE_SET; i += nthr) drs[i] = rs[i];
   }
-  if (g < n && th.state == S_READY) {
+  if (tid < n && th.state == S_READY) {
     TSs.t = t;
     TSs.th = th;
     TSs.sweep = sweep;
     TSs.E = E;
     TSs.lastStep = lastStep;
-    TSs.tid = g;
+    TSs.tid = tid;
     P.tailBlk[sl] = lb;
   }
 }
@@ -1346,6 +1362,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
   const uint32_t Lt = n - 1;
   bool justSolo = true;  // the next-run table is valid only after a full sweep
   bool noTail = false;   // a tail slot was refused: no further suspension attempts
+  uint32_t aloneFrom = ~0u;  // first block-level sweep with one unfinished thread
   bool released = false;  // an episode completed at the loop top (closed-form release)
   uint32_t relT = 0;
   uint32_t soloH = ~0u;   // solo: the first sweep another warp can step
@@ -1419,17 +1436,19 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
         break;
       }
       // ---- the serial tail: one unfinished thread left and it is READY
-      // (K = 1).  The block is suspended into a tail slot -- its shared
+      // The block is suspended into a tail slot -- its shared
       // state, the thread's interpreter state and the block's counters --
       // and the CTA is freed; tail_kernel finishes it, one lane per block ----
-      if (K == 1 && P.tailCap && !noTail && nfin == (int)SLOTS - 1) {
+      if (nfin == (int)SLOTS - 1 && aloneFrom == ~0u) aloneFrom = sweep;
+      if (P.tailCap && !noTail && nfin == (int)SLOTS - 1 && sweep - aloneFrom >= TAIL_MIN) {
         if (g == 0) {
           const uint32_t sl = atomicAdd(P.tailCount, 1u);
           bs.tailSlot = sl < P.tailCap ? (int)sl : -2;
         }
         __syncthreads();
         if (bs.tailSlot >= 0) {
-          suspend_block(P, bs, L, t[0], th[0], g, CT, n, sweep, E, lastStep, lb);
+          const int kk = ready_sub<K>(th, g, CT, n);
+          suspend_block(P, bs, L, t[kk], th[kk], g, (uint32_t)kk * CT + g, CT, n, sweep, E, lastStep, lb);
           break;
         }
         __syncthreads();
@@ -1490,7 +1509,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       justSolo = true;
       continue;
     }
-    if (solo && K == 1 && P.tailCap && !noTail && *(volatile int*)&bs.fin == (int)SLOTS - 1) {
+    if (solo && P.tailCap && !noTail && sweep - soloS0 >= TAIL_MIN && *(volatile int*)&bs.fin == (int)SLOTS - 1) {
       // the solo warp's last thread is the block's last: suspend it (the
       // other warps are parked and join the exit below)
       int sl = 0;
@@ -1502,7 +1521,8 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       if (sl >= 0) {
         if (lane == 0) bs.tailSlot = sl;
         __syncwarp();
-        suspend_block(P, bs, L, t[0], th[0], g, 32u, n, sweep, E, lastStep, lb);
+        const int kk = ready_sub<K>(th, g, CT, n);
+        suspend_block(P, bs, L, t[kk], th[kk], g, (uint32_t)kk * CT + g, 32u, n, sweep, E, lastStep, lb);
         soloCycles += clock64() - soloC0;
         soloSweeps += sweep - soloS0;
         if (lane == 0) bs.soloSweep = sweep;
@@ -1630,8 +1650,20 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
       bool arrivedNow = false;
 #pragma unroll 1
       for (int k = 0; k < K; ++k) arrivedNow |= ((runMask >> k) & 1u) && th[k].state == S_WAIT;
+      bool decide = false;
       if (__any_sync(0xFFFFFFFFu, arrivedNow)) {
-        // a lane arrived at a barrier: the block decides what happens next
+        // a lane arrived at a barrier.  Only an arrival that completes the
+        // episode or leaves the block quiescent (deadlock) changes what the
+        // other warps can do; any other one keeps the warp solo (round 1
+        // handed the block back on every arrival: one full-block sweep per
+        // thread of a release cascade)
+        const int p = (E + 1) & 1;
+        const int arrived = *(volatile int*)&bs.wait[p] - (need[p] - (int)n);
+        const int nfin = *(volatile int*)&bs.fin;
+        decide = arrived == (int)n || arrived + nfin == (int)SLOTS;
+      }
+      if (decide) {
+        // the block decides what happens next
         if (lane == 0) bs.soloSweep = sweep;
         solo = false;
         soloCycles += clock64() - soloC0;
@@ -1655,9 +1687,12 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
     // suspended: the counters of every thread but the tail's go to the
     // block's partial outputs; tail_kernel adds the rest
     unsigned long long mySteps = 0, myAllocs = 0;
-    if (!(g < n && th[0].state == S_READY)) {
-      mySteps = t[0].steps;
-      myAllocs = t[0].allocs;
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+      const uint32_t tid = (uint32_t)k * CT + g;
+      if (tid < n && th[k].state == S_READY) continue;  // the tail's own
+      mySteps += t[k].steps;
+      myAllocs += t[k].allocs;
     }
     atomicAdd(&bs.steps, mySteps);
     atomicAdd(&bs.allocs, myAllocs);
@@ -2266,7 +2301,7 @@ struct Replica {
   DBuf<k1::BlockOut> blocks;
   DBuf<uint32_t> tarr;
   DBuf<int> err;
-  DBuf<k1::TailState> tails;        // suspended serial tails (K = 1)
+  DBuf<k1::TailState> tails;        // suspended serial tails
   DBuf<uint8_t> tailSmem;
   DBuf<uint32_t> tailCnt, tailBlk;
   uint32_t tailCap = 0;             // tail slots of the current grid (0: none)
@@ -2721,12 +2756,12 @@ class CudaEngine final : public DeviceEngine {
       kp.tarr = g.trace ? R.tarr.p : nullptr;
       kp.markDirty = (D > 1 || exch_) ? 1 : 0;
       kp.maxSweeps = (uint32_t)std::min<uint64_t>((1ull << 26) - 1, g.stepBudget + 2);
-      // serial-tail slots (K = 1; MCKG_K1_TAILS=0 turns the offload off)
+      // serial-tail slots (MCKG_K1_TAILS=0 turns the offload off)
       static const bool tailsOn = [] {
         const char* e = getenv("MCKG_K1_TAILS");
         return !(e && e[0] == '0');
       }();
-      const uint32_t tailCap = (K == 1 && tailsOn) ? (uint32_t)std::min<size_t>(nb, 1u << 16) : 0u;
+      const uint32_t tailCap = tailsOn ? (uint32_t)std::min<size_t>(nb, 1u << 16) : 0u;
       const SmemLay TL = tailLayout(g.shmemBytes, g.raceCheck ? 1 : 0);
       if (tailCap && (!R.tails.ensure(tailCap, err) || !R.tailSmem.ensure((size_t)tailCap * TL.end, err) ||
                       !R.tailCnt.ensure(1, err) || !R.tailBlk.ensure(tailCap, err)))
