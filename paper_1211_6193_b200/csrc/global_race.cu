@@ -1512,7 +1512,12 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   used = false;
   unsigned long long hm[2];
   if (int rc = sample_span(events, n, hm, s, launches)) return rc;
-  // window buckets live in the sampled span (records outside it are foreign)
+  // window buckets live in the sampled span (records outside it are
+  // foreign), widened on both sides: the sample can miss the extremes, and
+  // the records it misses would otherwise all be foreign in one edge bucket
+  const uint64_t margin = ((hm[1] - hm[0]) >> 6) + 65536;
+  hm[0] = hm[0] > margin ? hm[0] - margin : 0;
+  hm[1] = hm[1] + margin;
   const uint64_t base = hm[0] & ~(uint64_t)((1u << FB_SHIFT) - 1);
   const uint64_t nbk64 = ((hm[1] - base) >> FB_SHIFT) + 1;
   if (nbk64 > (1ull << 22)) return MCKG_OK;  // > 8 GiB: the bitmap would not pay (anchors keep 23 bits)
