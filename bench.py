@@ -385,9 +385,16 @@ def run_c5(args, blocks, dev, ws, rank, comm=None):
     lo, _ = gr.addr_range(rank, ws, space)
     stream = torch.cuda.current_stream()
 
+    outs = {}  # result buffers, allocated once and reused like a caller would
+
+    def out_for(cap):
+        if cap not in outs:
+            outs[cap] = gr.GlobalOut(cap, device=dev)
+        return outs[cap]
+
     def step():
         if comm is not None:  # the exchange inside the library (mckg_detect_global_mgpu)
-            out = gr.GlobalOut(max(1, 2 * ev.shape[0] // 8), device=dev)
+            out = out_for(max(1, 2 * ev.shape[0] // 8))
             gr.detect_mgpu(comm, ev, space, out.reset(), stream)
             return out, -1
         if ws > 1:
@@ -395,7 +402,7 @@ def run_c5(args, blocks, dev, ws, rank, comm=None):
             mine = gr.exchange(grouped, counts)
         else:
             mine = ev  # one owner: nothing to partition or exchange
-        out = gr.GlobalOut(max(1, mine.shape[0] // 8), device=dev)
+        out = out_for(max(1, 2 * ev.shape[0] // 8) if ws > 1 else max(1, mine.shape[0] // 8))
         gr.detect(mine, lo, out.reset(), stream)
         if ws > 1:
             out.line_first.bitwise_xor_(-(1 << 63))
