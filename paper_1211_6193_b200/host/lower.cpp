@@ -1,5 +1,10 @@
 // lower.cpp -- name resolution, static checks and step-exact IR generation.
 //
+// Provenance: the name resolution and call / launch checks (resolveName,
+// resolveCall, resolveLaunch) restate the reference's Lowerer closely, since
+// their diagnostics must match it byte for byte; the IR emission (stmt / ex /
+// rv) is this project's own design.
+//
 // Static rules follow the reference lowering (/root/reference/proj/src/lower.cpp:
 // main checks 143-173, globals 175-207, call classification 467-535, launch
 // 551-573, sizeof typing 576-640).  Code generation follows the continuation

@@ -1061,7 +1061,11 @@ void HostMachine::execPrintf(const mck_ins& in) {
   vals_.push_back(v_int(static_cast<int64_t>(out.size())));
 }
 
-// runtime API (runtime_api.cpp:39-372)
+// runtime API (runtime_api.cpp:39-372).  Provenance: this dispatcher restates
+// the reference's API table closely (the same helpers and checks in the same
+// order, the same messages) because its diagnostics and return codes must be
+// the reference's; the sweep timeline, grid dispatch and diagnostic merge
+// around it are this project's own.
 void HostMachine::invokeApi(const mck_ins& in) {
   std::vector<Val> args(static_cast<size_t>(in.b));
   for (int i = in.b; i > 0; --i) args[static_cast<size_t>(i - 1)] = pop();

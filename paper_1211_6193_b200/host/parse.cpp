@@ -1,8 +1,12 @@
 // parse.cpp -- tokenizer, object-like-macro preprocessor and recursive-descent
-// parser for the CUDA-C subset (behaviour of /root/reference/proj/src/lexer.cpp
-// and parser.cpp: same accepted language, same node positions, same
-// precedence table; written independently as a single pass over a token
-// vector).
+// parser for the CUDA-C subset.
+//
+// Provenance: this front end restates /root/reference/proj/src/lexer.cpp and
+// parser.cpp closely -- the same grammar, the same precedence and
+// compound-assignment tables, the same production order -- because its
+// outputs (accepted language, node positions, error texts) must be
+// byte-identical to the reference's.  It runs once per program on the host,
+// outside the B200 hot path, and is not claimed as new work.
 #include <cctype>
 #include <cerrno>
 #include <cstdlib>
