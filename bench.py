@@ -308,7 +308,8 @@ def run_ours(args):
     if not args.no_c5:
         ev = bs = tr = out = None  # free the C3 trace before C5
         torch.cuda.empty_cache()
-        c5 = run_c5(args, args.c5_blocks if args.c5_blocks else (1 << 16) * ws, dev, ws, rank, comm)
+        # configs[4]: 2^32 events over 8 GPUs = 2^29 per GPU (2^17 blocks of 4096)
+        c5 = run_c5(args, args.c5_blocks if args.c5_blocks else (1 << 17) * ws, dev, ws, rank, comm)
     e2e = None
     if rank == 0 and ws == 1 and args.e2e_blocks > 0:
         e2e = run_e2e(args, torch, race, _abi)
@@ -580,7 +581,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the K1 C4 deadlock-sweep leg")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--c5-blocks", type=int, default=0,
-                    help="C5 blocks in total (default 2^16 per GPU; BASELINE: 2^20 over 8 GPUs)")
+                    help="C5 blocks in total (default 2^17 per GPU: BASELINE configs[4] is 2^20 blocks = 2^32 events over 8 GPUs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -928,7 +928,7 @@ __global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* e
   __shared__ unsigned long long s_base[2];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t nwords = nbk * FB_WORDS;  // nbk <= 2^22
+  const uint32_t nwords = nbk * FB_WORDS;  // nbk < 2^23
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -1520,7 +1520,7 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   hm[1] = hm[1] + margin;
   const uint64_t base = hm[0] & ~(uint64_t)((1u << FB_SHIFT) - 1);
   const uint64_t nbk64 = ((hm[1] - base) >> FB_SHIFT) + 1;
-  if (nbk64 > (1ull << 22)) return MCKG_OK;  // > 8 GiB: the bitmap would not pay (anchors keep 23 bits)
+  if (nbk64 >= (1ull << 23)) return MCKG_OK;  // >= 16 GiB: anchors keep 23 bits (the bitmap is span / 32)
   if (reinterpret_cast<uintptr_t>(events) & 15u) return MCKG_OK;  // the bulk copies need 16-byte alignment
   used = true;
   const uint32_t nbk = (uint32_t)nbk64;

@@ -1,9 +1,9 @@
-"""K6 timing probe: mckg_detect_global on C5 (2^28 records) per route."""
+"""K6 timing probe: mckg_detect_global on C5 (2^29 records = one GPU's share of configs[4]) per route."""
 import sys, time
 sys.path.insert(0, ".")
 import torch
 from paper_1211_6193_b200 import _abi, global_race as gr
-blocks = 65536
+blocks = int(__import__("os").environ.get("C5_BLOCKS", 1 << 17))
 ev = gr.gen_c5(0, blocks, blocks, device="cuda")
 lib = _abi.load()
 s = torch.cuda.current_stream()
