@@ -182,3 +182,12 @@ def test_block_clustered_traces(case):
 def test_c5_two_million_records():
     """2^21 C5 records: the size at which the tile path is the default."""
     assert _check(ob.gen_c5(0, 512, 512)) > 0
+
+
+def test_block_clustered_million_records():
+    """2^20 block-clustered records with every tile-path hazard at once
+    (in-tile candidates, foreign and word-crossing records, half-overlapping
+    windows): the size at which the tile path is the default route."""
+    ev = _tiled(256, 11, shared_words=6, bids_per_tile=2, foreign=0.02, unaligned=0.005)
+    ev2 = _tiled(64, 12, shared_words=3, bids_per_tile=3, overlap=True)
+    assert _check(np.concatenate([ev, ev2])) > 0
