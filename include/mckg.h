@@ -172,9 +172,12 @@ int mckg_abi_version(void);
 const char* mckg_last_error(void);
 int mckg_device_count(int* n);
 int mckg_get_launch_stats(mckg_launch_stats* out);
-/* Experiment / test switches of the detector (the MCKG_DEBUG environment
- * variable read once at load; 32 = the fused K2 kernel alone, which the
- * tests exercise beside the default two-kernel path). */
+/* Test switches that force one route of a detector, so the tests cover every
+ * route at small sizes (initial value: the MCKG_DEBUG environment variable,
+ * read once at load).  Bits: 32 = K2's general (TMA) kernel for every block
+ * instead of the warp-per-block fast path; 128 = K6's bucket pipeline in
+ * sparse (hashed) mode; 256 = K6 never takes the tile path; 512 = K6 takes
+ * the tile path at any size (default: from 2^20 records). */
 void mckg_set_debug(uint32_t flags);
 
 int mckg_race_out_reset(const mckg_race_out* out, void* stream);
