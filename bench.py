@@ -12,7 +12,7 @@ north star's roofline target is stated on.
 
 Second workload (`k1` object in the same line): BASELINE.json configs[1], C2
 -- the Fig. 1 reduction scaled to 2^24 ints (65536 blocks x 256 threads),
-checked end to end through mck_run_source (host interpreter + K1 grid engine +
+checked end to end through mck_run (result records) (host interpreter + K1 grid engine +
 fused race detector): simulated thread-steps/s and race-checked shared
 events/s of the grid kernel (CUDA events), plus the whole-program wall time.
 
@@ -474,7 +474,8 @@ def _k1_run(src, name, ws, rank, dev, shared):
             dist.broadcast_object_list(obj, src=0)
             kw["comm"] = obj[0]
     t0 = time.perf_counter()
-    r = checker.run_source(src, name, step_limit=8_000_000_000, **kw)
+    # the result-record ABI (no JSON): the end-to-end time is the checker's
+    r = checker.run(src, name, step_limit=8_000_000_000, stuck_lists=64, **kw)
     return r, time.perf_counter() - t0
 
 

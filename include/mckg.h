@@ -415,6 +415,15 @@ int mck_result_stuck(const mck_result* r, uint64_t i, mck_stuck_rec* out);
 /* triples [first, first + count) of RaceState::reported (machine.hpp:91) */
 int mck_result_reported(const mck_result* r, uint64_t first, uint64_t count, mckg_race_triple* out);
 const char* mck_result_trace(const mck_result* r, uint64_t i);
+/* the engine's counters of the run (mck::EngineStats; not a reference
+ * interface: what bench.py and the tests read instead of parsing JSON) */
+typedef struct mck_run_stats {
+  uint64_t host_steps, device_steps, barrier_rules, dispatches, shared_events, grids, sweeps;
+  double grid_ms;             /* device time of the grid kernels (CUDA events)      */
+  uint32_t kernel_launches, pad;
+  uint64_t block_sweeps, solo_sweeps, block_cycles, solo_cycles;
+} mck_run_stats;
+int mck_result_stats(const mck_result* r, mck_run_stats* out);
 void mck_result_free(mck_result* r);
 /* oracleRace (oracle.hpp:34): every interleaving of the shared accesses of a
  * small program's grid, explored on the GPU. */

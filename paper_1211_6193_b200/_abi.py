@@ -59,6 +59,7 @@ EXPORTS = [
     "mck_result_diag",
     "mck_result_stuck",
     "mck_result_reported",
+    "mck_result_stats",
     "mck_result_trace",
     "mck_result_free",
 ]

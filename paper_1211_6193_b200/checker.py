@@ -163,18 +163,29 @@ def _rec_lib():
         lib.mck_result_reported.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint64, vp]
         lib.mck_result_trace.argtypes = [vp, ctypes.c_uint64]
         lib.mck_result_trace.restype = ctypes.c_char_p
+        lib.mck_result_stats.argtypes = [vp, ctypes.POINTER(RunStats)]
         lib.mck_result_free.argtypes = [vp]
         lib.mck_result_free.restype = None
         lib._mck_rec_bound = True
     return lib
 
 
-def run(src, filename="test.cu", **kw):
+class RunStats(ctypes.Structure):
+    _fields_ = [("host_steps", ctypes.c_uint64), ("device_steps", ctypes.c_uint64),
+                ("barrier_rules", ctypes.c_uint64), ("dispatches", ctypes.c_uint64),
+                ("shared_events", ctypes.c_uint64), ("grids", ctypes.c_uint64), ("sweeps", ctypes.c_uint64),
+                ("grid_ms", ctypes.c_double), ("kernel_launches", ctypes.c_uint32), ("pad", ctypes.c_uint32),
+                ("block_sweeps", ctypes.c_uint64), ("solo_sweeps", ctypes.c_uint64),
+                ("block_cycles", ctypes.c_uint64), ("solo_cycles", ctypes.c_uint64)]
+
+
+def run(src, filename="test.cu", stuck_lists=None, **kw):
     """Machine::run through the result-record ABI.  Same keys as run_source
     (exit, output, steps, stuck, main_return, diags, stuck_reports,
-    report_text, engine_error, trace), but `reported` is a numpy array of
-    (obj, byte, line) records in std::set order -- fit for millions of
-    triples."""
+    report_text, engine_error, trace, stats), but `reported` is a numpy
+    array of (obj, byte, line) records in std::set order -- fit for millions
+    of triples.  stuck_lists=N: waiting/missing lists for the first N stuck
+    reports only (every report keeps kind, gid and bid)."""
     lib = _rec_lib()
     o = _opts(**kw)
     h = ctypes.c_void_p()
@@ -195,9 +206,14 @@ def run(src, filename="test.cu", **kw):
         for i in range(sm.n_stuck):
             r = StuckRec()
             _abi.check(lib.mck_result_stuck(h, i, ctypes.byref(r)), "mck_result_stuck")
+            full = stuck_lists is None or i < stuck_lists
             stuck.append({"kind": STUCK_KINDS[r.kind], "gid": r.gid, "bid": r.bid,
-                          "waiting": [r.waiting[k] for k in range(r.n_waiting)],
-                          "missing": [r.missing[k] for k in range(r.n_missing)], "reason": r.reason.decode()})
+                          "waiting": [r.waiting[k] for k in range(r.n_waiting)] if full else None,
+                          "missing": [r.missing[k] for k in range(r.n_missing)] if full else None,
+                          "reason": r.reason.decode()})
+        st = RunStats()
+        _abi.check(lib.mck_result_stats(h, ctypes.byref(st)), "mck_result_stats")
+        stats = {f: getattr(st, f) for f, _ in RunStats._fields_ if f != "pad"}
         rep = np.zeros(sm.n_reported, dtype=TRIPLE_DTYPE)
         if sm.n_reported:
             _abi.check(lib.mck_result_reported(h, 0, sm.n_reported, rep.ctypes.data), "mck_result_reported")
@@ -206,7 +222,7 @@ def run(src, filename="test.cu", **kw):
                 "main_return": sm.main_return if sm.has_main_return else None,
                 "engine_error": sm.engine_error.decode(), "diags": diags, "stuck_reports": stuck,
                 "report_text": sm.report_text.decode(), "reported": rep,
-                "trace": [lib.mck_result_trace(h, i).decode() for i in range(sm.n_trace)]}
+                "trace": [lib.mck_result_trace(h, i).decode() for i in range(sm.n_trace)], "stats": stats}
     finally:
         lib.mck_result_free(h)
 

@@ -226,6 +226,26 @@ extern "C" int mck_result_stuck(const mck_result* r, uint64_t i, mck_stuck_rec* 
   return MCKG_OK;
 }
 
+extern "C" int mck_result_stats(const mck_result* r, mck_run_stats* out) {
+  if (!r || !out) return MCKG_E_ARG;
+  const mck::EngineStats& st = r->run.stats;
+  *out = mck_run_stats{};
+  out->host_steps = st.hostSteps;
+  out->device_steps = st.deviceSteps;
+  out->barrier_rules = st.barrierRules;
+  out->dispatches = st.dispatches;
+  out->shared_events = st.sharedEvents;
+  out->grids = st.grids;
+  out->sweeps = st.sweeps;
+  out->grid_ms = st.gridMs;
+  out->kernel_launches = st.kernelLaunches;
+  out->block_sweeps = st.blockSweeps;
+  out->solo_sweeps = st.soloSweeps;
+  out->block_cycles = st.blockCycles;
+  out->solo_cycles = st.soloCycles;
+  return MCKG_OK;
+}
+
 extern "C" int mck_result_reported(const mck_result* r, uint64_t first, uint64_t count, mckg_race_triple* out) {
   if (!r || (!out && count)) return MCKG_E_ARG;
   const auto& rep = r->run.reported;
