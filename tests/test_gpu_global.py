@@ -191,3 +191,54 @@ def test_block_clustered_million_records():
     ev = _tiled(256, 11, shared_words=6, bids_per_tile=2, foreign=0.02, unaligned=0.005)
     ev2 = _tiled(64, 12, shared_words=3, bids_per_tile=3, overlap=True)
     assert _check(np.concatenate([ev, ev2])) > 0
+
+
+@pytest.mark.parametrize("k6_mode", ["tile"], indirect=True)
+def test_c5_full_share_matches_port(k6_mode):
+    """One GPU's full share of configs[4] (2^29 records, the default tile
+    route) against the C checker, run address-partitioned over the host's
+    cores: a byte lives in exactly one address range, so the per-range race
+    sets are disjoint and the line table is their minimum."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    import psutil
+    from paper_1211_6193_b200 import _abi
+    from paper_1211_6193_b200 import global_race as gr
+    if psutil.virtual_memory().available < (48 << 30):
+        pytest.skip("needs ~48 GiB of host memory for the 8.6 GB trace and its partition")
+    _abi.load().mckg_set_debug(0)  # the default route at this size
+    blocks = 1 << 17
+    ev_d = gr.gen_c5(0, blocks, blocks)
+    out = gr.GlobalOut(ev_d.shape[0] // 8)
+    gr.detect(ev_d, 0, out.reset())
+    races, n, lf, st = gr.fetch(out)
+    assert st == 0 and n == len(races)
+    ev = ev_d.cpu().numpy().view(ob.GACCESS_DTYPE).reshape(-1)
+    del ev_d, out
+    addr = ev["a"] & np.uint64(0xFFFFFFFFFF)
+    ln = (ev["a"] >> np.uint64(40)) & np.uint64(0xF)
+    parts = 64
+    shift = max(3, int(addr.max()).bit_length() - 6)  # 64 ranges, each a multiple of 8 bytes
+    owner = (addr >> np.uint64(shift)).astype(np.uint8)
+    assert np.array_equal(owner, ((addr + ln - np.uint64(1)) >> np.uint64(shift)).astype(np.uint8))
+    del addr, ln
+    order = np.argsort(owner, kind="stable")
+    bounds = np.concatenate([[0], np.cumsum(np.bincount(owner, minlength=parts))])
+    del owner
+
+    def check(p):
+        part = np.ascontiguousarray(ev[order[bounds[p]:bounds[p + 1]]])
+        if len(part) == 0:
+            return np.zeros(0, dtype=ob.GRACE_DTYPE), 0, np.full(len(lf), ob.TS_NONE, dtype=np.uint64)
+        rc, want, wn, wlf = ob.port_detect_global(part, capacity=4 * len(part) + 16)
+        assert rc == 0
+        return want, wn, wlf
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
+        res = list(pool.map(check, range(parts)))
+    want = np.concatenate([r[0] for r in res])
+    assert sum(r[1] for r in res) == n
+    got = races[np.lexsort((races["line"], races["addr"]))]
+    want = want[np.lexsort((want["line"], want["addr"]))]
+    assert np.array_equal(got["addr"], want["addr"]) and np.array_equal(got["line"], want["line"])
+    assert np.array_equal(lf, np.minimum.reduce([r[2] for r in res]))
