@@ -1686,12 +1686,19 @@ mck::RunResult HostMachine::run() {
       // keeps stepping until a step changes what can move (a stream item,
       // an await, a halt) or the limit is reached
       const uint64_t lim = o_.stepLimit;
+      const mck_ins* code = P_->code.data();
       do {
         if (steps_ >= lim) {
           hitLimit = true;
           break;
         }
-        hostStep();
+        // expansion steps (nop) cost a step and touch nothing: no dispatch
+        while (code[pc_].op == OP_JMP) pc_ = code[pc_].a;
+        if (code[pc_].op == OP_NOP) {
+          ++pc_;
+        } else {
+          hostStep();
+        }
         ++steps_;
         ++stats_.hostSteps;
         ++sweep_;
