@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "mckg.h"
 
 namespace mckg {
@@ -76,5 +78,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+
+// Frees the stream-ordered allocations of a host routine when it returns,
+// the early error returns of MCKG_CUDA_TRY included.
+struct PoolGuard {
+  cudaStream_t s;
+  std::vector<void*> p;
+  explicit PoolGuard(cudaStream_t st) : s(st) {}
+  PoolGuard(const PoolGuard&) = delete;
+  PoolGuard& operator=(const PoolGuard&) = delete;
+  template <typename T>
+  cudaError_t alloc(T** out, size_t bytes) {
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), bytes, s);
+    if (e == cudaSuccess) p.push_back(*out);
+    return e;
+  }
+  ~PoolGuard() {
+    for (void* x : p) cudaFreeAsync(x, s);
+  }
+};
 
 }  // namespace mckg

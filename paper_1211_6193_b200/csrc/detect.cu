@@ -990,10 +990,11 @@ int detect_oversize(const mckg_trace* tr, const mckg_race_out* out, cudaStream_t
   unsigned long long* cnt = nullptr;  // [0] races, [1..] K6 line table
   uint32_t* st6 = nullptr;
   const uint64_t rcap = maxn * 8 + 64;
-  MCKG_CUDA_TRY(cudaMallocAsync(&g, maxn * sizeof(mckg_gaccess), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&races, rcap * sizeof(mckg_grace), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&cnt, (1 + MCKG_MAX_LINES) * sizeof(unsigned long long), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&st6, sizeof(uint32_t), s));
+  PoolGuard pg(s);
+  MCKG_CUDA_TRY(pg.alloc(&g, maxn * sizeof(mckg_gaccess)));
+  MCKG_CUDA_TRY(pg.alloc(&races, rcap * sizeof(mckg_grace)));
+  MCKG_CUDA_TRY(pg.alloc(&cnt, (1 + MCKG_MAX_LINES) * sizeof(unsigned long long)));
+  MCKG_CUDA_TRY(pg.alloc(&st6, sizeof(uint32_t)));
   for (uint32_t b : blocks) {
     const uint64_t n = hbs[b + 1] - hbs[b];
     if (n == 0) continue;
@@ -1009,10 +1010,6 @@ int detect_oversize(const mckg_trace* tr, const mckg_race_out* out, cudaStream_t
     oversize_lines_kernel<<<MCKG_MAX_LINES / 256, 256, 0, s>>>(cnt + 1, ev, tr->bid_base + b, out->line_first);
     MCKG_CUDA_TRY(cudaGetLastError());
   }
-  cudaFreeAsync(g, s);
-  cudaFreeAsync(races, s);
-  cudaFreeAsync(cnt, s);
-  cudaFreeAsync(st6, s);
   return MCKG_OK;
 }
 
@@ -1151,8 +1148,9 @@ extern "C" int mckg_sort_triples(mckg_race_triple* triples, uint64_t n, uint32_t
   // (obj - obj_base):22 | byte:20 | line:16 keys, radix-sorted (sort.cu),
   // optionally reduced to the distinct ones, decoded back in place
   unsigned long long *k0 = nullptr, *k1 = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&k0, n * sizeof(unsigned long long), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&k1, n * sizeof(unsigned long long), s));
+  PoolGuard pg(s);
+  MCKG_CUDA_TRY(pg.alloc(&k0, n * sizeof(unsigned long long)));
+  MCKG_CUDA_TRY(pg.alloc(&k1, n * sizeof(unsigned long long)));
   uint32_t nb = (uint32_t)((n + 255) / 256);
   uint32_t launches = 1;
   encode_triples<<<nb, 256, 0, s>>>(triples, k0, n, obj_base);
@@ -1164,8 +1162,6 @@ extern "C" int mckg_sort_triples(mckg_race_triple* triples, uint64_t n, uint32_t
     decode_triples<<<nb, 256, 0, s>>>(k0, triples, nullptr, n, obj_base);
   }
   MCKG_CUDA_TRY(cudaGetLastError());
-  cudaFreeAsync(k0, s);
-  cudaFreeAsync(k1, s);
   add_launches(launches + 1);
   return MCKG_OK;
 }

@@ -1344,9 +1344,10 @@ extern "C" int mckg_partition_global(const mckg_gaccess* events, uint64_t n, uin
   }
   cudaStream_t s = (cudaStream_t)stream;
   keep_pool_memory();
+  PoolGuard pg(s);
   unsigned long long* cursor = nullptr;
   MCKG_CUDA_TRY(cudaMemsetAsync(counts, 0, n_ranks * sizeof(uint64_t), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&cursor, n_ranks * sizeof(unsigned long long), s));
+  MCKG_CUDA_TRY(pg.alloc(&cursor, n_ranks * sizeof(unsigned long long)));
   MCKG_CUDA_TRY(cudaMemsetAsync(cursor, 0, n_ranks * sizeof(unsigned long long), s));
   if (n) {
     const uint32_t g = grid_for(n);
@@ -1357,7 +1358,6 @@ extern "C" int mckg_partition_global(const mckg_gaccess* events, uint64_t n, uin
                                             cursor, out);
     MCKG_CUDA_TRY(cudaGetLastError());
   }
-  cudaFreeAsync(cursor, s);
   add_launches(2);
   return MCKG_OK;
 }
@@ -1368,8 +1368,9 @@ namespace {
 // the sampled address span of n records: {min, max} over a strided sample
 int sample_span(const mckg_gaccess* events, uint64_t n, unsigned long long hm[2], cudaStream_t s,
                 uint32_t& launches) {
+  PoolGuard pg(s);
   unsigned long long* mm = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&mm, 2 * sizeof(unsigned long long), s));
+  MCKG_CUDA_TRY(pg.alloc(&mm, 2 * sizeof(unsigned long long)));
   const unsigned long long init[2] = {~0ull, 0ull};
   MCKG_CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s));
   const uint64_t stride = n > (1u << 16) ? n >> 16 : 1;
@@ -1377,7 +1378,6 @@ int sample_span(const mckg_gaccess* events, uint64_t n, unsigned long long hm[2]
   ++launches;
   MCKG_CUDA_TRY(cudaMemcpyAsync(hm, mm, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   MCKG_CUDA_TRY(cudaStreamSynchronize(s));
-  cudaFreeAsync(mm, s);
   return MCKG_OK;
 }
 
@@ -1407,13 +1407,14 @@ int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaSt
   }
   const uint32_t nb = (uint32_t)((span >> shift) + 1);
   // 2-4. count, scan, scatter
+  PoolGuard pg(s);
   uint32_t *cnt = nullptr, *cur = nullptr, *big = nullptr;
   uint64_t* off = nullptr;
   mckg_gaccess* recs = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&cnt, (size_t)nb * 4, s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&cur, (size_t)nb * 4, s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&off, ((size_t)nb + 1) * 8, s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&big, ((size_t)nb + 1) * 4, s));
+  MCKG_CUDA_TRY(pg.alloc(&cnt, (size_t)nb * 4));
+  MCKG_CUDA_TRY(pg.alloc(&cur, (size_t)nb * 4));
+  MCKG_CUDA_TRY(pg.alloc(&off, ((size_t)nb + 1) * 8));
+  MCKG_CUDA_TRY(pg.alloc(&big, ((size_t)nb + 1) * 4));
   MCKG_CUDA_TRY(cudaMemsetAsync(cnt, 0, (size_t)nb * 4, s));
   MCKG_CUDA_TRY(cudaMemsetAsync(cur, 0, (size_t)nb * 4, s));
   MCKG_CUDA_TRY(cudaMemsetAsync(big, 0, 4, s));
@@ -1423,7 +1424,7 @@ int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaSt
   MCKG_CUDA_TRY(cudaGetLastError());
   // a record counts once per bucket it touches (at most two): 2n slots
   // bound the layout without waiting for the count
-  MCKG_CUDA_TRY(cudaMallocAsync(&recs, 2 * n * sizeof(mckg_gaccess), s));
+  MCKG_CUDA_TRY(pg.alloc(&recs, 2 * n * sizeof(mckg_gaccess)));
   bucket_scatter_kernel<<<g, 256, 0, s>>>(events, n, nb, shift, base, off, cur, recs);
   launches += 2;
   // 5. detection
@@ -1435,7 +1436,7 @@ int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaSt
   if (dense) {
     // warp per bucket; the buckets it hands back go to the general kernel
     uint32_t* mid = nullptr;
-    MCKG_CUDA_TRY(cudaMallocAsync(&mid, ((size_t)nb + 2) * 4, s));
+    MCKG_CUDA_TRY(pg.alloc(&mid, ((size_t)nb + 2) * 4));
     MCKG_CUDA_TRY(cudaMemsetAsync(mid, 0, 8, s));  // [0] handed-back buckets, [1] claim counter
     MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FB_SMEM));
     MCKG_CUDA_TRY(cudaFuncSetAttribute(bucket_fast_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -1445,8 +1446,7 @@ int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaSt
     bucket_fast_kernel<<<gf, FB_WARPS * 32, FB_SMEM, s>>>(recs, off, nb, base, O, mid + 2, mid, mid + 1);
     bucket_detect_kernel<<<gd, BT, BD_SMEM, s>>>(recs, off, nb, shift, base, mid + 2, mid, O, big + 1, big);
     MCKG_CUDA_TRY(cudaGetLastError());
-    cudaFreeAsync(mid, s);
-    launches += 2;
+      launches += 2;
   } else {
     bucket_detect_kernel<<<gd < nb ? gd : nb, BT, BD_SMEM, s>>>(recs, off, nb, shift, base, nullptr, nullptr, O,
                                                                  big + 1, big);
@@ -1477,7 +1477,8 @@ int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaSt
       uint8_t* scratch = nullptr;
       const size_t cand_bytes = (m * 4 + 15) & ~(size_t)15;  // keeps the 8-byte tables aligned
       const size_t bytes = ws * 16 + cand_bytes + bs * 40 + ds * 8;
-      MCKG_CUDA_TRY(cudaMallocAsync(&scratch, bytes, s));
+      PoolGuard sg(s);
+      MCKG_CUDA_TRY(sg.alloc(&scratch, bytes));
       MCKG_CUDA_TRY(cudaMemsetAsync(scratch, 0, bytes, s));
       BTab T;
       T.wkey = reinterpret_cast<unsigned long long*>(scratch);
@@ -1493,15 +1494,9 @@ int detect_buckets(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaSt
       T.dmask = (uint32_t)(ds - 1);
       bucket_detect_big_kernel<<<1, BT, 0, s>>>(recs, off, b, nb, shift, base, T, O);
       MCKG_CUDA_TRY(cudaGetLastError());
-      cudaFreeAsync(scratch, s);
       ++launches;
     }
   }
-  cudaFreeAsync(recs, s);
-  cudaFreeAsync(cnt, s);
-  cudaFreeAsync(cur, s);
-  cudaFreeAsync(off, s);
-  cudaFreeAsync(big, s);
   return MCKG_OK;
 }
 
@@ -1525,20 +1520,21 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   used = true;
   const uint32_t nbk = (uint32_t)nbk64;
   const uint64_t ntiles = (n + TT - 1) / TT;
+  PoolGuard pg(s);
   uint32_t *claim = nullptr, *bits = nullptr;
   unsigned long long* win = nullptr;
   mckg_gaccess* side = nullptr;
   unsigned long long* nside = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&claim, (size_t)nbk * 4, s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&bits, (size_t)nbk * (FB_WORDS / 8), s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&win, (size_t)ntiles * 8, s));
-  MCKG_CUDA_TRY(cudaMallocAsync(&side, (size_t)n * sizeof(mckg_gaccess), s));  // each record joins at most once
-  MCKG_CUDA_TRY(cudaMallocAsync(&nside, 8, s));
+  MCKG_CUDA_TRY(pg.alloc(&claim, (size_t)nbk * 4));
+  MCKG_CUDA_TRY(pg.alloc(&bits, (size_t)nbk * (FB_WORDS / 8)));
+  MCKG_CUDA_TRY(pg.alloc(&win, (size_t)ntiles * 8));
+  MCKG_CUDA_TRY(pg.alloc(&side, (size_t)n * sizeof(mckg_gaccess)));  // each record joins at most once
+  MCKG_CUDA_TRY(pg.alloc(&nside, 8));
   MCKG_CUDA_TRY(cudaMemsetAsync(claim, 0, (size_t)nbk * 4, s));
   MCKG_CUDA_TRY(cudaMemsetAsync(bits, 0, (size_t)nbk * (FB_WORDS / 8), s));
   MCKG_CUDA_TRY(cudaMemsetAsync(nside, 0, 8, s));
   uint32_t* multi = nullptr;  // [ntiles] tiles for tile_multi, then their count
-  MCKG_CUDA_TRY(cudaMallocAsync(&multi, ((size_t)ntiles + 1) * 4, s));
+  MCKG_CUDA_TRY(pg.alloc(&multi, ((size_t)ntiles + 1) * 4));
   MCKG_CUDA_TRY(cudaMemsetAsync(multi + ntiles, 0, 4, s));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -1561,12 +1557,6 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   MCKG_CUDA_TRY(cudaMemcpyAsync(&ns, nside, 8, cudaMemcpyDeviceToHost, s));
   MCKG_CUDA_TRY(cudaStreamSynchronize(s));
   int rc = ns ? detect_buckets(side, ns, O, s, launches, hm) : MCKG_OK;
-  cudaFreeAsync(claim, s);
-  cudaFreeAsync(bits, s);
-  cudaFreeAsync(win, s);
-  cudaFreeAsync(side, s);
-  cudaFreeAsync(nside, s);
-  cudaFreeAsync(multi, s);
   return rc;
 }
 

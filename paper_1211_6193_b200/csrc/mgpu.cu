@@ -116,8 +116,9 @@ extern "C" int mckg_detect_global_mgpu(mckg_comm* c, const mckg_gaccess* events,
     return MCKG_OK;
   }
   // 1. K3: records grouped by owner, per-owner counts
+  PoolGuard pg(s);
   mckg_gaccess* grouped = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&grouped, (n ? n : 1) * sizeof(mckg_gaccess), s));
+  MCKG_CUDA_TRY(pg.alloc(&grouped, (n ? n : 1) * sizeof(mckg_gaccess)));
   int rc = mckg_partition_global(events, n, (uint32_t)P, addr_space, grouped, c->counts, stream);
   if (rc != MCKG_OK) return rc;
   // 2. every rank's counts to every rank
@@ -133,7 +134,7 @@ extern "C" int mckg_detect_global_mgpu(mckg_comm* c, const mckg_gaccess* events,
   }
   const uint64_t nrecv = recvOff[P];
   mckg_gaccess* mine = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&mine, (nrecv ? nrecv : 1) * sizeof(mckg_gaccess), s));
+  MCKG_CUDA_TRY(pg.alloc(&mine, (nrecv ? nrecv : 1) * sizeof(mckg_gaccess)));
   // 3. the all-to-all of the records (NVLink peer to peer)
   MCKG_NCCL_TRY(ncclGroupStart());
   for (int r = 0; r < P; ++r) {
@@ -147,7 +148,5 @@ extern "C" int mckg_detect_global_mgpu(mckg_comm* c, const mckg_gaccess* events,
   rc = mckg_detect_global(mine, nrecv, lo, races, capacity, n_races, line_first, status, stream);
   if (rc != MCKG_OK) return rc;
   MCKG_NCCL_TRY(ncclAllReduce(line_first, line_first, MCKG_MAX_LINES, ncclUint64, ncclMin, c->nccl, s));
-  cudaFreeAsync(grouped, s);
-  cudaFreeAsync(mine, s);
   return MCKG_OK;
 }

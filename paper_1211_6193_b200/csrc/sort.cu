@@ -198,8 +198,9 @@ uint32_t grid_of(uint64_t n) {
 
 cudaError_t exclusive_scan_u32(const uint32_t* in, uint64_t n, uint64_t* out, cudaStream_t s, uint32_t* launches) {
   const uint64_t tiles = (n + SCT - 1) / SCT;
+  PoolGuard pg(s);
   uint64_t* ts = nullptr;
-  cudaError_t e = cudaMallocAsync(&ts, (tiles ? tiles : 1) * sizeof(uint64_t), s);
+  cudaError_t e = pg.alloc(&ts, (tiles ? tiles : 1) * sizeof(uint64_t));
   if (e != cudaSuccess) return e;
   if (n == 0) {
     e = cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
@@ -210,7 +211,6 @@ cudaError_t exclusive_scan_u32(const uint32_t* in, uint64_t n, uint64_t* out, cu
     e = cudaGetLastError();
     if (launches) *launches += 3;
   }
-  cudaFreeAsync(ts, s);
   return e;
 }
 
@@ -218,11 +218,12 @@ cudaError_t radix_sort_u64(unsigned long long* keys, unsigned long long* tmp, ui
                            cudaStream_t s, uint32_t* launches) {
   if (n < 2) return cudaSuccess;
   const uint32_t ntiles = (uint32_t)((n + RTILE - 1) / RTILE);
+  PoolGuard pg(s);
   uint32_t* hist = nullptr;
   uint64_t* base = nullptr;
   cudaError_t e;
-  if ((e = cudaMallocAsync(&hist, (size_t)RBINS * ntiles * sizeof(uint32_t), s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync(&base, ((size_t)RBINS * ntiles + 1) * sizeof(uint64_t), s)) != cudaSuccess) return e;
+  if ((e = pg.alloc(&hist, (size_t)RBINS * ntiles * sizeof(uint32_t))) != cudaSuccess) return e;
+  if ((e = pg.alloc(&base, ((size_t)RBINS * ntiles + 1) * sizeof(uint64_t))) != cudaSuccess) return e;
   unsigned long long *src = keys, *dst = tmp;
   uint32_t passes = 0;
   for (uint32_t shift = 0; shift < bits; shift += 8, ++passes) {
@@ -237,44 +238,40 @@ cudaError_t radix_sort_u64(unsigned long long* keys, unsigned long long* tmp, ui
   }
   if (e == cudaSuccess && src != keys) e = cudaMemcpyAsync(keys, src, n * sizeof(unsigned long long),
                                                            cudaMemcpyDeviceToDevice, s);
-  cudaFreeAsync(hist, s);
-  cudaFreeAsync(base, s);
   return e;
 }
 
 cudaError_t unique_sorted_u64(const unsigned long long* sorted, uint64_t n, unsigned long long* out,
                               unsigned long long* n_out, cudaStream_t s, uint32_t* launches) {
+  PoolGuard pg(s);
   uint32_t* f = nullptr;
   uint64_t* pos = nullptr;
   cudaError_t e;
-  if ((e = cudaMallocAsync(&f, (n ? n : 1) * sizeof(uint32_t), s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync(&pos, (n + 1) * sizeof(uint64_t), s)) != cudaSuccess) return e;
+  if ((e = pg.alloc(&f, (n ? n : 1) * sizeof(uint32_t))) != cudaSuccess) return e;
+  if ((e = pg.alloc(&pos, (n + 1) * sizeof(uint64_t))) != cudaSuccess) return e;
   head_flags_kernel<<<grid_of(n), 256, 0, s>>>(sorted, n, f);
   if ((e = exclusive_scan_u32(f, n, pos, s, launches)) == cudaSuccess) {
     gather_keys_kernel<<<grid_of(n), 256, 0, s>>>(sorted, f, pos, n, out, n_out);
     e = cudaGetLastError();
     if (launches) *launches += 2;
   }
-  cudaFreeAsync(f, s);
-  cudaFreeAsync(pos, s);
   return e;
 }
 
 cudaError_t select_flagged_index(const uint8_t* flags, uint64_t n, uint32_t first, uint32_t* out, uint32_t* n_out,
                                  cudaStream_t s, uint32_t* launches) {
+  PoolGuard pg(s);
   uint32_t* f = nullptr;
   uint64_t* pos = nullptr;
   cudaError_t e;
-  if ((e = cudaMallocAsync(&f, (n ? n : 1) * sizeof(uint32_t), s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync(&pos, (n + 1) * sizeof(uint64_t), s)) != cudaSuccess) return e;
+  if ((e = pg.alloc(&f, (n ? n : 1) * sizeof(uint32_t))) != cudaSuccess) return e;
+  if ((e = pg.alloc(&pos, (n + 1) * sizeof(uint64_t))) != cudaSuccess) return e;
   u8_to_u32_kernel<<<grid_of(n), 256, 0, s>>>(flags, n, f);
   if ((e = exclusive_scan_u32(f, n, pos, s, launches)) == cudaSuccess) {
     gather_index_kernel<<<grid_of(n), 256, 0, s>>>(flags, pos, n, first, out, n_out);
     e = cudaGetLastError();
     if (launches) *launches += 2;
   }
-  cudaFreeAsync(f, s);
-  cudaFreeAsync(pos, s);
   return e;
 }
 

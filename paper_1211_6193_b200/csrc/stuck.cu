@@ -66,15 +66,15 @@ extern "C" int mckg_scan_stuck(const uint32_t* arrivals, uint32_t n_blocks, uint
     return MCKG_OK;
   }
   const uint32_t words = (block_dim + 31u) / 32u;
+  PoolGuard pg(s);
   uint8_t* flags = nullptr;
-  MCKG_CUDA_TRY(cudaMallocAsync(&flags, n_blocks, s));
+  MCKG_CUDA_TRY(pg.alloc(&flags, n_blocks));
   uint32_t grid = n_blocks < (uint32_t)sm_count() * 8u ? n_blocks : (uint32_t)sm_count() * 8u;
   stuck_kernel<<<grid, NT, 0, s>>>(arrivals, n_blocks, block_dim, words, waiting_mask, flags);
   MCKG_CUDA_TRY(cudaGetLastError());
   // the deadlocked bids in ascending order (hand-written compaction, sort.cu)
   uint32_t launches = 1;
   MCKG_CUDA_TRY(select_flagged_index(flags, n_blocks, bid_base, dl_bids, n_dl, s, &launches));
-  cudaFreeAsync(flags, s);
   note_launch(launches, grid, NT, 0);
   return MCKG_OK;
 }
