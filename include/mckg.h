@@ -384,6 +384,9 @@ typedef struct mck_summary {
   const char* frontend_stage; /* "" or "lex" / "parse" / "semantic"                 */
   const char* frontend_message;
   const char* report_text;    /* formatStuckReports(stuckReports) (machine.hpp:449) */
+  const char* engine_note;    /* RunResult::engineNote: "" unless the run departs from the
+                                 reference (a non-round-robin schedule requested; a grid with
+                                 cross-block global conflicts, whose values follow block order) */
 } mck_summary;
 
 typedef struct mck_diag_rec {

@@ -137,7 +137,8 @@ class Summary(ctypes.Structure):
                 ("n_diags", ctypes.c_uint64), ("n_stuck", ctypes.c_uint64), ("n_reported", ctypes.c_uint64),
                 ("n_trace", ctypes.c_uint64), ("output_bytes", ctypes.c_uint64), ("output", ctypes.c_char_p),
                 ("engine_error", ctypes.c_char_p), ("frontend_stage", ctypes.c_char_p),
-                ("frontend_message", ctypes.c_char_p), ("report_text", ctypes.c_char_p)]
+                ("frontend_message", ctypes.c_char_p), ("report_text", ctypes.c_char_p),
+                ("engine_note", ctypes.c_char_p)]
 
 
 class DiagRec(ctypes.Structure):
@@ -220,7 +221,8 @@ def run(src, filename="test.cu", stuck_lists=None, **kw):
         return {"exit": sm.exit_code, "output": ctypes.string_at(sm.output, sm.output_bytes).decode(),
                 "steps": sm.steps, "stuck": bool(sm.stuck),
                 "main_return": sm.main_return if sm.has_main_return else None,
-                "engine_error": sm.engine_error.decode(), "diags": diags, "stuck_reports": stuck,
+                "engine_error": sm.engine_error.decode(), "engine_note": sm.engine_note.decode(),
+                "diags": diags, "stuck_reports": stuck,
                 "report_text": sm.report_text.decode(), "reported": rep,
                 "trace": [lib.mck_result_trace(h, i).decode() for i in range(sm.n_trace)], "stats": stats}
     finally:

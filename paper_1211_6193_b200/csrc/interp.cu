@@ -153,6 +153,7 @@ struct KP {
   mckg_gaccess* glog;
   unsigned long long* nglog;
   unsigned long long glogCap;
+  int glogStrict;  // a full log is an engine error (globalRaceCheck); else the probe gives up
   // outputs
   unsigned long long* lineFirst;
   int32_t* triples;           // (obj, byte, line) records of 3 x int32
@@ -811,7 +812,7 @@ __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq
         g.sweep = c.sweep;
         g.b = (c.bid & 0xFFFFFFu) | (((ln >> 8) & 0xFFu) << 24);
         P.glog[i] = g;
-      } else {
+      } else if (P.glogStrict) {
         set_error(P, ERR_GLOG_FULL, 0);
       }
     }
@@ -2305,6 +2306,7 @@ struct Replica {
   DBuf<uint8_t> tailSmem;
   DBuf<uint32_t> tailCnt, tailBlk;
   uint32_t tailCap = 0;             // tail slots of the current grid (0: none)
+  size_t glogCap = 0;               // global-access log records of the current grid
   DBuf<mckg_gaccess> glog;          // RunOptions::globalRaceCheck
   DBuf<unsigned long long> gcnt;    // [0] log length, [1] K6 races, [2..] K6 line table
   DBuf<uint32_t> gstat;
@@ -2659,6 +2661,8 @@ class CudaEngine final : public DeviceEngine {
     }
     void (*kern)(KP) = K == 1 ? grid_kernel<1> : K == 2 ? grid_kernel<2> : K == 4 ? grid_kernel<4> : grid_kernel<8>;
     const size_t total = (size_t)g.gridDim;
+    // the conflict probe needs the same single-device, single-rank log
+    const bool glogOn = g.globalRaceCheck || (g.conflictProbe && !exch_ && reps_.size() == 1 && total < MCKG_MAX_BID);
     if (g.globalRaceCheck && (exch_ || reps_.size() > 1 || total >= MCKG_MAX_BID)) {
       out.error = "globalRaceCheck runs a grid of < 2^21 blocks on one device and one rank";
       return false;
@@ -2712,13 +2716,13 @@ class CudaEngine final : public DeviceEngine {
         return false;
       // the global-race log: up to 64 accesses per simulated thread, within
       // [2^20, 2^27] records; a fuller log is an engine error, never a miss
-      const size_t glogCap = g.globalRaceCheck
+      const size_t glogCap = glogOn
                                  ? std::min<size_t>(1ull << 27, std::max<size_t>(1ull << 20, 64 * nb * (size_t)g.blockDim))
                                  : 0;
-      if (g.globalRaceCheck && (!R.glog.ensure(glogCap, err) || !R.gcnt.ensure(2 + LINES, err) ||
+      if (glogOn && (!R.glog.ensure(glogCap, err) || !R.gcnt.ensure(2 + LINES, err) ||
                                 !R.gstat.ensure(1, err)))
         return false;
-      if (g.globalRaceCheck) CK(cudaMemsetAsync(R.gcnt.p, 0, sizeof(unsigned long long), R.stream));
+      if (glogOn) CK(cudaMemsetAsync(R.gcnt.p, 0, sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.line.p, 0xFF, LINES * sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.ntri.p, 0, sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.diag.p, 0, diagN * sizeof(DevDiagRec), R.stream));
@@ -2774,9 +2778,11 @@ class CudaEngine final : public DeviceEngine {
       kp.tailCap = tailCap;
       kp.tailStride = TL.end;
       R.tailCap = tailCap;
-      kp.glog = g.globalRaceCheck ? R.glog.p : nullptr;
-      kp.nglog = g.globalRaceCheck ? R.gcnt.p : nullptr;
+      R.glogCap = glogCap;
+      kp.glog = glogOn ? R.glog.p : nullptr;
+      kp.nglog = glogOn ? R.gcnt.p : nullptr;
       kp.glogCap = glogCap;
+      kp.glogStrict = g.globalRaceCheck ? 1 : 0;
       kp.lineFirst = R.line.p;
       kp.triples = R.tri.p;
       kp.tripleCap = triCaps[ri];
@@ -2888,7 +2894,10 @@ class CudaEngine final : public DeviceEngine {
       std::vector<unsigned long long> lf(LINES);
       CK(cudaMemcpy(lf.data(), R.line.p, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
       for (int l = 0; l < LINES; ++l) lfAll[(size_t)l] = std::min(lfAll[(size_t)l], lf[(size_t)l]);
-      if (g.globalRaceCheck) {
+      unsigned long long nlogProbe = 0;
+      if (glogOn && !g.globalRaceCheck)
+        CK(cudaMemcpy(&nlogProbe, R.gcnt.p, sizeof nlogProbe, cudaMemcpyDeviceToHost));
+      if (glogOn && (g.globalRaceCheck || nlogProbe <= R.glogCap)) {
         // cross-block global races of this grid: K6 over the access log
         // (a builder-defined extension, off by default)
         unsigned long long nlog = 0;
@@ -2905,6 +2914,8 @@ class CudaEngine final : public DeviceEngine {
         CK(cudaStreamSynchronize(R.stream));
         out.launches += 6;
         for (int l = 0; l < LINES; ++l)
+          if (gl[(size_t)l] != ~0ull) out.globalConflicts = true;
+        for (int l = 0; l < LINES && g.globalRaceCheck; ++l)
           if (gl[(size_t)l] != ~0ull) {
             // K6 key sweep:32 | bid:21 | tid:11 -> the device-diagnostic key
             const unsigned long long k = gl[(size_t)l];

@@ -73,7 +73,7 @@ extern "C" int mck_run_source(const char* src, const char* filename, const mck_r
     o = "{\"exit\":" + std::to_string(r.exitCode) + ",\"output\":" + js(r.output) +
         ",\"steps\":" + std::to_string(r.steps) + ",\"stuck\":" + (r.stuck ? "true" : "false") +
         ",\"main_return\":" + (r.mainReturn ? std::to_string(*r.mainReturn) : std::string("null")) +
-        ",\"engine_error\":" + js(r.engineError) + ",\"diags\":[";
+        ",\"engine_error\":" + js(r.engineError) + ",\"engine_note\":" + js(r.engineNote) + ",\"diags\":[";
     for (size_t i = 0; i < r.diagnostics.size(); ++i) {
       const auto& d = r.diagnostics[i];
       o += std::string(i ? "," : "") + "{\"cat\":" + js(mck::categoryName(d.category)) + ",\"sev\":" +
@@ -192,6 +192,7 @@ extern "C" int mck_result_summary(const mck_result* r, mck_summary* out) {
   out->output_bytes = x.output.size();
   out->output = x.output.c_str();
   out->engine_error = x.engineError.c_str();
+  out->engine_note = x.engineNote.c_str();
   out->frontend_stage = r->frontendStage.c_str();
   out->frontend_message = r->frontendMessage.c_str();
   out->report_text = r->reportText.c_str();

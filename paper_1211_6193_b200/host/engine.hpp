@@ -52,6 +52,9 @@ struct GridSpec {
   std::vector<std::array<uint32_t, 3>> sharedRanges;
   bool trace = false;               // record barrier arrivals (GridResult::arrivals)
   bool globalRaceCheck = false;     // log global accesses, run K6 on them after the grid
+  // without globalRaceCheck: the same log and K6 pass, reporting only whether
+  // the grid had cross-block global conflicts (GridResult::globalConflicts)
+  bool conflictProbe = false;
 };
 
 struct DevDiag {
@@ -82,6 +85,7 @@ struct GridResult {
   uint32_t launches = 0;
   std::string error;            // engine limitation hit: run abandoned
   bool stepLimitHit = false;    // the grid ran out of the run's step budget
+  bool globalConflicts = false; // conflictProbe: blocks touched a global byte, one of them writing
   // trace mode: per block, completed barrier episodes, and the local arrival
   // sweep + 1 of every thread in its first TRACE_EPISODES episodes (0 = none)
   std::vector<uint32_t> episodes;   // [gridDim]

@@ -210,6 +210,7 @@ class HostMachine {
   std::vector<mck::RaceTriple> reported_;
   mck::EngineStats stats_;
   std::string engineError_;
+  std::vector<uint32_t> conflictGids_;  // grids with cross-block global conflicts (the probe)
 
   // ---------------- helpers ----------------
   std::string at(int line) const { return " at " + P_->filename + ":" + std::to_string(line) + "."; }
@@ -1415,6 +1416,9 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   g.sharedRanges = sharedRanges_;
   g.trace = o_.trace;
   g.globalRaceCheck = o_.globalRaceCheck;
+  // small grids are probed for cross-block global conflicts: their values
+  // follow this engine's block order (DESIGN §3 divergence 2), so the run says so
+  g.conflictProbe = !o_.globalRaceCheck && static_cast<uint64_t>(l.grid) * static_cast<uint64_t>(l.block) <= 65536;
   const int nparams = P_->fns[static_cast<size_t>(l.kernel)].n_params;
   // spawnGrid allocates gridDim shared objects, then nparams objects per thread
   const uint64_t reserve = static_cast<uint64_t>(l.grid) + static_cast<uint64_t>(l.grid) * l.block * nparams;
@@ -1479,6 +1483,7 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   stats_.soloSweeps += rec.res.soloSweeps;
   stats_.blockCycles += rec.res.blockCycles;
   stats_.soloCycles += rec.res.soloCycles;
+  if (rec.res.globalConflicts) conflictGids_.push_back(g.gid);
   // device diagnostics, timestamped by (global sweep, gid, bid, tid, sub)
   for (const DevDiag& r : rec.res.diags) {
     uint64_t lsweep = r.key >> 38;
@@ -1751,6 +1756,15 @@ mck::RunResult HostMachine::run() {
   r.output = output_;
   r.mainReturn = exitValue_;
   r.engineError = engineError_;
+  if (!conflictGids_.empty()) {
+    std::string ids;
+    for (size_t i = 0; i < conflictGids_.size() && i < 8; ++i) ids += (i ? ", " : "") + std::to_string(conflictGids_[i]);
+    if (conflictGids_.size() > 8) ids += ", ...";
+    r.engineNote = "cross-block global-memory conflicts in grid(s) gid " + ids +
+                   ": blocks of one grid touched a global byte with at least one write; the engine orders those "
+                   "accesses by block, not by the reference's interleaving, so values read there may differ "
+                   "(RunOptions::globalRaceCheck reports them)";
+  }
   if (hitLimit) {
     DiagEv e;
     e.sweep = NEVER;
@@ -1876,13 +1890,15 @@ RunResult Machine::run() {
   h.out = onOutput;
   impl_->m.reset(new mckb::HostMachine(prog_, opts_, std::move(h)));
   RunResult r = impl_->m->run();
+  std::string note;
   if (opts_.policy == SchedulePolicy::SeededRandom && opts_.seed != 0)
-    r.engineNote = "SchedulePolicy::SeededRandom (seed " + std::to_string(opts_.seed) +
-                   ") was run under the round-robin schedule: the B200 engine executes the round-robin "
-                   "interleaving only (it equals the seed-0 run on the BASELINE program families)";
+    note = "SchedulePolicy::SeededRandom (seed " + std::to_string(opts_.seed) +
+           ") was run under the round-robin schedule: the B200 engine executes the round-robin "
+           "interleaving only (it equals the seed-0 run on the BASELINE program families)";
   if (opts_.policy == SchedulePolicy::Exhaustive)
-    r.engineNote = "SchedulePolicy::Exhaustive was run under the round-robin schedule (the interleaving "
-                   "explorer is oracleRace)";
+    note = "SchedulePolicy::Exhaustive was run under the round-robin schedule (the interleaving "
+           "explorer is oracleRace)";
+  if (!note.empty()) r.engineNote = r.engineNote.empty() ? note : note + "; " + r.engineNote;
   if (onTrace)
     for (const std::string& t : r.trace) onTrace(t);
   impl_->last = r;

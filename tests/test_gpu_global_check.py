@@ -51,3 +51,17 @@ def test_full_size_c2_has_no_global_race():
     r = checker.run_source(gp.scaled(1 << 20, 256), "c2.cu", step_limit=8_000_000_000, global_race_check=True)
     assert r["engine_error"] == ""
     assert r["exit"] == 0 and r["diags"] == []
+
+
+@pytest.mark.parametrize("name", sorted(PROGRAMS))
+def test_conflicts_flagged_without_the_option(name):
+    """With the option off the run stays the reference's, but a small grid
+    with cross-block global conflicts -- whose values follow this engine's
+    block order, not the reference's interleaving -- is named in
+    RunResult::engineNote instead of diverging silently."""
+    from paper_1211_6193_b200 import checker
+    src, lines = PROGRAMS[name]
+    for r in (checker.run_source(src, filename="g.cu"), checker.run(src, "g.cu")):
+        assert r["engine_error"] == ""
+        assert ("cross-block global-memory conflicts" in r["engine_note"]) == bool(lines), r["engine_note"]
+        assert r["output"] == GOLD[name]["output"] and r["exit"] == GOLD[name]["exit"]
