@@ -2913,6 +2913,32 @@ class CudaEngine final : public DeviceEngine {
         CK(cudaMemcpyAsync(gl.data(), glf, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost, R.stream));
         CK(cudaStreamSynchronize(R.stream));
         out.launches += 6;
+        if (nlog && nlog <= (1ull << 20) && nlog <= R.glogCap) {
+          // the grid's global footprint per object (for in-flight overlap checks)
+          std::vector<mckg_gaccess> lg(nlog);
+          CK(cudaMemcpy(lg.data(), R.glog.p, nlog * sizeof(mckg_gaccess), cudaMemcpyDeviceToHost));
+          std::vector<size_t> ord(g.objects.size());
+          for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+          std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return g.objects[a].base < g.objects[b].base; });
+          std::map<uint32_t, std::array<int64_t, 5>> fp;
+          for (const mckg_gaccess& x : lg) {
+            const uint64_t a = x.a & 0xFFFFFFFFFFull;
+            const int64_t len = (int64_t)((x.a >> 40) & 0xF);
+            const bool wr = (x.a >> 44) & 1u;
+            auto it = std::upper_bound(ord.begin(), ord.end(), a,
+                                       [&](uint64_t v, size_t k) { return v < g.objects[k].base; });
+            if (it == ord.begin()) continue;
+            const DevObjInfo& o = g.objects[*(it - 1)];
+            const int64_t off = (int64_t)(a - o.base);
+            if (off >= o.size) continue;
+            auto& e = fp.emplace(o.id, std::array<int64_t, 5>{(int64_t)o.id, INT64_MAX, INT64_MIN, INT64_MAX,
+                                                              INT64_MIN}).first->second;
+            const int k = wr ? 3 : 1;
+            e[k] = std::min(e[k], off);
+            e[k + 1] = std::max(e[k + 1], off + len);
+          }
+          for (auto& kv : fp) out.footprint.push_back(kv.second);
+        }
         for (int l = 0; l < LINES; ++l)
           if (gl[(size_t)l] != ~0ull) out.globalConflicts = true;
         for (int l = 0; l < LINES && g.globalRaceCheck; ++l)

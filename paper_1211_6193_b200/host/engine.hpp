@@ -86,6 +86,11 @@ struct GridResult {
   std::string error;            // engine limitation hit: run abandoned
   bool stepLimitHit = false;    // the grid ran out of the run's step budget
   bool globalConflicts = false; // conflictProbe: blocks touched a global byte, one of them writing
+  // conflictProbe / globalRaceCheck: per device-global object the grid touched,
+  // {object id, read lo, read hi, write lo, write hi} (byte offsets, hi
+  // exclusive; lo > hi: none) -- the host checks stream operations issued
+  // while the grid is in flight against it
+  std::vector<std::array<int64_t, 5>> footprint;
   // trace mode: per block, completed barrier episodes, and the local arrival
   // sweep + 1 of every thread in its first TRACE_EPISODES episodes (0 = none)
   std::vector<uint32_t> episodes;   // [gridDim]

@@ -211,6 +211,26 @@ class HostMachine {
   mck::EngineStats stats_;
   std::string engineError_;
   std::vector<uint32_t> conflictGids_;  // grids with cross-block global conflicts (the probe)
+  // grids whose global bytes another stream touched while they were in
+  // flight (the engine applies a grid's effects at its dispatch sweep)
+  std::vector<uint32_t> inflightGids_;
+  // does an access [lo, hi) of object `obj` (write: `wr`) overlap what a
+  // running grid on another stream read or wrote, with a write on either side?
+  void checkInflight(uint32_t sid, uint32_t obj, int64_t lo, int64_t hi, bool wr) {
+    if (lo >= hi) return;
+    for (const auto& [gid, g] : grids_) {
+      if (g.completed || g.stream == sid || g.endSweep <= sweep_) continue;
+      for (const auto& e : g.res.footprint) {
+        if ((uint32_t)e[0] != obj) continue;
+        const bool hitW = e[3] < hi && lo < e[4];
+        const bool hitR = e[1] < hi && lo < e[2];
+        if (hitW || (wr && hitR)) {
+          if (std::find(inflightGids_.begin(), inflightGids_.end(), gid) == inflightGids_.end())
+            inflightGids_.push_back(gid);
+        }
+      }
+    }
+  }
 
   // ---------------- helpers ----------------
   std::string at(int line) const { return " at " + P_->filename + ":" + std::to_string(line) + "."; }
@@ -1372,6 +1392,8 @@ void HostMachine::performCopy(const CopyRec& c, uint32_t sid) {
     apiDiag("memory transfer of " + std::to_string(n) + " bytes is out of range", c.line, 3, sid);
     return;
   }
+  if (s->space != SP_HOST) checkInflight(sid, c.src.obj, c.src.i, c.src.i + n, false);
+  if (d->space != SP_HOST) checkInflight(sid, c.dst.obj, c.dst.i, c.dst.i + n, true);
   std::vector<uint8_t> b(static_cast<size_t>(n)), m(static_cast<size_t>(n));
   if (s->space == SP_HOST) {
     std::memcpy(b.data(), s->bytes.data() + c.src.i, static_cast<size_t>(n));
@@ -1484,6 +1506,10 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   stats_.blockCycles += rec.res.blockCycles;
   stats_.soloCycles += rec.res.soloCycles;
   if (rec.res.globalConflicts) conflictGids_.push_back(g.gid);
+  for (const auto& e : rec.res.footprint) {  // this grid against the grids still in flight
+    checkInflight(sid, (uint32_t)e[0], e[1], e[2], false);
+    checkInflight(sid, (uint32_t)e[0], e[3], e[4], true);
+  }
   // device diagnostics, timestamped by (global sweep, gid, bid, tid, sub)
   for (const DevDiag& r : rec.res.diags) {
     uint64_t lsweep = r.key >> 38;
@@ -1756,11 +1782,20 @@ mck::RunResult HostMachine::run() {
   r.output = output_;
   r.mainReturn = exitValue_;
   r.engineError = engineError_;
+  if (!inflightGids_.empty()) {
+    std::string ids;
+    for (size_t i = 0; i < inflightGids_.size() && i < 8; ++i) ids += (i ? ", " : "") + std::to_string(inflightGids_[i]);
+    if (inflightGids_.size() > 8) ids += ", ...";
+    r.engineNote = "grid(s) gid " + ids +
+                   " had global bytes touched by another stream's copy or grid while in flight; the engine applies "
+                   "a grid's effects at its dispatch sweep, so values there may differ from the reference's "
+                   "interleaving";
+  }
   if (!conflictGids_.empty()) {
     std::string ids;
     for (size_t i = 0; i < conflictGids_.size() && i < 8; ++i) ids += (i ? ", " : "") + std::to_string(conflictGids_[i]);
     if (conflictGids_.size() > 8) ids += ", ...";
-    r.engineNote = "cross-block global-memory conflicts in grid(s) gid " + ids +
+    r.engineNote += std::string(r.engineNote.empty() ? "" : "; ") + "cross-block global-memory conflicts in grid(s) gid " + ids +
                    ": blocks of one grid touched a global byte with at least one write; the engine orders those "
                    "accesses by block, not by the reference's interleaving, so values read there may differ "
                    "(RunOptions::globalRaceCheck reports them)";

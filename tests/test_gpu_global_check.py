@@ -65,3 +65,40 @@ def test_conflicts_flagged_without_the_option(name):
         assert r["engine_error"] == ""
         assert ("cross-block global-memory conflicts" in r["engine_note"]) == bool(lines), r["engine_note"]
         assert r["output"] == GOLD[name]["output"] and r["exit"] == GOLD[name]["exit"]
+
+
+INFLIGHT = r"""#include <stdio.h>
+__global__ void slow(int* g, int n) {
+  int t = threadIdx.x, i, acc = t;
+  for (i = 0; i < n; ++i) { acc = acc * 3 + i; }
+  g[t] = acc %% 1000;
+}
+int main(void) {
+  int *g, h[64];
+  cudaStream_t s1, s2;
+  cudaStreamCreate(&s1);
+  cudaStreamCreate(&s2);
+  cudaMalloc(&g, 64 * sizeof(int));
+  cudaMemset(g, 0, 64 * sizeof(int));
+  slow<<<1, 64, 0, s1>>>(g, 40);
+  %s
+  cudaMemcpyAsync(h, g, 64 * sizeof(int), cudaMemcpyDeviceToHost, s2);
+  cudaDeviceSynchronize();
+  printf("%%d %%d\n", h[0], h[63]);
+  return 0;
+}
+"""
+
+
+def test_inflight_overlap_flagged():
+    """A copy on another stream reads a grid's output while the grid is in
+    flight: the reference copies the bytes as of that sweep ("0 0", its own
+    run), this engine applies the grid at its dispatch -- the run says so in
+    engine_note.  Synchronised first, the run is the reference's and says
+    nothing (reference output "-444 -893", exit 1, 74,537 steps)."""
+    from paper_1211_6193_b200 import checker
+    r = checker.run(INFLIGHT % "", "f.cu")
+    assert "in flight" in r["engine_note"], r["engine_note"]
+    r = checker.run(INFLIGHT % "cudaStreamSynchronize(s1);", "f.cu")
+    assert r["engine_note"] == ""
+    assert r["output"] == "-444 -893\n" and r["exit"] == 1 and r["steps"] == 74537
