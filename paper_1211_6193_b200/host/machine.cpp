@@ -1228,6 +1228,7 @@ void HostMachine::invokeApi(const mck_ins& in) {
       int64_t off = p.i, n = args[2].i;
       if (off < 0 || off + n > o->size) return err(kInval, "fill range is out of bounds");
       if (n > 0) {
+        checkInflight(~0u, p.obj, off, off + n, true);  // the host fills at once, whatever is in flight
         eng_->fill(o->devBase + static_cast<uint64_t>(off), static_cast<uint8_t>(args[1].i), META_DEF, n);
         int64_t lo = std::max<int64_t>(0, off - 7);
         if (lo < off) {
