@@ -119,4 +119,9 @@ def edge_cases():
     out["recursion_depth_20"] = ("rec.cu", 50_000_000, RECURSION % dict(n=20))
     out["wide_race_1024x16k"] = ("wide.cu", 200_000_000, WIDE_RACE % dict(words=4096, threads=1024, blocks=1))
     out["wide_race_2x512x8k"] = ("wide2.cu", 200_000_000, WIDE_RACE % dict(words=2048, threads=512, blocks=2))
+    # serial tails of blocks over 256 threads (several simulated threads per
+    # GPU thread): thread 0 sums the partials alone for thousands of sweeps
+    import gen_programs as gp
+    out["tail_512x3"] = ("t512.cu", 200_000_000, gp.scaled(512 * 3, 512))
+    out["tail_1024x2_racy"] = ("t1024.cu", 200_000_000, gp.scaled(1024 * 2, 1024, racy=True))
     return out
