@@ -211,7 +211,7 @@ def run(src, filename="test.cu", stuck_lists=None, **kw):
             stuck.append({"kind": STUCK_KINDS[r.kind], "gid": r.gid, "bid": r.bid,
                           "waiting": [r.waiting[k] for k in range(r.n_waiting)] if full else None,
                           "missing": [r.missing[k] for k in range(r.n_missing)] if full else None,
-                          "reason": r.reason.decode()})
+                          "n_waiting": r.n_waiting, "n_missing": r.n_missing, "reason": r.reason.decode()})
         st = RunStats()
         _abi.check(lib.mck_result_stats(h, ctypes.byref(st)), "mck_result_stats")
         stats = {f: getattr(st, f) for f, _ in RunStats._fields_ if f != "pad"}
