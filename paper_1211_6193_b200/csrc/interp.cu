@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <vector>
 
 #include "../host/engine.hpp"
@@ -151,6 +152,9 @@ struct KP {
   uint32_t tailCap, tailStride;
   // RunOptions::globalRaceCheck: every global access appended here (K6 input)
   mckg_gaccess* glog;
+  // per log record (writes only): old bytes, old meta, new bytes, pointer
+  // flag -- the grid's write history for mid-flight copies (probe mode)
+  uint4* glogv;   // 2 x uint4 per record
   unsigned long long* nglog;
   unsigned long long glogCap;
   int glogStrict;  // a full log is an engine error (globalRaceCheck); else the probe gives up
@@ -802,6 +806,19 @@ __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq
     m = P.gmeta + rq.base + rq.off;
     if (P.glog) {  // the global-race log: one 16-byte record per access
       const unsigned long long i = atomicAdd(P.nglog, 1ull);
+      if (i < P.glogCap && rq.kind == 2 && P.glogv) {
+        // what this write overwrites (bytes, meta); 'complex' when a pointer
+        // slot is stored or erased
+        uint32_t ob[2] = {0, 0}, om[2] = {0, 0}, cx = rq.ptr ? 1u : 0u;
+        for (int k = 0; k < len; ++k) {
+          ob[k >> 2] |= (uint32_t)b[k] << (8 * (k & 3));
+          om[k >> 2] |= (uint32_t)m[k] << (8 * (k & 3));
+          cx |= (m[k] & META_PTR) ? 1u : 0u;
+        }
+        for (int64_t k = rq.off - 7 < 0 ? 0 : rq.off - 7; k < rq.off; ++k) cx |= (m[k - rq.off] & META_PTR) ? 1u : 0u;
+        P.glogv[2 * i] = make_uint4(ob[0], ob[1], om[0], om[1]);
+        P.glogv[2 * i + 1] = make_uint4((uint32_t)rq.raw, (uint32_t)(rq.raw >> 32), cx, 0u);
+      }
       if (i < P.glogCap) {
         mckg_gaccess g;
         const uint64_t addr = rq.base + (uint64_t)rq.off;
@@ -1941,6 +1958,7 @@ __global__ void __launch_bounds__(64, 1) oracle_kernel(KP P0, OQ Q) {
   P.raceCheck = 0;  // the oracle runs the shadow itself
   P.tarr = nullptr;
   P.glog = nullptr;
+  P.glogv = nullptr;
   P.markDirty = 0;
   uint8_t* arena = Q.arenas + (size_t)gt * 2 * Q.arenaSize;
   P.gbytes = arena;
@@ -2308,6 +2326,7 @@ struct Replica {
   uint32_t tailCap = 0;             // tail slots of the current grid (0: none)
   size_t glogCap = 0;               // global-access log records of the current grid
   DBuf<mckg_gaccess> glog;          // RunOptions::globalRaceCheck
+  DBuf<uint4> glogv;                // the probe's write history (2 x uint4 per record)
   DBuf<unsigned long long> gcnt;    // [0] log length, [1] K6 races, [2..] K6 line table
   DBuf<uint32_t> gstat;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -2723,6 +2742,8 @@ class CudaEngine final : public DeviceEngine {
                                 !R.gstat.ensure(1, err)))
         return false;
       if (glogOn) CK(cudaMemsetAsync(R.gcnt.p, 0, sizeof(unsigned long long), R.stream));
+      const bool histOn = glogOn && g.conflictProbe;  // the write history (mid-flight copies)
+      if (histOn && !R.glogv.ensure(2 * glogCap, err)) return false;
       CK(cudaMemsetAsync(R.line.p, 0xFF, LINES * sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.ntri.p, 0, sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.diag.p, 0, diagN * sizeof(DevDiagRec), R.stream));
@@ -2783,6 +2804,7 @@ class CudaEngine final : public DeviceEngine {
       kp.nglog = glogOn ? R.gcnt.p : nullptr;
       kp.glogCap = glogCap;
       kp.glogStrict = g.globalRaceCheck ? 1 : 0;
+      kp.glogv = histOn ? R.glogv.p : nullptr;
       kp.lineFirst = R.line.p;
       kp.triples = R.tri.p;
       kp.tripleCap = triCaps[ri];
@@ -2921,7 +2943,14 @@ class CudaEngine final : public DeviceEngine {
           for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
           std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return g.objects[a].base < g.objects[b].base; });
           std::map<uint32_t, std::array<int64_t, 5>> fp;
-          for (const mckg_gaccess& x : lg) {
+          std::vector<uint4> hv;
+          if (g.conflictProbe && R.glogv.p) {
+            hv.resize(2 * nlog);
+            CK(cudaMemcpy(hv.data(), R.glogv.p, hv.size() * sizeof(uint4), cudaMemcpyDeviceToHost));
+          }
+          bool complexAny = false;
+          for (size_t li = 0; li < lg.size(); ++li) {
+            const mckg_gaccess& x = lg[li];
             const uint64_t a = x.a & 0xFFFFFFFFFFull;
             const int64_t len = (int64_t)((x.a >> 40) & 0xF);
             const bool wr = (x.a >> 44) & 1u;
@@ -2936,8 +2965,31 @@ class CudaEngine final : public DeviceEngine {
             const int k = wr ? 3 : 1;
             e[k] = std::min(e[k], off);
             e[k + 1] = std::max(e[k + 1], off + len);
+            if (wr && !hv.empty()) {
+              const uint4 v0 = hv[2 * li], v1 = hv[2 * li + 1];
+              complexAny |= v1.z != 0u;
+              GridResult::Write w;
+              w.obj = o.id;
+              w.lsweep = x.sweep;
+              w.bid = x.b & 0xFFFFFFu;
+              w.tid = (uint32_t)((x.a >> 45) & 0x7FFu);
+              w.off = off;
+              w.len = (uint32_t)len;
+              const uint32_t ob[2] = {v0.x, v0.y}, om[2] = {v0.z, v0.w}, nw[2] = {v1.x, v1.y};
+              for (int q = 0; q < 8; ++q) {
+                w.oldB[q] = (uint8_t)(ob[q >> 2] >> (8 * (q & 3)));
+                w.oldM[q] = (uint8_t)(om[q >> 2] >> (8 * (q & 3)));
+                w.newB[q] = (uint8_t)(nw[q >> 2] >> (8 * (q & 3)));
+              }
+              out.writes.push_back(w);
+            }
           }
           for (auto& kv : fp) out.footprint.push_back(kv.second);
+          if (complexAny) out.writes.clear();
+          // global order of the writes: (local sweep, bid, tid)
+          std::stable_sort(out.writes.begin(), out.writes.end(), [](const GridResult::Write& p, const GridResult::Write& q) {
+            return std::tie(p.lsweep, p.bid, p.tid) < std::tie(q.lsweep, q.bid, q.tid);
+          });
         }
         for (int l = 0; l < LINES; ++l)
           if (gl[(size_t)l] != ~0ull) out.globalConflicts = true;

@@ -91,6 +91,17 @@ struct GridResult {
   // exclusive; lo > hi: none) -- the host checks stream operations issued
   // while the grid is in flight against it
   std::vector<std::array<int64_t, 5>> footprint;
+  // ... and every global write of the grid with what it overwrote, so that a
+  // copy on another stream reading the grid's bytes mid-flight sees them as
+  // of its sweep (empty when any write stored or erased a pointer slot)
+  struct Write {
+    uint32_t obj;
+    uint32_t lsweep, bid, tid;  // local sweep (global = dispatch sweep + lsweep)
+    int64_t off;
+    uint32_t len;
+    uint8_t oldB[8], oldM[8], newB[8];
+  };
+  std::vector<Write> writes;
   // trace mode: per block, completed barrier episodes, and the local arrival
   // sweep + 1 of every thread in its first TRACE_EPISODES episodes (0 = none)
   std::vector<uint32_t> episodes;   // [gridDim]

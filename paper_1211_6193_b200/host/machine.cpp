@@ -101,6 +101,7 @@ enum class EvStatus { Created, Pending, Recorded };
 struct GridRec {
   uint32_t gid;
   uint32_t stream;
+  uint64_t spawnSweep = 0;  // dispatch sweep: local sweep l runs at spawnSweep + l
   int64_t gridDim, blockDim;
   uint32_t sharedBase;
   uint64_t endSweep;  // NEVER = deadlocked
@@ -230,6 +231,44 @@ class HostMachine {
         }
       }
     }
+  }
+
+  // Bytes [lo, lo + n) of device object `obj` as a copy dispatched now on
+  // stream sid sees them while a grid on another stream is in flight: the
+  // grid's writes up to this sweep (global order) over what they overwrote.
+  // false (b / m untouched) when no grid applies, two do, or the grid's
+  // write history is incomplete.
+  bool midflight(uint32_t sid, uint32_t obj, int64_t lo, int64_t n, uint8_t* b, uint8_t* m) {
+    const GridRec* G = nullptr;
+    for (const auto& [gid, g] : grids_) {
+      if (g.completed || g.stream == sid || g.endSweep <= sweep_) continue;
+      bool hits = false;
+      for (const auto& e : g.res.footprint)
+        if ((uint32_t)e[0] == obj && e[3] < lo + n && lo < e[4]) hits = true;
+      if (!hits) continue;
+      if (G || g.res.writes.empty()) return false;
+      G = &g;
+    }
+    if (!G) return false;
+    std::vector<char> seen(static_cast<size_t>(n), 0);
+    for (const GridResult::Write& w : G->res.writes) {
+      if (w.obj != obj) continue;
+      const bool done = G->spawnSweep + w.lsweep <= sweep_;  // device steps precede this sweep's dispatches
+      for (uint32_t q = 0; q < w.len; ++q) {
+        const int64_t x = w.off + q - lo;
+        if (x < 0 || x >= n) continue;
+        if (!seen[static_cast<size_t>(x)]) {  // the value before the grid's first write
+          b[x] = w.oldB[q];
+          m[x] = w.oldM[q];
+          seen[static_cast<size_t>(x)] = 1;
+        }
+        if (done) {
+          b[x] = w.newB[q];
+          m[x] |= META_DEF;
+        }
+      }
+    }
+    return true;
   }
 
   // ---------------- helpers ----------------
@@ -1393,7 +1432,6 @@ void HostMachine::performCopy(const CopyRec& c, uint32_t sid) {
     apiDiag("memory transfer of " + std::to_string(n) + " bytes is out of range", c.line, 3, sid);
     return;
   }
-  if (s->space != SP_HOST) checkInflight(sid, c.src.obj, c.src.i, c.src.i + n, false);
   if (d->space != SP_HOST) checkInflight(sid, c.dst.obj, c.dst.i, c.dst.i + n, true);
   std::vector<uint8_t> b(static_cast<size_t>(n)), m(static_cast<size_t>(n));
   if (s->space == SP_HOST) {
@@ -1401,6 +1439,10 @@ void HostMachine::performCopy(const CopyRec& c, uint32_t sid) {
     std::memcpy(m.data(), s->meta.data() + c.src.i, static_cast<size_t>(n));
   } else {
     eng_->read(s->devBase + static_cast<uint64_t>(c.src.i), b.data(), m.data(), n);
+    // a grid in flight on another stream that writes these bytes: read them
+    // as of this sweep (its write history), else say the values may differ
+    if (!midflight(sid, c.src.obj, c.src.i, n, b.data(), m.data()))
+      checkInflight(sid, c.src.obj, c.src.i, c.src.i + n, false);
   }
   // slots that would extend past the copied range are not copied
   for (int64_t i = std::max<int64_t>(0, n - 7); i < n; ++i) m[static_cast<size_t>(i)] &= static_cast<uint8_t>(~META_PTR);
@@ -1454,6 +1496,7 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
     }
   GridRec rec;
   rec.gid = g.gid;
+  rec.spawnSweep = g.spawnSweep;
   rec.stream = sid;
   rec.gridDim = l.grid;
   rec.blockDim = l.block;

@@ -90,15 +90,58 @@ int main(void) {
 """
 
 
-def test_inflight_overlap_flagged():
+def test_inflight_copy_reads_grid_as_of_its_sweep():
     """A copy on another stream reads a grid's output while the grid is in
-    flight: the reference copies the bytes as of that sweep ("0 0", its own
-    run), this engine applies the grid at its dispatch -- the run says so in
-    engine_note.  Synchronised first, the run is the reference's and says
-    nothing (reference output "-444 -893", exit 1, 74,537 steps)."""
+    flight: the reference copies the bytes as of that sweep.  The grid ran at
+    its dispatch, so the copy is rebuilt from the grid's write history (every
+    write up to the copy's sweep over what it overwrote): "0 0", exactly the
+    reference's own run.  Synchronised first, the copy sees the whole grid
+    (reference: "-444 -893", exit 1, 74,537 steps)."""
     from paper_1211_6193_b200 import checker
     r = checker.run(INFLIGHT % "", "f.cu")
-    assert "in flight" in r["engine_note"], r["engine_note"]
+    assert r["output"] == "0 0\n" and r["exit"] == 1 and r["steps"] == 74530, r
+    assert r["engine_note"] == ""
     r = checker.run(INFLIGHT % "cudaStreamSynchronize(s1);", "f.cu")
     assert r["engine_note"] == ""
     assert r["output"] == "-444 -893\n" and r["exit"] == 1 and r["steps"] == 74537
+
+
+STAIRCASE = r"""#include <stdio.h>
+__global__ void staircase(int* g) {
+  int t = threadIdx.x, i, acc = 0;
+  for (i = 0; i < t; ++i) { acc = acc + i; }
+  g[t] = acc + 1;
+}
+int main(void) {
+  int *g, h[32], i, spin = 0;
+  cudaStream_t s1, s2;
+  cudaStreamCreate(&s1);
+  cudaStreamCreate(&s2);
+  cudaMalloc(&g, 32 * sizeof(int));
+  cudaMemset(g, 0, 32 * sizeof(int));
+  staircase<<<1, 32, 0, s1>>>(g);
+  for (i = 0; i != %d; ++i) { spin = spin + i; }
+  cudaMemcpyAsync(h, g, 32 * sizeof(int), cudaMemcpyDeviceToHost, s2);
+  cudaDeviceSynchronize();
+  for (i = 0; i != 32; ++i) printf("%%d ", h[i]);
+  printf("\n%%d\n", spin);
+  return 0;
+}
+"""
+_TRI = [1, 1, 2, 4, 7, 11, 16, 22, 29, 37, 46, 56, 67, 79, 92, 106, 121, 137, 154, 172, 191, 211, 232, 254, 277,
+        301, 326, 352, 379, 407, 436, 466]
+# the reference's own runs (oracle/_ref, round robin): (host spin, steps, thread values copied, spin)
+STAIR_GOLD = [(0, 14567, 0, 0), (10, 14807, 10, 45), (30, 15287, 29, 435), (60, 16007, 32, 1770),
+              (200, 19367, 32, 19900)]
+
+
+@pytest.mark.parametrize("k,steps,copied,spin", STAIR_GOLD)
+def test_inflight_copy_sees_partial_grid(k, steps, copied, spin):
+    """Threads finish at staggered sweeps; the host spins k iterations, then
+    copies on another stream: the copy holds exactly the threads done by its
+    sweep (reference goldens)."""
+    from paper_1211_6193_b200 import checker
+    r = checker.run(STAIRCASE % k, "m.cu")
+    vals = _TRI[:copied] + [0] * (32 - copied)
+    assert r["output"] == " ".join(map(str, vals)) + " \n%d\n" % spin, r["output"]
+    assert r["exit"] == 0 and r["steps"] == steps and r["engine_note"] == ""
