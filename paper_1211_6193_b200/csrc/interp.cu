@@ -2742,7 +2742,7 @@ class CudaEngine final : public DeviceEngine {
                                 !R.gstat.ensure(1, err)))
         return false;
       if (glogOn) CK(cudaMemsetAsync(R.gcnt.p, 0, sizeof(unsigned long long), R.stream));
-      const bool histOn = glogOn && g.conflictProbe;  // the write history (mid-flight copies)
+      const bool histOn = glogOn && g.conflictProbe && g.wantHistory;  // the write history (mid-flight copies)
       if (histOn && !R.glogv.ensure(2 * glogCap, err)) return false;
       CK(cudaMemsetAsync(R.line.p, 0xFF, LINES * sizeof(unsigned long long), R.stream));
       CK(cudaMemsetAsync(R.ntri.p, 0, sizeof(unsigned long long), R.stream));
@@ -2935,7 +2935,7 @@ class CudaEngine final : public DeviceEngine {
         CK(cudaMemcpyAsync(gl.data(), glf, LINES * sizeof(unsigned long long), cudaMemcpyDeviceToHost, R.stream));
         CK(cudaStreamSynchronize(R.stream));
         out.launches += 6;
-        if (nlog && nlog <= (1ull << 20) && nlog <= R.glogCap) {
+        if (nlog && nlog <= (1ull << 18) && nlog <= R.glogCap) {
           // the grid's global footprint per object (for in-flight overlap checks)
           std::vector<mckg_gaccess> lg(nlog);
           CK(cudaMemcpy(lg.data(), R.glog.p, nlog * sizeof(mckg_gaccess), cudaMemcpyDeviceToHost));
@@ -2944,7 +2944,7 @@ class CudaEngine final : public DeviceEngine {
           std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return g.objects[a].base < g.objects[b].base; });
           std::map<uint32_t, std::array<int64_t, 5>> fp;
           std::vector<uint4> hv;
-          if (g.conflictProbe && R.glogv.p) {
+          if (g.conflictProbe && g.wantHistory && R.glogv.p) {
             hv.resize(2 * nlog);
             CK(cudaMemcpy(hv.data(), R.glogv.p, hv.size() * sizeof(uint4), cudaMemcpyDeviceToHost));
           }

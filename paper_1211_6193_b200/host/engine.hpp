@@ -55,6 +55,9 @@ struct GridSpec {
   // without globalRaceCheck: the same log and K6 pass, reporting only whether
   // the grid had cross-block global conflicts (GridResult::globalConflicts)
   bool conflictProbe = false;
+  // ... and keep the grid's write history (another stream exists, so a
+  // copy may read the grid's bytes while it is in flight)
+  bool wantHistory = false;
 };
 
 struct DevDiag {

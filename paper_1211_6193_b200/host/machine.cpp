@@ -1484,6 +1484,7 @@ void HostMachine::spawnGrid(uint32_t sid, const LaunchRec& l) {
   // small grids are probed for cross-block global conflicts: their values
   // follow this engine's block order (DESIGN §3 divergence 2), so the run says so
   g.conflictProbe = !o_.globalRaceCheck && static_cast<uint64_t>(l.grid) * static_cast<uint64_t>(l.block) <= 65536;
+  g.wantHistory = g.conflictProbe && streams_.size() > 1;
   const int nparams = P_->fns[static_cast<size_t>(l.kernel)].n_params;
   // spawnGrid allocates gridDim shared objects, then nparams objects per thread
   const uint64_t reserve = static_cast<uint64_t>(l.grid) + static_cast<uint64_t>(l.grid) * l.block * nparams;
