@@ -786,9 +786,30 @@ __device__ int mem_write(TS& t, const KP& P, Ctx& c, Thread& th, uint32_t obj, i
   return 1;
 }
 
+// Probe mode: the write history record i -- what this write overwrites
+// (bytes, meta), the new bytes, and 'complex' when a pointer slot is stored
+// or erased.
+__device__ __noinline__ void log_overwrite(const KP& P, unsigned long long i, const Req& rq, const uint8_t* b,
+                                           const uint8_t* m, int len) {
+  uint32_t ob[2] = {0, 0}, om[2] = {0, 0}, cx = rq.ptr ? 1u : 0u;
+  for (int k = 0; k < len; ++k) {
+    ob[k >> 2] |= (uint32_t)b[k] << (8 * (k & 3));
+    om[k >> 2] |= (uint32_t)m[k] << (8 * (k & 3));
+    cx |= (m[k] & META_PTR) ? 1u : 0u;
+  }
+  for (int64_t k = rq.off - 7 < 0 ? 0 : rq.off - 7; k < rq.off; ++k) cx |= (m[k - rq.off] & META_PTR) ? 1u : 0u;
+  P.glogv[2 * i] = make_uint4(ob[0], ob[1], om[0], om[1]);
+  P.glogv[2 * i + 1] = make_uint4((uint32_t)rq.raw, (uint32_t)(rq.raw >> 32), cx, 0u);
+}
+
 // Performs a pending shared/global request (memory phase).
+// HIST: the grid keeps a write history (KP::glogv).  A compile-time switch:
+// the history path, even never taken, costs the interpreter ~5% of its step
+// rate through register pressure (C2 42.8 -> 45.0 ms measured), so only
+// probed grids run the kernel instance that has it.
 // sb: the base of the block's shared state laid out by L (the CTA's shared
 // memory, or a suspended block's copy in global memory)
+template <bool HIST>
 __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq, const SmemLay& L, uint32_t stamp,
                                         uint32_t bstamp, unsigned long long& sharedEvents, uint8_t* sb) {
   int len = (int)t_scalar(rq.ty);
@@ -806,19 +827,7 @@ __device__ __noinline__ void do_request(const KP& P, Ctx& c, Thread& th, Req& rq
     m = P.gmeta + rq.base + rq.off;
     if (P.glog) {  // the global-race log: one 16-byte record per access
       const unsigned long long i = atomicAdd(P.nglog, 1ull);
-      if (i < P.glogCap && rq.kind == 2 && P.glogv) {
-        // what this write overwrites (bytes, meta); 'complex' when a pointer
-        // slot is stored or erased
-        uint32_t ob[2] = {0, 0}, om[2] = {0, 0}, cx = rq.ptr ? 1u : 0u;
-        for (int k = 0; k < len; ++k) {
-          ob[k >> 2] |= (uint32_t)b[k] << (8 * (k & 3));
-          om[k >> 2] |= (uint32_t)m[k] << (8 * (k & 3));
-          cx |= (m[k] & META_PTR) ? 1u : 0u;
-        }
-        for (int64_t k = rq.off - 7 < 0 ? 0 : rq.off - 7; k < rq.off; ++k) cx |= (m[k - rq.off] & META_PTR) ? 1u : 0u;
-        P.glogv[2 * i] = make_uint4(ob[0], ob[1], om[0], om[1]);
-        P.glogv[2 * i + 1] = make_uint4((uint32_t)rq.raw, (uint32_t)(rq.raw >> 32), cx, 0u);
-      }
+      if (HIST && i < P.glogCap && rq.kind == 2 && P.glogv) log_overwrite(P, i, rq, b, m, len);
       if (i < P.glogCap) {
         mckg_gaccess g;
         const uint64_t addr = rq.base + (uint64_t)rq.off;
@@ -1264,7 +1273,7 @@ __device__ void suspend_block(const KP& P, BlockShared& bs, const SmemLay& L, co
 // (CT = blockDim.x, a multiple of 32).  Smaller CTAs let more simulated
 // blocks stay resident, which is what long serial stretches (one live thread
 // per block) need; inside a sweep the K sub-threads step in tid order.
-template <int K>
+template <int K, bool HIST>
 #ifndef MCKG_K1_MINB
 #define MCKG_K1_MINB 4  // K = 1 serves blocks of <= 256 threads
 #endif
@@ -1638,7 +1647,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
         if (!((pendMask >> k) & 1u)) continue;
         c.tid = (uint32_t)k * CT + g;
         c.sub = 1;
-        do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents, smem);
+        do_request<HIST>(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents, smem);
         finish_request(t[k], P, th[k], rq[k], pd[k]);
         if (th[k].state == S_FIN) atomicAdd(&bs.fin, 1);
       }
@@ -1652,7 +1661,7 @@ __global__ void __launch_bounds__(256, K == 1 ? MCKG_K1_MINB : 4) grid_kernel(KP
               if (lane == l && ((pendMask >> k) & 1u)) {
                 c.tid = (uint32_t)k * CT + g;
                 c.sub = 1;
-                do_request(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents, smem);
+                do_request<HIST>(P, c, th[k], rq[k], L, E & 0xFF, bid, sharedEvents, smem);
                 finish_request(t[k], P, th[k], rq[k], pd[k]);
                 if (th[k].state == S_FIN) atomicAdd(&bs.fin, 1);
               }
@@ -1852,7 +1861,7 @@ __global__ void __launch_bounds__(32) tail_kernel(KP P) {
     rq.kind = 0;
     if (step(t, P, c, th, rq, pd, S.bs, n) && th.state != S_FIN) {
       c.sub = 1;
-      do_request(P, c, th, rq, TL, E & 0xFF, bid, sharedEvents, sb);
+      do_request<true>(P, c, th, rq, TL, E & 0xFF, bid, sharedEvents, sb);
       finish_request(t, P, th, rq, pd);
     }
   }
@@ -2056,7 +2065,7 @@ __global__ void __launch_bounds__(64, 1) oracle_kernel(KP P0, OQ Q) {
             aborted = true, err = err ? err : 3u;
         }
         unsigned long long se = 0;
-        do_request(P, c, th[i], rq, L, 0, 0, se, osm);
+        do_request<false>(P, c, th[i], rq, L, 0, 0, se, osm);
         finish_request(t[i], P, th[i], rq, pd);
       }
       // barrier: a block whose threads all wait is released (the up /
@@ -2363,8 +2372,9 @@ class CudaEngine final : public DeviceEngine {
       if (r.dev >= 0 && r.dev < 64 && !reserved[r.dev]) {
         cudaFuncAttributes fa;
         size_t frame = 0;
-        if (cudaFuncGetAttributes(&fa, k1::grid_kernel<1>) == cudaSuccess) frame = std::max(frame, fa.localSizeBytes);
-        if (cudaFuncGetAttributes(&fa, k1::grid_kernel<4>) == cudaSuccess) frame = std::max(frame, fa.localSizeBytes);
+        if (cudaFuncGetAttributes(&fa, k1::grid_kernel<1, false>) == cudaSuccess) frame = std::max(frame, fa.localSizeBytes);
+        if (cudaFuncGetAttributes(&fa, k1::grid_kernel<4, false>) == cudaSuccess) frame = std::max(frame, fa.localSizeBytes);
+        if (cudaFuncGetAttributes(&fa, k1::grid_kernel<4, true>) == cudaSuccess) frame = std::max(frame, fa.localSizeBytes);
         size_t cur = 0;
         cudaDeviceGetLimit(&cur, cudaLimitStackSize);
         if (frame > cur) CK(cudaDeviceSetLimit(cudaLimitStackSize, frame));
@@ -2678,7 +2688,6 @@ class CudaEngine final : public DeviceEngine {
                   " bytes) exceeds the engine's on-chip shadow capacity";
       return false;
     }
-    void (*kern)(KP) = K == 1 ? grid_kernel<1> : K == 2 ? grid_kernel<2> : K == 4 ? grid_kernel<4> : grid_kernel<8>;
     const size_t total = (size_t)g.gridDim;
     // the conflict probe needs the same single-device, single-rank log
     const bool glogOn = g.globalRaceCheck || (g.conflictProbe && !exch_ && reps_.size() == 1 && total < MCKG_MAX_BID);
@@ -2805,6 +2814,14 @@ class CudaEngine final : public DeviceEngine {
       kp.glogCap = glogCap;
       kp.glogStrict = g.globalRaceCheck ? 1 : 0;
       kp.glogv = histOn ? R.glogv.p : nullptr;
+      void (*kern)(KP) = histOn ? (K == 1   ? grid_kernel<1, true>
+                                   : K == 2 ? grid_kernel<2, true>
+                                   : K == 4 ? grid_kernel<4, true>
+                                            : grid_kernel<8, true>)
+                                : (K == 1   ? grid_kernel<1, false>
+                                   : K == 2 ? grid_kernel<2, false>
+                                   : K == 4 ? grid_kernel<4, false>
+                                            : grid_kernel<8, false>);
       kp.lineFirst = R.line.p;
       kp.triples = R.tri.p;
       kp.tripleCap = triCaps[ri];
