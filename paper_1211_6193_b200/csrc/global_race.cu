@@ -585,7 +585,16 @@ __device__ __noinline__ void fb_exact(const BOut& O, const mckg_gaccess* recs, c
   }
   const unsigned long long gkey = race ? ((unsigned long long)(xa >> 2) << 16) | (line & 0xFFFFu) : ~0ull - lane;
   const uint32_t grp = __match_any_sync(0xFFFFFFFFu, gkey);
-  const uint32_t mine = __reduce_or_sync(grp, race);
+  // OR of the group's byte masks.  Not __reduce_or_sync(grp, ...): with a
+  // different mask per group it runs once per distinct group (up to 32
+  // serial redux), while groups here are mostly singletons -- this loop runs
+  // (largest group - 1) shuffles
+  uint32_t mine = race;
+  for (uint32_t q = grp & ~(1u << lane); __any_sync(0xFFFFFFFFu, q != 0u);) {
+    const uint32_t y = q ? (uint32_t)__ffs(q) - 1u : lane;
+    q &= q - 1u;
+    mine |= __shfl_sync(0xFFFFFFFFu, race, y);
+  }
   const bool rep = race && (grp & rm & ((1u << lane) - 1u)) == 0u;
   const uint32_t cnt = rep ? __popc(mine) : 0u;
   uint32_t ci = cnt;
