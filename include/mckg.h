@@ -177,7 +177,9 @@ int mckg_get_launch_stats(mckg_launch_stats* out);
  * read once at load).  Bits: 32 = K2's general (TMA) kernel for every block
  * instead of the warp-per-block fast path; 128 = K6's bucket pipeline in
  * sparse (hashed) mode; 256 = K6 never takes the tile path; 512 = K6 takes
- * the tile path at any size (default: from 2^20 records). */
+ * the tile path at any size (default: from 2^20 records); 1024 = the tile
+ * path's pass 1 re-reads every tile (default: only tiles whose in-window
+ * records come from two or more blocks; the others from pass 0's codes). */
 void mckg_set_debug(uint32_t flags);
 
 int mckg_race_out_reset(const mckg_race_out* out, void* stream);

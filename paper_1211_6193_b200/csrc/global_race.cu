@@ -930,10 +930,11 @@ __device__ __forceinline__ void side_write(uint32_t fm, uint32_t slot, unsigned 
 __global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* ev, uint64_t n, uint64_t ntiles,
                                                            uint64_t base, uint32_t nbk, uint32_t* claim,
                                                            uint32_t* bits, unsigned long long* win,
-                                                           mckg_gaccess* side, unsigned long long* nside) {
+                                                           mckg_gaccess* side, unsigned long long* nside,
+                                                           uint16_t* code, uint8_t* tmulti) {
   extern __shared__ __align__(16) uint8_t sm[];
   const uint4* stage = reinterpret_cast<const uint4*>(sm);
-  __shared__ uint32_t s_anchor, s_occ[2], s_cnt[2];
+  __shared__ uint32_t s_anchor, s_occ[2], s_cnt[2], s_bmin[2], s_bmax[2];
   __shared__ unsigned long long s_base[2];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t lane = threadIdx.x & 31u;
@@ -943,6 +944,8 @@ __global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* e
     fence_mbar_init();
     s_occ[0] = s_occ[1] = 0;
     s_cnt[0] = s_cnt[1] = 0;
+    s_bmin[0] = s_bmin[1] = ~0u;
+    s_bmax[0] = s_bmax[1] = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x < ntiles) tile_fetch(ev, n, blockIdx.x, sm, &bar);
@@ -978,18 +981,28 @@ __global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* e
     const uint32_t anchor = s_anchor;
     const uint64_t wbase = base + ((uint64_t)anchor << FB_SHIFT);
     const uint32_t jmax = anchor == ~0u ? 0u : min(TW, nbk - anchor);
-    uint32_t fm = 0, occ = 0;
+    uint32_t fm = 0, occ = 0, bmin = ~0u, bmax = 0;
 #pragma unroll
     for (uint32_t k = 0; k < TR; ++k) {
       const uint32_t i = k * TB + threadIdx.x;
-      if (i >= m) continue;
-      const uint4 r = stage[i];
-      uint32_t rel;
-      const uint32_t j = win_slot(r, wbase, jmax, &rel);
-      if (j != ~0u) {
-        occ |= 1u << j;
-        continue;
+      uint32_t c = 0xFFFFu;  // the record's pass-1 code: window word, or none
+      if (i < m) {
+        const uint4 r = stage[i];
+        uint32_t rel;
+        const uint32_t j = win_slot(r, wbase, jmax, &rel);
+        if (j != ~0u) {
+          occ |= 1u << j;
+          // j << 9 | word in the bucket, its bitmap word x = c >> 5 swizzled
+          // as pass 1 stores it (x ^ ((x >> 5) & 7))
+          c = rel >> 2;
+          c = ((c >> 5) ^ ((c >> 10) & 7u)) << 5 | (c & 31u);
+          bmin = min(bmin, r.w & 0xFFFFFFu);
+          bmax = max(bmax, r.w & 0xFFFFFFu);
+        }
       }
+      if (code) code[r0 + i] = (uint16_t)c;
+      if (c != 0xFFFFu || i >= m) continue;
+      const uint4 r = stage[i];
       const unsigned long long a64 = rec_a(r);
       fm |= 1u << k;
       // foreign: mark the words it touches (clipped to the span)
@@ -1004,16 +1017,25 @@ __global__ void __launch_bounds__(TB, 2) tile_claim_kernel(const mckg_gaccess* e
     }
     occ = __reduce_or_sync(0xFFFFFFFFu, occ);
     if (lane == 0 && occ) atomicOr(&s_occ[cb], occ);
+    bmin = __reduce_min_sync(0xFFFFFFFFu, bmin);
+    bmax = __reduce_max_sync(0xFFFFFFFFu, bmax);
+    if (lane == 0 && bmin != ~0u) {
+      atomicMin(&s_bmin[cb], bmin);
+      atomicMax(&s_bmax[cb], bmax);
+    }
     const uint32_t slot = side_slot(fm, &s_cnt[cb]);
-    __syncthreads();  // #2: the stage is free; s_occ / s_cnt of this tile final
+    __syncthreads();  // #2: the stage is free; s_occ / s_cnt / s_bmin / s_bmax of this tile final
     if (threadIdx.x == 0) {
       if (t + gridDim.x < ntiles) tile_fetch(ev, n, t + gridDim.x, sm, &bar);
       s_base[cb] = s_cnt[cb] ? atomicAdd(nside, (unsigned long long)s_cnt[cb]) : 0ull;
       s_cnt[cb ^ 1u] = 0;  // the next tile's (last read before #2)
       s_occ[cb ^ 1u] = 0;
+      s_bmin[cb ^ 1u] = ~0u;
+      s_bmax[cb ^ 1u] = 0;
     }
     const uint32_t so = s_occ[cb];
     if (threadIdx.x == 32) win[t] = (anchor == ~0u || !so) ? ~0ull : ((unsigned long long)so << 32) | anchor;
+    if (threadIdx.x == 64 && tmulti) tmulti[t] = s_bmin[cb] != s_bmax[cb] ? 1 : 0;
     if (threadIdx.x < TW && ((so >> threadIdx.x) & 1u)) atomicAdd(claim + anchor + threadIdx.x, 1u);
     pfm = fm;
     pslot = slot;
@@ -1032,7 +1054,8 @@ __global__ void __launch_bounds__(TB, 3) tile_detect_kernel(const mckg_gaccess* 
                                                             uint64_t base, uint32_t nbk, const uint32_t* claim,
                                                             const uint32_t* bits, const unsigned long long* win,
                                                             mckg_gaccess* side, unsigned long long* nside,
-                                                            uint32_t* multi, uint32_t* nmulti) {
+                                                            uint32_t* multi, uint32_t* nmulti,
+                                                            const uint32_t* list, const uint32_t* nlist) {
   extern __shared__ __align__(16) uint8_t sm[];
   const uint4* stage = reinterpret_cast<const uint4*>(sm);
   __shared__ uint32_t s_anc[2], s_ok[2], s_bmin[2], s_bmax[2], s_cnt[2];
@@ -1041,6 +1064,9 @@ __global__ void __launch_bounds__(TB, 3) tile_detect_kernel(const mckg_gaccess* 
   __shared__ __align__(8) uint64_t bar;
   const uint32_t lane = threadIdx.x & 31u;
   // the window metadata of tile t into buffer q (s_ok[q] is 0 on entry)
+  // the tiles: every tile, or the listed ones
+  const uint64_t cnt = list ? (uint64_t)*nlist : ntiles;
+  auto tile = [&](uint64_t idx) -> uint64_t { return list ? (uint64_t)list[idx] : idx; };
   auto meta = [&](uint32_t q, uint64_t t) {
     const unsigned long long wv = win[t];
     const uint32_t anchor = (uint32_t)wv, occ = (uint32_t)(wv >> 32);
@@ -1062,14 +1088,15 @@ __global__ void __launch_bounds__(TB, 3) tile_detect_kernel(const mckg_gaccess* 
     }
   }
   __syncthreads();
-  if (blockIdx.x < ntiles) {
-    if (threadIdx.x == 0) tile_fetch(ev, n, blockIdx.x, sm, &bar);
-    meta(0, blockIdx.x);
+  if (blockIdx.x < cnt) {
+    if (threadIdx.x == 0) tile_fetch(ev, n, tile(blockIdx.x), sm, &bar);
+    meta(0, tile(blockIdx.x));
   }
   uint32_t pmm = 0, pslot = 0;           // the previous tile's mixed records (deferred)
   uint64_t pr0 = 0;
   uint32_t it = 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+  for (uint64_t idx = blockIdx.x; idx < cnt; idx += gridDim.x, ++it) {
+    const uint64_t t = tile(idx);
     const uint32_t cb = it & 1u;
     const uint64_t r0 = t * TT;
     const uint32_t m = (uint32_t)(n - r0 < TT ? n - r0 : TT);
@@ -1112,10 +1139,10 @@ __global__ void __launch_bounds__(TB, 3) tile_detect_kernel(const mckg_gaccess* 
     const uint32_t slot = side_slot(mm, &s_cnt[cb]);
     __syncthreads();  // #2: the stage is free; this tile's counters final
     if (threadIdx.x == 0) {
-      if (t + gridDim.x < ntiles) tile_fetch(ev, n, t + gridDim.x, sm, &bar);
+      if (idx + gridDim.x < cnt) tile_fetch(ev, n, tile(idx + gridDim.x), sm, &bar);
       s_base[cb] = s_cnt[cb] ? atomicAdd(nside, (unsigned long long)s_cnt[cb]) : 0ull;
     }
-    if (t + gridDim.x < ntiles) meta(cb ^ 1u, t + gridDim.x);
+    if (idx + gridDim.x < cnt) meta(cb ^ 1u, tile(idx + gridDim.x));
     pmm = mm;
     pslot = slot;
     pr0 = r0;
@@ -1123,6 +1150,106 @@ __global__ void __launch_bounds__(TB, 3) tile_detect_kernel(const mckg_gaccess* 
   }
   __syncthreads();
   if (pmm) side_write(pmm, pslot, s_base[(it - 1u) & 1u], ev, pr0, side);
+}
+
+// Pass 1 without re-reading the records (the default): a warp per tile
+// reads the tile's 2-byte codes from pass 0 (window word per record, 8 KiB
+// per tile instead of 64 KiB of records) and sends its MIXED records to the
+// side list -- exactly pass 1's classification.  A tile whose in-window
+// records come from two or more blocks (tmulti) may have own records that
+// race among themselves: it is listed for the full pass 1 (tile_detect on
+// the list), which re-reads it.
+constexpr uint32_t TQ = TT / 8 / 32;  // uint4 code groups per lane
+__global__ void __launch_bounds__(TB, 4) tile_mixed_kernel(const mckg_gaccess* ev, uint64_t ntiles,
+                                                           const uint32_t* claim, const uint32_t* bits,
+                                                           const unsigned long long* win, const uint16_t* code,
+                                                           const uint8_t* tmulti, mckg_gaccess* side,
+                                                           unsigned long long* nside, uint32_t* full,
+                                                           uint32_t* nfull) {
+  __shared__ uint32_t sbits_all[TB / 32][TW * TBW];
+  __shared__ uint32_t s_tot[TB / 32];
+  __shared__ unsigned long long s_off[TB / 32];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  uint32_t* sb = sbits_all[warp];
+  const uint4* c4 = reinterpret_cast<const uint4*>(code);
+  // the CTA's warps take TB / 32 consecutive tiles per round and reserve
+  // their side-list ranges with one atomic (one per tile would serialise
+  // 2^17 same-address atomics at C5 scale)
+  for (uint64_t t0 = (uint64_t)blockIdx.x * (TB / 32); t0 < ntiles; t0 += (uint64_t)gridDim.x * (TB / 32)) {
+    const uint64_t t = t0 + warp;
+    const unsigned long long wv = t < ntiles ? win[t] : ~0ull;
+    const uint32_t anchor = (uint32_t)wv, occ = (uint32_t)(wv >> 32);
+    uint32_t mw[TQ / 4] = {};
+    uint32_t c = 0, incl = 0;
+    if (anchor != ~0u && tmulti[t]) {
+      if (lane == 0) full[atomicAdd(nfull, 1u)] = (uint32_t)t;
+    } else if (anchor != ~0u) {  // (no window: every record foreign, sent in pass 0)
+      const bool own = lane < TW && ((occ >> lane) & 1u) && claim[anchor + lane] == 1u;
+      const uint32_t ok = __ballot_sync(0xFFFFFFFFu, own);
+#pragma unroll
+      for (uint32_t q = 0; q < TW * TBW / 32; ++q) {
+        const uint32_t x = q * 32u + lane;
+        // word x of the window's bitmap, all-ones when its bucket is not
+        // solely this tile's (so a set bit = MIXED), stored swizzled at
+        // x ^ ((x >> 5) & 7): lanes holding records a fixed stride apart,
+        // e.g. one per thread of a simulated block, hit 8 words of one bank
+        // otherwise (pass 0's codes carry the swizzled index)
+        if ((occ >> (x / TBW)) & 1u)
+          sb[x ^ ((x >> 5) & 7u)] = ((ok >> (x / TBW)) & 1u) ? bits[(uint64_t)anchor * TBW + x] : ~0u;
+      }
+      __syncwarp();
+      // lane l holds code groups g = q * 32 + l (records 8g .. 8g + 7)
+#pragma unroll
+      for (uint32_t q = 0; q < TQ; ++q) {
+        const uint4 c = c4[t * (TT / 8) + q * 32u + lane];
+        const uint32_t cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (uint32_t e = 0; e < 8; ++e) {
+          const uint32_t v = (cc[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+          if (v == 0xFFFFu) continue;
+          const uint32_t b = sb[v >> 5];
+          mw[q >> 2] |= (__funnelshift_r(b, b, v) & 1u) << ((q & 3u) * 8u + e);
+        }
+      }
+#pragma unroll
+      for (uint32_t h = 0; h < TQ / 4; ++h) c += __popc(mw[h]);
+      incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= (uint32_t)d) incl += y;
+      }
+    }
+    if (lane == 31) s_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t v = lane < TB / 32 ? s_tot[lane] : 0u;
+      uint32_t x = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+        if (lane >= (uint32_t)d) x += y;
+      }
+      unsigned long long b = 0;
+      const uint32_t all = __shfl_sync(0xFFFFFFFFu, x, 31);
+      if (lane == 0 && all) b = atomicAdd(nside, (unsigned long long)all);
+      b = __shfl_sync(0xFFFFFFFFu, b, 0);
+      if (lane < TB / 32) s_off[lane] = b + x - v;
+    }
+    __syncthreads();
+    const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (tot) {
+      unsigned long long p = s_off[warp] + incl - c;
+      const uint64_t r0 = t * TT;
+#pragma unroll
+      for (uint32_t h = 0; h < TQ / 4; ++h)
+        for (uint32_t f = mw[h]; f; f &= f - 1u) {
+          const uint32_t bit = (uint32_t)__ffs(f) - 1u, q = h * 4u + (bit >> 3), e = bit & 7u;
+          side[p++] = ev[r0 + (uint64_t)(q * 32u + lane) * 8u + e];
+        }
+    }
+    __syncthreads();  // s_tot / s_off and sb are rewritten next round
+  }
 }
 
 // The listed tiles of pass 1 (own records from two or more blocks): the own
@@ -1545,6 +1672,17 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   uint32_t* multi = nullptr;  // [ntiles] tiles for tile_multi, then their count
   MCKG_CUDA_TRY(pg.alloc(&multi, ((size_t)ntiles + 1) * 4));
   MCKG_CUDA_TRY(cudaMemsetAsync(multi + ntiles, 0, 4, s));
+  // pass 1 from pass 0's codes (debug 1024: every tile re-read instead)
+  const bool compact = !(debug_flags() & 1024u);
+  uint16_t* code = nullptr;  // [ntiles * TT] window word per record
+  uint8_t* tmulti = nullptr;  // [ntiles] in-window records from >= 2 blocks
+  uint32_t* full = nullptr;  // [ntiles] tiles for the full pass 1, then their count
+  if (compact) {
+    MCKG_CUDA_TRY(pg.alloc(&code, (size_t)ntiles * TT * 2));
+    MCKG_CUDA_TRY(pg.alloc(&tmulti, (size_t)ntiles));
+    MCKG_CUDA_TRY(pg.alloc(&full, ((size_t)ntiles + 1) * 4));
+    MCKG_CUDA_TRY(cudaMemsetAsync(full + ntiles, 0, 4, s));
+  }
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_claim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TD_SMEM));
@@ -1554,9 +1692,20 @@ int detect_tiles(const mckg_gaccess* events, uint64_t n, const BOut& O, cudaStre
   MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pd, tile_detect_kernel, TB, TD_SMEM));
   const uint64_t gc = std::min<uint64_t>(ntiles, (uint64_t)sm_count() * (uint64_t)(pc > 0 ? pc : 1));
   const uint64_t gdt = std::min<uint64_t>(ntiles, (uint64_t)sm_count() * (uint64_t)(pd > 0 ? pd : 1));
-  tile_claim_kernel<<<(unsigned)gc, TB, TC_SMEM, s>>>(events, n, ntiles, base, nbk, claim, bits, win, side, nside);
+  tile_claim_kernel<<<(unsigned)gc, TB, TC_SMEM, s>>>(events, n, ntiles, base, nbk, claim, bits, win, side, nside,
+                                                      code, tmulti);
+  if (compact) {
+    int pm = 0;
+    MCKG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pm, tile_mixed_kernel, TB, 0));
+    const uint64_t gm = std::min<uint64_t>((ntiles + TB / 32 - 1) / (TB / 32),
+                                           (uint64_t)sm_count() * (uint64_t)(pm > 0 ? pm : 1));
+    tile_mixed_kernel<<<(unsigned)gm, TB, 0, s>>>(events, ntiles, claim, bits, win, code, tmulti, side, nside, full,
+                                                  full + ntiles);
+    ++launches;
+  }
   tile_detect_kernel<<<(unsigned)gdt, TB, TD_SMEM, s>>>(events, n, ntiles, base, nbk, claim, bits, win, side, nside,
-                                                        multi, multi + ntiles);
+                                                        multi, multi + ntiles, compact ? full : nullptr,
+                                                        compact ? full + ntiles : nullptr);
   MCKG_CUDA_TRY(cudaFuncSetAttribute(tile_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TM_SMEM));
   tile_multi_kernel<<<(unsigned)gdt, TB, TM_SMEM, s>>>(events, n, base, nbk, claim, bits, win, multi, multi + ntiles,
                                                        side, nside, O);

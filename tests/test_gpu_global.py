@@ -10,7 +10,7 @@ import oracle_bind as ob
 pytestmark = pytest.mark.gpu
 
 
-MODES = {"dense": 256, "sparse": 128 | 256, "tile": 512}
+MODES = {"dense": 256, "sparse": 128 | 256, "tile": 512, "tile_reread": 512 | 1024}
 
 
 @pytest.fixture(autouse=True, params=list(MODES))
@@ -20,7 +20,8 @@ def k6_mode(request):
     sparse mode (hashed tables only, mckg_set_debug(128)), and the in-place
     tile path (pass 0 claim / foreign, pass 1 own words, the side list through
     the bucket pipeline), forced at any size by mckg_set_debug(512) and taken
-    by default from 2^20 records."""
+    by default from 2^20 records -- its pass 1 from pass 0's per-record codes
+    (single-block tiles) or re-reading every tile (mckg_set_debug(1024))."""
     from paper_1211_6193_b200 import _abi
     lib = _abi.load()
     lib.mckg_set_debug(MODES[request.param])
