@@ -1167,17 +1167,11 @@ __global__ void __launch_bounds__(TB, 4) tile_mixed_kernel(const mckg_gaccess* e
                                                            unsigned long long* nside, uint32_t* full,
                                                            uint32_t* nfull) {
   __shared__ uint32_t sbits_all[TB / 32][TW * TBW];
-  __shared__ uint32_t s_tot[TB / 32];
-  __shared__ unsigned long long s_off[TB / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   uint32_t* sb = sbits_all[warp];
   const uint4* c4 = reinterpret_cast<const uint4*>(code);
-  // the CTA's warps take TB / 32 consecutive tiles per round and reserve
-  // their side-list ranges with one atomic (one per tile would serialise
-  // 2^17 same-address atomics at C5 scale)
-  for (uint64_t t0 = (uint64_t)blockIdx.x * (TB / 32); t0 < ntiles; t0 += (uint64_t)gridDim.x * (TB / 32)) {
-    const uint64_t t = t0 + warp;
-    const unsigned long long wv = t < ntiles ? win[t] : ~0ull;
+  for (uint64_t t = (uint64_t)blockIdx.x * (TB / 32) + warp; t < ntiles; t += (uint64_t)gridDim.x * (TB / 32)) {
+    const unsigned long long wv = win[t];
     const uint32_t anchor = (uint32_t)wv, occ = (uint32_t)(wv >> 32);
     uint32_t mw[TQ / 4] = {};
     uint32_t c = 0, incl = 0;
@@ -1220,26 +1214,11 @@ __global__ void __launch_bounds__(TB, 4) tile_mixed_kernel(const mckg_gaccess* e
         if (lane >= (uint32_t)d) incl += y;
       }
     }
-    if (lane == 31) s_tot[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t v = lane < TB / 32 ? s_tot[lane] : 0u;
-      uint32_t x = v;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
-        if (lane >= (uint32_t)d) x += y;
-      }
-      unsigned long long b = 0;
-      const uint32_t all = __shfl_sync(0xFFFFFFFFu, x, 31);
-      if (lane == 0 && all) b = atomicAdd(nside, (unsigned long long)all);
-      b = __shfl_sync(0xFFFFFFFFu, b, 0);
-      if (lane < TB / 32) s_off[lane] = b + x - v;
-    }
-    __syncthreads();
     const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
     if (tot) {
-      unsigned long long p = s_off[warp] + incl - c;
+      unsigned long long b = 0;
+      if (lane == 31) b = atomicAdd(nside, (unsigned long long)tot);
+      unsigned long long p = __shfl_sync(0xFFFFFFFFu, b, 31) + incl - c;
       const uint64_t r0 = t * TT;
 #pragma unroll
       for (uint32_t h = 0; h < TQ / 4; ++h)
@@ -1248,7 +1227,7 @@ __global__ void __launch_bounds__(TB, 4) tile_mixed_kernel(const mckg_gaccess* e
           side[p++] = ev[r0 + (uint64_t)(q * 32u + lane) * 8u + e];
         }
     }
-    __syncthreads();  // s_tot / s_off and sb are rewritten next round
+    __syncwarp();  // sb is rewritten for the warp's next tile
   }
 }
 
