@@ -832,13 +832,17 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
 //     Every other record of the tile (outside the window, crossing a word,
 //     out of range) is FOREIGN: appended to the side list, its words marked
 //     in a bitmap over the span;
-//   pass 1 (tile_detect): a record in its tile's window is OWN when its bucket
-//     was claimed by that tile alone and its word is unmarked.  No record of
-//     another tile touches an own record's word, so a tile whose own records
-//     all come from one block has no race among them (races are
-//     cross-block); otherwise they run the word filter of bucket_fast over
-//     the window's TW x 512 words.  The rest (contested buckets, marked
-//     words) are MIXED and join the side list;
+//   pass 1: a record in its tile's window is OWN when its bucket was claimed
+//     by that tile alone and its word is unmarked.  No record of another
+//     tile touches an own record's word, so a tile whose own records all
+//     come from one block has no race among them (races are cross-block);
+//     otherwise they run the word filter of bucket_fast over the window's
+//     TW x 512 words.  The rest (contested buckets, marked words) are MIXED
+//     and join the side list.  Pass 0 leaves a 2-byte code per record (its
+//     window word) and whether the tile's in-window records span blocks;
+//     tile_mixed classifies single-block tiles from the codes alone (8 KiB
+//     per tile instead of 64 KiB of records) and lists the others for
+//     tile_detect, which re-reads them;
 //   the side list (foreign + mixed, every record on their words) then runs
 //     through the bucket pipeline.
 // Each word is decided by exactly one of the two, so the race sets are
