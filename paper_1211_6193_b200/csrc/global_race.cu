@@ -497,7 +497,7 @@ constexpr uint32_t FB_ROWS = 16;               // records per lane
 constexpr uint32_t FB_MAX = FB_ROWS * 32;
 constexpr uint32_t FB_WARPS = 16;
 constexpr int FB_BR = 2;                       // rows per load batch
-constexpr uint32_t FB_STAGE = 64;              // staged races per warp
+constexpr uint32_t FB_STAGE = 128;             // staged races per warp
 constexpr uint32_t FB_WARP_BYTES = FB_WORDS * 8 + 32 * 8 + FB_STAGE * 16;
 constexpr uint32_t FB_SMEM = FB_WARPS * FB_WARP_BYTES;
 
