@@ -30,6 +30,10 @@ __device__ __forceinline__ unsigned long long sm64(unsigned long long x) {
 }
 
 __device__ __forceinline__ uint64_t ga_addr(uint64_t a) { return a & 0xFFFFFFFFFFull; }
+// a record's address word from its 16-byte image
+__device__ __forceinline__ unsigned long long rec_a(const uint4& r) {
+  return ((unsigned long long)r.y << 32) | r.x;
+}
 __device__ __forceinline__ uint32_t ga_len(uint64_t a) { return (uint32_t)((a >> 40) & 0xFu); }
 __device__ __forceinline__ uint32_t ga_write(uint64_t a) { return (uint32_t)((a >> 44) & 1u); }
 __device__ __forceinline__ uint32_t ga_tid(uint64_t a) { return (uint32_t)((a >> 45) & 0x7FFu); }
@@ -498,7 +502,7 @@ constexpr uint32_t FB_MAX = FB_ROWS * 32;
 constexpr uint32_t FB_WARPS = 16;
 constexpr int FB_BR = 2;                       // rows per load batch
 constexpr uint32_t FB_STAGE = 128;             // staged races per warp
-constexpr uint32_t FB_WARP_BYTES = FB_WORDS * 8 + 32 * 8 + FB_STAGE * 16;
+constexpr uint32_t FB_WARP_BYTES = FB_WORDS * 8 + 32 * 16 + FB_STAGE * 16;
 constexpr uint32_t FB_SMEM = FB_WARPS * FB_WARP_BYTES;
 
 struct LineCache {  // lane-owned first-racing-key cache of one warp
@@ -548,14 +552,19 @@ __device__ __forceinline__ void fb_flush(const BOut& O, const mckg_grace* stg, u
 // (byte, line) pairs are reported once (the group of a (word, line) ORs its
 // byte masks), staged per warp; the first racing key per line goes to the
 // warp's line cache.
-__device__ __noinline__ void fb_exact(const BOut& O, const mckg_gaccess* recs, const uint64_t* cl, uint32_t nc,
+__device__ __noinline__ void fb_exact(const BOut& O, const uint4* cl, uint32_t nc,
                                       LineCache& C, mckg_grace* stg, uint32_t& nstg, uint32_t& flags) {
   const uint32_t lane = threadIdx.x & 31u;
   __syncwarp();
   if (nc == 0) return;
   const bool act = lane < nc;
   mckg_gaccess X{};
-  if (act) X = recs[cl[lane]];
+  if (act) {
+    const uint4 r = cl[lane];
+    X.a = rec_a(r);
+    X.sweep = r.z;
+    X.b = r.w;
+  }
   const uint64_t xa = ga_addr(X.a);
   const unsigned long long xw = act ? (unsigned long long)(xa >> 2) : ~0ull - lane;
   const uint32_t xmask = act ? ((1u << ga_len(X.a)) - 1u) << (xa & 3u) : 0u;
@@ -638,8 +647,8 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   uint32_t* tag = reinterpret_cast<uint32_t*>(sm + warp * FB_WARP_BYTES);
   uint32_t* flg = tag + FB_WORDS;
-  uint64_t* cl = reinterpret_cast<uint64_t*>(flg + FB_WORDS);  // the candidate batch
-  mckg_grace* stg = reinterpret_cast<mckg_grace*>(cl + 32);     // staged races
+  uint4* cl = reinterpret_cast<uint4*>(flg + FB_WORDS);  // the candidate batch (records)
+  mckg_grace* stg = reinterpret_cast<mckg_grace*>(cl + 32);  // staged races
   uint32_t nbatch = 0;                                          // warp-uniform
   uint32_t nstg = 0;                                          // warp-uniform
   for (uint32_t i = lane; i < FB_WORDS; i += 32) flg[i] = 0u;
@@ -681,7 +690,7 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
       // records, disjoint words) of <= 32 records joins the exact batch --
       // the filter only prunes, fb_exact decides every pair itself
       if (nbatch + (uint32_t)(o1 - o0) > 32u) {
-        fb_exact(O, recs, cl, nbatch, C, stg, nstg, flags);
+        fb_exact(O, cl, nbatch, C, stg, nstg, flags);
         nbatch = 0;
       }
       const uint32_t room = 32u - nbatch;
@@ -690,8 +699,10 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
       const uint64_t e = __shfl_sync(0xFFFFFFFFu, lo1, bl + r - 1u);
       const uint32_t len = (uint32_t)(e - o0);
       bool badr = false;
+      uint4 rr = make_uint4(0, 0, 0, 0);
       if (lane < len) {
-        const uint64_t a64 = recs[o0 + lane].a;
+        rr = __ldg(reinterpret_cast<const uint4*>(recs) + o0 + lane);
+        const uint64_t a64 = rec_a(rr);
         badr = (ga_addr(a64) & 3u) + ga_len(a64) > 4u;  // a word-contained record lies in its bucket
       }
       const uint32_t badm = __ballot_sync(0xFFFFFFFFu, badr);
@@ -705,13 +716,13 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
         b = b0 + hb + 1;
         if (hb > bl) {  // the buckets before it are clean
           const uint32_t clen = (uint32_t)(__shfl_sync(0xFFFFFFFFu, lo0, hb) - o0);
-          if (lane < clen) cl[nbatch + lane] = o0 + lane;
+          if (lane < clen) cl[nbatch + lane] = rr;
           nbatch += clen;
         }
         __syncwarp();
         continue;
       }
-      if (lane < len) cl[nbatch + lane] = o0 + lane;
+      if (lane < len) cl[nbatch + lane] = rr;
       nbatch += len;
       b = b0 + bl + r;
       __syncwarp();
@@ -806,15 +817,15 @@ __global__ void __launch_bounds__(FB_WARPS * 32, 2) bucket_fast_kernel(const mck
     }
     // the bucket's candidates join the warp's batch (exact pass per 32)
     if (nbatch + nc > 32u) {
-      fb_exact(O, recs, cl, nbatch, C, stg, nstg, flags);
+      fb_exact(O, cl, nbatch, C, stg, nstg, flags);
       nbatch = 0;
     }
     uint32_t pos = nbatch + incl - c;
-    for (uint32_t g = cm; g; g &= g - 1u) cl[pos++] = o0 + (uint64_t)((__ffs(g) - 1) * 32u + lane);
+    for (uint32_t g = cm; g; g &= g - 1u) cl[pos++] = __ldg(R4 + (uint64_t)((__ffs(g) - 1) * 32u + lane));
     nbatch += nc;
     __syncwarp();
   }
-  fb_exact(O, recs, cl, nbatch, C, stg, nstg, flags);
+  fb_exact(O, cl, nbatch, C, stg, nstg, flags);
   fb_flush(O, stg, nstg, flags);
   if (C.line != 0xFFFFFFFFu) atomicMin(O.line_first + C.line, C.ts);
   flags = __reduce_or_sync(0xFFFFFFFFu, flags);
@@ -882,9 +893,6 @@ __device__ __forceinline__ void tile_fetch(const mckg_gaccess* ev, uint64_t n, u
   bulk_g2s(stage, ev + r0, bytes, bar);
 }
 
-__device__ __forceinline__ unsigned long long rec_a(const uint4& r) {
-  return ((unsigned long long)r.y << 32) | r.x;
-}
 
 // The window slot of record r for a tile whose window starts at byte wbase
 // and has jmax = min(TW, nbk - anchor) buckets, else ~0u -- exactly
@@ -1250,7 +1258,7 @@ __global__ void __launch_bounds__(TB) tile_multi_kernel(const mckg_gaccess* ev, 
   __shared__ uint32_t s_ok, s_nc, s_cnt;
   __shared__ unsigned long long s_base;
   __shared__ uint32_t sbits[TW * TBW];
-  __shared__ uint64_t cl[32];
+  __shared__ uint4 cl[32];
   __shared__ mckg_grace stg[FB_STAGE];
   LineCache C{0xFFFFFFFFu, ~0ull, 0u};  // warp 0's
   uint32_t nstg = 0, flags = 0;          // warp 0's
@@ -1312,7 +1320,7 @@ __global__ void __launch_bounds__(TB) tile_multi_kernel(const mckg_gaccess* ev, 
     const uint32_t c = __popc(cm);
     uint32_t pos = c ? atomicAdd(&s_nc, c) : 0u;
     for (uint32_t q = cm; q; q &= q - 1u, ++pos)
-      if (pos < 32) cl[pos] = r0 + (uint64_t)((__ffs(q) - 1) * TB + threadIdx.x);
+      if (pos < 32) cl[pos] = reinterpret_cast<const uint4*>(ev)[r0 + (uint64_t)((__ffs(q) - 1) * TB + threadIdx.x)];
     __syncthreads();
     const uint32_t nc = s_nc;
     if (nc > 32) {
@@ -1327,7 +1335,7 @@ __global__ void __launch_bounds__(TB) tile_multi_kernel(const mckg_gaccess* ev, 
       __syncthreads();
       if (om) side_write(om, os, s_base, ev, r0, side);
     } else if (nc && threadIdx.x < 32) {
-      fb_exact(O, ev, cl, nc, C, stg, nstg, flags);
+      fb_exact(O, cl, nc, C, stg, nstg, flags);
     }
     __syncthreads();  // tables reused by the next tile
   }
