@@ -180,6 +180,19 @@ def test_block_clustered_traces(case):
     assert n >= 0
 
 
+def test_single_and_multi_block_tiles_mixed():
+    """One input whose tiles alternate between one block (pass 1 from pass
+    0's codes, tile_mixed) and two blocks (listed for the re-reading pass),
+    with foreign records between them, in-tile candidates, word-crossing
+    records and a partial last tile (codes past its end are unused)."""
+    ev = _tiled(40, 13, shared_words=5, bids_per_tile=2, foreign=0.02, unaligned=0.003)
+    t = np.repeat(np.arange(40), 4096)
+    single = (t % 2) == 0
+    b = ev["b"] & 0xFFFFFF
+    ev["b"][single] = (ev["b"][single] & 0xFF000000) | (b[single] & ~np.uint32(1))
+    assert _check(ev[: 40 * 4096 - 1000]) > 0
+
+
 def test_c5_two_million_records():
     """2^21 C5 records: the size at which the tile path is the default."""
     assert _check(ob.gen_c5(0, 512, 512)) > 0
